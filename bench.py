@@ -1,0 +1,348 @@
+#!/usr/bin/env python
+"""Benchmark of the ADMM light-field super-resolution hot path (arXiv 2206.05047).
+
+A "step" is one ADMM iteration (Alg.1: weights, data shrink/dual, NLTV
+shrink/dual, v, and K = 5 CG steps of Alg.2) over the whole synthetic light field of
+the bench workload (default C3: 9x9 views, 256x256 LR -> x2, 512x512 HR, sigma=0.05 +
+20 % impulse; BASELINE.json configs[2], the "9x9 LF x2" of the metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
+
+Timing: W untimed warm-up steps, then exactly K steps, each bracketed by CUDA events on
+the solver's stream, with an L2 flush (a 512 MiB write) between steps outside the events;
+the sum of the K step times is the step time; barrier + synchronize on both sides; max
+over ranks.  value = (ADMM iterations done by all ranks) / that time.  Multi-GPU: every
+rank solves its own light field (independent reference views / problems, weak scaling,
+no data-path collective); see DESIGN.md §10.
+
+--impl reference times the fp64 CPU oracle (oracle/, the only baseline this tier has)
+on the same workload, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "ADMM iters/s and HR Mpix/s, 9x9 LF x2/x3 SR; HBM GB/s vs B200 peak"
+UNIT = "ADMM iters/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-flush", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- algorithmic model
+def algorithmic(cfg, d):
+    """Per-launch algorithmic bytes and flops of the kernels."""
+    sk, p, q = cfg.n_views, cfg.H * cfg.W, cfg.lr_h * cfg.lr_w
+    sd = (2 * d.radius + 1) ** 2 - 1
+    z = cfg.scale
+    R = math.ceil(3 * 0.25 * math.sqrt(z * z - 1))
+    fA = 10 + 2 * (2 * R + 1) * (1.0 / z + 1.0 / z ** 2)     # flops per HR px per view, one direction
+    K = d.cg_max_iters
+    normal_flops = 2 * sk * fA * p + 7 * sd * p              # A + A^T over all views + S^T S stencil
+    normal_bytes = 4 * p * 6                                 # r, p_prev (read), p (write), omega, m, q (RED)
+    wz_flops = 2 * sk * fA * p + 10 * sd * p + 8 * sk * q
+    wz_bytes = 4 * (3 * sk * q + 2 * sd * p + 5 * p)
+    upd_bytes = 4 * p * 7
+    iter_bytes = wz_bytes + K * (normal_bytes + upd_bytes)
+    iter_flops = wz_flops + K * normal_flops
+    return dict(normal_flops=normal_flops, normal_bytes=normal_bytes, wz_flops=wz_flops, wz_bytes=wz_bytes,
+                upd_bytes=upd_bytes, iter_bytes=iter_bytes, iter_flops=iter_flops)
+
+
+def peaks():
+    """Measured HBM copy bandwidth (MEASURED_PEAKS.json) and the FP32 CUDA-core peak derived from
+    the unit counts and clock (148 SMs x 128 FP32 lanes x 2 flop x sm_max_mhz)."""
+    hbm, sm_mhz, src = 6650.0, 1965.0, "fallback (B200_PROFILING.md)"
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        try:
+            j = json.load(open(path))
+            hbm = float(j.get("hbm_gbs", hbm))
+            sm_mhz = float(j.get("sm_max_mhz", sm_mhz))
+            src = "measured (MEASURED_PEAKS.json)"
+        except Exception:
+            pass
+    fp32 = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
+    return hbm, fp32, src
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([v.strip() for v in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm = [float(s[0]) for s in self.samples if len(s) >= 7 and s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if len(s) >= 7 and s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            if len(s) >= 7:
+                for n, v in zip(names, s[3:7]):
+                    if v.lower() == "active":
+                        reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- CPU oracle
+def oracle_params(cfg, d):
+    import oracle as O
+    return O.Params(n_views=cfg.n_views, lr_h=cfg.lr_h, lr_w=cfg.lr_w, scale=cfg.scale, ref_view=cfg.ref_view,
+                    radius=d.radius, lambda1=d.lambda1, lambda2=d.lambda2, lambda_reg=d.lambda_reg,
+                    sigma_s=d.sigma_s, sigma_e=d.sigma_e, sigma_o1=d.sigma_o1, sigma_o2=d.sigma_o2, theta=d.theta,
+                    cg_max_iters=d.cg_max_iters, cg_tol=d.cg_tol)
+
+
+def time_oracle(lf, cfg, d, iters=1):
+    """Seconds per ADMM iteration of the fp64 oracle as it stands (all host cores)."""
+    import oracle as O
+    O.build()
+    P = oracle_params(cfg, d)
+    t0 = time.perf_counter()
+    O.admm(P, lf.y, lf.view_offsets, lf.omega, iters)
+    return (time.perf_counter() - t0) / iters
+
+
+def cores():
+    return int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+
+
+def run_reference(args, cfg, d, rank):
+    if rank != 0:
+        return
+    import lfsr_synth as S
+    lf = S.make_lightfield(cfg)
+    sample = "%s: one full ADMM iteration (K=%d CG steps) per step, fp64 oracle, OMP threads=%d" % (
+        cfg.name, d.cg_max_iters, cores())
+    for _ in range(min(args.warmup, 1)):   # a CPU program needs no long warm-up
+        time_oracle(lf, cfg, d, 1)
+    ts = [time_oracle(lf, cfg, d, 1) for _ in range(args.steps)]
+    t = sum(ts)
+    value = args.steps / t
+    hr_mpix = cfg.H * cfg.W / 1e6
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": min(args.warmup, 1), "ms_per_step": 1000 * t / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "hr_mpix_it_per_s": value * hr_mpix,
+            "config": {"workload": cfg.name, "desc": cfg.note, "views": cfg.n_views, "scale": cfg.scale,
+                       "hr": [cfg.H, cfg.W], "cg_steps": d.cg_max_iters, "l2_flush": "n/a (CPU)"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores(), "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- ours
+def main():
+    args = parse()
+    import lfsr_synth as S
+    cfg = S.CONFIGS[args.config]
+    d = S.SolverDefaults()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, cfg, d, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_2206_05047_b200 as L
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # each rank super-resolves its own light field (independent problem, own seed)
+    lf = S.make_lightfield(cfg, seed=None if rank == 0 else 10007 * rank + 1000)
+    stream = torch.cuda.Stream()          # a real (non-legacy) stream shared by torch and liblfsr
+    torch.cuda.set_stream(stream)
+    p = L.params_for(cfg, d, device=local)
+    sol = L.Solver(p, stream=stream.cuda_stream)
+    dev_in = [torch.from_numpy(a).cuda() for a in (lf.y, lf.view_offsets, lf.omega)]
+    sol.set_observations(*dev_in)
+    flush = None if args.no_flush else torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def do_flush():
+        if flush is not None:
+            flush.fill_(1.0)
+
+    for _ in range(args.warmup):
+        do_flush()
+        sol.admm_enqueue(1)
+    sol.admm_stats(1, args.warmup) if args.warmup else None
+    sol.profile(True)
+    first = args.warmup + 1
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    for i in range(args.steps):
+        do_flush()
+        ev[i][0].record(stream)
+        sol.admm_enqueue(1)
+        ev[i][1].record(stream)
+        ev[i][1].synchronize()
+        sol.profile_read()
+    barrier()
+    clk = clocks.stop()
+    t_ms = sum(a.elapsed_time(b) for a, b in ev)
+    kms, kn = sol.profile_read()
+    stats = sol.admm_stats(first, args.steps)   # raises on divergence
+    t_max = t_ms
+    if world > 1:
+        tt = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max = float(tt.item())
+    total_iters = args.steps * world
+    value = total_iters / (t_max / 1000.0)
+    hr_mpix = cfg.H * cfg.W / 1e6
+
+    # ---- end to end through the public API with host buffers (full solves of N iterations)
+    e2e = None
+    if args.e2e_steps > 0:
+        host = [torch.from_numpy(a).pin_memory() for a in (lf.y, lf.view_offsets, lf.omega)]
+        xout = torch.empty((cfg.H, cfg.W), dtype=torch.float32).pin_memory()
+        n_it = cfg.n_iters
+        sol.profile(False)
+        # warm (allocations are reused for the same geometry)
+        sol.set_observations(*host)
+        sol.admm_run(n_it, want_stats=False)
+        sol.get_hr(xout)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        tot = 0.0
+        for _ in range(args.e2e_steps):
+            do_flush()
+            e0.record(stream)
+            sol.set_observations(*host)            # H2D of y, offsets, omega + setup (a1)
+            sol.admm_run(n_it, want_stats=False)   # N iterations, divergence-checked
+            sol.get_hr(xout)                       # D2H of x (blocks)
+            e1.record(stream)
+            e1.synchronize()
+            tot += e0.elapsed_time(e1)
+        if world > 1:
+            tt = torch.tensor([tot], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            tot = float(tt.item())
+        h2d = sum(int(h.numel()) * 4 for h in host)
+        e2e = {"value": args.e2e_steps * n_it * world / (tot / 1000.0), "unit": UNIT,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(xout.numel()) * 4 + 8 * 11 * n_it,
+               "step": "full solve: set_observations (H2D + setup) + %d ADMM iterations + get_hr (D2H)" % n_it,
+               "ms_per_solve": tot / args.e2e_steps, "psnr_db": L.psnr(xout.numpy(), lf.x_gt)}
+
+    # ---- roofline of the dominant kernel (the CG normal-operator tile kernel)
+    alg = algorithmic(cfg, d)
+    hbm_peak, fp32_peak, peak_src = peaks()
+    k_normal_ms = kms[1] / max(kn[1], 1)
+    k_wz_ms = kms[0] / max(kn[0], 1)
+    k_upd_ms = kms[2] / max(kn[2], 1)
+    achieved = alg["normal_flops"] / (k_normal_ms / 1000.0) / 1e12
+    traffic = None
+    tr_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tr_path):
+        try:
+            traffic = json.load(open(tr_path)).get(cfg.name, {}).get("k_tile_normal_dram_bytes")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "alu", "kernel": "k_tile<NORMAL> (CG normal operator q = M p, a8)",
+                "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s", "frac": achieved / fp32_peak,
+                "traffic": traffic, "peak_source": "FP32 CUDA cores, 148 SM x 128 lanes x 2 x sm_max_mhz (%s)" % peak_src,
+                "algorithmic_flops_per_launch": alg["normal_flops"], "avg_launch_ms": k_normal_ms,
+                "share_of_step": kms[1] / max(sum(kms), 1e-9),
+                "wz_step": {"avg_launch_ms": k_wz_ms, "alg_bytes": alg["wz_bytes"],
+                            "hbm_gbs": alg["wz_bytes"] / (k_wz_ms / 1000.0) / 1e9,
+                            "hbm_frac": alg["wz_bytes"] / (k_wz_ms / 1000.0) / 1e9 / hbm_peak},
+                "cg_update": {"avg_launch_ms": k_upd_ms, "alg_bytes": alg["upd_bytes"],
+                              "hbm_gbs": alg["upd_bytes"] / (k_upd_ms / 1000.0) / 1e9},
+                "iteration_hbm_gbs": alg["iter_bytes"] * total_iters / (t_max / 1000.0) / 1e9 / world,
+                "iteration_hbm_frac": alg["iter_bytes"] * total_iters / (t_max / 1000.0) / 1e9 / world / hbm_peak,
+                "hbm_peak_gbs": hbm_peak}
+
+    # ---- CPU baseline: the oracle as it stands, on a bounded sample, rank 0 at N = 1 only
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            sec = time_oracle(lf, cfg, d, 1)
+            cpu = {"value": 1.0 / sec, "unit": UNIT, "cores": cores(), "kind": "oracle",
+                   "sample": "%s: one full ADMM iteration (K=%d) of the fp64 oracle on the host cores" %
+                             (cfg.name, d.cg_max_iters)}
+        except Exception as e:  # pragma: no cover
+            cpu = {"value": None, "unit": UNIT, "cores": cores(), "kind": "oracle", "sample": "failed: %s" % e}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "hr_mpix_it_per_s": value * hr_mpix,
+                "config": {"workload": cfg.name, "desc": cfg.note, "views": cfg.n_views, "scale": cfg.scale,
+                           "hr": [cfg.H, cfg.W], "cg_steps": d.cg_max_iters, "nltv_window": "5x5",
+                           "l2_flush": "512 MiB write between timed steps (outside the events)" if flush is not None else "none",
+                           "parallelism": "dp%d (independent light fields per rank)" % world},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": sol.launches_per_iter * args.steps * world,
+                "clocks": clk,
+                "kernel_ms_per_launch": {"wz": k_wz_ms, "normal": k_normal_ms, "cg_update": k_upd_ms},
+                "final_J": stats[-1]["J"], "cg_iters": stats[-1]["cg_iters"]}
+        print(json.dumps(line), flush=True)
+    sol.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

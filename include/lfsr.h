@@ -1,0 +1,203 @@
+/*
+ * lfsr.h — C ABI of the B200-native ADMM light-field super-resolution library
+ * (liblfsr.so), the data-parallel hot path of arXiv 2206.05047:
+ * "A GPU-Accelerated Light-field Super-resolution Framework Based on Mixed
+ * Noise Model and Weighted Regularization" (Tran, Sun, Simon).
+ *
+ * Citation key: P:Lnnn = line nnn of the paper's LaTeX source;
+ * S:Lnnn = SPEC.md; readings A1..A27 = DESIGN.md §3.
+ *
+ * The library minimises (Eq. sr_fin)
+ *     J(x) = l1 sum_k |A_k x - y_k|_1 + l2 sum_k |A_k x - y_k|_2^2
+ *          + sum_d |W_d (.) (S_d - I) x|_1 ,      A_k = D B W_k
+ * with the restructured scaled-dual ADMM of Algorithm 1 and the
+ * conjugate-gradient x-step of Algorithm 2 (textbook readings
+ * A1-A4).  Every step runs in hand-written sm_100a CUDA kernels; there is no
+ * CPU fallback: without a usable CUDA device every call that needs one
+ * returns LFSR_ERR_CUDA.
+ *
+ * Conventions (all calls):
+ *   - All arrays are dense, row-major, fp32 (float) unless stated.
+ *   - HR size H x W = (scale*lr_height) x (scale*lr_width); p = H*W, q = h*w.
+ *   - `mem` says whether every pointer of that call is host (LFSR_MEM_HOST) or
+ *     device (LFSR_MEM_DEVICE, same CUDA device as the ctx) memory.
+ *   - The caller owns every pointer it passes; the library copies inputs and
+ *     never keeps a caller pointer.  Host inputs are fully consumed before the
+ *     call returns; device inputs are read in the order of the ctx stream.
+ *   - Calls never throw; C++ exceptions never cross this boundary.
+ *   - A ctx is single-threaded; different ctxs are independent.
+ *   - After LFSR_ERR_CUDA / LFSR_ERR_NCCL the ctx is poisoned: every later call
+ *     except lfsr_destroy / lfsr_last_error returns LFSR_ERR_STATE.
+ */
+#ifndef LFSR_H_
+#define LFSR_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LFSR_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define LFSR_API __attribute__((visibility("default")))
+#else
+#define LFSR_API
+#endif
+
+typedef struct lfsr_ctx lfsr_ctx; /* opaque; owns all device state */
+
+typedef enum {
+  LFSR_OK = 0,
+  LFSR_ERR_INVALID_ARG = 1, /* validation failed; no side effects              */
+  LFSR_ERR_STATE = 2,       /* wrong call order or poisoned ctx                */
+  LFSR_ERR_OOM = 3,         /* device allocation failed                        */
+  LFSR_ERR_CUDA = 4,        /* CUDA error (incl. no device); ctx poisoned      */
+  LFSR_ERR_NCCL = 5,        /* NCCL error; ctx poisoned                        */
+  LFSR_ERR_DIVERGED = 6,    /* non-finite x or cost; see stats[].nonfinite     */
+  LFSR_ERR_UNSUPPORTED = 7  /* valid but not supported by this build           */
+} lfsr_status;
+
+typedef enum { LFSR_MEM_HOST = 0, LFSR_MEM_DEVICE = 1 } lfsr_mem;
+
+/* Disparity layout.  SHARED: one HR map omega on theta_0's grid used by every
+ * view (reading A12).  PER_VIEW (the paper's omega_k): not in
+ * this build (LFSR_ERR_UNSUPPORTED). */
+typedef enum { LFSR_DISP_SHARED = 0, LFSR_DISP_PER_VIEW = 1 } lfsr_disp_mode;
+
+typedef struct {
+  int32_t n_views;      /* s_k >= 1                                         */
+  int32_t lr_height;    /* s_y >= 1                                                  */
+  int32_t lr_width;     /* s_x >= 1                                                  */
+  int32_t scale;        /* zeta in {2,3,4}                              */
+  int32_t ref_view;     /* index of theta_0 in [0, n_views)                  */
+  int32_t nltv_radius;  /* r in [1,4]; window (2r+1)^2, s_d = (2r+1)^2-1 (A9) */
+  float lambda1;        /* >= 0, l1 data weight                          */
+  float lambda2;        /* >= 0, l2 data weight; lambda1 + lambda2 > 0                */
+  float lambda_reg;     /* >= 0 multiplier on W_d (A19); J itself has none   */
+  float sigma_s;        /* > 0 spatial weight falloff w_d = exp(-|d|^2/sigma_s) (A8)  */
+  float sigma_e;        /* > 0 edge weight falloff (A8); INFINITY disables    */
+  float sigma_o1;       /* > 0 occlusion-boundary falloff (Eq. weight_occ); INF off   */
+  float sigma_o2;       /* > 0 projection-error falloff (Eq. weight_occ); INF off     */
+  float theta;          /* > 0 ADMM penalty vartheta                         */
+  int32_t cg_max_iters; /* K in [1, 64]                                      */
+  float cg_tol;         /* tau >= 0 on <r,r>; 0 => always K steps (A1, A18)   */
+  int32_t reweight_every_iter; /* 1 = paper (weights from x^{n-1}); 0 = W
+                                  frozen at the value computed from x^0              */
+  int32_t device;       /* CUDA device ordinal                                       */
+  int32_t rank;         /* 0 (multi-GPU strips: not in this build)                   */
+  int32_t n_ranks;      /* 1                                                         */
+  const void* nccl_unique_id; /* NULL                                               */
+  void* stream;         /* cudaStream_t to run on (e.g. torch.cuda.current_stream()
+                           .cuda_stream), or NULL for a ctx-owned stream             */
+} lfsr_params;
+
+/* Per-ADMM-iteration record.  J terms refer to x^{n-1} and the
+ * weights computed from it (reading A26): J = lambda1*data_l1 + lambda2*data_l2
+ * + reg_l1.  primal_res = |w^n - w^{n-1}|_2 in scaled units (A27).  cg_pi0 =
+ * <r0,r0>, cg_pi_last = <r,r> after the last CG step taken. */
+typedef struct {
+  int32_t iter;       /* 1-based ADMM iteration index since set_observations */
+  int32_t cg_iters;   /* CG steps taken (<= K)                              */
+  int32_t breakdown;  /* 1 if CG stopped on <p,Mp> <= 0                     */
+  int32_t nonfinite;  /* 1 if x or J became non-finite                      */
+  double J, data_l1, data_l2, reg_l1, primal_res, cg_pi0, cg_pi_last;
+} lfsr_iter_stats;
+
+/* Create a ctx on params->device and allocate nothing large yet.
+ * Errors: LFSR_ERR_INVALID_ARG (any field out of range; `out` untouched),
+ * LFSR_ERR_UNSUPPORTED (n_ranks != 1), LFSR_ERR_CUDA (no usable device). */
+LFSR_API lfsr_status lfsr_create(const lfsr_params* params, lfsr_ctx** out);
+
+/* Load the observations and reset the solver state (x = x0, w = 0) (Alg.1
+ * lines 1-2).
+ *   lr_views     [n_views][lr_height][lr_width]  y_k
+ *   view_offsets [n_views][2] = (drho_k, dtau_k) = theta_k - theta_0 in angular
+ *                steps; drho shifts along X (columns), dtau along Y (rows) (A13)
+ *   disparity    [H][W] omega on theta_0's HR grid, HR px per angular step
+ *   x0           [H][W] initial guess, or NULL => bicubic (Catmull-Rom a=-0.5)
+ *                up-sampling of the reference view (A15)
+ * Also computes the static occlusion weight w_o (Eq. weight_occ, P:L424-444,
+ * A16/A17) and the weight map from x0.  Synchronises the ctx stream (it needs
+ * max|omega| and the view offsets on the host to size the kernel halos).
+ * Errors: INVALID_ARG (NULL arrays, non-finite offsets), UNSUPPORTED
+ * (PER_VIEW), OOM, CUDA, STATE. */
+LFSR_API lfsr_status lfsr_set_observations(lfsr_ctx* ctx, const float* lr_views, const float* view_offsets,
+                                  const float* disparity, lfsr_disp_mode disp_mode,
+                                  const float* x0, lfsr_mem mem);
+
+/* Run n_iters >= 0 ADMM iterations (Alg.1 lines 3-10) continuing from the
+ * current (x, w_A, w_S): run(a); run(b) == run(a+b).  Each iteration is one
+ * CUDA-graph launch on the ctx stream.  Blocks until done.  stats: NULL or an
+ * array of n_iters records.  Errors: STATE (before set_observations),
+ * DIVERGED (non-finite x/J; the state is kept for inspection), CUDA. */
+LFSR_API lfsr_status lfsr_admm_run(lfsr_ctx* ctx, int32_t n_iters, lfsr_iter_stats* stats);
+
+/* Enqueue n_iters >= 0 ADMM iterations (graph launches) on the ctx stream and
+ * return immediately (no host synchronisation, no divergence check).  The
+ * iterations' records can be read later with lfsr_admm_stats.  Errors: STATE,
+ * INVALID_ARG, CUDA. */
+LFSR_API lfsr_status lfsr_admm_enqueue(lfsr_ctx* ctx, int32_t n_iters);
+
+/* Blocking read of the records of iterations [first_iter, first_iter+n_iters)
+ * (1-based, counted since set_observations; the device keeps the last 4096).
+ * stats may be NULL (divergence check only).  Returns LFSR_ERR_DIVERGED if any
+ * of them saw a non-finite x or cost; INVALID_ARG if outside the window. */
+LFSR_API lfsr_status lfsr_admm_stats(lfsr_ctx* ctx, int32_t first_iter, int32_t n_iters, lfsr_iter_stats* stats);
+
+/* Bench/profiling: enable (1) or disable (0) external event-record nodes around
+ * every kernel of the iteration graph (rebuilds the graph; resets the
+ * accumulators).  lfsr_profile_read adds the per-kernel device times of the
+ * MOST RECENT replay to three accumulators and returns them: ms[0] wz-step
+ * (tile kernel, mode WZ), ms[1] CG normal operator (tile kernel, mode NORMAL),
+ * ms[2] CG update; launches[i] = number of kernel launches accumulated. */
+LFSR_API lfsr_status lfsr_profile(lfsr_ctx* ctx, int32_t enable);
+LFSR_API lfsr_status lfsr_profile_read(lfsr_ctx* ctx, double* ms /*[3]*/, int64_t* launches /*[3]*/);
+
+/* Copy the current HR estimate x [H][W] into x_out.  HOST: blocks;
+ * DEVICE: stream-ordered on the ctx stream. */
+LFSR_API lfsr_status lfsr_get_hr(lfsr_ctx* ctx, float* x_out, lfsr_mem mem);
+
+/* Dump the state for parity checks: w_A [n_views][h][w], w_S [s_d][H][W]
+ * (scaled duals, A6), x [H][W], m [H][W] (current weight map, W_d = w_d m).
+ * Any pointer may be NULL.  Blocks for HOST. */
+LFSR_API lfsr_status lfsr_get_state(lfsr_ctx* ctx, float* w_A, float* w_S, float* x, float* m, lfsr_mem mem);
+
+/* Test/bench operators on the current state (frozen weight map m):
+ *   A       : in HR [H][W]            -> out [n_views][h][w]   A_k x
+ *   AT      : in [n_views][h][w]      -> out HR                sum_k A_k^T r_k
+ *   S       : in HR                   -> out [s_d][H][W]       W_d (.) Delta_d x
+ *   ST      : in [s_d][H][W]          -> out HR                div^{U,V}
+ *   NORMAL  : in HR                   -> out HR                M x (A7)
+ *   WEIGHTS : in HR x                 -> out HR m(x) = lambda_reg w_o w_e(x)
+ * NORMAL/A/AT run the same tile kernels as lfsr_admm_run.  Blocks for HOST. */
+typedef enum {
+  LFSR_OP_A = 0,
+  LFSR_OP_AT = 1,
+  LFSR_OP_S = 2,
+  LFSR_OP_ST = 3,
+  LFSR_OP_NORMAL = 4,
+  LFSR_OP_WEIGHTS = 5
+} lfsr_op;
+LFSR_API lfsr_status lfsr_op_apply(lfsr_ctx* ctx, lfsr_op op, const float* in, float* out, lfsr_mem mem);
+
+/* Number of kernel launches one ADMM iteration issues (for the bench's
+ * gpu_launches count).  Valid after set_observations; 0 otherwise. */
+LFSR_API int32_t lfsr_launches_per_iter(const lfsr_ctx* ctx);
+
+/* Free everything; NULL-safe. */
+LFSR_API void lfsr_destroy(lfsr_ctx* ctx);
+
+/* Last error message of ctx (or of the last failed lfsr_create if ctx is
+ * NULL); owned by the library, valid until the next call on that ctx. */
+LFSR_API const char* lfsr_last_error(const lfsr_ctx* ctx);
+
+/* LFSR_ABI_VERSION of the loaded library. */
+LFSR_API int32_t lfsr_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LFSR_H_ */

@@ -1,0 +1,9 @@
+"""B200-native ADMM light-field super-resolution (arXiv 2206.05047) — the hot path.
+
+``lfsr.Solver`` wraps the C ABI of ``liblfsr.so`` (include/lfsr.h), whose
+sm_100a kernels run every step of Algorithm 1/2.  Build with ``build.build()``.
+"""
+from .lfsr import (Params, Solver, LFSRError, load_library, params_for, psnr, LIB_PATH, EXPORTS,  # noqa: F401
+                   STAT_KEYS)
+
+__all__ = ["Params", "Solver", "LFSRError", "load_library", "params_for", "psnr", "LIB_PATH", "EXPORTS"]

@@ -1,0 +1,272 @@
+// aux_kernels.cu — setup, CG update and test-operator kernels of liblfsr.
+#include "internal.h"
+#include <cfloat>
+
+namespace lfsr {
+
+// ---------------------------------------------------------------------------
+// Setup (once per solve).
+// ---------------------------------------------------------------------------
+
+// Bilinear sample of an LR image at continuous LR (row, col), clamped (reading A17).
+__device__ __forceinline__ float bilin_lr(const float* img, int h, int w, int lps, float r, float c) {
+  r = fminf(fmaxf(r, 0.f), (float)(h - 1));
+  c = fminf(fmaxf(c, 0.f), (float)(w - 1));
+  float fr = floorf(r), fc = floorf(c);
+  int r0 = (int)fr, c0 = (int)fc;
+  int r1 = min(r0 + 1, h - 1), c1 = min(c0 + 1, w - 1);
+  float a = r - fr, b = c - fc;
+  return (1.f - a) * ((1.f - b) * img[(size_t)r0 * lps + c0] + b * img[(size_t)r0 * lps + c1]) +
+         a * ((1.f - b) * img[(size_t)r1 * lps + c0] + b * img[(size_t)r1 * lps + c1]);
+}
+
+// Static occlusion weight w_o (Eq. weight_occ; readings A16/A17):
+//   b = min(0, forward-difference divergence of omega), p = mean over non-reference
+//   views of |y_ref(z/zeta) - y_k((z - dtheta_k omega(z))/zeta)|.
+__global__ void k_setup_wo(const Geom G, const Views V, const float* __restrict__ y,
+                           const float* __restrict__ omega, float* __restrict__ wo) {
+  int X = blockIdx.x * blockDim.x + threadIdx.x, Y = blockIdx.y;
+  if (X >= G.W || Y >= G.H) return;
+  const int ps = G.ps;
+  float om = omega[(size_t)Y * ps + X];
+  float dx = X + 1 < G.W ? omega[(size_t)Y * ps + X + 1] - om : 0.f;
+  float dy = Y + 1 < G.H ? omega[(size_t)(Y + 1) * ps + X] - om : 0.f;
+  float b = fminf(dx + dy, 0.f);
+  const float iz = 1.f / (float)G.scale;
+  const size_t lstride = (size_t)G.h * G.lps;
+  float ref = bilin_lr(y + G.ref_view * lstride, G.h, G.w, G.lps, Y * iz, X * iz);
+  float acc = 0.f;
+  int cnt = 0;
+  for (int k = 0; k < G.n_views; ++k) {
+    if (k == G.ref_view) continue;
+    float2 o = V.off[k];
+    float v = bilin_lr(y + k * lstride, G.h, G.w, G.lps, ((float)Y - o.y * om) * iz, ((float)X - o.x * om) * iz);
+    acc += fabsf(ref - v);
+    ++cnt;
+  }
+  float p = cnt > 0 ? acc / (float)cnt : 0.f;
+  wo[(size_t)Y * ps + X] = expf(-b * b * G.inv_2s1sq) * expf(-p * p * G.inv_2s2sq);
+}
+
+__device__ __forceinline__ float keys_cubic(float t) {  // Catmull-Rom, a = -0.5 (reading A15)
+  const float a = -0.5f;
+  t = fabsf(t);
+  if (t <= 1.f) return ((a + 2.f) * t - (a + 3.f)) * t * t + 1.f;
+  if (t < 2.f) return ((a * t - 5.f * a) * t + 8.f * a) * t - 4.f * a;
+  return 0.f;
+}
+
+// x0 = bicubic up-sampling of the reference LR view at (Y/zeta, X/zeta) (A15).
+__global__ void k_bicubic(const Geom G, const float* __restrict__ y, float* __restrict__ x) {
+  int X = blockIdx.x * blockDim.x + threadIdx.x, Y = blockIdx.y;
+  if (X >= G.W || Y >= G.H) return;
+  const float* yr = y + (size_t)G.ref_view * G.h * G.lps;
+  float fy = (float)Y / (float)G.scale, fx = (float)X / (float)G.scale;
+  float iyf = floorf(fy), ixf = floorf(fx);
+  int iy = (int)iyf, ix = (int)ixf;
+  float ty = fy - iyf, tx = fx - ixf;
+  float s = 0.f;
+#pragma unroll
+  for (int a = -1; a <= 2; ++a) {
+    int rr = min(max(iy + a, 0), G.h - 1);
+    float wy = keys_cubic(ty - (float)a);
+    float row = 0.f;
+#pragma unroll
+    for (int b = -1; b <= 2; ++b) row += keys_cubic(tx - (float)b) * yr[(size_t)rr * G.lps + min(max(ix + b, 0), G.w - 1)];
+    s += wy * row;
+  }
+  x[(size_t)Y * G.ps + X] = s;
+}
+
+// m = lambda_R w_o exp(-|grad x|^2/sigma_e) (A8, A17, A19).
+__global__ void k_weights(const Geom G, const float* __restrict__ x, const float* __restrict__ wo,
+                          float* __restrict__ m) {
+  int X = blockIdx.x * blockDim.x + threadIdx.x, Y = blockIdx.y;
+  if (X >= G.W || Y >= G.H) return;
+  const int ps = G.ps;
+  const float* row = x + (size_t)Y * ps;
+  float gx = 0.5f * (row[min(X + 1, G.W - 1)] - row[max(X - 1, 0)]);
+  float gy = 0.5f * (x[(size_t)min(Y + 1, G.H - 1) * ps + X] - x[(size_t)max(Y - 1, 0) * ps + X]);
+  m[(size_t)Y * ps + X] = G.lambda_reg * wo[(size_t)Y * ps + X] * expf(-(gx * gx + gy * gy) * G.inv_sigma_e);
+}
+
+// max |v| over an [H][ps] array (non-negative floats order like their bit patterns).
+__global__ void k_absmax(const float* __restrict__ v, size_t n, unsigned* out) {
+  float mx = 0.f;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    mx = fmaxf(mx, fabsf(v[i]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(mx));
+}
+
+// ---------------------------------------------------------------------------
+// CG update (Alg.2 lines 8-9 and 11 with readings A1-A4):
+//   alpha = pi_{k-1} / <p_k, q_k>; x += alpha p_k; r -= alpha q_k; pi_k = <r, r>.
+// Also zeroes q (the next normal operator accumulates into it) and, at k = K,
+// zeroes r for the next wz-step.  The last block to finish closes the step:
+// it records CG bookkeeping and, at k = K, writes the iteration's stats record
+// and resets the scalar slots (threadfence reduction pattern).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_cg_update(const Geom G, float* __restrict__ x, float* __restrict__ r,
+                                                   const float* __restrict__ p, float* __restrict__ q,
+                                                   Control* ctl, int k) {
+  __shared__ double red[8 * 2];
+  __shared__ bool am_last;
+  const double pi_prev = ctl->cur[S_PI + k - 1];
+  const double pq = ctl->cur[S_PQ + k];
+  const bool stopped = ctl->cur[S_STOP] != 0.0;
+  const bool active = !stopped && !(pi_prev < (double)G.cg_tol) && pi_prev != 0.0 && pq > 0.0;
+  const float alpha = active ? (float)(pi_prev / pq) : 0.f;
+  const bool last = (k == G.K);
+  double pi_part = 0.0, nf_part = 0.0;
+  const size_t n4 = (size_t)G.H * G.ps / 4;
+  float4* x4 = reinterpret_cast<float4*>(x);
+  float4* r4 = reinterpret_cast<float4*>(r);
+  const float4* p4 = reinterpret_cast<const float4*>(p);
+  float4* q4 = reinterpret_cast<float4*>(q);
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
+    float4 qv = q4[i];
+    if (active) {
+      float4 xv = x4[i], rv = r4[i], pv = p4[i];
+      xv.x += alpha * pv.x; xv.y += alpha * pv.y; xv.z += alpha * pv.z; xv.w += alpha * pv.w;
+      rv.x -= alpha * qv.x; rv.y -= alpha * qv.y; rv.z -= alpha * qv.z; rv.w -= alpha * qv.w;
+      pi_part += (double)rv.x * rv.x + (double)rv.y * rv.y + (double)rv.z * rv.z + (double)rv.w * rv.w;
+      x4[i] = xv;
+      if (!last) r4[i] = rv;
+      if (last) nf_part += (float)(!isfinite(xv.x)) + (!isfinite(xv.y)) + (!isfinite(xv.z)) + (!isfinite(xv.w));
+    } else if (last) {
+      float4 xv = x4[i];
+      nf_part += (float)(!isfinite(xv.x)) + (!isfinite(xv.y)) + (!isfinite(xv.z)) + (!isfinite(xv.w));
+    }
+    q4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (last) r4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    pi_part += __shfl_xor_sync(0xffffffffu, pi_part, o);
+    nf_part += __shfl_xor_sync(0xffffffffu, nf_part, o);
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) { red[warp * 2] = pi_part; red[warp * 2 + 1] = nf_part; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < (int)(blockDim.x / 32); ++w) { a += red[w * 2]; b += red[w * 2 + 1]; }
+    if (active && a != 0.0) atomicAdd(&ctl->cur[S_PI + k], a);
+    if (b != 0.0) atomicAdd(&ctl->cur[S_NF], b);
+    __threadfence();
+    unsigned prev = atomicAdd(&ctl->done, 1u);
+    am_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!am_last || threadIdx.x != 0) return;
+  // ---- last block: close CG step k ----
+  __threadfence();
+  volatile double* cur = ctl->cur;
+  if (active) {
+    cur[S_CGIT] = cur[S_CGIT] + 1.0;
+  } else if (!stopped) {
+    cur[S_STOP] = 1.0;
+    if (!(pi_prev < (double)G.cg_tol) && pi_prev != 0.0 && !(pq > 0.0)) cur[S_BREAK] = 1.0;
+  }
+  if (last) {
+    int cgit = (int)cur[S_CGIT];
+    double J = (double)G.lambda1 * cur[S_L1] + (double)G.lambda2 * cur[S_L2] + cur[S_REG];
+    double pil = cur[S_PI + cgit];
+    double* rec = ctl->ring + (size_t)(ctl->iter % ctl->cap) * T_COUNT;
+    rec[T_ITER] = (double)(ctl->iter + 1);
+    rec[T_CGIT] = (double)cgit;
+    rec[T_BREAK] = cur[S_BREAK];
+    rec[T_NF] = (cur[S_NF] > 0.0 || !isfinite(J) || !isfinite(pil)) ? 1.0 : 0.0;
+    rec[T_J] = J;
+    rec[T_L1] = cur[S_L1];
+    rec[T_L2] = cur[S_L2];
+    rec[T_REG] = cur[S_REG];
+    rec[T_RES] = sqrt(cur[S_RES2]);
+    rec[T_PI0] = cur[S_PI];
+    rec[T_PILAST] = pil;
+    for (int s = 0; s < S_COUNT; ++s) cur[s] = 0.0;
+    ctl->iter = ctl->iter + 1;
+  }
+  __threadfence();
+  ctl->done = 0u;
+}
+
+// ---------------------------------------------------------------------------
+// Test operators S / S^T (weighted directional gradient / divergence,
+// P:L585-601, reading A10) on dense [s_d][H][ps] stacks.
+// ---------------------------------------------------------------------------
+__global__ void k_apply_S(const Geom G, const float* __restrict__ x, const float* __restrict__ m,
+                          float* __restrict__ out) {
+  int X = blockIdx.x * blockDim.x + threadIdx.x, Y = blockIdx.y;
+  if (X >= G.W || Y >= G.H) return;
+  const int ps = G.ps;
+  float xz = x[(size_t)Y * ps + X], mz = m[(size_t)Y * ps + X];
+  for (int d = 0; d < G.s_d; ++d) {
+    int yy = Y + G.ody[d], xx = X + G.odx[d];
+    float g = 0.f;
+    if (yy >= 0 && yy < G.H && xx >= 0 && xx < G.W) g = G.wd[d] * mz * (xz - x[(size_t)yy * ps + xx]);
+    out[((size_t)d * G.H + Y) * ps + X] = g;
+  }
+}
+
+__global__ void k_apply_ST(const Geom G, const float* __restrict__ hin, const float* __restrict__ m,
+                           float* __restrict__ out) {
+  int X = blockIdx.x * blockDim.x + threadIdx.x, Y = blockIdx.y;
+  if (X >= G.W || Y >= G.H) return;
+  const int ps = G.ps;
+  float s = 0.f;
+  for (int d = 0; d < G.s_d; ++d) {
+    int dy = G.ody[d], dx = G.odx[d];
+    const float* hd = hin + (size_t)d * G.H * ps;
+    if (Y + dy >= 0 && Y + dy < G.H && X + dx >= 0 && X + dx < G.W)
+      s += G.wd[d] * m[(size_t)Y * ps + X] * hd[(size_t)Y * ps + X];
+    if (Y - dy >= 0 && Y - dy < G.H && X - dx >= 0 && X - dx < G.W)
+      s -= G.wd[d] * m[(size_t)(Y - dy) * ps + X - dx] * hd[(size_t)(Y - dy) * ps + X - dx];
+  }
+  out[(size_t)Y * ps + X] = s;
+}
+
+// ---------------------------------------------------------------------------
+// Launchers
+// ---------------------------------------------------------------------------
+static dim3 hr_grid(const Geom& G, int bx) { return dim3((G.W + bx - 1) / bx, G.H); }
+
+cudaError_t launch_setup_wo(const Geom& G, const Views& V, const float* y, const float* omega, float* wo,
+                            cudaStream_t st) {
+  k_setup_wo<<<hr_grid(G, 128), 128, 0, st>>>(G, V, y, omega, wo);
+  return cudaGetLastError();
+}
+cudaError_t launch_bicubic(const Geom& G, const float* y, float* x, cudaStream_t st) {
+  k_bicubic<<<hr_grid(G, 128), 128, 0, st>>>(G, y, x);
+  return cudaGetLastError();
+}
+cudaError_t launch_weights(const Geom& G, const float* x, const float* wo, float* m, cudaStream_t st) {
+  k_weights<<<hr_grid(G, 128), 128, 0, st>>>(G, x, wo, m);
+  return cudaGetLastError();
+}
+cudaError_t launch_absmax(const float* v, size_t n, unsigned* out, cudaStream_t st) {
+  k_absmax<<<256, 256, 0, st>>>(v, n, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_cg_update(const Geom& G, float* x, float* r, const float* p, float* q, Control* ctl, int k,
+                             int num_sms, cudaStream_t st) {
+  size_t n4 = (size_t)G.H * G.ps / 4;
+  int blocks = (int)((n4 + 255) / 256);
+  int cap = num_sms * 4;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  k_cg_update<<<blocks, 256, 0, st>>>(G, x, r, p, q, ctl, k);
+  return cudaGetLastError();
+}
+cudaError_t launch_apply_S(const Geom& G, const float* x, const float* m, float* out, cudaStream_t st) {
+  k_apply_S<<<hr_grid(G, 128), 128, 0, st>>>(G, x, m, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_apply_ST(const Geom& G, const float* h, const float* m, float* out, cudaStream_t st) {
+  k_apply_ST<<<hr_grid(G, 128), 128, 0, st>>>(G, h, m, out);
+  return cudaGetLastError();
+}
+
+}  // namespace lfsr

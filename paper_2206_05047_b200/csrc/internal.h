@@ -1,0 +1,123 @@
+// internal.h — device-side data structures shared by the liblfsr kernels and
+// the C-ABI host code.  Nothing here is visible through include/lfsr.h.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace lfsr {
+
+constexpr int kMaxViews = 1024;  // view offsets travel in the kernel parameter block
+constexpr int kMaxTaps = 8;      // blur radius R <= 3 for zeta <= 4 (Appendix B of DESIGN.md)
+constexpr int kMaxOffsets = 80;  // s_d for r <= 4
+constexpr int kMaxK = 64;        // CG steps per ADMM iteration
+constexpr int kThreads = 256;    // threads per tile CTA
+
+// Scalar slots of the current ADMM iteration (doubles in Control::cur).
+enum Slot : int {
+  S_L1 = 0,     // sum |e|
+  S_L2 = 1,     // sum e^2
+  S_REG = 2,    // sum_d sum_z |W_d Delta_d x|
+  S_RES2 = 3,   // |w^n - w^{n-1}|^2
+  S_NF = 4,     // non-finite count
+  S_CGIT = 5,   // CG steps taken
+  S_BREAK = 6,  // CG breakdown flag
+  S_STOP = 7,   // CG stopped flag (pi < tau, pi == 0 or breakdown)
+  S_PI = 8,     // pi_k = <r_k, r_k>, k = 0..K      at S_PI + k
+  S_PQ = S_PI + kMaxK + 1,  // <p_k, M p_k>, k = 1..K at S_PQ + k
+  S_COUNT = S_PQ + kMaxK + 1
+};
+
+// Stats record layout in the ring (doubles).
+enum StatSlot : int {
+  T_ITER = 0, T_CGIT, T_BREAK, T_NF, T_J, T_L1, T_L2, T_REG, T_RES, T_PI0, T_PILAST, T_COUNT
+};
+
+struct Control {
+  double cur[S_COUNT];
+  double* ring;       // [cap][T_COUNT]
+  int32_t cap;
+  int32_t iter;       // ADMM iterations completed since set_observations
+  uint32_t done;      // last-block counter for the closing kernel
+  int32_t pad;
+};
+
+// Geometry + solver constants, passed by value to every kernel.
+struct Geom {
+  int32_t H, W, h, w;         // HR / LR sizes
+  int32_t ps, lps;            // HR row pitch, LR row pitch (floats, multiples of 32)
+  int32_t scale, R;           // zeta, blur radius
+  int32_t n_views, ref_view;
+  int32_t radius, s_d;        // NLTV window radius and offset count
+  int32_t SY, SX;             // ceil(max |dtau * omega|), ceil(max |drho * omega|)
+  int32_t K;                  // CG max steps
+  float lambda1, lambda2, lambda_reg, theta, inv_theta;
+  float inv_sigma_e, inv_2s1sq, inv_2s2sq;  // 0 when the factor is disabled (sigma = inf)
+  float cg_tol;
+  float cA;                   // lambda2 + (theta/2) lambda1^2   (A7)
+  float cS;                   // theta / 2
+  float taps[kMaxTaps * 2 + 1];
+  float wd[kMaxOffsets];      // spatial weights w_d
+  int8_t ody[kMaxOffsets], odx[kMaxOffsets];
+};
+
+struct Views {
+  float2 off[kMaxViews];      // (drho, dtau)
+};
+
+// Tile decomposition of the HR grid; every field is derived on the host.
+struct TileGeom {
+  int32_t LY, LX;             // LR pixels per tile
+  int32_t TY, TX;             // HR pixels per tile (= zeta * L)
+  int32_t EY, EX;             // E region (positions whose warp sample feeds own LR pixels)
+  int32_t HY, HX;             // p-tile halo (top/left) = R + max(S, r)
+  int32_t PH, PW;             // p-tile rows / row pitch in shared memory
+  int32_t MH, MW;             // m-tile (own + r halo) rows / pitch
+  int32_t ntY, ntX;           // tiles per axis
+  int32_t groups;             // view groups (split-K over views)
+  int32_t vpg;                // views per group
+  size_t smem;                // dynamic shared memory bytes
+};
+
+// Pointers of one tile-kernel launch (see tile_kernels.cu).
+struct TileIO {
+  const float* in_hr;    // x (WZ) | r (NORMAL-CG) | p (NORMAL-op, A)
+  const float* in_hr2;   // p_{k-1} (NORMAL-CG) or nullptr
+  float* p_out;          // p_k written for own pixels (NORMAL-CG) or nullptr
+  const float* omega;
+  const float* y;        // WZ
+  float* wA;             // WZ (in/out)
+  float* wS;             // WZ (in/out)
+  const float* wo;       // WZ (weights)
+  float* m;              // WZ: written (if reweight) / read; NORMAL: read
+  const float* in_lr;    // AT
+  float* out_lr;         // A
+  float* out_hr;         // accumulated (RED.ADD) output: r (WZ, sign -1) | q (NORMAL) | AT
+  Control* ctl;
+  int32_t cg_k;          // NORMAL-CG: step index k >= 1; 0 = plain operator
+  int32_t reweight;      // WZ: recompute m from x
+  int32_t do_nltv;       // NORMAL: include the (th/2) S^T S term
+  int32_t pad;
+};
+
+enum TileMode : int { MODE_WZ = 0, MODE_NORMAL = 1, MODE_A = 2, MODE_AT = 3 };
+
+struct State {
+  // persistent solver state (pitched)
+  float* x;      // [H][ps]
+  float* y;      // [n_views][h][lps]
+  float* wA;     // [n_views][h][lps]
+  float* wS;     // [s_d][H][ps]
+  float* omega;  // [H][ps]
+  float* wo;     // [H][ps]
+  float* m;      // [H][ps]
+  // CG vectors
+  float* r;      // [H][ps]
+  float* p[2];   // ping-pong
+  float* q;      // [H][ps]
+  // scratch for ops
+  float* tmp_hr;   // [H][ps]
+  float* tmp_lr;   // [n_views][h][lps]
+  Control* ctl;
+};
+
+}  // namespace lfsr

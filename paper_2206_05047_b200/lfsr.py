@@ -1,0 +1,318 @@
+"""Thin ctypes binding of liblfsr.so (include/lfsr.h) — argument marshalling only.
+
+Every step of the ADMM hot path runs in the library's sm_100a kernels; this
+module converts numpy arrays / torch tensors to pointers and status codes to
+exceptions.  There is no CPU fallback: if liblfsr.so is missing or no B200 is
+visible, constructing a :class:`Solver` raises.
+
+Names follow the paper (arXiv 2206.05047): ``lambda1``/``lambda2``,
+``theta`` (vartheta), ``cg_max_iters`` K and ``cg_tol`` tau,
+``scale`` zeta, ``view_offsets`` theta_k - theta_0.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+from dataclasses import dataclass, fields
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liblfsr.so")
+
+LFSR_OK, LFSR_ERR_INVALID_ARG, LFSR_ERR_STATE, LFSR_ERR_OOM, LFSR_ERR_CUDA, LFSR_ERR_NCCL, \
+    LFSR_ERR_DIVERGED, LFSR_ERR_UNSUPPORTED = range(8)
+STATUS_NAMES = ["OK", "INVALID_ARG", "STATE", "OOM", "CUDA", "NCCL", "DIVERGED", "UNSUPPORTED"]
+MEM_HOST, MEM_DEVICE = 0, 1
+OP_A, OP_AT, OP_S, OP_ST, OP_NORMAL, OP_WEIGHTS = range(6)
+OPS = {"A": OP_A, "AT": OP_AT, "S": OP_S, "ST": OP_ST, "NORMAL": OP_NORMAL, "WEIGHTS": OP_WEIGHTS}
+
+# every symbol include/lfsr.h declares (checked by tests/test_abi.py)
+EXPORTS = ("lfsr_create", "lfsr_set_observations", "lfsr_admm_run", "lfsr_admm_enqueue", "lfsr_admm_stats",
+           "lfsr_get_hr", "lfsr_get_state", "lfsr_op_apply", "lfsr_launches_per_iter", "lfsr_profile",
+           "lfsr_profile_read", "lfsr_destroy", "lfsr_last_error", "lfsr_abi_version")
+
+
+class LFSRError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        self.status = status
+        name = STATUS_NAMES[status] if 0 <= status < len(STATUS_NAMES) else str(status)
+        super().__init__("LFSR_ERR_%s: %s" % (name, msg))
+
+
+class _CParams(ctypes.Structure):
+    _fields_ = [("n_views", ctypes.c_int32), ("lr_height", ctypes.c_int32), ("lr_width", ctypes.c_int32),
+                ("scale", ctypes.c_int32), ("ref_view", ctypes.c_int32), ("nltv_radius", ctypes.c_int32),
+                ("lambda1", ctypes.c_float), ("lambda2", ctypes.c_float), ("lambda_reg", ctypes.c_float),
+                ("sigma_s", ctypes.c_float), ("sigma_e", ctypes.c_float), ("sigma_o1", ctypes.c_float),
+                ("sigma_o2", ctypes.c_float), ("theta", ctypes.c_float), ("cg_max_iters", ctypes.c_int32),
+                ("cg_tol", ctypes.c_float), ("reweight_every_iter", ctypes.c_int32), ("device", ctypes.c_int32),
+                ("rank", ctypes.c_int32), ("n_ranks", ctypes.c_int32), ("nccl_unique_id", ctypes.c_void_p),
+                ("stream", ctypes.c_void_p)]
+
+
+class _CStats(ctypes.Structure):
+    _fields_ = [("iter", ctypes.c_int32), ("cg_iters", ctypes.c_int32), ("breakdown", ctypes.c_int32),
+                ("nonfinite", ctypes.c_int32), ("J", ctypes.c_double), ("data_l1", ctypes.c_double),
+                ("data_l2", ctypes.c_double), ("reg_l1", ctypes.c_double), ("primal_res", ctypes.c_double),
+                ("cg_pi0", ctypes.c_double), ("cg_pi_last", ctypes.c_double)]
+
+
+STAT_KEYS = [f[0] for f in _CStats._fields_]
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load liblfsr.so; raises if it has not been built (no silent fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError("liblfsr.so not found at %s — build it with `python -c 'import __graft_entry__ as g; "
+                           "g.build()'` (nvcc, sm_100a); there is no CPU fallback" % path)
+    lib = ctypes.CDLL(path)
+    P = ctypes.POINTER
+    vp = ctypes.c_void_p
+    st = ctypes.c_int
+    lib.lfsr_create.argtypes = [P(_CParams), P(vp)]
+    lib.lfsr_create.restype = st
+    lib.lfsr_set_observations.argtypes = [vp, vp, vp, vp, ctypes.c_int, vp, ctypes.c_int]
+    lib.lfsr_set_observations.restype = st
+    lib.lfsr_admm_run.argtypes = [vp, ctypes.c_int32, P(_CStats)]
+    lib.lfsr_admm_run.restype = st
+    lib.lfsr_admm_enqueue.argtypes = [vp, ctypes.c_int32]
+    lib.lfsr_admm_enqueue.restype = st
+    lib.lfsr_admm_stats.argtypes = [vp, ctypes.c_int32, ctypes.c_int32, P(_CStats)]
+    lib.lfsr_admm_stats.restype = st
+    lib.lfsr_profile.argtypes = [vp, ctypes.c_int32]
+    lib.lfsr_profile.restype = st
+    lib.lfsr_profile_read.argtypes = [vp, P(ctypes.c_double), P(ctypes.c_int64)]
+    lib.lfsr_profile_read.restype = st
+    lib.lfsr_get_hr.argtypes = [vp, vp, ctypes.c_int]
+    lib.lfsr_get_hr.restype = st
+    lib.lfsr_get_state.argtypes = [vp, vp, vp, vp, vp, ctypes.c_int]
+    lib.lfsr_get_state.restype = st
+    lib.lfsr_op_apply.argtypes = [vp, ctypes.c_int, vp, vp, ctypes.c_int]
+    lib.lfsr_op_apply.restype = st
+    lib.lfsr_launches_per_iter.argtypes = [vp]
+    lib.lfsr_launches_per_iter.restype = ctypes.c_int32
+    lib.lfsr_destroy.argtypes = [vp]
+    lib.lfsr_destroy.restype = None
+    lib.lfsr_last_error.argtypes = [vp]
+    lib.lfsr_last_error.restype = ctypes.c_char_p
+    lib.lfsr_abi_version.argtypes = []
+    lib.lfsr_abi_version.restype = ctypes.c_int32
+    _lib = lib
+    return lib
+
+
+@dataclass
+class Params:
+    """lfsr_params (include/lfsr.h).  Defaults: reading A20 starting point, K=5, 5x5 window."""
+    n_views: int
+    lr_height: int
+    lr_width: int
+    scale: int = 2
+    ref_view: int = 0
+    nltv_radius: int = 2
+    lambda1: float = 1.0
+    lambda2: float = 10.0
+    lambda_reg: float = 0.05
+    sigma_s: float = 3.0
+    sigma_e: float = 0.01
+    sigma_o1: float = 0.5
+    sigma_o2: float = 0.2
+    theta: float = 1.0
+    cg_max_iters: int = 5
+    cg_tol: float = 0.0
+    reweight_every_iter: int = 1
+    device: int = 0
+
+    @property
+    def H(self):
+        return self.lr_height * self.scale
+
+    @property
+    def W(self):
+        return self.lr_width * self.scale
+
+    @property
+    def s_d(self):
+        return (2 * self.nltv_radius + 1) ** 2 - 1
+
+    def to_c(self, stream=None) -> _CParams:
+        c = _CParams()
+        for f in fields(self):
+            setattr(c, f.name, getattr(self, f.name))
+        c.rank, c.n_ranks, c.nccl_unique_id = 0, 1, None
+        c.stream = stream
+        return c
+
+
+def _is_torch(a):
+    return type(a).__module__.startswith("torch")
+
+
+class Solver:
+    """One lfsr_ctx.  Inputs may be numpy arrays (host) or torch tensors (host or cuda)."""
+
+    def __init__(self, params: Params, stream: int | None = None):
+        self.lib = load_library()
+        self.params = params
+        cp = params.to_c(stream)
+        h = ctypes.c_void_p()
+        s = self.lib.lfsr_create(ctypes.byref(cp), ctypes.byref(h))
+        if s != LFSR_OK:
+            raise LFSRError(s, self.lib.lfsr_last_error(None).decode())
+        self._h = h
+        self._keep = []
+
+    # -- helpers ------------------------------------------------------------
+    def _check(self, s):
+        if s != LFSR_OK:
+            raise LFSRError(s, self.lib.lfsr_last_error(self._h).decode())
+
+    @staticmethod
+    def _ptr_in(a):
+        """(pointer, mem, keepalive) of a float32 contiguous input."""
+        if a is None:
+            return None, None, None
+        if _is_torch(a):
+            import torch
+            t = a.detach()
+            if t.dtype != torch.float32:
+                t = t.float()
+            t = t.contiguous()
+            return t.data_ptr(), (MEM_DEVICE if t.is_cuda else MEM_HOST), t
+        arr = np.ascontiguousarray(a, dtype=np.float32)
+        return arr.ctypes.data, MEM_HOST, arr
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self.lib.lfsr_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -- API ----------------------------------------------------------------
+    def set_observations(self, lr_views, view_offsets, disparity, x0=None):
+        ptrs = [self._ptr_in(a) for a in (lr_views, view_offsets, disparity, x0)]
+        mems = {p[1] for p in ptrs if p[1] is not None}
+        if len(mems) != 1:
+            raise ValueError("all inputs of one call must be either host or device memory")
+        mem = mems.pop()
+        s = self.lib.lfsr_set_observations(self._h, ptrs[0][0], ptrs[1][0], ptrs[2][0], 0, ptrs[3][0], mem)
+        self._check(s)
+
+    def admm_run(self, n_iters: int, want_stats: bool = True):
+        st = (_CStats * max(int(n_iters), 1))() if want_stats else None
+        s = self.lib.lfsr_admm_run(self._h, int(n_iters), st)
+        stats = [{k: getattr(st[i], k) for k in STAT_KEYS} for i in range(n_iters)] if want_stats else None
+        if s == LFSR_ERR_DIVERGED:
+            err = LFSRError(s, self.lib.lfsr_last_error(self._h).decode())
+            err.stats = stats
+            raise err
+        self._check(s)
+        return stats
+
+    def admm_enqueue(self, n_iters: int):
+        """Stream-ordered launch of n_iters iterations; no host sync (see lfsr_admm_stats)."""
+        self._check(self.lib.lfsr_admm_enqueue(self._h, int(n_iters)))
+
+    def admm_stats(self, first_iter: int, n_iters: int):
+        st = (_CStats * max(int(n_iters), 1))()
+        s = self.lib.lfsr_admm_stats(self._h, int(first_iter), int(n_iters), st)
+        stats = [{k: getattr(st[i], k) for k in STAT_KEYS} for i in range(n_iters)]
+        if s == LFSR_ERR_DIVERGED:
+            err = LFSRError(s, self.lib.lfsr_last_error(self._h).decode())
+            err.stats = stats
+            raise err
+        self._check(s)
+        return stats
+
+    def profile(self, enable: bool = True):
+        self._check(self.lib.lfsr_profile(self._h, 1 if enable else 0))
+
+    def profile_read(self):
+        """(ms[3], launches[3]) accumulated for (wz tile, normal tile, cg update) kernels."""
+        ms = (ctypes.c_double * 3)()
+        n = (ctypes.c_int64 * 3)()
+        self._check(self.lib.lfsr_profile_read(self._h, ms, n))
+        return list(ms), list(n)
+
+    def get_hr(self, out=None):
+        """Returns x [H][W]: into `out` (torch tensor, host or device) or a new numpy array."""
+        H, W = self.params.H, self.params.W
+        if out is None:
+            out = np.empty((H, W), dtype=np.float32)
+            self._check(self.lib.lfsr_get_hr(self._h, out.ctypes.data, MEM_HOST))
+            return out
+        mem = MEM_DEVICE if (_is_torch(out) and out.is_cuda) else MEM_HOST
+        ptr = out.data_ptr() if _is_torch(out) else out.ctypes.data
+        self._check(self.lib.lfsr_get_hr(self._h, ptr, mem))
+        return out
+
+    def get_state(self):
+        p = self.params
+        wA = np.empty((p.n_views, p.lr_height, p.lr_width), np.float32)
+        wS = np.empty((p.s_d, p.H, p.W), np.float32)
+        x = np.empty((p.H, p.W), np.float32)
+        m = np.empty((p.H, p.W), np.float32)
+        self._check(self.lib.lfsr_get_state(self._h, wA.ctypes.data, wS.ctypes.data, x.ctypes.data,
+                                            m.ctypes.data, MEM_HOST))
+        return {"wA": wA, "wS": wS, "x": x, "m": m}
+
+    def op(self, name: str, inp):
+        p = self.params
+        op = OPS[name]
+        out_shape = {OP_A: (p.n_views, p.lr_height, p.lr_width), OP_AT: (p.H, p.W),
+                     OP_S: (p.s_d, p.H, p.W), OP_ST: (p.H, p.W), OP_NORMAL: (p.H, p.W),
+                     OP_WEIGHTS: (p.H, p.W)}[op]
+        ptr, mem, keep = self._ptr_in(inp)
+        if mem == MEM_DEVICE:
+            import torch
+            out = torch.empty(out_shape, dtype=torch.float32, device=keep.device)
+            self._check(self.lib.lfsr_op_apply(self._h, op, ptr, out.data_ptr(), MEM_DEVICE))
+            return out
+        out = np.empty(out_shape, np.float32)
+        self._check(self.lib.lfsr_op_apply(self._h, op, ptr, out.ctypes.data, MEM_HOST))
+        return out
+
+    @property
+    def launches_per_iter(self) -> int:
+        return int(self.lib.lfsr_launches_per_iter(self._h))
+
+
+def params_for(lf_meta_or_cfg, defaults=None, **over) -> Params:
+    """Params for an lfsr_synth config (shape fields) + SolverDefaults (numbers)."""
+    cfg = lf_meta_or_cfg
+    d = {} if defaults is None else {k: getattr(defaults, k) for k in
+                                      ("lambda1", "lambda2", "lambda_reg", "sigma_s", "sigma_e", "sigma_o1",
+                                       "sigma_o2", "theta", "cg_max_iters", "cg_tol")}
+    if defaults is not None:
+        d["nltv_radius"] = defaults.radius
+    d.update(n_views=cfg.n_views, lr_height=cfg.lr_h, lr_width=cfg.lr_w, scale=cfg.scale, ref_view=cfg.ref_view)
+    d.update(over)
+    return Params(**d)
+
+
+def psnr(x, gt, crop: int = 8) -> float:
+    """PSNR = 10 log10(1/MSE) of clip(x, 0, 1) vs gt on an interior crop (reading A25)."""
+    x = np.clip(np.asarray(x, dtype=np.float64), 0.0, 1.0)
+    gt = np.asarray(gt, dtype=np.float64)
+    if crop > 0:
+        x, gt = x[crop:-crop, crop:-crop], gt[crop:-crop, crop:-crop]
+    mse = float(np.mean((x - gt) ** 2))
+    return math.inf if mse == 0 else 10.0 * math.log10(1.0 / mse)

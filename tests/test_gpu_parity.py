@@ -1,0 +1,237 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on identical
+seeded inputs.  Bars (BASELINE.json north_star): per-iterate relative L2 error of x^n
+<= 1e-4 and final PSNR within 0.01 dB; operators within fp32 rounding (1e-5 relative
+L2, derived in DESIGN.md §9)."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+import lfsr_synth as S
+
+pytestmark = pytest.mark.gpu
+
+OP_TOL = 2e-5      # relative L2, single operator application in fp32
+ITER_TOL = 1e-4    # north_star per-iterate bar
+PSNR_TOL = 0.01    # dB
+
+
+def rel_l2(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def oparams(gp):
+    return O.Params(n_views=gp.n_views, lr_h=gp.lr_height, lr_w=gp.lr_width, scale=gp.scale, ref_view=gp.ref_view,
+                    radius=gp.nltv_radius, lambda1=gp.lambda1, lambda2=gp.lambda2, lambda_reg=gp.lambda_reg,
+                    sigma_s=gp.sigma_s, sigma_e=gp.sigma_e, sigma_o1=gp.sigma_o1, sigma_o2=gp.sigma_o2,
+                    theta=gp.theta, cg_max_iters=gp.cg_max_iters, cg_tol=gp.cg_tol,
+                    reweight_every_iter=gp.reweight_every_iter)
+
+
+def f32(a):
+    return np.asarray(a, dtype=np.float32)
+
+
+# shapes spanning several tiles and ragged tails, all three scales
+OP_CASES = [
+    dict(seed=1, nv=3, h=7, w=9, z=2),
+    dict(seed=2, nv=5, h=40, w=70, z=2),
+    dict(seed=3, nv=4, h=23, w=47, z=3),
+    dict(seed=4, nv=2, h=17, w=33, z=4),
+    dict(seed=5, nv=1, h=5, w=5, z=2),
+    dict(seed=6, nv=9, h=33, w=31, z=2, grid=3),
+]
+
+
+def make_solver(lfsr_mod, case, **over):
+    y, vo, om, x = S.random_instance(case["seed"], case["nv"], case["h"], case["w"], case["z"],
+                                     grid=case.get("grid"))
+    p = lfsr_mod.Params(n_views=case["nv"], lr_height=case["h"], lr_width=case["w"], scale=case["z"],
+                        ref_view=case["nv"] // 2, **over)
+    s = lfsr_mod.Solver(p)
+    s.set_observations(y, vo, om)
+    return s, p, y, vo, om, x
+
+
+@pytest.mark.parametrize("case", OP_CASES, ids=lambda c: "nv%d_%dx%d_z%d" % (c["nv"], c["h"], c["w"], c["z"]))
+def test_operator_parity(lfsr_mod, case):
+    s, p, y, vo, om, x = make_solver(lfsr_mod, case)
+    P = oparams(p)
+    g = np.random.default_rng(case["seed"] + 99)
+    xin = g.uniform(-1, 1, (p.H, p.W)).astype(np.float32)
+    rin = g.uniform(-1, 1, (p.n_views, p.lr_height, p.lr_width)).astype(np.float32)
+    hin = g.uniform(-1, 1, (p.s_d, p.H, p.W)).astype(np.float32)
+    st = s.get_state()
+    m = st["m"]
+    # A, A^T, normal operator
+    assert rel_l2(s.op("A", xin), O.apply_A(P, vo, om, xin)) < OP_TOL
+    assert rel_l2(s.op("AT", rin), O.apply_AT(P, vo, om, rin)) < OP_TOL
+    assert rel_l2(s.op("NORMAL", xin), O.normal(P, vo, om, m, xin)) < OP_TOL
+    # NLTV S, S^T with the library's current weight map
+    assert rel_l2(s.op("S", xin), O.apply_S(xin, m, p.nltv_radius, p.sigma_s)) < OP_TOL
+    assert rel_l2(s.op("ST", hin), O.apply_ST(hin, m, p.nltv_radius, p.sigma_s)) < OP_TOL
+    # setup: bicubic x0, w_o and m
+    wo, _, _ = O.setup_wo(P, y, vo, om)
+    x0 = O.bicubic(y[p.ref_view], p.scale)
+    assert rel_l2(st["x"], x0) < 1e-6
+    assert rel_l2(m, O.weights_m(x0, wo, p.lambda_reg, p.sigma_e)) < 1e-5
+    assert rel_l2(s.op("WEIGHTS", xin), O.weights_m(xin, wo, p.lambda_reg, p.sigma_e)) < 1e-5
+    s.close()
+
+
+@pytest.mark.parametrize("case", OP_CASES[:4], ids=lambda c: "z%d" % c["z"])
+def test_gpu_adjoint_identities(lfsr_mod, case):
+    s, p, y, vo, om, x = make_solver(lfsr_mod, case)
+    g = np.random.default_rng(7)
+    for _ in range(5):
+        xin = g.standard_normal((p.H, p.W)).astype(np.float32)
+        rin = g.standard_normal((p.n_views, p.lr_height, p.lr_width)).astype(np.float32)
+        lhs = float(np.vdot(s.op("A", xin).astype(np.float64), rin))
+        rhs = float(np.vdot(xin.astype(np.float64), s.op("AT", rin)))
+        assert abs(lhs - rhs) <= 1e-5 * max(abs(lhs), 1e-3 * np.linalg.norm(xin) * np.linalg.norm(rin))
+        x2 = g.standard_normal((p.H, p.W)).astype(np.float32)
+        a = float(np.vdot(s.op("NORMAL", xin).astype(np.float64), x2))
+        b = float(np.vdot(xin.astype(np.float64), s.op("NORMAL", x2)))
+        assert abs(a - b) <= 1e-5 * max(abs(a), abs(b))
+        assert float(np.vdot(s.op("NORMAL", xin).astype(np.float64), xin)) > 0
+    s.close()
+
+
+def run_pair(lfsr_mod, lf, n_iters, **over):
+    cfg_defaults = S.SolverDefaults()
+    p = lfsr_mod.Params(n_views=lf.n_views, lr_height=lf.y.shape[1], lr_width=lf.y.shape[2], scale=lf.scale,
+                        ref_view=lf.ref_view, nltv_radius=cfg_defaults.radius, lambda1=cfg_defaults.lambda1,
+                        lambda2=cfg_defaults.lambda2, lambda_reg=cfg_defaults.lambda_reg,
+                        sigma_s=cfg_defaults.sigma_s, sigma_e=cfg_defaults.sigma_e, sigma_o1=cfg_defaults.sigma_o1,
+                        sigma_o2=cfg_defaults.sigma_o2, theta=cfg_defaults.theta,
+                        cg_max_iters=cfg_defaults.cg_max_iters, cg_tol=cfg_defaults.cg_tol)
+    for k, v in over.items():
+        setattr(p, k, v)
+    ora = O.admm(oparams(p), lf.y, lf.view_offsets, lf.omega, n_iters)
+    s = lfsr_mod.Solver(p)
+    s.set_observations(lf.y, lf.view_offsets, lf.omega)
+    xs = [s.get_hr()]
+    stats = []
+    for n in range(n_iters):
+        stats += s.admm_run(1)
+        xs.append(s.get_hr())
+    st = s.get_state()
+    s.close()
+    return p, ora, np.array(xs), stats, st
+
+
+def check_iterates(p, ora, xs, stats, st, gt=None):
+    errs = [rel_l2(xs[n], ora.x_iters[n]) for n in range(len(xs))]
+    assert max(errs) <= ITER_TOL, errs
+    for n, (g, o) in enumerate(zip(stats, ora.stats)):
+        assert g["cg_iters"] == o["cg_iters"], n
+        assert abs(g["J"] - o["J"]) <= ITER_TOL * abs(o["J"]), (n, g["J"], o["J"])
+        assert abs(g["primal_res"] - o["primal_res"]) <= ITER_TOL * max(o["primal_res"], 1e-12), n
+        assert not g["nonfinite"]
+    scale = max(np.linalg.norm(ora.wA), 1e-3 * math.sqrt(ora.wA.size) / p.theta)
+    assert np.linalg.norm(st["wA"] - ora.wA) <= ITER_TOL * scale
+    scale = max(np.linalg.norm(ora.wS), 1e-3 * math.sqrt(ora.wS.size) / p.theta)
+    assert np.linalg.norm(st["wS"] - ora.wS) <= ITER_TOL * scale
+    if gt is not None:
+        assert abs(O.psnr(xs[-1], gt) - O.psnr(ora.x_iters[-1], gt)) <= PSNR_TOL
+        assert abs(O.psnr(xs[-1], gt, crop=0) - O.psnr(ora.x_iters[-1], gt, crop=0)) <= PSNR_TOL
+    return errs
+
+
+def test_admm_parity_C1(lfsr_mod):
+    lf = S.make_lightfield("C1")
+    p, ora, xs, stats, st = run_pair(lfsr_mod, lf, 20)
+    errs = check_iterates(p, ora, xs, stats, st, lf.x_gt)
+    print("C1 per-iterate rel L2:", ["%.2e" % e for e in errs])
+
+
+def test_admm_parity_C1_variants(lfsr_mod):
+    """l1-only, l2-only, frozen weights, K=1 and a tau > 0 early stop."""
+    lf = S.make_lightfield("C1")
+    for over in (dict(lambda2=0.0), dict(lambda1=0.0), dict(reweight_every_iter=0), dict(cg_max_iters=1),
+                 dict(cg_tol=1e-3, cg_max_iters=12), dict(nltv_radius=1, theta=3.0)):
+        p, ora, xs, stats, st = run_pair(lfsr_mod, lf, 5, **over)
+        check_iterates(p, ora, xs, stats, st, lf.x_gt)
+
+
+@pytest.mark.parametrize("cfg,n", [("C2", 4), ("C3", 2), ("C4", 2)])
+def test_admm_parity_full_size(lfsr_mod, cfg, n):
+    """BASELINE configs at full size, in the launch configuration bench.py times."""
+    lf = S.make_lightfield(cfg)
+    p, ora, xs, stats, st = run_pair(lfsr_mod, lf, n)
+    errs = check_iterates(p, ora, xs, stats, st, lf.x_gt)
+    print(cfg, "per-iterate rel L2:", ["%.2e" % e for e in errs])
+
+
+def test_continuation_and_determinism(lfsr_mod):
+    lf = S.make_lightfield("C1")
+    p = lfsr_mod.Params(n_views=9, lr_height=32, lr_width=32, scale=2, ref_view=4)
+    a = lfsr_mod.Solver(p)
+    a.set_observations(lf.y, lf.view_offsets, lf.omega)
+    a.admm_run(3)
+    a.admm_run(4)
+    xa = a.get_hr()
+    b = lfsr_mod.Solver(p)
+    b.set_observations(lf.y, lf.view_offsets, lf.omega)
+    st = b.admm_run(7)
+    xb = b.get_hr()
+    assert [r["iter"] for r in st] == list(range(1, 8))
+    assert rel_l2(xa, xb) < 1e-6
+    b.set_observations(lf.y, lf.view_offsets, lf.omega)   # reset: x = x0, w = 0
+    b.admm_run(7)
+    assert rel_l2(b.get_hr(), xb) < 1e-6
+
+
+def test_device_pointer_path(lfsr_mod):
+    import torch
+    lf = S.make_lightfield("C1")
+    p = lfsr_mod.Params(n_views=9, lr_height=32, lr_width=32, scale=2, ref_view=4)
+    a = lfsr_mod.Solver(p, stream=torch.cuda.current_stream().cuda_stream)
+    a.set_observations(torch.from_numpy(lf.y).cuda(), torch.from_numpy(lf.view_offsets).cuda(),
+                       torch.from_numpy(lf.omega).cuda())
+    a.admm_run(3)
+    out = torch.empty((64, 64), device="cuda")
+    a.get_hr(out)
+    torch.cuda.synchronize()
+    b = lfsr_mod.Solver(p)
+    b.set_observations(lf.y, lf.view_offsets, lf.omega)
+    b.admm_run(3)
+    assert rel_l2(out.cpu().numpy(), b.get_hr()) < 1e-6
+
+
+def test_error_paths(lfsr_mod):
+    p = lfsr_mod.Params(n_views=9, lr_height=32, lr_width=32, scale=2, ref_view=4)
+    s = lfsr_mod.Solver(p)
+    with pytest.raises(lfsr_mod.LFSRError) as ei:
+        s.admm_run(1)
+    assert ei.value.status == 2  # LFSR_ERR_STATE
+    lf = S.make_lightfield("C1")
+    bad = lf.view_offsets.copy()
+    bad[0, 0] = np.nan
+    with pytest.raises(lfsr_mod.LFSRError) as ei:
+        s.set_observations(lf.y, bad, lf.omega)
+    assert ei.value.status == 1
+    # divergence guard: NaN disparity is rejected up front
+    om = lf.omega.copy()
+    om[3, 3] = np.inf
+    with pytest.raises(lfsr_mod.LFSRError):
+        s.set_observations(lf.y, lf.view_offsets, om)
+    s.set_observations(lf.y, lf.view_offsets, lf.omega)
+    assert len(s.admm_run(2)) == 2
+    assert s.launches_per_iter == 1 + 2 * p.cg_max_iters
+
+
+def test_divergence_guard(lfsr_mod):
+    lf = S.make_lightfield("C1")
+    p = lfsr_mod.Params(n_views=9, lr_height=32, lr_width=32, scale=2, ref_view=4)
+    s = lfsr_mod.Solver(p)
+    y = lf.y.copy()
+    y[0, 0, 0] = np.nan
+    s.set_observations(y, lf.view_offsets, lf.omega)
+    with pytest.raises(lfsr_mod.LFSRError) as ei:
+        s.admm_run(2)
+    assert ei.value.status == 6  # LFSR_ERR_DIVERGED
+    assert ei.value.stats[0]["nonfinite"] == 1

@@ -1,0 +1,32 @@
+"""Quick device timing of the ADMM iteration on a config (development aid)."""
+import sys, os, time, json
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import lfsr_synth as S
+import paper_2206_05047_b200 as L
+
+cfgname = sys.argv[1] if len(sys.argv) > 1 else "C3"
+iters = int(sys.argv[2]) if len(sys.argv) > 2 else 10
+t0 = time.time()
+lf = S.make_lightfield(cfgname)
+print("gen %.1fs" % (time.time() - t0), flush=True)
+cfg = S.CONFIGS[cfgname]
+p = L.params_for(cfg, S.SolverDefaults())
+stream = torch.cuda.Stream()
+torch.cuda.set_stream(stream)
+s = L.Solver(p, stream=stream.cuda_stream)
+s.set_observations(*[torch.from_numpy(a).cuda() for a in (lf.y, lf.view_offsets, lf.omega)])
+s.admm_run(2)
+s.profile(True)
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+tot = 0.0
+for i in range(iters):
+    e0.record(stream); s.admm_enqueue(1); e1.record(stream); e1.synchronize()
+    tot += e0.elapsed_time(e1)
+    s.profile_read()
+ms, n = s.profile_read()
+st = s.admm_stats(3, iters)
+print(json.dumps({"cfg": cfgname, "ms_per_iter": tot / iters, "it_per_s": 1000 * iters / tot,
+                  "kernel_ms_per_launch": [m / max(c, 1) for m, c in zip(ms, n)], "launches": n,
+                  "J_first": st[0]["J"], "J_last": st[-1]["J"], "psnr": L.psnr(s.get_hr(), lf.x_gt),
+                  "psnr_x0": None}))
