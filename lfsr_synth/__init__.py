@@ -269,8 +269,8 @@ def _render(layers, Ys, Xs, drho, dtau):
         msk = L.inside(Yr, Xr)
         if not msk.any():
             continue
-        img = np.where(msk, L.tex(Yr, Xr), img)
-        disp = np.where(msk, L.disparity(Yr, Xr), disp)
+        img[msk] = L.tex(Yr[msk], Xr[msk])       # evaluate textures only where the layer is seen
+        disp[msk] = L.disparity(Yr[msk], Xr[msk])
     return img, disp
 
 

@@ -48,6 +48,29 @@ __global__ void k_setup_wo(const Geom G, const Views V, const float* __restrict_
   wo[(size_t)Y * ps + X] = expf(-b * b * G.inv_2s1sq) * expf(-p * p * G.inv_2s2sq);
 }
 
+// Splat density D(z) = sum_k (W_k^T 1)(z): the total bilinear weight all views'
+// exact adjoint warps deposit on cell z.  Its maximum bounds the fixed-point
+// accumulators of the tile kernels.  Setup only.
+__global__ void k_density(const Geom G, const Views V, const float* __restrict__ omega, float* __restrict__ D) {
+  int X = blockIdx.x * blockDim.x + threadIdx.x, Y = blockIdx.y;
+  if (X >= G.W || Y >= G.H) return;
+  const int ps = G.ps;
+  const float om = omega[(size_t)Y * ps + X];
+  for (int k = 0; k < G.n_views; ++k) {
+    const float2 o = V.off[k];
+    const float sy = fminf(fmaxf((float)Y + o.y * om, 0.f), (float)(G.H - 1));
+    const float sx = fminf(fmaxf((float)X + o.x * om, 0.f), (float)(G.W - 1));
+    const float fy = floorf(sy), fx = floorf(sx);
+    const int y0 = (int)fy, x0 = (int)fx;
+    const int y1 = min(y0 + 1, G.H - 1), x1 = min(x0 + 1, G.W - 1);
+    const float a = sy - fy, b = sx - fx;
+    atomicAdd(&D[(size_t)y0 * ps + x0], (1.f - a) * (1.f - b));
+    atomicAdd(&D[(size_t)y0 * ps + x1], (1.f - a) * b);
+    atomicAdd(&D[(size_t)y1 * ps + x0], a * (1.f - b));
+    atomicAdd(&D[(size_t)y1 * ps + x1], a * b);
+  }
+}
+
 __device__ __forceinline__ float keys_cubic(float t) {  // Catmull-Rom, a = -0.5 (reading A15)
   const float a = -0.5f;
   t = fabsf(t);
@@ -236,6 +259,10 @@ static dim3 hr_grid(const Geom& G, int bx) { return dim3((G.W + bx - 1) / bx, G.
 cudaError_t launch_setup_wo(const Geom& G, const Views& V, const float* y, const float* omega, float* wo,
                             cudaStream_t st) {
   k_setup_wo<<<hr_grid(G, 128), 128, 0, st>>>(G, V, y, omega, wo);
+  return cudaGetLastError();
+}
+cudaError_t launch_density(const Geom& G, const Views& V, const float* omega, float* D, cudaStream_t st) {
+  k_density<<<hr_grid(G, 128), 128, 0, st>>>(G, V, omega, D);
   return cudaGetLastError();
 }
 cudaError_t launch_bicubic(const Geom& G, const float* y, float* x, cudaStream_t st) {

@@ -18,6 +18,7 @@ cudaError_t launch_tile(int mode, const Geom& G, const Views& V, const TileGeom&
 cudaError_t launch_setup_wo(const Geom& G, const Views& V, const float* y, const float* omega, float* wo,
                             cudaStream_t st);
 cudaError_t launch_bicubic(const Geom& G, const float* y, float* x, cudaStream_t st);
+cudaError_t launch_density(const Geom& G, const Views& V, const float* omega, float* D, cudaStream_t st);
 cudaError_t launch_weights(const Geom& G, const float* x, const float* wo, float* m, cudaStream_t st);
 cudaError_t launch_absmax(const float* v, size_t n, unsigned* out, cudaStream_t st);
 cudaError_t launch_cg_update(const Geom& G, float* x, float* r, const float* p, float* q, Control* ctl, int k,
@@ -142,6 +143,13 @@ static void fill_geom(lfsr_ctx* c) {
   double sum = 0.0, t[2 * kMaxTaps + 1];
   for (int u = -R; u <= R; ++u) sum += (t[u + R] = std::exp(-(double)u * u / (2.0 * sig * sig)));
   for (int u = 0; u <= 2 * R; ++u) G.taps[u] = (float)(t[u] / sum);
+  double gmax = 0.0;
+  for (int ph = 0; ph < p.scale; ++ph) {
+    double sp = 0.0;
+    for (int u = ph; u <= 2 * R; u += p.scale) sp += t[u] / sum;
+    gmax = std::fmax(gmax, sp);
+  }
+  G.gpoly2 = (float)(gmax * gmax * 1.0001);
   // NLTV offsets U and spatial weights w_d = exp(-|d|^2/sigma_s) (A8, A9)
   int n = 0;
   for (int dy = -p.nltv_radius; dy <= p.nltv_radius; ++dy)
@@ -341,7 +349,9 @@ lfsr_status lfsr_set_observations(lfsr_ctx* c, const float* lr_views, const floa
     ALLOC(S.x, hr * 4);
     ALLOC(S.y, lr * 4);
     ALLOC(S.wA, lr * 4);
-    ALLOC(S.wS, ws * 4);
+    ALLOC(S.wS[0], ws * 4);
+    ALLOC(S.wS[1], ws * 4);
+    ALLOC(S.density, hr * 4);
     ALLOC(S.omega, hr * 4);
     ALLOC(S.wo, hr * 4);
     ALLOC(S.m, hr * 4);
@@ -360,7 +370,9 @@ lfsr_status lfsr_set_observations(lfsr_ctx* c, const float* lr_views, const floa
     memcpy(c->alloc_key, key, sizeof key);
   } else {  // same geometry: reset the state in place (Alg.1 lines 1-2: w = 0)
     CK(c, cudaMemsetAsync(S.wA, 0, lr * 4, c->stream));
-    CK(c, cudaMemsetAsync(S.wS, 0, ws * 4, c->stream));
+    CK(c, cudaMemsetAsync(S.wS[0], 0, ws * 4, c->stream));
+    CK(c, cudaMemsetAsync(S.wS[1], 0, ws * 4, c->stream));
+    CK(c, cudaMemsetAsync(S.density, 0, hr * 4, c->stream));
     CK(c, cudaMemsetAsync(S.r, 0, hr * 4, c->stream));
     CK(c, cudaMemsetAsync(S.q, 0, hr * 4, c->stream));
     CK(c, cudaMemsetAsync(S.p[0], 0, hr * 4, c->stream));
@@ -398,6 +410,19 @@ lfsr_status lfsr_set_observations(lfsr_ctx* c, const float* lr_views, const floa
     G.SX = std::min(G.SX, G.W);
     G.SY = std::min(G.SY, G.H);
   }
+  // fixed-point bounds: max |y| and the splat density max_z sum_k (W_k^T 1)(z)
+  CK(c, launch_density(G, c->V, S.omega, S.density, c->stream));
+  CK(c, cudaMemsetAsync(umax, 0, 4, c->stream));
+  CK(c, launch_absmax(S.density, hr, umax, c->stream));
+  CK(c, cudaMemcpyAsync(&ubits, umax, 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(c, cudaStreamSynchronize(c->stream));
+  memcpy(&G.dmax, &ubits, 4);
+  CK(c, cudaMemsetAsync(umax, 0, 4, c->stream));
+  CK(c, launch_absmax(S.y, lr, umax, c->stream));
+  CK(c, cudaMemcpyAsync(&ubits, umax, 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(c, cudaStreamSynchronize(c->stream));
+  memcpy(&G.ymax, &ubits, 4);
+  if (!std::isfinite(G.ymax)) G.ymax = 0.f;  // non-finite observations surface as DIVERGED
   c->T = make_tile_geom(G, c->num_sms);
   if (c->T.smem > 227 * 1024) {
     FAIL(c, LFSR_ERR_UNSUPPORTED, "disparity range too large for the shared-memory tile (halo > ~60 px)");
@@ -443,7 +468,8 @@ static lfsr_status enqueue_iteration(lfsr_ctx* c, cudaStream_t st) {
   io.in_hr = S.x;
   io.y = S.y;
   io.wA = S.wA;
-  io.wS = S.wS;
+  io.wS0 = S.wS[0];
+  io.wS1 = S.wS[1];
   io.wo = S.wo;
   io.out_hr = S.r;
   io.reweight = c->prm.reweight_every_iter;
@@ -622,7 +648,7 @@ lfsr_status lfsr_get_state(lfsr_ctx* c, float* w_A, float* w_S, float* x, float*
   }
   if (w_S) {
     if ((st = check_ptr(c, w_S, mem, "w_S")) != LFSR_OK) return st;
-    CK(c, get2d(c, w_S, G.W, c->S.wS, G.ps, (size_t)G.s_d * G.H, mem));
+    CK(c, get2d(c, w_S, G.W, c->S.wS[c->h_iter & 1], G.ps, (size_t)G.s_d * G.H, mem));
   }
   if (x) {
     if ((st = check_ptr(c, x, mem, "x")) != LFSR_OK) return st;
@@ -670,7 +696,13 @@ lfsr_status lfsr_op_apply(lfsr_ctx* c, lfsr_op op, const float* in, float* out, 
     case LFSR_OP_AT: {
       CK(c, put2d(c, S.tmp_lr, G.lps, in, G.w, (size_t)G.n_views * G.h, mem));
       CK(c, cudaMemsetAsync(c->tmp_hr2, 0, hr * 4, s));
+      CK(c, cudaMemsetAsync(c->umax, 0, 4, s));
+      CK(c, launch_absmax(S.tmp_lr, (size_t)G.n_views * G.h * G.lps, c->umax, s));
+      unsigned ub = 0;
+      CK(c, cudaMemcpyAsync(&ub, c->umax, 4, cudaMemcpyDeviceToHost, s));
+      CK(c, cudaStreamSynchronize(s));
       TileIO io = base_io(c);
+      memcpy(&io.tmax_in, &ub, 4);
       io.in_lr = S.tmp_lr;
       io.out_hr = c->tmp_hr2;
       CK(c, launch_tile(MODE_AT, G, c->V, c->T, io, s));

@@ -54,6 +54,9 @@ struct Geom {
   float inv_sigma_e, inv_2s1sq, inv_2s2sq;  // 0 when the factor is disabled (sigma = inf)
   float cg_tol;
   float cA;                   // lambda2 + (theta/2) lambda1^2   (A7)
+  float dmax;                 // max_z sum_k (W_k^T 1)(z) (set at set_observations)
+  float ymax;                 // max |y|
+  float gpoly2;               // (max polyphase tap sum)^2: |B^T D^T rho| <= gpoly2 max|rho|
   float cS;                   // theta / 2
   float taps[kMaxTaps * 2 + 1];
   float wd[kMaxOffsets];      // spatial weights w_d
@@ -65,16 +68,21 @@ struct Views {
 };
 
 // Tile decomposition of the HR grid; every field is derived on the host.
+// A tile = a band of BL LR rows x a strip of LX LR columns (one warp column of
+// 32 lanes, lane = LR column); its "E region" is the set of HR positions whose
+// blurred warped value reaches an own LR pixel: EY rows x ECOL (= 32 zeta)
+// columns, of which EXv are real.
 struct TileGeom {
-  int32_t LY, LX;             // LR pixels per tile
-  int32_t TY, TX;             // HR pixels per tile (= zeta * L)
-  int32_t EY, EX;             // E region (positions whose warp sample feeds own LR pixels)
-  int32_t HY, HX;             // p-tile halo (top/left) = R + max(S, r)
-  int32_t PH, PW;             // p-tile rows / row pitch in shared memory
-  int32_t MH, MW;             // m-tile (own + r halo) rows / pitch
+  int32_t BL, LX;             // LR rows / columns per tile
+  int32_t TY, TX;             // own HR pixels per tile (= zeta * BL, zeta * LX)
+  int32_t EY, ECOL, EXv;      // E region rows, allocated columns, valid columns
+  int32_t SYe, SXe;           // halo of the input tile around the E region (>= radius)
+  int32_t PH, PW, PWZ;        // input tile rows, row pitch (= zeta * PWZ), phase pitch
+  int32_t MH, MW;             // m tile (own + radius halo)
   int32_t ntY, ntX;           // tiles per axis
-  int32_t groups;             // view groups (split-K over views)
+  int32_t groups;             // view groups (CTAs per tile)
   int32_t vpg;                // views per group
+  int32_t nwarps;             // warps per CTA (views of a group are dealt round-robin)
   size_t smem;                // dynamic shared memory bytes
 };
 
@@ -86,17 +94,18 @@ struct TileIO {
   const float* omega;
   const float* y;        // WZ
   float* wA;             // WZ (in/out)
-  float* wS;             // WZ (in/out)
+  float* wS0;            // WZ: w_S ping-pong buffers; read wS[iter&1], write wS[(iter&1)^1]
+  float* wS1;
   const float* wo;       // WZ (weights)
   float* m;              // WZ: written (if reweight) / read; NORMAL: read
   const float* in_lr;    // AT
   float* out_lr;         // A
   float* out_hr;         // accumulated (RED.ADD) output: r (WZ, sign -1) | q (NORMAL) | AT
   Control* ctl;
+  float tmax_in;         // AT: max |in_lr| (bound for the fixed-point scale)
   int32_t cg_k;          // NORMAL-CG: step index k >= 1; 0 = plain operator
   int32_t reweight;      // WZ: recompute m from x
   int32_t do_nltv;       // NORMAL: include the (th/2) S^T S term
-  int32_t pad;
 };
 
 enum TileMode : int { MODE_WZ = 0, MODE_NORMAL = 1, MODE_A = 2, MODE_AT = 3 };
@@ -106,7 +115,8 @@ struct State {
   float* x;      // [H][ps]
   float* y;      // [n_views][h][lps]
   float* wA;     // [n_views][h][lps]
-  float* wS;     // [s_d][H][ps]
+  float* wS[2];  // [s_d][H][ps] ping-pong (read iter&1, write the other)
+  float* density;  // [H][ps] splat density sum_k W_k^T 1 (fixed-point bound)
   float* omega;  // [H][ps]
   float* wo;     // [H][ps]
   float* m;      // [H][ps]

@@ -1,41 +1,50 @@
-// tile_kernels.cu — the fused observation-operator tile kernel of liblfsr.
+// tile_kernels.cu — the fused observation-operator tile kernel of liblfsr (v2).
 //
-// One CTA owns an LR tile of LY x LX pixels (an HR tile of zeta*LY x zeta*LX)
-// and a group of views.  For each view k it runs, entirely in shared memory:
-//   P1  warp W_k: bilinear gather of the HR input at z + dtheta_k*omega(z) for
-//       every HR position z of the "E region" (the positions whose blurred
-//       value reaches an own LR pixel)                     P:L580-583, A12/A13
-//   P2  horizontal Gaussian blur evaluated at LR columns only        P:L579, A11
-//   P3  vertical blur at LR rows = D B W_k x (A_k x)   + the per-LR-pixel
-//       epilogue: (WZ) e = A_k x - y_k, clamp-form prox + scaled dual update
-//       (Alg.1 lines 4-8, A5/A6) -> rho_k; (NORMAL) rho = c_A A_k p
-//   P4  vertical adjoint blur (polyphase: only LR taps)          B^T D^T (A11/A14)
-//   P5  horizontal adjoint blur + exact bilinear scatter W_k^T into a shared
-//       accumulator (the transpose of P1, reading A12)
-// then the weighted NLTV part for the own HR pixels, and finally
-// flushes the accumulator (tile + halo) to global memory with RED.ADD so that
-// neighbouring tiles' halo contributions sum up.  MODE_WZ is the whole wz-step
-// of Alg.1 (lines 4-9) and writes r = -v (Alg.2 line 2 with reading A3);
-// MODE_NORMAL is q = M p with the CG direction update
-// p_k = r_k + beta p_{k-1} fused into the tile load (Alg.2 line 10, A2).
+// One CTA owns a tile = a band of BL LR rows x a strip of LX LR columns, and a
+// group of views.  Every warp of the CTA takes whole views (round robin) and
+// streams the tile's "E region" (the HR positions whose blurred warped value
+// reaches an own LR pixel) row by row, lane = LR column, each lane holding the
+// zeta HR columns under its LR column:
+//   W_k    bilinear gather at z + dtheta_k * omega(z) from the shared input tile
+//          (replicate-clamped coordinate)                       P:L580-583, A12/A13
+//   B, D   Gaussian blur evaluated at LR positions only: horizontal taps by warp
+//          shuffles, vertical taps in a register ring (decimation is free) P:L577-579
+//   epilogue per LR pixel: (WZ) e = A_k x - y_k, clamp-form prox + scaled dual
+//          (Alg.1 lines 4-8, A5/A6) -> rho; (NORMAL) rho = c_A A_k p
+//   D^T B^T polyphase adjoint blur (register ring + shuffles)           A11/A14
+//   W_k^T  exact bilinear scatter into a shared int32 fixed-point accumulator
+//          (native ATOMS.ADD, order-independent -> deterministic per CTA)  A12
+// No barrier inside the view loop.  Then the weighted NLTV term in gather form
+// for the own pixels (the CTA's view group takes every G-th offset),
+// and one RED.ADD flush of accumulator + NLTV term (tile + halo) to global so
+// neighbouring tiles and view groups sum.
+//
+// Fixed-point scale: every CTA bounds |t| (the blurred adjoint value of one
+// source) by tb (c_A max|p| for NORMAL; l2 (max|x| + max|y|) + (th/2) l1 3/th for
+// WZ) and the accumulated weight per cell by the splat density max_z sum_k
+// (W_k^T 1)(z) (computed once at setup), and picks 2^s with |w t 2^s| < 2^21 and
+// |acc| < 2^30: the per-contribution rounding is <= 2^-22 tb.
 #include "internal.h"
 #include <cfloat>
+#include <cmath>
 
 namespace lfsr {
 
 template <int Z> struct TileCfg;
-template <> struct TileCfg<2> { static constexpr int R = 2, LY = 16, LX = 32; };
-template <> struct TileCfg<3> { static constexpr int R = 3, LY = 11, LX = 22; };
-template <> struct TileCfg<4> { static constexpr int R = 3, LY = 8, LX = 16; };
+template <> struct TileCfg<2> { static constexpr int R = 2, LX = 30, BL = 16; };
+template <> struct TileCfg<3> { static constexpr int R = 3, LX = 30, BL = 11; };
+template <> struct TileCfg<4> { static constexpr int R = 3, LX = 31, BL = 8; };
 
-template <int Z> struct TileC {
-  static constexpr int R = TileCfg<Z>::R, LY = TileCfg<Z>::LY, LX = TileCfg<Z>::LX;
-  static constexpr int TY = Z * LY, TX = Z * LX;
-  static constexpr int EY = Z * (LY - 1) + 2 * R + 1, EX = Z * (LX - 1) + 2 * R + 1;
-  static constexpr int E = EY * EX;
-  static constexpr int MAXP = (E + kThreads - 1) / kThreads;
+template <int Z> struct TC {
+  static constexpr int R = TileCfg<Z>::R, LX = TileCfg<Z>::LX, BL = TileCfg<Z>::BL;
+  static constexpr int NTAP = 2 * R + 1;
+  static constexpr int KEEP = NTAP - Z;           // forward-ring rows carried between LR rows
+  static constexpr int TY = Z * BL, TX = Z * LX;
+  static constexpr int EY = Z * BL + KEEP;        // = Z (BL - 1) + 2R + 1
+  static constexpr int ECOL = 32 * Z;
+  static constexpr int EXv = Z * (LX - 1) + NTAP;
+  static_assert(EXv <= ECOL, "strip too wide for one warp");
 };
-
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -47,7 +56,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 template <int NV>
 __device__ __forceinline__ void block_reduce_add(double (&v)[NV], double* red, double* dst,
                                                  const int (&slot)[NV]) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
 #pragma unroll
   for (int i = 0; i < NV; ++i) v[i] = warp_sum(v[i]);
   __syncthreads();
@@ -58,62 +67,400 @@ __device__ __forceinline__ void block_reduce_add(double (&v)[NV], double* red, d
   __syncthreads();
   if (threadIdx.x < NV) {
     double s = 0.0;
-    for (int w = 0; w < kThreads / 32; ++w) s += red[w * NV + threadIdx.x];
+    for (int w = 0; w < nw; ++w) s += red[w * NV + threadIdx.x];
     if (s != 0.0) atomicAdd(dst + slot[threadIdx.x], s);
   }
 }
 
+// Two-word fixed-point accumulation: v (already scaled by 2^s,
+// |v| < 2^22) is split into its rounded integer part q1 and the residual
+// r = v - q1 in [-1/2, 1/2], which goes to a second accumulator in units of 2^-15
+// (|q2| <= 2^14, so 2^17 contributions per cell cannot overflow).  Both rounding
+// steps use the 1.5*2^23 magic (FADD + IADD, no XU-pipe conversion); integer
+// atomics are native (ATOMS.ADD) and associative, so the result does not depend
+// on the order of the atomics.  Resolution 2^-(s+15) ~ 2^-37 of the per-CTA bound.
+constexpr float kMagic = 12582912.0f;   // 1.5 * 2^23
+constexpr int kMagicBits = 0x4B400000;
+constexpr int kLoBits = 15;
+
+__device__ __forceinline__ int fix(float v) { return __float_as_int(v + kMagic) - kMagicBits; }
+
+__device__ __forceinline__ void acc_add(int* hi, int lo_off, int i, float v) {
+  const float t = v + kMagic;
+  const int q1 = __float_as_int(t) - kMagicBits;
+  const float r = v - (t - kMagic);
+  const int q2 = __float_as_int(fmaf(r, (float)(1 << kLoBits), kMagic)) - kMagicBits;
+  atomicAdd(hi + i, q1);
+  atomicAdd(hi + lo_off + i, q2);
+}
+
+// phase-split shared index of tile-local (py, px): columns of equal px % Z are
+// contiguous, so lanes zeta columns apart hit consecutive banks.
+template <int Z>
+__device__ __forceinline__ int pidx(int py, int px, int PW, int PWZ) {
+  const unsigned ux = (unsigned)px;
+  return py * PW + (int)((ux % Z) * PWZ + ux / Z);
+}
+
+// Tile-local arithmetic of one CTA.  INT (interior tile): every E position and
+// every sample lies inside the image, so no clamping or validity test is needed.
+template <int Z, bool INT>
+struct Tile {
+  const float* P;
+  int* ACC;
+  const float* OM;
+  int PW, PWZ, PY0, PX0, YE0, XE0, H, W;
+  unsigned colmask;   // bit s: the lane's E column Z*lane+s is a real column inside the image
+  float tscale;
+  int lo;             // offset of the residual accumulator from ACC (ints)
+
+  // floor and fraction without the XU pipe: round(s - 1/2) by the 1.5*2^23 magic
+  // (|s| < 2^22).  At exact integers s = n this may return n - 1 with fraction 1,
+  // which selects the same bilinear value (the input tile has one spare row/column).
+  __device__ __forceinline__ static void axis(float s, int org, int& n, float& f) {
+    const float r = (s - 0.5f) + 12582912.0f;
+    n = __float_as_int(r) - (0x4B400000 + org);
+    f = s - (r - 12582912.0f);
+  }
+
+  // Tile-local phase-split indices of the sample's top-left / top-right cells and
+  // the bilinear fractions for the E position at HR (Yf, Xf) (A12/A13).
+  // No clamping: the input tile holds the image replicate-padded, and a bilinear
+  // sample of the replicate-padded image equals the sample at the clamped
+  // coordinate; the adjoint scatters into the padding and phase 4 folds it back
+  // onto the edge cells (the transpose of the padding).
+  __device__ __forceinline__ void sample(float Yf, float Xf, float om, float drho, float dtau,
+                                         int& i00, int& i01, float& a, float& b) const {
+    const float sy = fmaf(dtau, om, Yf), sx = fmaf(drho, om, Xf);
+    int iy, ix;
+    axis(sy, PY0, iy, a);
+    axis(sx, PX0, ix, b);
+    const unsigned ux = (unsigned)ix, ph = ux % Z, q = ux / Z;
+    i00 = iy * PW + (int)(ph * PWZ + q);
+    i01 = (ph == Z - 1) ? i00 - (Z - 1) * PWZ + 1 : i00 + PWZ;
+  }
+
+  // E positions outside the image carry zero (blur zero padding, A11): row test is
+  // warp uniform, the column mask is per lane and fixed for the tile.
+  __device__ __forceinline__ bool valid(int er, int s) const {
+    if (INT) return true;
+    const int Y = YE0 + er;
+    return Y >= 0 && Y < H && ((colmask >> s) & 1u);
+  }
+
+  __device__ __forceinline__ void load_om(int er, int lane, float (&om)[Z]) const {
+    const float* src = OM + er * TC<Z>::ECOL + Z * lane;
+    if constexpr (Z == 2) {
+      float2 v = *reinterpret_cast<const float2*>(src);
+      om[0] = v.x; om[1] = v.y;
+    } else if constexpr (Z == 4) {
+      float4 v = *reinterpret_cast<const float4*>(src);
+      om[0] = v.x; om[1] = v.y; om[2] = v.z; om[3] = v.w;
+    } else {
+#pragma unroll
+      for (int s = 0; s < Z; ++s) om[s] = src[s];
+    }
+  }
+
+  // W_k then the horizontal blur taps at this lane's LR column, for E row er.
+  __device__ __forceinline__ float fwd_row(int er, int lane, float drho, float dtau, const float* taps) const {
+    float om[Z], wp[Z];
+    load_om(er, lane, om);
+    const float Yf = (float)(YE0 + er);
+#pragma unroll
+    for (int s = 0; s < Z; ++s) {
+      int i00, i01;
+      float a, b;
+      sample(Yf, (float)(XE0 + Z * lane + s), om[s], drho, dtau, i00, i01, a, b);
+      const float p00 = P[i00], p01 = P[i01], p10 = P[i00 + PW], p11 = P[i01 + PW];
+      const float top = fmaf(b, p01 - p00, p00), bot = fmaf(b, p11 - p10, p10);
+      const float v = fmaf(a, bot - top, top);
+      wp[s] = valid(er, s) ? v : 0.f;
+    }
+    float h = 0.f;
+#pragma unroll
+    for (int v = 0; v < TC<Z>::NTAP; ++v) {
+      const float val = (v < Z) ? wp[v % Z] : __shfl_down_sync(0xffffffffu, wp[v % Z], v / Z);
+      h = fmaf(taps[v], val, h);
+    }
+    return h;
+  }
+
+  // Horizontal adjoint blur of the row's LR-column values t1b and the exact bilinear
+  // scatter (W_k^T) of the lane's zeta positions into the fixed-point accumulator.
+  // When every lane's positions hit adjacent source columns (smooth disparity) the
+  // shared columns are merged first: 2 zeta + 2 atomics instead of 4 zeta.
+  __device__ __forceinline__ void adj_row(int er, int lane, float t1b, float drho, float dtau,
+                                          const float* taps) const {
+    constexpr int NJ = 2 * TC<Z>::R / Z + 1;
+    float tv[NJ];
+    tv[0] = t1b;
+#pragma unroll
+    for (int j = 1; j < NJ; ++j) {
+      const float v = __shfl_up_sync(0xffffffffu, t1b, j);
+      tv[j] = lane >= j ? v : 0.f;
+    }
+    float om[Z];
+    load_om(er, lane, om);
+    const float Yf = (float)(YE0 + er);
+    int i00[Z], i01[Z];
+    float v00[Z], v01[Z], v10[Z], v11[Z];
+    bool adj = true;
+#pragma unroll
+    for (int s = 0; s < Z; ++s) {
+      float t = 0.f;
+#pragma unroll
+      for (int j = 0; j < NJ; ++j)
+        if (Z * j + s <= 2 * TC<Z>::R) t = fmaf(taps[Z * j + s], tv[j], t);
+      float a, b;
+      sample(Yf, (float)(XE0 + Z * lane + s), om[s], drho, dtau, i00[s], i01[s], a, b);
+      const float ts = valid(er, s) ? t * tscale : 0.f;
+      const float ta = ts * a, t1a = ts - ta;
+      v01[s] = t1a * b;
+      v00[s] = t1a - v01[s];
+      v11[s] = ta * b;
+      v10[s] = ta - v11[s];
+      if (s > 0) adj = adj && (i00[s] == i01[s - 1]);
+    }
+    if (__all_sync(0xffffffffu, adj)) {
+      acc_add(ACC, lo, i00[0], v00[0]);
+      acc_add(ACC, lo, i00[0] + PW, v10[0]);
+#pragma unroll
+      for (int s = 1; s < Z; ++s) {
+        acc_add(ACC, lo, i00[s], v00[s] + v01[s - 1]);
+        acc_add(ACC, lo, i00[s] + PW, v10[s] + v11[s - 1]);
+      }
+      acc_add(ACC, lo, i01[Z - 1], v01[Z - 1]);
+      acc_add(ACC, lo, i01[Z - 1] + PW, v11[Z - 1]);
+    } else {
+#pragma unroll
+      for (int s = 0; s < Z; ++s) {
+        acc_add(ACC, lo, i00[s], v00[s]);
+        acc_add(ACC, lo, i01[s], v01[s]);
+        acc_add(ACC, lo, i00[s] + PW, v10[s]);
+        acc_add(ACC, lo, i01[s] + PW, v11[s]);
+      }
+    }
+  }
+};
+
+// Weighted NLTV term of one own pixel z (readings A9/A10):
+//   NORMAL: sum_d Delta_d^T (W_d^2 Delta_d p)(z) and its <p, .> share (W_d = w_d m)
+//   WZ:     z/w steps of the NLTV rows (Alg.1 lines 5-8, clamp form A5/A6) for the
+//           pairs (z, z+d), written to the other w_S buffer, and
+//           sum_d Delta_d^T (W_d f_d)(z) with the backward neighbour's f_d
+//           recomputed from the old duals (gather form: no atomics, no race).
+// RAD > 0: offsets unrolled at compile time (paper's 5x5 window: RAD = 2).
+struct NltvCtx {
+  const float* P;
+  const float* M;
+  const float* wSr;
+  float* wSw;
+  size_t plane;
+  int PW, PWZ, MW, H, W, ps;
+  float ith;
+};
+
+template <int Z, int MODE, bool CHECK, int RAD>
+__device__ __forceinline__ float nltv_pixel(const NltvCtx& c, const Geom& G, int Y, int X, int py, int px, int mi,
+                                            size_t gi, double& pq, double& reg, double& res) {
+  const float xz = c.P[pidx<Z>(py, px, c.PW, c.PWZ)];
+  const float mz = c.M[mi];
+  float acc = 0.f;
+  auto one = [&](int d, int dy, int dx) {
+    const float wd = G.wd[d];
+    const bool fin = !CHECK || ((Y + dy >= 0) && (Y + dy < c.H) && (X + dx >= 0) && (X + dx < c.W));
+    const bool bin = !CHECK || ((Y - dy >= 0) && (Y - dy < c.H) && (X - dx >= 0) && (X - dx < c.W));
+    const float xf = c.P[pidx<Z>(py + dy, px + dx, c.PW, c.PWZ)];   // in the tile even when outside Omega
+    const float xb = c.P[pidx<Z>(py - dy, px - dx, c.PW, c.PWZ)];
+    const float mb = c.M[mi - dy * c.MW - dx];
+    if (MODE == MODE_NORMAL) {
+      const float wz = wd * mz, wb = wd * mb;
+      const float dp = xz - xf;
+      const float f2 = fin ? wz * wz : 0.f;
+      acc = fmaf(f2, dp, acc);
+      pq += (double)(f2 * dp) * dp;
+      const float b2 = bin ? wb * wb : 0.f;
+      acc = fmaf(-b2, xb - xz, acc);
+    } else {
+      const size_t pl = (size_t)d * c.plane;
+      const float wz = wd * mz;
+      const float g = fin ? wz * (xz - xf) : 0.f;             // W_d (.) Delta_d x
+      const float wso = c.wSr[pl + gi];
+      const float wn = fminf(fmaxf(g + wso, -c.ith), c.ith);
+      c.wSw[pl + gi] = wn;
+      reg += fabs((double)g);
+      res += (double)(wn - wso) * (wn - wso);
+      if (fin) acc = fmaf(wz, 2.f * wn - wso, acc);
+      if (bin) {
+        const float wb = wd * mb;
+        const float wsb = c.wSr[pl + gi - (size_t)dy * c.ps - dx];
+        const float wnb = fminf(fmaxf(fmaf(wb, xb - xz, wsb), -c.ith), c.ith);
+        acc = fmaf(-wb, 2.f * wnb - wsb, acc);
+      }
+    }
+  };
+  if constexpr (RAD > 0) {
+#pragma unroll
+    for (int dy = -RAD; dy <= RAD; ++dy) {
+#pragma unroll
+      for (int dx = -RAD; dx <= RAD; ++dx) {
+        if (dy == 0 && dx == 0) continue;
+        const int lin = (dy + RAD) * (2 * RAD + 1) + (dx + RAD);
+        const int d = lin > (2 * RAD + 1) * RAD + RAD ? lin - 1 : lin;   // row-major order, centre skipped (A9)
+        one(d, dy, dx);
+      }
+    }
+  } else {
+    for (int d = 0; d < G.s_d; ++d) one(d, G.ody[d], G.odx[d]);
+  }
+  return acc;
+}
+
+// Phase 2 of k_tile: every warp streams whole views through the tile (see header).
+template <int Z, int MODE, bool INT>
+__device__ __forceinline__ void views(const Tile<Z, INT>& t, const Geom& G, const Views& V, const TileGeom& T,
+                                      const TileIO& io, int grp, int lane, int warp, int NW, int i0, int j0,
+                                      double& red_a, double& red_b, double& red_c) {
+  using C = TC<Z>;
+  constexpr int LX = C::LX, BL = C::BL, NTAP = C::NTAP, KEEP = C::KEEP;
+  constexpr bool kFwd = (MODE != MODE_AT);
+  constexpr bool kAdj = (MODE != MODE_A);
+  const int kbeg = grp * T.vpg;
+  const int kend = min(G.n_views, kbeg + T.vpg);
+  const float lam1 = G.lambda1, lam2 = G.lambda2, ith = G.inv_theta;
+  const float* taps = G.taps;
+  const int j = j0 + lane;
+  const bool col_ok = lane < LX && j < G.w;
+  for (int k = kbeg + warp; k < kend; k += NW) {
+    const float drho = V.off[k].x, dtau = V.off[k].y;
+    float fr[NTAP], br[NTAP];
+#pragma unroll
+    for (int u = 0; u < NTAP; ++u) { fr[u] = 0.f; br[u] = 0.f; }
+    if (kFwd) {
+#pragma unroll
+      for (int u = 0; u < KEEP; ++u) fr[u] = t.fwd_row(u, lane, drho, dtau, taps);
+    }
+    const size_t lrow0 = ((size_t)k * G.h) * G.lps + j;
+    // software prefetch of the next LR row's observation and dual (WZ)
+    float y_nx = 0.f, wa_nx = 0.f;
+    if (MODE == MODE_WZ && col_ok && i0 < G.h) {
+      y_nx = io.y[lrow0 + (size_t)i0 * G.lps];
+      wa_nx = io.wA[lrow0 + (size_t)i0 * G.lps];
+    }
+    for (int li = 0; li < BL; ++li) {
+      const int i = i0 + li;
+      const bool ok = col_ok && i < G.h;
+      const size_t lg = lrow0 + (size_t)i * G.lps;
+      float y_cur = y_nx, wa_cur = wa_nx;
+      if (MODE == MODE_WZ && col_ok && li + 1 < BL && i + 1 < G.h) {
+        y_nx = io.y[lg + G.lps];
+        wa_nx = io.wA[lg + G.lps];
+      }
+      float rho = 0.f;
+      if (kFwd) {
+#pragma unroll
+        for (int u = 0; u < Z; ++u) fr[KEEP + u] = t.fwd_row(Z * li + KEEP + u, lane, drho, dtau, taps);
+        float a = 0.f;
+#pragma unroll
+        for (int u = 0; u < NTAP; ++u) a = fmaf(taps[u], fr[u], a);   // A_k x at LR pixel (i, j)
+        if (ok) {
+          if (MODE == MODE_A) {
+            io.out_lr[lg] = a;
+          } else if (MODE == MODE_NORMAL) {
+            rho = G.cA * a;
+            red_a += (double)G.cA * (double)a * (double)a;      // <p, c_A A^T A p> = c_A |A p|^2
+          } else if (MODE == MODE_WZ) {
+            const float e_ = a - y_cur;                         // e = A_k x - y_k (Alg.1 line 4)
+            const float wa = wa_cur;
+            const float u = lam1 * e_ + wa;                     // u = F x - b' + w (line 5)
+            const float wn = fminf(fmaxf(u, -ith), ith);        // w+ = u - prox(u) = clamp (A5/A6)
+            const float f = 2.f * wn - wa;                      // f = 2w^n - w^{n-1} (line 8)
+            rho = lam2 * e_ + G.cS * lam1 * f;                  // A^T a + (th/2) F^T f, data rows
+            io.wA[lg] = wn;
+            red_a += fabs((double)e_);
+            red_b += (double)e_ * e_;
+            red_c += (double)(wn - wa) * (wn - wa);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < KEEP; ++u) fr[u] = fr[u + Z];
+      } else {
+        rho = ok ? io.in_lr[lg] : 0.f;
+      }
+      if (kAdj) {
+#pragma unroll
+        for (int u = 0; u < NTAP; ++u) br[u] = fmaf(taps[u], rho, br[u]);  // vertical adjoint (polyphase)
+#pragma unroll
+        for (int u = 0; u < Z; ++u) t.adj_row(Z * li + u, lane, br[u], drho, dtau, taps);
+#pragma unroll
+        for (int u = 0; u < NTAP; ++u) br[u] = (u < KEEP) ? br[u + Z] : 0.f;
+      }
+    }
+    if (kAdj) {
+#pragma unroll
+      for (int u = 0; u < KEEP; ++u) t.adj_row(Z * BL + u, lane, br[u], drho, dtau, taps);
+    }
+  }
+}
+
 template <int Z, int MODE>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(384)
 k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
-  using C = TileC<Z>;
-  constexpr int R = C::R, LY = C::LY, LX = C::LX, TY = C::TY, TX = C::TX;
-  constexpr int EY = C::EY, EX = C::EX, E = C::E, MAXP = C::MAXP;
+  using C = TC<Z>;
+  constexpr int R = C::R, LX = C::LX, BL = C::BL, TY = C::TY, TX = C::TX;
+  constexpr int EY = C::EY, ECOL = C::ECOL, NTAP = C::NTAP, KEEP = C::KEEP;
   constexpr bool kFwd = (MODE != MODE_AT);
   constexpr bool kAdj = (MODE != MODE_A);
 
   extern __shared__ __align__(16) float smem[];
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int NT = blockDim.x, NW = NT >> 5;
   const int ntiles = T.ntY * T.ntX;
   const int tile = blockIdx.x % ntiles;
   const int grp = blockIdx.x / ntiles;
   const int ti = tile / T.ntX, tj = tile % T.ntX;
-  const int i0 = ti * LY, j0 = tj * LX;     // LR origin
-  const int Y0 = i0 * Z, X0 = j0 * Z;       // HR origin of the own tile
-  const int PY0 = Y0 - T.HY, PX0 = X0 - T.HX;  // p-tile origin
-  const int PH = T.PH, PW = T.PW;
+  const int i0 = ti * BL, j0 = tj * LX;          // LR origin of the tile
+  const int Y0 = i0 * Z, X0 = j0 * Z;             // HR origin of the own pixels
+  const int YE0 = Y0 - R, XE0 = X0 - R;           // E-region origin
+  const int PY0 = YE0 - T.SYe - 1, PX0 = XE0 - T.SXe - 1;  // input-tile origin (+1 spare, see axis())
+  const int PH = T.PH, PW = T.PW, PWn = ECOL + 2 * T.SXe + 2;
   const int H = G.H, W = G.W, ps = G.ps;
-
   Control* ctl = io.ctl;
   if (MODE == MODE_NORMAL && io.cg_k >= 2 && ctl->cur[S_STOP] != 0.0) return;  // CG stopped
 
-  float* P = smem;                  // PH*PW   input tile
-  float* ACC = P + PH * PW;         // PH*PW   adjoint accumulator
-  float* WP = ACC + PH * PW;        // E       warped input on the E region
-  float* T1 = WP + E;               // EY*LX   forward horizontal blur
-  float* T1b = T1 + EY * LX;        // EY*LX   adjoint vertical blur
-  float* RHO = T1b + EY * LX;       // LY*LX   LR residual / weights
-  float* MT = RHO + LY * LX;        // MH*MW   m tile (NORMAL with NLTV)
-  // reduction scratch: first 8-byte aligned slot after MT
-  const size_t red_off = ((size_t)(MT - smem) + (size_t)T.MH * T.MW + 1) & ~(size_t)1;
+  float* P = smem;                                           // PH*PW  input tile (phase split)
+  int* ACC = reinterpret_cast<int*>(P + PH * PW);            // 2*PH*PW fixed-point accumulator (hi, lo)
+  const int LO = PH * PW;
+  float* OM = P + 3 * PH * PW;                               // EY*ECOL disparity on the E region
+  float* M = OM + EY * ECOL;                                 // MH*MW  weight map, own + radius
+  float* NL = OM;                                            // TY*TX  NLTV term (aliases OM after the views)
+  const size_t red_off = ((size_t)(M - smem) + (size_t)T.MH * T.MW + 1) & ~(size_t)1;
   double* RED = reinterpret_cast<double*>(smem + red_off);
+  __shared__ float s_max;
+  __shared__ float s_scale[2];
 
-  // ---- tile load (and CG direction update) --------------------------------
+  const int PWZ = T.PWZ;
+
+  // ---- phase 1: input tile (+ CG direction update), disparity, m -----------
   double pi0_part = 0.0;
-  float beta = 0.f;
+  float beta = 0.f, pmax = 0.f;
   if (MODE == MODE_NORMAL && io.cg_k >= 2) {
     double pim1 = ctl->cur[S_PI + io.cg_k - 1], pim2 = ctl->cur[S_PI + io.cg_k - 2];
     beta = (float)(pim1 / pim2);    // Alg.2 line 10 (reading A2): p_k = r_k + beta p_{k-1}
   }
-  for (int e = tid; e < PH * PW; e += kThreads) {
-    int py = e / PW, px = e - py * PW;
-    int gy = PY0 + py, gx = PX0 + px;
+  if (tid == 0) s_max = 0.f;
+  for (int e = tid; e < PH * PWn; e += NT) {
+    const int py = e / PWn, px = e - py * PWn;
+    const int gy = PY0 + py, gx = PX0 + px;
+    // replicate padding outside the image (see Tile::sample)
+    const int cy = min(max(gy, 0), H - 1), cx = min(max(gx, 0), W - 1);
     float v = 0.f;
-    if (kFwd && gy >= 0 && gy < H && gx >= 0 && gx < W) {
-      size_t gi = (size_t)gy * ps + gx;
+    if (kFwd) {
+      const size_t gi = (size_t)cy * ps + cx;
       v = io.in_hr[gi];
       if (MODE == MODE_NORMAL && io.cg_k >= 1) {
-        bool own = gy >= Y0 && gy < Y0 + TY && gx >= X0 && gx < X0 + TX;
+        const bool own = gy == cy && gx == cx && gy >= Y0 && gy < Y0 + TY && gx >= X0 && gx < X0 + TX;
         if (io.cg_k == 1) {
           if (own && grp == 0) pi0_part += (double)v * v;   // pi_0 = <r_0, r_0> (Alg.2 line 3)
         } else {
@@ -122,248 +469,159 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
         if (own && grp == 0) io.p_out[gi] = v;
       }
     }
-    if (kFwd) P[e] = v;
-    if (kAdj) ACC[e] = 0.f;
+    pmax = fmaxf(pmax, fabsf(v));
+    const int i = pidx<Z>(py, px, PW, PWZ);
+    if (kFwd) P[i] = v;
+    if (kAdj) { ACC[i] = 0; ACC[LO + i] = 0; }
   }
-  // m tile for the NLTV normal term (own + radius halo)
-  const int rr = G.radius;
-  if (MODE == MODE_NORMAL && io.do_nltv && grp == 0) {
-    for (int e = tid; e < T.MH * T.MW; e += kThreads) {
-      int my = e / T.MW, mx = e - my * T.MW;
-      int gy = Y0 - rr + my, gx = X0 - rr + mx;
-      MT[e] = (gy >= 0 && gy < H && gx >= 0 && gx < W) ? io.m[(size_t)gy * ps + gx] : 0.f;
+  if (kAdj && PW > PWn) {  // phase-split padding cells of the accumulator
+    for (int e = tid; e < PH * (PW - PWn); e += NT) {
+      const int py = e / (PW - PWn), px = PWn + e - py * (PW - PWn);
+      const int i = pidx<Z>(py, px, PW, PWZ);
+      ACC[i] = 0;
+      ACC[LO + i] = 0;
     }
   }
-  // disparity on the E region, kept in registers for all views
-  float om[MAXP];
+  for (int e = tid; e < EY * ECOL; e += NT) {
+    const int er = e / ECOL, c = e - er * ECOL;
+    const int Y = YE0 + er, X = XE0 + c;
+    OM[e] = (Y >= 0 && Y < H && X >= 0 && X < W) ? io.omega[(size_t)Y * ps + X] : 0.f;
+  }
+  const int rr = G.radius, MW = T.MW;
+  if (MODE == MODE_NORMAL && io.do_nltv) {
+    for (int e = tid; e < T.MH * MW; e += NT) {
+      const int my = e / MW, mx = e - my * MW;
+      const int gy = Y0 - rr + my, gx = X0 - rr + mx;
+      M[e] = (gy >= 0 && gy < H && gx >= 0 && gx < W) ? io.m[(size_t)gy * ps + gx] : 0.f;
+    }
+  }
+  // block max of |input| -> fixed-point scale
 #pragma unroll
-  for (int s = 0; s < MAXP; ++s) {
-    int e = tid + s * kThreads;
-    om[s] = 0.f;
-    if (e < E) {
-      int er = e / EX, ec = e - er * EX;
-      int Y = Y0 - R + er, X = X0 - R + ec;
-      if (Y >= 0 && Y < H && X >= 0 && X < W) om[s] = io.omega[(size_t)Y * ps + X];
-    }
-  }
+  for (int o = 16; o > 0; o >>= 1) pmax = fmaxf(pmax, __shfl_xor_sync(0xffffffffu, pmax, o));
   __syncthreads();
-
-  // ---- per-view observation operator (forward + adjoint) -------------------
-  double red_a = 0.0, red_b = 0.0, red_c = 0.0;  // WZ: l1, l2, res2 ; NORMAL: pq
-  const int kbeg = grp * T.vpg;
-  const int kend = min(G.n_views, kbeg + T.vpg);
-  const float lam1 = G.lambda1, lam2 = G.lambda2, ith = G.inv_theta;
-  for (int k = kbeg; k < kend; ++k) {
-    const float drho = V.off[k].x, dtau = V.off[k].y;
-    int cidx[MAXP];
-    float ca[MAXP], cb[MAXP];
-    // P1: W_k (bilinear gather, replicate-clamped coordinate)
-#pragma unroll
-    for (int s = 0; s < MAXP; ++s) {
-      int e = tid + s * kThreads;
-      cidx[s] = -1;
-      ca[s] = 0.f;
-      cb[s] = 0.f;
-      if (e < E) {
-        int er = e / EX, ec = e - er * EX;
-        int Y = Y0 - R + er, X = X0 - R + ec;
-        float wp = 0.f;
-        if (Y >= 0 && Y < H && X >= 0 && X < W) {
-          float sy = fminf(fmaxf((float)Y + dtau * om[s], 0.f), (float)(H - 1));
-          float sx = fminf(fmaxf((float)X + drho * om[s], 0.f), (float)(W - 1));
-          float fy = floorf(sy), fx = floorf(sx);
-          float a = sy - fy, b = sx - fx;
-          int idx = ((int)fy - PY0) * PW + ((int)fx - PX0);
-          cidx[s] = idx;
-          ca[s] = a;
-          cb[s] = b;
-          if (kFwd) {
-            float p00 = P[idx], p01 = P[idx + 1], p10 = P[idx + PW], p11 = P[idx + PW + 1];
-            wp = (1.f - a) * ((1.f - b) * p00 + b * p01) + a * ((1.f - b) * p10 + b * p11);
-          }
-        }
-        if (kFwd) WP[e] = wp;
-      }
+  if (lane == 0 && pmax > 0.f) atomicMax(reinterpret_cast<unsigned*>(&s_max), __float_as_uint(pmax));
+  __syncthreads();
+  if (tid == 0) {
+    float tb = 0.f;
+    if (MODE == MODE_NORMAL) tb = G.cA * s_max;
+    if (MODE == MODE_WZ) tb = G.lambda2 * (s_max + G.ymax) + G.cS * G.lambda1 * 3.f * G.inv_theta;
+    if (MODE == MODE_AT) tb = io.tmax_in;
+    tb *= G.gpoly2;   // the polyphase adjoint blur shrinks max|rho|
+    float sc = 0.f, isc = 0.f;
+    if (tb > 0.f && isfinite(tb)) {
+      int e1, e2;
+      frexpf(tb, &e1);
+      frexpf(tb * fmaxf(G.dmax, 1.f) * 1.02f, &e2);
+      const int s = min(21 - e1, 30 - e2);
+      sc = ldexpf(1.f, s);
+      isc = ldexpf(1.f, -s);
     }
-    __syncthreads();
-    if (kFwd) {
-      // P2: horizontal blur at LR columns
-      for (int e = tid; e < EY * LX; e += kThreads) {
-        int er = e / LX, lj = e - er * LX;
-        const float* row = WP + er * EX + Z * lj;
-        float s = 0.f;
-#pragma unroll
-        for (int v = 0; v <= 2 * R; ++v) s += G.taps[v] * row[v];
-        T1[e] = s;
-      }
-      __syncthreads();
-      // P3: vertical blur at LR rows -> A_k x ; per-pixel epilogue
-      for (int l = tid; l < LY * LX; l += kThreads) {
-        int li = l / LX, lj = l - li * LX;
-        int i = i0 + li, j = j0 + lj;
-        float a = 0.f;
-#pragma unroll
-        for (int u = 0; u <= 2 * R; ++u) a += G.taps[u] * T1[(Z * li + u) * LX + lj];
-        float rho = 0.f;
-        if (i < G.h && j < G.w) {
-          size_t li_g = ((size_t)k * G.h + i) * G.lps + j;
-          if (MODE == MODE_A) {
-            io.out_lr[li_g] = a;
-          } else if (MODE == MODE_NORMAL) {
-            rho = G.cA * a;
-            red_a += (double)G.cA * (double)a * (double)a;   // <p, c_A A^T A p> = c_A |A p|^2
-          } else if (MODE == MODE_WZ) {
-            float e_ = a - io.y[li_g];                        // e = A_k x - y_k (Alg.1 line 4)
-            float wa = io.wA[li_g];
-            float u = lam1 * e_ + wa;                          // u = F x - b' + w (line 5)
-            float wn = fminf(fmaxf(u, -ith), ith);             // w+ = u - prox(u) = clamp (A5/A6)
-            float f = 2.f * wn - wa;                           // f = 2w^n - w^{n-1} (line 8)
-            rho = lam2 * e_ + G.cS * lam1 * f;                 // A^T a + (th/2) F^T f, data rows
-            io.wA[li_g] = wn;
-            red_a += fabs((double)e_);
-            red_b += (double)e_ * e_;
-            red_c += (double)(wn - wa) * (wn - wa);
-          }
-        }
-        RHO[l] = rho;
-      }
-      __syncthreads();
-    } else {
-      for (int l = tid; l < LY * LX; l += kThreads) {
-        int li = l / LX, lj = l - li * LX;
-        int i = i0 + li, j = j0 + lj;
-        RHO[l] = (i < G.h && j < G.w) ? io.in_lr[((size_t)k * G.h + i) * G.lps + j] : 0.f;
-      }
-      __syncthreads();
-    }
-    if (kAdj) {
-      // P4: vertical adjoint blur (polyphase: only the LR rows within R)
-      for (int e = tid; e < EY * LX; e += kThreads) {
-        int er = e / LX, lj = e - er * LX;
-        int lo = er - 2 * R;
-        int li_lo = lo <= 0 ? 0 : (lo + Z - 1) / Z;
-        int li_hi = min(LY - 1, er / Z);
-        float s = 0.f;
-        for (int li = li_lo; li <= li_hi; ++li) s += G.taps[er - Z * li] * RHO[li * LX + lj];
-        T1b[e] = s;
-      }
-      __syncthreads();
-      // P5: horizontal adjoint blur + exact bilinear scatter (W_k^T)
-#pragma unroll
-      for (int s = 0; s < MAXP; ++s) {
-        int e = tid + s * kThreads;
-        if (e < E && cidx[s] >= 0) {
-          int er = e / EX, ec = e - er * EX;
-          int lo = ec - 2 * R;
-          int lj_lo = lo <= 0 ? 0 : (lo + Z - 1) / Z;
-          int lj_hi = min(LX - 1, ec / Z);
-          float t = 0.f;
-          for (int lj = lj_lo; lj <= lj_hi; ++lj) t += G.taps[ec - Z * lj] * T1b[er * LX + lj];
-          if (t != 0.f) {
-            float a = ca[s], b = cb[s];
-            int idx = cidx[s];
-            atomicAdd(&ACC[idx], (1.f - a) * (1.f - b) * t);
-            atomicAdd(&ACC[idx + 1], (1.f - a) * b * t);
-            atomicAdd(&ACC[idx + PW], a * (1.f - b) * t);
-            atomicAdd(&ACC[idx + PW + 1], a * b * t);
-          }
-        }
-      }
-      // no barrier: the next view's P1 writes WP only; T1b/RHO are rewritten
-      // after three more barriers.
-    }
+    s_scale[0] = sc;
+    s_scale[1] = isc;
   }
-
-  // ---- NLTV part (group 0) ---------------------------------------------------
-  double red_reg = 0.0;
-  if ((MODE == MODE_WZ || (MODE == MODE_NORMAL && io.do_nltv)) && grp == 0) {
-    if (MODE == MODE_NORMAL) __syncthreads();  // MT visible (loaded before the view loop)
-    const int sd = G.s_d;
-    for (int e = tid; e < TY * TX; e += kThreads) {
-      int oy = e / TX, ox = e - oy * TX;
-      int Y = Y0 + oy, X = X0 + ox;
-      if (Y >= H || X >= W) continue;
-      const int pz = (Y - PY0) * PW + (X - PX0);
-      const float xz = P[pz];
-      if (MODE == MODE_WZ) {
-        // m = lambda_R w_o exp(-|grad x|^2 / sigma_e), central differences, replicate
-        // border (readings A8/A17/A19), recomputed from x^{n-1}
-        float mz;
-        size_t gi = (size_t)Y * ps + X;
+  if (MODE == MODE_WZ) {  // m over own + radius from x (A8/A17/A19)
+    __syncthreads();      // P complete
+    for (int e = tid; e < T.MH * MW; e += NT) {
+      const int my = e / MW, mx = e - my * MW;
+      const int gy = Y0 - rr + my, gx = X0 - rr + mx;
+      float mz = 0.f;
+      if (gy >= 0 && gy < H && gx >= 0 && gx < W) {
+        const size_t gi = (size_t)gy * ps + gx;
         if (io.reweight) {
-          float xr = P[(Y - PY0) * PW + (min(X + 1, W - 1) - PX0)];
-          float xl = P[(Y - PY0) * PW + (max(X - 1, 0) - PX0)];
-          float xd = P[(min(Y + 1, H - 1) - PY0) * PW + (X - PX0)];
-          float xu = P[(max(Y - 1, 0) - PY0) * PW + (X - PX0)];
-          float gx = 0.5f * (xr - xl), gy = 0.5f * (xd - xu);
-          mz = G.lambda_reg * io.wo[gi] * expf(-(gx * gx + gy * gy) * G.inv_sigma_e);
-          if (grp == 0) io.m[gi] = mz;
+          const int py = gy - PY0, px = gx - PX0;
+          const float xr = P[pidx<Z>(py, min(gx + 1, W - 1) - PX0, PW, PWZ)], xl = P[pidx<Z>(py, max(gx - 1, 0) - PX0, PW, PWZ)];
+          const float xd = P[pidx<Z>(min(gy + 1, H - 1) - PY0, px, PW, PWZ)], xu = P[pidx<Z>(max(gy - 1, 0) - PY0, px, PW, PWZ)];
+          const float gxv = 0.5f * (xr - xl), gyv = 0.5f * (xd - xu);
+          mz = G.lambda_reg * io.wo[gi] * expf(-(gxv * gxv + gyv * gyv) * G.inv_sigma_e);
+          const bool own = gy >= Y0 && gy < Y0 + TY && gx >= X0 && gx < X0 + TX;
+          if (own && grp == 0) io.m[gi] = mz;
         } else {
           mz = io.m[gi];
         }
-        float vown = 0.f;
-        for (int d = 0; d < sd; ++d) {
-          const int dy = G.ody[d], dx = G.odx[d];
-          const bool in = (Y + dy >= 0) && (Y + dy < H) && (X + dx >= 0) && (X + dx < W);
-          const float Wd = G.wd[d] * mz;
-          float g = 0.f;
-          if (in) g = Wd * (xz - P[pz + dy * PW + dx]);       // W_d (.) Delta_d x
-          float* wsp = io.wS + (size_t)d * H * ps + gi;
-          float wso = *wsp;
-          float u = g + wso;                                    // u = F x - b' + w, NLTV rows
-          float wn = fminf(fmaxf(u, -ith), ith);                // clamp form of z/w steps
-          float f = 2.f * wn - wso;
-          *wsp = wn;
-          red_reg += fabs((double)g);
-          red_c += (double)(wn - wso) * (wn - wso);
-          if (in) {                                             // (th/2) Delta_d^T (W_d f_d)
-            float hcon = G.cS * Wd * f;
-            vown += hcon;
-            atomicAdd(&ACC[pz + dy * PW + dx], -hcon);
-          }
-        }
-        atomicAdd(&ACC[pz], vown);
-      } else {
-        // (th/2) sum_d Delta_d^T (W_d^2 Delta_d p) in gather form, using the m tile
-        const int MW = T.MW;
-        const int mzi = (oy + rr) * MW + (ox + rr);
-        const float mz = MT[mzi];
-        float qs = 0.f, pq = 0.f;
-        for (int d = 0; d < sd; ++d) {
-          const int dy = G.ody[d], dx = G.odx[d];
-          const float wd = G.wd[d];
-          if ((Y + dy >= 0) && (Y + dy < H) && (X + dx >= 0) && (X + dx < W)) {
-            float dp = xz - P[pz + dy * PW + dx];
-            float w2 = (wd * mz) * (wd * mz);
-            qs += w2 * dp;
-            pq += w2 * dp * dp;
-          }
-          if ((Y - dy >= 0) && (Y - dy < H) && (X - dx >= 0) && (X - dx < W)) {
-            float dpb = P[pz - dy * PW - dx] - xz;
-            float mb = wd * MT[mzi - dy * MW - dx];
-            qs -= mb * mb * dpb;
-          }
-        }
-        atomicAdd(&ACC[pz], G.cS * qs);
-        red_b += (double)G.cS * pq;
       }
+      M[e] = mz;
+    }
+  }
+  __syncthreads();
+
+  // ---- phase 2: views (no barriers) ----------------------------------------
+  double red_a = 0.0, red_b = 0.0, red_c = 0.0;
+  {
+    // columns of this lane's E positions that are real image columns
+    unsigned colmask = 0;
+#pragma unroll
+    for (int s2 = 0; s2 < Z; ++s2) {
+      const int c = Z * lane + s2, X = XE0 + c;
+      if (c < C::EXv && X >= 0 && X < W) colmask |= 1u << s2;
+    }
+    // interior tile: every E position is inside the image (no masks needed)
+    const bool interior = (YE0 >= 0) && (YE0 + EY <= H) && (XE0 >= 0) && (XE0 + C::EXv <= W);
+    if (interior) {
+      Tile<Z, true> t{P, ACC, OM, PW, PWZ, PY0, PX0, YE0, XE0, H, W, colmask, s_scale[0], LO};
+      views<Z, MODE, true>(t, G, V, T, io, grp, lane, warp, NW, i0, j0, red_a, red_b, red_c);
+    } else {
+      Tile<Z, false> t{P, ACC, OM, PW, PWZ, PY0, PX0, YE0, XE0, H, W, colmask, s_scale[0], LO};
+      views<Z, MODE, false>(t, G, V, T, io, grp, lane, warp, NW, i0, j0, red_a, red_b, red_c);
     }
   }
   if (MODE == MODE_A) return;
-  __syncthreads();
+  __syncthreads();   // views done: ACC complete, OM free (NL aliases it)
 
-  // ---- flush the accumulator (tile + halo) with RED.ADD --------------------
-  if (kAdj) {
-    const float sign = (MODE == MODE_WZ) ? -1.f : 1.f;   // WZ writes r = -v (reading A3)
-    for (int e = tid; e < PH * PW; e += kThreads) {
-      float v = ACC[e];
-      if (v == 0.f) continue;
-      int py = e / PW, px = e - py * PW;
-      int gy = PY0 + py, gx = PX0 + px;
-      if (gy >= 0 && gy < H && gx >= 0 && gx < W) atomicAdd(&io.out_hr[(size_t)gy * ps + gx], sign * v);
+  // ---- phase 3: NLTV term of the own pixels; view group g takes own rows g, g+G, ...
+  double red_reg = 0.0;
+  const int ng = T.groups;
+  const bool nltv = (MODE == MODE_WZ) || (MODE == MODE_NORMAL && io.do_nltv);
+  if (nltv) {
+    NltvCtx c;
+    c.P = P; c.M = M; c.PW = PW; c.PWZ = PWZ; c.MW = MW; c.H = H; c.W = W; c.ps = ps;
+    c.ith = G.inv_theta;
+    const int rd = ctl->iter & 1;
+    c.wSr = rd ? io.wS1 : io.wS0;
+    c.wSw = rd ? io.wS0 : io.wS1;
+    c.plane = (size_t)H * ps;
+    const int my_rows = TY > grp ? (TY - grp + ng - 1) / ng : 0;
+    for (int e = tid; e < my_rows * TX; e += NT) {
+      const int oy = grp + ng * (e / TX), ox = e % TX;
+      const int Y = Y0 + oy, X = X0 + ox;
+      float acc = 0.f;
+      if (Y < H && X < W) {
+        const int py = Y - PY0, px = X - PX0;
+        const int mi = (oy + rr) * MW + (ox + rr);
+        const size_t gi = (size_t)Y * ps + X;
+        double pq = 0.0;
+        const bool inner = Y >= rr && Y < H - rr && X >= rr && X < W - rr;
+        if (rr == 2) {
+          acc = inner ? nltv_pixel<Z, MODE, false, 2>(c, G, Y, X, py, px, mi, gi, pq, red_reg, red_c)
+                      : nltv_pixel<Z, MODE, true, 2>(c, G, Y, X, py, px, mi, gi, pq, red_reg, red_c);
+        } else {
+          acc = nltv_pixel<Z, MODE, true, 0>(c, G, Y, X, py, px, mi, gi, pq, red_reg, red_c);
+        }
+        acc *= G.cS;
+        red_b += (double)G.cS * pq;
+      }
+      NL[oy * TX + ox] = acc;
     }
   }
-  // ---- reductions --------------------------------------------------------------
+  __syncthreads();
+
+  // ---- phase 4: flush accumulator + NLTV (tile + halo) with RED.ADD ----------
+  {
+    const float isc = s_scale[1];
+    const float sign = (MODE == MODE_WZ) ? -1.f : 1.f;   // WZ writes r = -v (reading A3)
+    for (int e = tid; e < PH * PWn; e += NT) {
+      const int py = e / PWn, px = e - py * PWn;
+      const int gy = PY0 + py, gx = PX0 + px;
+      const int ia = pidx<Z>(py, px, PW, PWZ);
+      float v = fmaf((float)ACC[LO + ia], 1.f / (float)(1 << kLoBits), (float)ACC[ia]) * isc;
+      const int oy = gy - Y0, ox = gx - X0;
+      if (nltv && gy < H && gx < W && oy >= 0 && oy < TY && ox >= 0 && ox < TX && (oy % ng) == grp)
+        v += NL[oy * TX + ox];
+      // padding cells fold onto their replicate source (transpose of the padding)
+      const int cy = min(max(gy, 0), H - 1), cx = min(max(gx, 0), W - 1);
+      if (v != 0.f) atomicAdd(&io.out_hr[(size_t)cy * ps + cx], sign * v);
+    }
+  }
+  // ---- reductions ----------------------------------------------------------------
   if (MODE == MODE_WZ) {
     double v[4] = {red_a, red_b, red_reg, red_c};
     const int slot[4] = {S_L1, S_L2, S_REG, S_RES2};
@@ -378,36 +636,34 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
 // --------------------------------------------------------------------------------
 // Host-side geometry and launchers
 // --------------------------------------------------------------------------------
-TileGeom make_tile_geom(const Geom& G, int num_sms) {
-  TileGeom T{};
-  int LY = 0, LX = 0, R = 0, EY = 0, EX = 0;
-  switch (G.scale) {
-    case 2: LY = TileC<2>::LY; LX = TileC<2>::LX; R = TileC<2>::R; EY = TileC<2>::EY; EX = TileC<2>::EX; break;
-    case 3: LY = TileC<3>::LY; LX = TileC<3>::LX; R = TileC<3>::R; EY = TileC<3>::EY; EX = TileC<3>::EX; break;
-    default: LY = TileC<4>::LY; LX = TileC<4>::LX; R = TileC<4>::R; EY = TileC<4>::EY; EX = TileC<4>::EX; break;
+template <int Z>
+static void fill_static(TileGeom& T) {
+  using C = TC<Z>;
+  T.BL = C::BL; T.LX = C::LX; T.TY = C::TY; T.TX = C::TX;
+  T.EY = C::EY; T.ECOL = C::ECOL; T.EXv = C::EXv;
+}
+
+static size_t smem_bytes(const TileGeom& T, int nwarps) {
+  size_t words = 3 * (size_t)T.PH * T.PW + (size_t)T.EY * T.ECOL + (size_t)T.MH * T.MW + 2;
+  return words * 4 + (size_t)nwarps * 4 * sizeof(double);
+}
+
+template <int Z, int MODE>
+static int occupancy(int threads, size_t smem) {
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_tile<Z, MODE>, threads, smem) != cudaSuccess) {
+    cudaGetLastError();
+    return 1;
   }
-  T.LY = LY; T.LX = LX; T.TY = G.scale * LY; T.TX = G.scale * LX;
-  T.EY = EY; T.EX = EX;
-  int sy = G.SY > G.radius ? G.SY : G.radius;
-  int sx = G.SX > G.radius ? G.SX : G.radius;
-  T.HY = R + sy;
-  T.HX = R + sx;
-  T.PH = EY + 2 * sy + 1;
-  T.PW = EX + 2 * sx + 1;
-  T.MH = T.TY + 2 * G.radius;
-  T.MW = T.TX + 2 * G.radius;
-  T.ntY = (G.h + LY - 1) / LY;
-  T.ntX = (G.w + LX - 1) / LX;
-  int tiles = T.ntY * T.ntX;
-  int groups = (2 * num_sms + tiles - 1) / tiles;
-  if (groups > G.n_views) groups = G.n_views;
-  if (groups < 1) groups = 1;
-  T.vpg = (G.n_views + groups - 1) / groups;
-  T.groups = (G.n_views + T.vpg - 1) / T.vpg;
-  size_t floats = 2 * (size_t)T.PH * T.PW + (size_t)EY * EX + 2 * (size_t)EY * LX + (size_t)LY * LX +
-                  (size_t)T.MH * T.MW + 2;  // +2: 8-byte alignment of the reduction scratch
-  T.smem = floats * sizeof(float) + (kThreads / 32) * 4 * sizeof(double);
-  return T;
+  return n > 0 ? n : 1;
+}
+
+static int occupancy_for(int scale, int threads, size_t smem) {
+  switch (scale) {
+    case 2: return occupancy<2, MODE_NORMAL>(threads, smem);
+    case 3: return occupancy<3, MODE_NORMAL>(threads, smem);
+    default: return occupancy<4, MODE_NORMAL>(threads, smem);
+  }
 }
 
 template <int Z, int MODE>
@@ -429,22 +685,67 @@ cudaError_t prepare_tile_kernels(int scale, size_t smem) {
   return e;
 }
 
+// Views per warp and warps per CTA: every warp of a group gets the same number of
+// views (or one less); view groups are added until the grid fills the GPU.
+TileGeom make_tile_geom(const Geom& G, int num_sms) {
+  TileGeom T{};
+  switch (G.scale) {
+    case 2: fill_static<2>(T); break;
+    case 3: fill_static<3>(T); break;
+    default: fill_static<4>(T); break;
+  }
+  T.SYe = G.SY > G.radius ? G.SY : G.radius;
+  T.SXe = G.SX > G.radius ? G.SX : G.radius;
+  T.PH = T.EY + 2 * T.SYe + 2;          // +1 spare row each side (axis() at exact integers)
+  const int PWn = T.ECOL + 2 * T.SXe + 2;
+  T.PWZ = (PWn + G.scale - 1) / G.scale;
+  T.PW = T.PWZ * G.scale;
+  T.MH = T.TY + 2 * G.radius;
+  T.MW = T.TX + 2 * G.radius;
+  T.ntY = (G.h + T.BL - 1) / T.BL;
+  T.ntX = (G.w + T.LX - 1) / T.LX;
+  const int tiles = T.ntY * T.ntX;
+  const int max_warps = 12;
+  T.smem = smem_bytes(T, max_warps);
+  if (prepare_tile_kernels(G.scale, T.smem) != cudaSuccess) cudaGetLastError();
+  int best_g = 1, best_w = 1;
+  double best = 1e30;
+  for (int g = 1; g <= G.n_views; ++g) {
+    const int vpg = (G.n_views + g - 1) / g;
+    if ((G.n_views + vpg - 1) / vpg != g) continue;
+    int nw = vpg < 6 ? vpg : 0, bestw = 1 << 30;
+    if (!nw) {
+      for (int w = 6; w <= max_warps; ++w) {
+        const int waste = ((vpg + w - 1) / w) * w - vpg;
+        if (waste < bestw) { bestw = waste; nw = w; }
+      }
+    }
+    const int occ = occupancy_for(G.scale, nw * 32, smem_bytes(T, nw));
+    const double waves = (double)tiles * g / ((double)num_sms * occ);
+    double cost = std::ceil(waves) * ((vpg + nw - 1) / nw) * (1.0 + 0.02 * g);  // flush cost grows with g
+    if (waves < 0.9) cost *= 1.0 + (0.9 - waves);
+    if (cost < best) { best = cost; best_g = g; best_w = nw; }
+  }
+  T.nwarps = best_w;
+  T.vpg = (G.n_views + best_g - 1) / best_g;
+  T.groups = (G.n_views + T.vpg - 1) / T.vpg;
+  T.smem = smem_bytes(T, T.nwarps);
+  return T;
+}
+
 template <int Z, int MODE>
-static cudaError_t launch_z(const Geom& G, const Views& V, const TileGeom& T, const TileIO& io,
-                            cudaStream_t st, int groups) {
-  auto kern = k_tile<Z, MODE>;
-  dim3 grid(T.ntY * T.ntX * groups);
-  kern<<<grid, kThreads, T.smem, st>>>(G, V, T, io);
+static cudaError_t launch_z(const Geom& G, const Views& V, const TileGeom& T, const TileIO& io, cudaStream_t st) {
+  dim3 grid(T.ntY * T.ntX * T.groups);
+  k_tile<Z, MODE><<<grid, T.nwarps * 32, T.smem, st>>>(G, V, T, io);
   return cudaGetLastError();
 }
 
 template <int MODE>
-static cudaError_t launch_mode(const Geom& G, const Views& V, const TileGeom& T, const TileIO& io,
-                               cudaStream_t st, int groups) {
+static cudaError_t launch_mode(const Geom& G, const Views& V, const TileGeom& T, const TileIO& io, cudaStream_t st) {
   switch (G.scale) {
-    case 2: return launch_z<2, MODE>(G, V, T, io, st, groups);
-    case 3: return launch_z<3, MODE>(G, V, T, io, st, groups);
-    case 4: return launch_z<4, MODE>(G, V, T, io, st, groups);
+    case 2: return launch_z<2, MODE>(G, V, T, io, st);
+    case 3: return launch_z<3, MODE>(G, V, T, io, st);
+    case 4: return launch_z<4, MODE>(G, V, T, io, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -452,10 +753,10 @@ static cudaError_t launch_mode(const Geom& G, const Views& V, const TileGeom& T,
 cudaError_t launch_tile(int mode, const Geom& G, const Views& V, const TileGeom& T, const TileIO& io,
                         cudaStream_t st) {
   switch (mode) {
-    case MODE_WZ: return launch_mode<MODE_WZ>(G, V, T, io, st, T.groups);
-    case MODE_NORMAL: return launch_mode<MODE_NORMAL>(G, V, T, io, st, T.groups);
-    case MODE_A: return launch_mode<MODE_A>(G, V, T, io, st, T.groups);
-    case MODE_AT: return launch_mode<MODE_AT>(G, V, T, io, st, T.groups);
+    case MODE_WZ: return launch_mode<MODE_WZ>(G, V, T, io, st);
+    case MODE_NORMAL: return launch_mode<MODE_NORMAL>(G, V, T, io, st);
+    case MODE_A: return launch_mode<MODE_A>(G, V, T, io, st);
+    case MODE_AT: return launch_mode<MODE_AT>(G, V, T, io, st);
   }
   return cudaErrorInvalidValue;
 }
