@@ -13,7 +13,9 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-LIB = os.path.join(HERE, "liblfsr.so")
+LIB = os.path.join(HERE, os.environ.get("LFSR_LIB_NAME", "liblfsr.so"))
+# development only: extra -D flags for A/B variants of the kernels (empty for the product build)
+VARIANT = os.environ.get("LFSR_VARIANT_DEFS", "").split()
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
@@ -38,8 +40,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     objs = []
     for src in sources():
-        obj = os.path.join(CSRC, os.path.basename(src)[:-3] + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
+        obj = os.path.join(CSRC, os.path.basename(src)[:-3] + ".%d.o" % os.getpid())
+        cmd = [NVCC, *ARCH, *FLAGS, *VARIANT, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
         if verbose:
             cmd += ["-Xptxas", "-v"]
             print(" ".join(cmd), file=sys.stderr)

@@ -83,7 +83,8 @@ struct TileGeom {
   int32_t groups;             // view groups (CTAs per tile)
   int32_t vpg;                // views per group
   int32_t nwarps;             // warps per CTA (views of a group are dealt round-robin)
-  size_t smem;                // dynamic shared memory bytes
+  size_t smem;                // dynamic shared memory bytes (largest mode)
+  size_t smem_normal;         // ... of the NORMAL mode
 };
 
 // Pointers of one tile-kernel launch (see tile_kernels.cu).

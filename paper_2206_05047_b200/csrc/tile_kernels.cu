@@ -28,6 +28,20 @@
 #include <cfloat>
 #include <cmath>
 
+#ifndef LFSR_MAXW
+#define LFSR_MAXW 12          // max warps per CTA
+#endif
+#ifndef LFSR_MINB
+#define LFSR_MINB 1           // min CTAs per SM requested from ptxas
+#endif
+#ifndef LFSR_CRING
+#define LFSR_CRING 0          // 1: the forward pass stores each sample's cells/fractions in a per-warp
+                              //    shared ring, the adjoint pass reloads them instead of recomputing
+#endif
+#ifndef LFSR_SMEM_DIET
+#define LFSR_SMEM_DIET 0      // 1: disparity and (NORMAL) weights read through L1 instead of shared tiles
+#endif
+
 namespace lfsr {
 
 template <int Z> struct TileCfg;
@@ -113,6 +127,9 @@ struct Tile {
   unsigned colmask;   // bit s: the lane's E column Z*lane+s is a real column inside the image
   float tscale;
   int lo;             // offset of the residual accumulator from ACC (ints)
+  const float* omega; // global disparity (LFSR_SMEM_DIET)
+  int ps;
+  int4* CR;           // this warp's coordinate ring [NTAP][Z][32] (LFSR_CRING) or nullptr
 
   // floor and fraction without the XU pipe: round(s - 1/2) by the 1.5*2^23 magic
   // (|s| < 2^22).  At exact integers s = n this may return n - 1 with fraction 1,
@@ -149,6 +166,12 @@ struct Tile {
   }
 
   __device__ __forceinline__ void load_om(int er, int lane, float (&om)[Z]) const {
+#if LFSR_SMEM_DIET
+    const int Y = min(max(YE0 + er, 0), H - 1);
+    const float* row = omega + (size_t)Y * ps;
+#pragma unroll
+    for (int s = 0; s < Z; ++s) om[s] = __ldg(row + min(max(XE0 + Z * lane + s, 0), W - 1));
+#else
     const float* src = OM + er * TC<Z>::ECOL + Z * lane;
     if constexpr (Z == 2) {
       float2 v = *reinterpret_cast<const float2*>(src);
@@ -160,6 +183,7 @@ struct Tile {
 #pragma unroll
       for (int s = 0; s < Z; ++s) om[s] = src[s];
     }
+#endif
   }
 
   // W_k then the horizontal blur taps at this lane's LR column, for E row er.
@@ -172,6 +196,8 @@ struct Tile {
       int i00, i01;
       float a, b;
       sample(Yf, (float)(XE0 + Z * lane + s), om[s], drho, dtau, i00, i01, a, b);
+      if (LFSR_CRING && CR)
+        CR[((er % TC<Z>::NTAP) * Z + s) * 32 + lane] = make_int4(i00, i01, __float_as_int(a), __float_as_int(b));
       const float p00 = P[i00], p01 = P[i01], p10 = P[i00 + PW], p11 = P[i01 + PW];
       const float top = fmaf(b, p01 - p00, p00), bot = fmaf(b, p11 - p10, p10);
       const float v = fmaf(a, bot - top, top);
@@ -201,8 +227,10 @@ struct Tile {
       tv[j] = lane >= j ? v : 0.f;
     }
     float om[Z];
-    load_om(er, lane, om);
+    const bool ring = LFSR_CRING && CR;
+    if (!ring) load_om(er, lane, om);
     const float Yf = (float)(YE0 + er);
+    const int4* slot = ring ? CR + (er % TC<Z>::NTAP) * Z * 32 + lane : nullptr;
     int i00[Z], i01[Z];
     float v00[Z], v01[Z], v10[Z], v11[Z];
     bool adj = true;
@@ -213,7 +241,15 @@ struct Tile {
       for (int j = 0; j < NJ; ++j)
         if (Z * j + s <= 2 * TC<Z>::R) t = fmaf(taps[Z * j + s], tv[j], t);
       float a, b;
-      sample(Yf, (float)(XE0 + Z * lane + s), om[s], drho, dtau, i00[s], i01[s], a, b);
+      if (ring) {
+        const int4 cr = slot[s * 32];
+        i00[s] = cr.x;
+        i01[s] = cr.y;
+        a = __int_as_float(cr.z);
+        b = __int_as_float(cr.w);
+      } else {
+        sample(Yf, (float)(XE0 + Z * lane + s), om[s], drho, dtau, i00[s], i01[s], a, b);
+      }
       const float ts = valid(er, s) ? t * tscale : 0.f;
       const float ta = ts * a, t1a = ts - ta;
       v01[s] = t1a * b;
@@ -254,8 +290,9 @@ struct Tile {
 struct NltvCtx {
   const float* P;
   const float* M;
-  const float* wSr;
-  float* wSw;
+  const float* __restrict__ mg;   // global weight map (LFSR_SMEM_DIET, NORMAL)
+  const float* __restrict__ wSr;
+  float* __restrict__ wSw;
   size_t plane;
   int PW, PWZ, MW, H, W, ps;
   float ith;
@@ -265,7 +302,8 @@ template <int Z, int MODE, bool CHECK, int RAD>
 __device__ __forceinline__ float nltv_pixel(const NltvCtx& c, const Geom& G, int Y, int X, int py, int px, int mi,
                                             size_t gi, double& pq, double& reg, double& res) {
   const float xz = c.P[pidx<Z>(py, px, c.PW, c.PWZ)];
-  const float mz = c.M[mi];
+  constexpr bool kMg = LFSR_SMEM_DIET && MODE == MODE_NORMAL;
+  const float mz = kMg ? __ldg(c.mg + gi) : c.M[mi];
   float acc = 0.f;
   auto one = [&](int d, int dy, int dx) {
     const float wd = G.wd[d];
@@ -273,7 +311,7 @@ __device__ __forceinline__ float nltv_pixel(const NltvCtx& c, const Geom& G, int
     const bool bin = !CHECK || ((Y - dy >= 0) && (Y - dy < c.H) && (X - dx >= 0) && (X - dx < c.W));
     const float xf = c.P[pidx<Z>(py + dy, px + dx, c.PW, c.PWZ)];   // in the tile even when outside Omega
     const float xb = c.P[pidx<Z>(py - dy, px - dx, c.PW, c.PWZ)];
-    const float mb = c.M[mi - dy * c.MW - dx];
+    const float mb = kMg ? (bin ? __ldg(c.mg + gi - (size_t)dy * c.ps - dx) : 0.f) : c.M[mi - dy * c.MW - dx];
     if (MODE == MODE_NORMAL) {
       const float wz = wd * mz, wb = wd * mb;
       const float dp = xz - xf;
@@ -286,7 +324,7 @@ __device__ __forceinline__ float nltv_pixel(const NltvCtx& c, const Geom& G, int
       const size_t pl = (size_t)d * c.plane;
       const float wz = wd * mz;
       const float g = fin ? wz * (xz - xf) : 0.f;             // W_d (.) Delta_d x
-      const float wso = c.wSr[pl + gi];
+      const float wso = __ldg(c.wSr + pl + gi);
       const float wn = fminf(fmaxf(g + wso, -c.ith), c.ith);
       c.wSw[pl + gi] = wn;
       reg += fabs((double)g);
@@ -294,7 +332,7 @@ __device__ __forceinline__ float nltv_pixel(const NltvCtx& c, const Geom& G, int
       if (fin) acc = fmaf(wz, 2.f * wn - wso, acc);
       if (bin) {
         const float wb = wd * mb;
-        const float wsb = c.wSr[pl + gi - (size_t)dy * c.ps - dx];
+        const float wsb = __ldg(c.wSr + pl + gi - (size_t)dy * c.ps - dx);
         const float wnb = fminf(fmaxf(fmaf(wb, xb - xz, wsb), -c.ith), c.ith);
         acc = fmaf(-wb, 2.f * wnb - wsb, acc);
       }
@@ -405,7 +443,7 @@ __device__ __forceinline__ void views(const Tile<Z, INT>& t, const Geom& G, cons
 }
 
 template <int Z, int MODE>
-__global__ void __launch_bounds__(384)
+__global__ void __launch_bounds__(LFSR_MAXW * 32, LFSR_MINB)
 k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
   using C = TC<Z>;
   constexpr int R = C::R, LX = C::LX, BL = C::BL, TY = C::TY, TX = C::TX;
@@ -432,13 +470,21 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
   float* P = smem;                                           // PH*PW  input tile (phase split)
   int* ACC = reinterpret_cast<int*>(P + PH * PW);            // 2*PH*PW fixed-point accumulator (hi, lo)
   const int LO = PH * PW;
+  constexpr bool kOMs = !LFSR_SMEM_DIET;                            // disparity tile in smem
+  constexpr bool kMs = (MODE == MODE_WZ) || !LFSR_SMEM_DIET;         // weight tile in smem
   float* OM = P + 3 * PH * PW;                               // EY*ECOL disparity on the E region
-  float* M = OM + EY * ECOL;                                 // MH*MW  weight map, own + radius
-  float* NL = OM;                                            // TY*TX  NLTV term (aliases OM after the views)
-  const size_t red_off = ((size_t)(M - smem) + (size_t)T.MH * T.MW + 1) & ~(size_t)1;
+  float* M = OM + (kOMs ? EY * ECOL : 0);                    // MH*MW  weight map, own + radius
+  float* NL = M + (kMs ? T.MH * T.MW : 0);                   // TY*TX  NLTV term of the own pixels
+  constexpr bool kRing = LFSR_CRING && kFwd && kAdj;
+  // per-warp coordinate rings, 16-byte aligned, after NL
+  const size_t ring_off = (((size_t)(NL - smem) + (size_t)TY * TX) + 3) & ~(size_t)3;
+  int4* RING = reinterpret_cast<int4*>(smem + ring_off);
+  const size_t ring_words = kRing ? (size_t)NW * C::NTAP * Z * 32 * 4 : 0;
+  const size_t red_off = (ring_off + ring_words + 1) & ~(size_t)1;
   double* RED = reinterpret_cast<double*>(smem + red_off);
   __shared__ float s_max;
   __shared__ float s_scale[2];
+  __shared__ int s_nl_next;
 
   const int PWZ = T.PWZ;
 
@@ -449,30 +495,50 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
     double pim1 = ctl->cur[S_PI + io.cg_k - 1], pim2 = ctl->cur[S_PI + io.cg_k - 2];
     beta = (float)(pim1 / pim2);    // Alg.2 line 10 (reading A2): p_k = r_k + beta p_{k-1}
   }
-  if (tid == 0) s_max = 0.f;
-  for (int e = tid; e < PH * PWn; e += NT) {
-    const int py = e / PWn, px = e - py * PWn;
-    const int gy = PY0 + py, gx = PX0 + px;
-    // replicate padding outside the image (see Tile::sample)
-    const int cy = min(max(gy, 0), H - 1), cx = min(max(gx, 0), W - 1);
-    float v = 0.f;
-    if (kFwd) {
-      const size_t gi = (size_t)cy * ps + cx;
-      v = io.in_hr[gi];
-      if (MODE == MODE_NORMAL && io.cg_k >= 1) {
-        const bool own = gy == cy && gx == cx && gy >= Y0 && gy < Y0 + TY && gx >= X0 && gx < X0 + TX;
-        if (io.cg_k == 1) {
-          if (own && grp == 0) pi0_part += (double)v * v;   // pi_0 = <r_0, r_0> (Alg.2 line 3)
-        } else {
-          v = v + beta * io.in_hr2[gi];
+  if (tid == 0) {
+    s_max = 0.f;
+    s_nl_next = 0;
+  }
+  {
+    // 4 independent loads in flight per thread (the tile load is latency bound)
+    constexpr int U = 4;
+    const int n = PH * PWn;
+    for (int e0 = tid; e0 < n; e0 += U * NT) {
+      float v[U], v2[U];
+      size_t gi[U];
+      bool own[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = e0 + u * NT;
+        const int py = e / PWn, px = e - py * PWn;
+        const int gy = PY0 + py, gx = PX0 + px;
+        // replicate padding outside the image (see Tile::sample)
+        const int cy = min(max(gy, 0), H - 1), cx = min(max(gx, 0), W - 1);
+        gi[u] = (size_t)cy * ps + cx;
+        own[u] = e < n && gy == cy && gx == cx && gy >= Y0 && gy < Y0 + TY && gx >= X0 && gx < X0 + TX;
+        v[u] = (kFwd && e < n) ? __ldg(io.in_hr + gi[u]) : 0.f;
+        v2[u] = (MODE == MODE_NORMAL && io.cg_k >= 2 && e < n) ? __ldg(io.in_hr2 + gi[u]) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int e = e0 + u * NT;
+        if (e >= n) break;
+        float val = v[u];
+        if (MODE == MODE_NORMAL && io.cg_k >= 1) {
+          if (io.cg_k == 1) {
+            if (own[u] && grp == 0) pi0_part += (double)val * val;   // pi_0 = <r_0, r_0> (Alg.2 line 3)
+          } else {
+            val = val + beta * v2[u];
+          }
+          if (own[u] && grp == 0) io.p_out[gi[u]] = val;
         }
-        if (own && grp == 0) io.p_out[gi] = v;
+        pmax = fmaxf(pmax, fabsf(val));
+        const int py = e / PWn, px = e - py * PWn;
+        const int i = pidx<Z>(py, px, PW, PWZ);
+        if (kFwd) P[i] = val;
+        if (kAdj) { ACC[i] = 0; ACC[LO + i] = 0; }
       }
     }
-    pmax = fmaxf(pmax, fabsf(v));
-    const int i = pidx<Z>(py, px, PW, PWZ);
-    if (kFwd) P[i] = v;
-    if (kAdj) { ACC[i] = 0; ACC[LO + i] = 0; }
   }
   if (kAdj && PW > PWn) {  // phase-split padding cells of the accumulator
     for (int e = tid; e < PH * (PW - PWn); e += NT) {
@@ -482,13 +548,13 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
       ACC[LO + i] = 0;
     }
   }
-  for (int e = tid; e < EY * ECOL; e += NT) {
+  for (int e = tid; kOMs && e < EY * ECOL; e += NT) {
     const int er = e / ECOL, c = e - er * ECOL;
     const int Y = YE0 + er, X = XE0 + c;
     OM[e] = (Y >= 0 && Y < H && X >= 0 && X < W) ? io.omega[(size_t)Y * ps + X] : 0.f;
   }
   const int rr = G.radius, MW = T.MW;
-  if (MODE == MODE_NORMAL && io.do_nltv) {
+  if (MODE == MODE_NORMAL && io.do_nltv && kMs) {
     for (int e = tid; e < T.MH * MW; e += NT) {
       const int my = e / MW, mx = e - my * MW;
       const int gy = Y0 - rr + my, gx = X0 - rr + mx;
@@ -557,52 +623,61 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
     // interior tile: every E position is inside the image (no masks needed)
     const bool interior = (YE0 >= 0) && (YE0 + EY <= H) && (XE0 >= 0) && (XE0 + C::EXv <= W);
     if (interior) {
-      Tile<Z, true> t{P, ACC, OM, PW, PWZ, PY0, PX0, YE0, XE0, H, W, colmask, s_scale[0], LO};
+      Tile<Z, true> t{P, ACC, OM, PW, PWZ, PY0, PX0, YE0, XE0, H, W, colmask, s_scale[0], LO, io.omega, ps,
+                        kRing ? RING + (size_t)warp * C::NTAP * Z * 32 : nullptr};
       views<Z, MODE, true>(t, G, V, T, io, grp, lane, warp, NW, i0, j0, red_a, red_b, red_c);
     } else {
-      Tile<Z, false> t{P, ACC, OM, PW, PWZ, PY0, PX0, YE0, XE0, H, W, colmask, s_scale[0], LO};
+      Tile<Z, false> t{P, ACC, OM, PW, PWZ, PY0, PX0, YE0, XE0, H, W, colmask, s_scale[0], LO, io.omega, ps,
+                         kRing ? RING + (size_t)warp * C::NTAP * Z * 32 : nullptr};
       views<Z, MODE, false>(t, G, V, T, io, grp, lane, warp, NW, i0, j0, red_a, red_b, red_c);
     }
   }
   if (MODE == MODE_A) return;
-  __syncthreads();   // views done: ACC complete, OM free (NL aliases it)
 
-  // ---- phase 3: NLTV term of the own pixels; view group g takes own rows g, g+G, ...
+  // ---- phase 3: NLTV term of the own pixels (view group g takes own rows g, g+G, ...);
+  // warps that finish their views early pull rows from a shared counter, so the NLTV
+  // work (the w_S stream in WZ) fills the wait for the slowest warp.
   double red_reg = 0.0;
   const int ng = T.groups;
   const bool nltv = (MODE == MODE_WZ) || (MODE == MODE_NORMAL && io.do_nltv);
   if (nltv) {
     NltvCtx c;
-    c.P = P; c.M = M; c.PW = PW; c.PWZ = PWZ; c.MW = MW; c.H = H; c.W = W; c.ps = ps;
+    c.P = P; c.M = M; c.mg = io.m; c.PW = PW; c.PWZ = PWZ; c.MW = MW; c.H = H; c.W = W; c.ps = ps;
     c.ith = G.inv_theta;
     const int rd = ctl->iter & 1;
     c.wSr = rd ? io.wS1 : io.wS0;
     c.wSw = rd ? io.wS0 : io.wS1;
     c.plane = (size_t)H * ps;
     const int my_rows = TY > grp ? (TY - grp + ng - 1) / ng : 0;
-    for (int e = tid; e < my_rows * TX; e += NT) {
-      const int oy = grp + ng * (e / TX), ox = e % TX;
-      const int Y = Y0 + oy, X = X0 + ox;
-      float acc = 0.f;
-      if (Y < H && X < W) {
-        const int py = Y - PY0, px = X - PX0;
-        const int mi = (oy + rr) * MW + (ox + rr);
-        const size_t gi = (size_t)Y * ps + X;
-        double pq = 0.0;
-        const bool inner = Y >= rr && Y < H - rr && X >= rr && X < W - rr;
-        if (rr == 2) {
-          acc = inner ? nltv_pixel<Z, MODE, false, 2>(c, G, Y, X, py, px, mi, gi, pq, red_reg, red_c)
-                      : nltv_pixel<Z, MODE, true, 2>(c, G, Y, X, py, px, mi, gi, pq, red_reg, red_c);
-        } else {
-          acc = nltv_pixel<Z, MODE, true, 0>(c, G, Y, X, py, px, mi, gi, pq, red_reg, red_c);
+    for (;;) {
+      int row = 0;
+      if (lane == 0) row = atomicAdd(&s_nl_next, 1);
+      row = __shfl_sync(0xffffffffu, row, 0);
+      if (row >= my_rows) break;
+      const int oy = grp + ng * row;
+      for (int ox = lane; ox < TX; ox += 32) {
+        const int Y = Y0 + oy, X = X0 + ox;
+        float acc = 0.f;
+        if (Y < H && X < W) {
+          const int py = Y - PY0, px = X - PX0;
+          const int mi = (oy + rr) * MW + (ox + rr);
+          const size_t gi = (size_t)Y * ps + X;
+          double pq = 0.0;
+          const bool inner = Y >= rr && Y < H - rr && X >= rr && X < W - rr;
+          if (rr == 2) {
+            acc = inner ? nltv_pixel<Z, MODE, false, 2>(c, G, Y, X, py, px, mi, gi, pq, red_reg, red_c)
+                        : nltv_pixel<Z, MODE, true, 2>(c, G, Y, X, py, px, mi, gi, pq, red_reg, red_c);
+          } else {
+            acc = nltv_pixel<Z, MODE, true, 0>(c, G, Y, X, py, px, mi, gi, pq, red_reg, red_c);
+          }
+          acc *= G.cS;
+          red_b += (double)G.cS * pq;
         }
-        acc *= G.cS;
-        red_b += (double)G.cS * pq;
+        NL[oy * TX + ox] = acc;
       }
-      NL[oy * TX + ox] = acc;
     }
   }
-  __syncthreads();
+  __syncthreads();   // views and NLTV done: ACC and NL complete
 
   // ---- phase 4: flush accumulator + NLTV (tile + halo) with RED.ADD ----------
   {
@@ -643,8 +718,12 @@ static void fill_static(TileGeom& T) {
   T.EY = C::EY; T.ECOL = C::ECOL; T.EXv = C::EXv;
 }
 
-static size_t smem_bytes(const TileGeom& T, int nwarps) {
-  size_t words = 3 * (size_t)T.PH * T.PW + (size_t)T.EY * T.ECOL + (size_t)T.MH * T.MW + 2;
+static size_t smem_bytes(const TileGeom& T, int nwarps, int mode = MODE_WZ) {
+  const bool om = !LFSR_SMEM_DIET, m = (mode == MODE_WZ) || !LFSR_SMEM_DIET;
+  const int ntap = 2 * (int)std::ceil(3.0 * 0.25 * std::sqrt((double)T.ECOL * T.ECOL / 1024.0 - 1.0)) + 1;
+  const int z = T.ECOL / 32;
+  size_t words = 3 * (size_t)T.PH * T.PW + (om ? (size_t)T.EY * T.ECOL : 0) + (m ? (size_t)T.MH * T.MW : 0) +
+                 (size_t)T.TY * T.TX + 8 + (LFSR_CRING ? (size_t)nwarps * ntap * z * 32 * 4 : 0);
   return words * 4 + (size_t)nwarps * 4 * sizeof(double);
 }
 
@@ -705,7 +784,7 @@ TileGeom make_tile_geom(const Geom& G, int num_sms) {
   T.ntY = (G.h + T.BL - 1) / T.BL;
   T.ntX = (G.w + T.LX - 1) / T.LX;
   const int tiles = T.ntY * T.ntX;
-  const int max_warps = 12;
+  const int max_warps = LFSR_MAXW;
   T.smem = smem_bytes(T, max_warps);
   if (prepare_tile_kernels(G.scale, T.smem) != cudaSuccess) cudaGetLastError();
   int best_g = 1, best_w = 1;
@@ -720,7 +799,7 @@ TileGeom make_tile_geom(const Geom& G, int num_sms) {
         if (waste < bestw) { bestw = waste; nw = w; }
       }
     }
-    const int occ = occupancy_for(G.scale, nw * 32, smem_bytes(T, nw));
+    const int occ = occupancy_for(G.scale, nw * 32, smem_bytes(T, nw, MODE_NORMAL));
     const double waves = (double)tiles * g / ((double)num_sms * occ);
     double cost = std::ceil(waves) * ((vpg + nw - 1) / nw) * (1.0 + 0.02 * g);  // flush cost grows with g
     if (waves < 0.9) cost *= 1.0 + (0.9 - waves);
@@ -730,13 +809,14 @@ TileGeom make_tile_geom(const Geom& G, int num_sms) {
   T.vpg = (G.n_views + best_g - 1) / best_g;
   T.groups = (G.n_views + T.vpg - 1) / T.vpg;
   T.smem = smem_bytes(T, T.nwarps);
+  T.smem_normal = smem_bytes(T, T.nwarps, MODE_NORMAL);
   return T;
 }
 
 template <int Z, int MODE>
 static cudaError_t launch_z(const Geom& G, const Views& V, const TileGeom& T, const TileIO& io, cudaStream_t st) {
   dim3 grid(T.ntY * T.ntX * T.groups);
-  k_tile<Z, MODE><<<grid, T.nwarps * 32, T.smem, st>>>(G, V, T, io);
+  k_tile<Z, MODE><<<grid, T.nwarps * 32, MODE == MODE_NORMAL ? T.smem_normal : T.smem, st>>>(G, V, T, io);
   return cudaGetLastError();
 }
 

@@ -19,7 +19,7 @@ from dataclasses import dataclass, fields
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblfsr.so")
+LIB_PATH = os.environ.get("LFSR_LIB") or os.path.join(_HERE, "liblfsr.so")
 
 LFSR_OK, LFSR_ERR_INVALID_ARG, LFSR_ERR_STATE, LFSR_ERR_OOM, LFSR_ERR_CUDA, LFSR_ERR_NCCL, \
     LFSR_ERR_DIVERGED, LFSR_ERR_UNSUPPORTED = range(8)
