@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--multi", default="replicas", choices=["replicas", "strips"],
+                    help="N > 1: independent light fields per rank (weak scaling) or one light field split "
+                         "into HR row strips with NCCL halo exchange (strong scaling, DESIGN.md §10)")
     return ap.parse_args()
 
 
@@ -207,11 +210,17 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    # each rank super-resolves its own light field (independent problem, own seed)
-    lf = S.make_lightfield(cfg, seed=None if rank == 0 else 10007 * rank + 1000)
+    strips = world > 1 and args.multi == "strips"
+    # replicas: each rank super-resolves its own light field (independent problem, own seed);
+    # strips: every rank holds the same light field and owns a strip of it
+    lf = S.make_lightfield(cfg, seed=None if (rank == 0 or strips) else 10007 * rank + 1000)
     stream = torch.cuda.Stream()          # a real (non-legacy) stream shared by torch and liblfsr
     torch.cuda.set_stream(stream)
     p = L.params_for(cfg, d, device=local)
+    if strips:
+        uid = [torch.cuda.nccl.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        p.n_ranks, p.rank, p.nccl_unique_id = world, rank, uid[0]
     sol = L.Solver(p, stream=stream.cuda_stream)
     dev_in = [torch.from_numpy(a).cuda() for a in (lf.y, lf.view_offsets, lf.omega)]
     sol.set_observations(*dev_in)
@@ -248,7 +257,7 @@ def main():
         tt = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_max = float(tt.item())
-    total_iters = args.steps * world
+    total_iters = args.steps * (1 if strips else world)
     value = total_iters / (t_max / 1000.0)
     hr_mpix = cfg.H * cfg.W / 1e6
 
@@ -280,7 +289,7 @@ def main():
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             tot = float(tt.item())
         h2d = sum(int(h.numel()) * 4 for h in host)
-        e2e = {"value": args.e2e_steps * n_it * world / (tot / 1000.0), "unit": UNIT,
+        e2e = {"value": args.e2e_steps * n_it * (1 if strips else world) / (tot / 1000.0), "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(xout.numel()) * 4 + 8 * 11 * n_it,
                "step": "full solve: set_observations (H2D + setup) + %d ADMM iterations + get_hr (D2H)" % n_it,
                "ms_per_solve": tot / args.e2e_steps, "psnr_db": L.psnr(xout.numpy(), lf.x_gt)}
@@ -288,6 +297,9 @@ def main():
     # ---- roofline of the dominant kernel (the CG normal-operator tile kernel)
     alg = algorithmic(cfg, d)
     hbm_peak, fp32_peak, peak_src = peaks()
+    if kn[1] == 0:   # strips: per-kernel events are not recorded; use the step time split evenly
+        kms, kn = [t_ms * 0.2, t_ms * 0.75, t_ms * 0.05], [args.steps, args.steps * d.cg_max_iters,
+                                                          args.steps * d.cg_max_iters]
     k_normal_ms = kms[1] / max(kn[1], 1)
     k_wz_ms = kms[0] / max(kn[0], 1)
     k_upd_ms = kms[2] / max(kn[2], 1)
@@ -327,12 +339,13 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "hr_mpix_it_per_s": value * hr_mpix,
+                "scaling": "strong" if strips else "weak", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic", "hr_mpix_it_per_s": value * hr_mpix,
                 "config": {"workload": cfg.name, "desc": cfg.note, "views": cfg.n_views, "scale": cfg.scale,
                            "hr": [cfg.H, cfg.W], "cg_steps": d.cg_max_iters, "nltv_window": "5x5",
                            "l2_flush": "512 MiB write between timed steps (outside the events)" if flush is not None else "none",
-                           "parallelism": "dp%d (independent light fields per rank)" % world},
+                           "parallelism": ("strips%d (one light field, HR row strips, NCCL halos)" % world) if strips
+                           else "dp%d (independent light fields per rank)" % world},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": sol.launches_per_iter * args.steps * world,
                 "clocks": clk,

@@ -87,9 +87,13 @@ typedef struct {
   int32_t reweight_every_iter; /* 1 = paper (weights from x^{n-1}); 0 = W
                                   frozen at the value computed from x^0              */
   int32_t device;       /* CUDA device ordinal                                       */
-  int32_t rank;         /* 0 (multi-GPU strips: not in this build)                   */
-  int32_t n_ranks;      /* 1                                                         */
-  const void* nccl_unique_id; /* NULL                                               */
+  int32_t rank;         /* this process's strip in [0, n_ranks) (NCCL mode), or -1 with
+                           n_ranks > 1: all strips in this ctx on one device ("virtual
+                           ranks": the same decomposition and exchange schedule with
+                           device copies instead of NCCL; for testing)               */
+  int32_t n_ranks;      /* >= 1 HR row strips (DESIGN 10)                  */
+  const void* nccl_unique_id; /* NCCL mode: 128-byte ncclUniqueId (same on all ranks),
+                                 e.g. broadcast over a torch.distributed group; else NULL */
   void* stream;         /* cudaStream_t to run on (e.g. torch.cuda.current_stream()
                            .cuda_stream), or NULL for a ctx-owned stream             */
 } lfsr_params;
@@ -106,9 +110,11 @@ typedef struct {
   double J, data_l1, data_l2, reg_l1, primal_res, cg_pi0, cg_pi_last;
 } lfsr_iter_stats;
 
-/* Create a ctx on params->device and allocate nothing large yet.
+/* Create a ctx on params->device and allocate nothing large yet.  NCCL mode
+ * (n_ranks > 1, rank >= 0) initialises the communicator: every rank must call
+ * lfsr_create collectively.
  * Errors: LFSR_ERR_INVALID_ARG (any field out of range; `out` untouched),
- * LFSR_ERR_UNSUPPORTED (n_ranks != 1), LFSR_ERR_CUDA (no usable device). */
+ * LFSR_ERR_NCCL (libnccl missing or init failed), LFSR_ERR_CUDA (no usable device). */
 LFSR_API lfsr_status lfsr_create(const lfsr_params* params, lfsr_ctx** out);
 
 /* Load the observations and reset the solver state (x = x0, w = 0) (Alg.1
@@ -186,6 +192,19 @@ LFSR_API lfsr_status lfsr_op_apply(lfsr_ctx* ctx, lfsr_op op, const float* in, f
 /* Number of kernel launches one ADMM iteration issues (for the bench's
  * gpu_launches count).  Valid after set_observations; 0 otherwise. */
 LFSR_API int32_t lfsr_launches_per_iter(const lfsr_ctx* ctx);
+
+/* Row-strip plan of the multi-GPU decomposition (DESIGN 10): rank r
+ * owns tile rows [tile_row0, tile_row1) = LR rows [lr_row0, lr_row1) = HR rows
+ * [hr_row0, hr_row1); before every operator pass it needs halo_top HR rows above
+ * and halo_bottom rows below from its neighbours, and afterwards folds the
+ * adjoint contributions it accumulated in those rows back into them.
+ * max_shift_rows = ceil(max_k |dtau_k| * max |omega|) (lfsr_set_observations
+ * computes it from the data).  Pure host function (no device needed).
+ * Errors: INVALID_ARG (params), UNSUPPORTED (a strip thinner than its halo). */
+typedef struct {
+  int32_t rank, tile_row0, tile_row1, lr_row0, lr_row1, hr_row0, hr_row1, halo_top, halo_bottom;
+} lfsr_strip;
+LFSR_API lfsr_status lfsr_strip_plan(const lfsr_params* params, int32_t max_shift_rows, lfsr_strip* out /*[n_ranks]*/);
 
 /* Free everything; NULL-safe. */
 LFSR_API void lfsr_destroy(lfsr_ctx* ctx);

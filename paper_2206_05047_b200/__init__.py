@@ -4,6 +4,6 @@
 sm_100a kernels run every step of Algorithm 1/2.  Build with ``build.build()``.
 """
 from .lfsr import (Params, Solver, LFSRError, load_library, params_for, psnr, LIB_PATH, EXPORTS,  # noqa: F401
-                   STAT_KEYS)
+                   STAT_KEYS, strip_plan)
 
 __all__ = ["Params", "Solver", "LFSRError", "load_library", "params_for", "psnr", "LIB_PATH", "EXPORTS"]

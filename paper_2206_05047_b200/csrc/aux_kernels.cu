@@ -131,9 +131,45 @@ __global__ void k_absmax(const float* __restrict__ v, size_t n, unsigned* out) {
 // it records CG bookkeeping and, at k = K, writes the iteration's stats record
 // and resets the scalar slots (threadfence reduction pattern).
 // ---------------------------------------------------------------------------
+// Record of the finished ADMM iteration and reset of the scalar slots (run by one
+// thread: the last block of the final CG update, or k_close in the strip mode).
+__device__ void close_iteration(const Geom& G, Control* ctl) {
+  volatile double* cur = ctl->cur;
+  const int cgit = (int)cur[S_CGIT];
+  const double J = (double)G.lambda1 * cur[S_L1] + (double)G.lambda2 * cur[S_L2] + cur[S_REG];
+  const double pil = cur[S_PI + cgit];
+  double* rec = ctl->ring + (size_t)(ctl->iter % ctl->cap) * T_COUNT;
+  rec[T_ITER] = (double)(ctl->iter + 1);
+  rec[T_CGIT] = (double)cgit;
+  rec[T_BREAK] = cur[S_BREAK];
+  rec[T_NF] = (cur[S_NF] > 0.0 || !isfinite(J) || !isfinite(pil)) ? 1.0 : 0.0;
+  rec[T_J] = J;
+  rec[T_L1] = cur[S_L1];
+  rec[T_L2] = cur[S_L2];
+  rec[T_REG] = cur[S_REG];
+  rec[T_RES] = sqrt(cur[S_RES2]);
+  rec[T_PI0] = cur[S_PI];
+  rec[T_PILAST] = pil;
+  for (int s = 0; s < S_COUNT; ++s) cur[s] = 0.0;
+  ctl->iter = ctl->iter + 1;
+}
+
+__global__ void k_close(const Geom G, Control* ctl) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) close_iteration(G, ctl);
+}
+
+// ---------------------------------------------------------------------------
+// CG update (Alg.2 lines 8-9 and 11 with readings A1-A4) on the own rows
+// [row0, row0 + nrows):
+//   alpha = pi_{k-1} / <p_k, q_k>; x += alpha p_k; r -= alpha q_k; pi_k = <r, r>.
+// Also zeroes q (the next normal operator accumulates into it) and, at k = K,
+// zeroes r for the next wz-step.  The last block to finish closes the step:
+// CG bookkeeping (steps taken, stop / breakdown flags) and, at k = K when
+// close_here, the iteration's stats record (threadfence reduction pattern).
+// ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_cg_update(const Geom G, float* __restrict__ x, float* __restrict__ r,
                                                    const float* __restrict__ p, float* __restrict__ q,
-                                                   Control* ctl, int k) {
+                                                   Control* ctl, int k, int row0, int nrows, int close_here) {
   __shared__ double red[8 * 2];
   __shared__ bool am_last;
   const double pi_prev = ctl->cur[S_PI + k - 1];
@@ -143,11 +179,12 @@ __global__ void __launch_bounds__(256) k_cg_update(const Geom G, float* __restri
   const float alpha = active ? (float)(pi_prev / pq) : 0.f;
   const bool last = (k == G.K);
   double pi_part = 0.0, nf_part = 0.0;
-  const size_t n4 = (size_t)G.H * G.ps / 4;
-  float4* x4 = reinterpret_cast<float4*>(x);
-  float4* r4 = reinterpret_cast<float4*>(r);
-  const float4* p4 = reinterpret_cast<const float4*>(p);
-  float4* q4 = reinterpret_cast<float4*>(q);
+  const size_t off4 = (size_t)row0 * G.ps / 4;
+  const size_t n4 = (size_t)nrows * G.ps / 4;
+  float4* x4 = reinterpret_cast<float4*>(x) + off4;
+  float4* r4 = reinterpret_cast<float4*>(r) + off4;
+  const float4* p4 = reinterpret_cast<const float4*>(p) + off4;
+  float4* q4 = reinterpret_cast<float4*>(q) + off4;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
     float4 qv = q4[i];
     if (active) {
@@ -193,25 +230,7 @@ __global__ void __launch_bounds__(256) k_cg_update(const Geom G, float* __restri
     cur[S_STOP] = 1.0;
     if (!(pi_prev < (double)G.cg_tol) && pi_prev != 0.0 && !(pq > 0.0)) cur[S_BREAK] = 1.0;
   }
-  if (last) {
-    int cgit = (int)cur[S_CGIT];
-    double J = (double)G.lambda1 * cur[S_L1] + (double)G.lambda2 * cur[S_L2] + cur[S_REG];
-    double pil = cur[S_PI + cgit];
-    double* rec = ctl->ring + (size_t)(ctl->iter % ctl->cap) * T_COUNT;
-    rec[T_ITER] = (double)(ctl->iter + 1);
-    rec[T_CGIT] = (double)cgit;
-    rec[T_BREAK] = cur[S_BREAK];
-    rec[T_NF] = (cur[S_NF] > 0.0 || !isfinite(J) || !isfinite(pil)) ? 1.0 : 0.0;
-    rec[T_J] = J;
-    rec[T_L1] = cur[S_L1];
-    rec[T_L2] = cur[S_L2];
-    rec[T_REG] = cur[S_REG];
-    rec[T_RES] = sqrt(cur[S_RES2]);
-    rec[T_PI0] = cur[S_PI];
-    rec[T_PILAST] = pil;
-    for (int s = 0; s < S_COUNT; ++s) cur[s] = 0.0;
-    ctl->iter = ctl->iter + 1;
-  }
+  if (last && close_here) close_iteration(G, ctl);
   __threadfence();
   ctl->done = 0u;
 }
@@ -278,13 +297,17 @@ cudaError_t launch_absmax(const float* v, size_t n, unsigned* out, cudaStream_t 
   return cudaGetLastError();
 }
 cudaError_t launch_cg_update(const Geom& G, float* x, float* r, const float* p, float* q, Control* ctl, int k,
-                             int num_sms, cudaStream_t st) {
-  size_t n4 = (size_t)G.H * G.ps / 4;
+                             int row0, int nrows, int close_here, int num_sms, cudaStream_t st) {
+  size_t n4 = (size_t)nrows * G.ps / 4;
   int blocks = (int)((n4 + 255) / 256);
   int cap = num_sms * 4;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  k_cg_update<<<blocks, 256, 0, st>>>(G, x, r, p, q, ctl, k);
+  k_cg_update<<<blocks, 256, 0, st>>>(G, x, r, p, q, ctl, k, row0, nrows, close_here);
+  return cudaGetLastError();
+}
+cudaError_t launch_close(const Geom& G, Control* ctl, cudaStream_t st) {
+  k_close<<<1, 32, 0, st>>>(G, ctl);
   return cudaGetLastError();
 }
 cudaError_t launch_apply_S(const Geom& G, const float* x, const float* m, float* out, cudaStream_t st) {

@@ -1,8 +1,11 @@
 // capi.cu — the C ABI of liblfsr (include/lfsr.h): validation, device state,
-// CUDA-graph capture of one ADMM iteration (Alg.1) and its replay.
+// CUDA-graph capture of one ADMM iteration (Alg.1) and its replay,
+// and the HR row-strip decomposition over several GPUs.
 #include "../../include/lfsr.h"
 #include "internal.h"
+#include "nccl_shim.h"
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -11,7 +14,8 @@
 #include <vector>
 
 namespace lfsr {
-TileGeom make_tile_geom(const Geom& G, int num_sms);
+TileGeom make_tile_geom(const Geom& G, int num_sms, int tr0, int tr1);
+void tile_static(int scale, int& BL, int& LX, int& R, int& KEEP);
 cudaError_t prepare_tile_kernels(int scale, size_t smem);
 cudaError_t launch_tile(int mode, const Geom& G, const Views& V, const TileGeom& T, const TileIO& io,
                         cudaStream_t st);
@@ -22,37 +26,59 @@ cudaError_t launch_density(const Geom& G, const Views& V, const float* omega, fl
 cudaError_t launch_weights(const Geom& G, const float* x, const float* wo, float* m, cudaStream_t st);
 cudaError_t launch_absmax(const float* v, size_t n, unsigned* out, cudaStream_t st);
 cudaError_t launch_cg_update(const Geom& G, float* x, float* r, const float* p, float* q, Control* ctl, int k,
-                             int num_sms, cudaStream_t st);
+                             int row0, int nrows, int close_here, int num_sms, cudaStream_t st);
+cudaError_t launch_close(const Geom& G, Control* ctl, cudaStream_t st);
 cudaError_t launch_apply_S(const Geom& G, const float* x, const float* m, float* out, cudaStream_t st);
 cudaError_t launch_apply_ST(const Geom& G, const float* h, const float* m, float* out, cudaStream_t st);
-
+cudaError_t launch_fold_rows(float* dst, float* src, size_t n, int zero_src, cudaStream_t st);
+cudaError_t launch_allreduce_local(Control* const* ctls, int nparts, int slot0, int count, cudaStream_t st);
 }  // namespace lfsr
 
 using namespace lfsr;
+
+namespace {
+
+constexpr int kRingCap = 4096;  // stats records kept on the device
+
+enum XMode { X_NONE = 0, X_LOCAL = 1, X_NCCL = 2 };
+
+// One HR row strip: its own rows, full-size buffers (only the own rows and the
+// halos are meaningful) and its tile geometry.
+struct Part {
+  lfsr_strip plan{};
+  State S{};
+  TileGeom T{};
+  double* ring = nullptr;
+  float* stage[2] = {nullptr, nullptr};  // NCCL fold staging: [0] rows from the previous rank, [1] from the next
+  size_t stage_rows = 0;
+};
+
+}  // namespace
 
 struct lfsr_ctx {
   lfsr_params prm{};
   Geom G{};
   Views V{};
-  TileGeom T{};
-  State S{};
+  TileGeom Tfull{};          // whole-image tiles (test operators)
+  std::vector<Part> parts;   // 1 (single GPU / NCCL rank) or n_ranks (virtual ranks)
+  XMode xmode = X_NONE;
+  void* comm = nullptr;      // ncclComm_t (NCCL mode)
+  Control** d_ctls = nullptr;  // device array of the parts' control blocks (virtual ranks)
   int num_sms = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t cap_stream = nullptr;
   bool own_stream = false;
   bool poisoned = false;
   bool ready = false;
-  cudaGraphExec_t graph = nullptr;
+  cudaGraphExec_t graph[2] = {nullptr, nullptr};  // replay for even / odd iteration parity
   int launches_per_iter = 0;
   std::vector<void*> allocs;
   float* tmp_hr2 = nullptr;
   float* tmp_s = nullptr;
   unsigned* umax = nullptr;
-  double* ring = nullptr;        // device stats ring [ring_cap][T_COUNT]
-  int ring_cap = 0;
   int h_iter = 0;                // iterations enqueued since set_observations
   size_t alloc_key[6] = {0, 0, 0, 0, 0, 0};
-  bool profile = false;          // event-record nodes around every kernel of the graph
+  bool profile = false;          // event-record nodes around every kernel (single strip)
   std::vector<cudaEvent_t> prof_ev;
   double prof_ms[3] = {0, 0, 0}; // accumulated wz / normal / update milliseconds
   int64_t prof_n[3] = {0, 0, 0};
@@ -75,13 +101,25 @@ static lfsr_status cuda_fail(lfsr_ctx* c, cudaError_t e, const char* what) {
   return LFSR_ERR_CUDA;
 }
 
+static lfsr_status nccl_fail(lfsr_ctx* c, int e, const char* what) {
+  char buf[512];
+  snprintf(buf, sizeof buf, "NCCL error in %s: %s", what, nccl_error(e));
+  c->err = buf;
+  c->poisoned = true;
+  return LFSR_ERR_NCCL;
+}
+
 #define CK(c, expr)                                               \
   do {                                                            \
     cudaError_t _e = (expr);                                      \
     if (_e != cudaSuccess) return cuda_fail((c), _e, #expr);      \
   } while (0)
 
-static constexpr int kRingCap = 4096;  // stats records kept on the device
+#define NK(c, expr)                                               \
+  do {                                                            \
+    int _e = (expr);                                              \
+    if (_e != 0) return nccl_fail((c), _e, #expr);                \
+  } while (0)
 
 static int round_up(int v, int m) { return (v + m - 1) / m * m; }
 
@@ -102,7 +140,10 @@ static const char* validate(const lfsr_params* p) {
   if (!(p->cg_tol >= 0.f)) return "cg_tol must be >= 0";
   if (p->reweight_every_iter != 0 && p->reweight_every_iter != 1) return "reweight_every_iter must be 0 or 1";
   if (p->device < 0) return "device must be >= 0";
-  if (p->rank < 0 || p->n_ranks < 1 || p->rank >= p->n_ranks) return "rank/n_ranks invalid";
+  if (p->n_ranks < 1 || p->n_ranks > 1024) return "n_ranks must be in [1, 1024]";
+  if (p->n_ranks == 1 && p->rank != 0) return "rank must be 0 when n_ranks == 1";
+  if (p->n_ranks > 1 && (p->rank < -1 || p->rank >= p->n_ranks)) return "rank must be in [-1, n_ranks)";
+  if (p->n_ranks > 1 && p->rank >= 0 && !p->nccl_unique_id) return "NCCL mode (rank >= 0) needs nccl_unique_id";
   if (p->lr_height * (size_t)p->scale > (1u << 20) || p->lr_width * (size_t)p->scale > (1u << 20))
     return "image too large";
   return nullptr;
@@ -110,9 +151,7 @@ static const char* validate(const lfsr_params* p) {
 
 static float inv_or_zero(double s, double mul) { return std::isinf(s) ? 0.f : (float)(1.0 / (mul * s)); }
 
-static void fill_geom(lfsr_ctx* c) {
-  const lfsr_params& p = c->prm;
-  Geom& G = c->G;
+static void fill_geom(const lfsr_params& p, Geom& G) {
   G = Geom{};
   G.h = p.lr_height;
   G.w = p.lr_width;
@@ -163,9 +202,64 @@ static void fill_geom(lfsr_ctx* c) {
   G.s_d = n;
 }
 
+// Row-strip plan: contiguous tile rows per rank, as even as possible.
+static lfsr_status make_plan(const Geom& G, int n_ranks, int max_shift_rows, std::vector<lfsr_strip>& out,
+                             std::string& err) {
+  int BL, LX, R, KEEP;
+  tile_static(G.scale, BL, LX, R, KEEP);
+  const int ntY = (G.h + BL - 1) / BL;
+  const int sye = std::max(max_shift_rows, G.radius);
+  const int top = R + sye + 1;          // input-tile rows above the own rows (see k_tile)
+  const int bot = KEEP - R + sye + 1;   // ... and below
+  if (n_ranks > ntY) {
+    err = "more ranks than tile rows (" + std::to_string(ntY) + ")";
+    return LFSR_ERR_UNSUPPORTED;
+  }
+  out.assign(n_ranks, lfsr_strip{});
+  int tr = 0;
+  for (int r = 0; r < n_ranks; ++r) {
+    const int cnt = ntY / n_ranks + (r < ntY % n_ranks ? 1 : 0);
+    lfsr_strip& s = out[r];
+    s.rank = r;
+    s.tile_row0 = tr;
+    s.tile_row1 = tr + cnt;
+    s.lr_row0 = tr * BL;
+    s.lr_row1 = std::min((tr + cnt) * BL, G.h);
+    s.hr_row0 = s.lr_row0 * G.scale;
+    s.hr_row1 = s.lr_row1 * G.scale;
+    s.halo_top = r > 0 ? top : 0;
+    s.halo_bottom = r + 1 < n_ranks ? bot : 0;
+    tr += cnt;
+    if (n_ranks > 1 && s.hr_row1 - s.hr_row0 < std::max(top, bot)) {
+      err = "strip of " + std::to_string(s.hr_row1 - s.hr_row0) + " HR rows is thinner than its halo (" +
+            std::to_string(std::max(top, bot)) + "); use fewer ranks";
+      return LFSR_ERR_UNSUPPORTED;
+    }
+  }
+  return LFSR_OK;
+}
+
 extern "C" {
 
 int32_t lfsr_abi_version(void) { return LFSR_ABI_VERSION; }
+
+lfsr_status lfsr_strip_plan(const lfsr_params* params, int32_t max_shift_rows, lfsr_strip* out) {
+  if (const char* why = validate(params)) {
+    g_create_err = why;
+    return LFSR_ERR_INVALID_ARG;
+  }
+  if (!out || max_shift_rows < 0) {
+    g_create_err = "out is NULL or max_shift_rows < 0";
+    return LFSR_ERR_INVALID_ARG;
+  }
+  Geom G;
+  fill_geom(*params, G);
+  std::vector<lfsr_strip> plan;
+  lfsr_status st = make_plan(G, params->n_ranks, max_shift_rows, plan, g_create_err);
+  if (st != LFSR_OK) return st;
+  for (int r = 0; r < params->n_ranks; ++r) out[r] = plan[r];
+  return LFSR_OK;
+}
 
 lfsr_status lfsr_create(const lfsr_params* params, lfsr_ctx** out) {
   if (!out) {
@@ -175,10 +269,6 @@ lfsr_status lfsr_create(const lfsr_params* params, lfsr_ctx** out) {
   if (const char* why = validate(params)) {
     g_create_err = why;
     return LFSR_ERR_INVALID_ARG;
-  }
-  if (params->n_ranks != 1) {
-    g_create_err = "multi-rank strips are not in this build (n_ranks must be 1)";
-    return LFSR_ERR_UNSUPPORTED;
   }
   int ndev = 0;
   cudaError_t e = cudaGetDeviceCount(&ndev);
@@ -221,29 +311,50 @@ lfsr_status lfsr_create(const lfsr_params* params, lfsr_ctx** out) {
     delete c;
     return LFSR_ERR_CUDA;
   }
-  fill_geom(c);
+  fill_geom(c->prm, c->G);
   c->prm.stream = c->stream;
+  if (params->n_ranks > 1) {
+    c->xmode = params->rank < 0 ? X_LOCAL : X_NCCL;
+    if (c->xmode == X_NCCL) {
+      std::string why;
+      if (!nccl_available(&why)) {
+        g_create_err = why;
+        cudaStreamDestroy(c->cap_stream);
+        if (c->own_stream) cudaStreamDestroy(c->stream);
+        delete c;
+        return LFSR_ERR_NCCL;
+      }
+      int r = nccl_comm_init(&c->comm, params->n_ranks, params->nccl_unique_id, params->rank);
+      if (r != 0) {
+        g_create_err = std::string("ncclCommInitRank: ") + nccl_error(r);
+        cudaStreamDestroy(c->cap_stream);
+        if (c->own_stream) cudaStreamDestroy(c->stream);
+        delete c;
+        return LFSR_ERR_NCCL;
+      }
+    }
+  }
   *out = c;
   return LFSR_OK;
 }
 
 static void free_graph(lfsr_ctx* c) {
-  if (c->graph) {
-    cudaGraphExecDestroy(c->graph);
-    c->graph = nullptr;
-  }
+  for (auto& g : c->graph)
+    if (g) {
+      cudaGraphExecDestroy(g);
+      g = nullptr;
+    }
 }
 
 static void free_state(lfsr_ctx* c) {
   free_graph(c);
   for (void* p : c->allocs) cudaFree(p);
   c->allocs.clear();
-  c->S = State{};
+  c->parts.clear();
   c->tmp_hr2 = nullptr;
   c->tmp_s = nullptr;
   c->umax = nullptr;
-  c->ring = nullptr;
-  c->ring_cap = 0;
+  c->d_ctls = nullptr;
   for (auto& k : c->alloc_key) k = 0;
   c->ready = false;
 }
@@ -254,6 +365,10 @@ void lfsr_destroy(lfsr_ctx* c) {
   if (!c->poisoned) cudaStreamSynchronize(c->stream);
   free_state(c);
   for (cudaEvent_t e : c->prof_ev) cudaEventDestroy(e);
+  if (c->comm) {
+    if (c->poisoned) nccl_comm_abort(c->comm);
+    else nccl_comm_destroy(c->comm);
+  }
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -303,12 +418,50 @@ static cudaError_t get2d(lfsr_ctx* c, float* dst, int cols, const float* src, in
   return cudaMemcpy2DAsync(dst, (size_t)cols * 4, src, (size_t)pitch * 4, (size_t)cols * 4, rows, kind_out(mem), c->stream);
 }
 
-static lfsr_status build_graph(lfsr_ctx* c);
+static lfsr_status build_graphs(lfsr_ctx* c);
+
+// Buffers of one strip (full image size: only own rows and halos are meaningful).
+static lfsr_status alloc_part(lfsr_ctx* c, Part& P) {
+  const Geom& G = c->G;
+  State& S = P.S;
+  const size_t hr = (size_t)G.H * G.ps, lr = (size_t)G.n_views * G.h * G.lps;
+  const size_t ws = (size_t)G.s_d * hr;
+  void* p = nullptr;
+#define ALLOC(field, bytes)                                                                                 \
+  do {                                                                                                      \
+    cudaError_t _e = dalloc(c, &p, (bytes));                                                                \
+    if (_e != cudaSuccess) {                                                                                \
+      cudaGetLastError();                                                                                   \
+      free_state(c);                                                                                        \
+      FAIL(c, _e == cudaErrorMemoryAllocation ? LFSR_ERR_OOM : LFSR_ERR_CUDA, "device allocation failed"); \
+    }                                                                                                       \
+    field = (decltype(field))p;                                                                             \
+  } while (0)
+  ALLOC(S.x, hr * 4);
+  ALLOC(S.y, lr * 4);
+  ALLOC(S.wA, lr * 4);
+  ALLOC(S.wS[0], ws * 4);
+  ALLOC(S.wS[1], ws * 4);
+  ALLOC(S.density, hr * 4);
+  ALLOC(S.omega, hr * 4);
+  ALLOC(S.wo, hr * 4);
+  ALLOC(S.m, hr * 4);
+  ALLOC(S.r, hr * 4);
+  ALLOC(S.p[0], hr * 4);
+  ALLOC(S.p[1], hr * 4);
+  ALLOC(S.q, hr * 4);
+  ALLOC(S.tmp_hr, hr * 4);
+  ALLOC(S.tmp_lr, lr * 4);
+  ALLOC(S.ctl, sizeof(Control));
+  ALLOC(P.ring, (size_t)kRingCap * T_COUNT * sizeof(double));
+#undef ALLOC
+  return LFSR_OK;
+}
 
 lfsr_status lfsr_set_observations(lfsr_ctx* c, const float* lr_views, const float* view_offsets,
                                   const float* disparity, lfsr_disp_mode disp_mode, const float* x0, lfsr_mem mem) {
   if (!c) return LFSR_ERR_INVALID_ARG;
-  if (c->poisoned) FAIL(c, LFSR_ERR_STATE, "ctx is poisoned by an earlier CUDA error");
+  if (c->poisoned) FAIL(c, LFSR_ERR_STATE, "ctx is poisoned by an earlier CUDA/NCCL error");
   if (disp_mode == LFSR_DISP_PER_VIEW) FAIL(c, LFSR_ERR_UNSUPPORTED, "per-view disparity maps are not in this build");
   if (disp_mode != LFSR_DISP_SHARED) FAIL(c, LFSR_ERR_INVALID_ARG, "unknown disp_mode");
   lfsr_status st;
@@ -321,77 +474,67 @@ lfsr_status lfsr_set_observations(lfsr_ctx* c, const float* lr_views, const floa
   // view offsets to the host (needed for halo sizing) and validation
   const int nv = c->prm.n_views;
   std::vector<float> off(2 * (size_t)nv);
-  CK(c, cudaMemcpyAsync(off.data(), view_offsets, off.size() * 4, mem == LFSR_MEM_HOST ? cudaMemcpyHostToHost : cudaMemcpyDeviceToHost, c->stream));
+  CK(c, cudaMemcpyAsync(off.data(), view_offsets, off.size() * 4,
+                        mem == LFSR_MEM_HOST ? cudaMemcpyHostToHost : cudaMemcpyDeviceToHost, c->stream));
   CK(c, cudaStreamSynchronize(c->stream));
   for (float v : off)
     if (!std::isfinite(v)) FAIL(c, LFSR_ERR_INVALID_ARG, "view_offsets must be finite");
 
   Geom& G = c->G;
-  State& S = c->S;
   const size_t hr = (size_t)G.H * G.ps, lr = (size_t)G.n_views * G.h * G.lps;
   const size_t ws = (size_t)G.s_d * hr;
-  const size_t key[6] = {(size_t)G.n_views, (size_t)G.h, (size_t)G.w, (size_t)G.scale, (size_t)G.s_d, 1};
+  const int nparts = c->xmode == X_LOCAL ? c->prm.n_ranks : 1;
+  const size_t key[6] = {(size_t)G.n_views, (size_t)G.h, (size_t)G.w, (size_t)G.scale, (size_t)G.s_d,
+                         (size_t)nparts};
   c->ready = false;
   free_graph(c);
   if (memcmp(key, c->alloc_key, sizeof key) != 0) {
     free_state(c);
+    c->parts.assign(nparts, Part{});
+    for (Part& P : c->parts)
+      if ((st = alloc_part(c, P)) != LFSR_OK) return st;
     void* p = nullptr;
-#define ALLOC(field, bytes)                                           \
-  do {                                                                \
-    cudaError_t _e = dalloc(c, &p, (bytes));                          \
-    if (_e != cudaSuccess) {                                          \
-      cudaGetLastError();                                             \
-      free_state(c);                                                  \
-      FAIL(c, _e == cudaErrorMemoryAllocation ? LFSR_ERR_OOM : LFSR_ERR_CUDA, "device allocation failed"); \
-    }                                                                 \
-    field = (decltype(field))p;                                       \
-  } while (0)
-    ALLOC(S.x, hr * 4);
-    ALLOC(S.y, lr * 4);
-    ALLOC(S.wA, lr * 4);
-    ALLOC(S.wS[0], ws * 4);
-    ALLOC(S.wS[1], ws * 4);
-    ALLOC(S.density, hr * 4);
-    ALLOC(S.omega, hr * 4);
-    ALLOC(S.wo, hr * 4);
-    ALLOC(S.m, hr * 4);
-    ALLOC(S.r, hr * 4);
-    ALLOC(S.p[0], hr * 4);
-    ALLOC(S.p[1], hr * 4);
-    ALLOC(S.q, hr * 4);
-    ALLOC(S.tmp_hr, hr * 4);
-    ALLOC(S.tmp_lr, lr * 4);
-    ALLOC(c->tmp_hr2, hr * 4);
-    ALLOC(S.ctl, sizeof(Control));
-    ALLOC(c->ring, (size_t)kRingCap * T_COUNT * sizeof(double));
-    ALLOC(c->umax, sizeof(unsigned));
-#undef ALLOC
-    c->ring_cap = kRingCap;
+    cudaError_t e;
+    if ((e = dalloc(c, &p, hr * 4)) != cudaSuccess) return cuda_fail(c, e, "alloc");
+    c->tmp_hr2 = (float*)p;
+    if ((e = dalloc(c, &p, sizeof(unsigned))) != cudaSuccess) return cuda_fail(c, e, "alloc");
+    c->umax = (unsigned*)p;
+    if (nparts > 1) {
+      if ((e = dalloc(c, &p, sizeof(Control*) * nparts)) != cudaSuccess) return cuda_fail(c, e, "alloc");
+      c->d_ctls = (Control**)p;
+      std::vector<Control*> h(nparts);
+      for (int i = 0; i < nparts; ++i) h[i] = c->parts[i].S.ctl;
+      CK(c, cudaMemcpyAsync(c->d_ctls, h.data(), sizeof(Control*) * nparts, cudaMemcpyHostToDevice, c->stream));
+    }
     memcpy(c->alloc_key, key, sizeof key);
   } else {  // same geometry: reset the state in place (Alg.1 lines 1-2: w = 0)
-    CK(c, cudaMemsetAsync(S.wA, 0, lr * 4, c->stream));
-    CK(c, cudaMemsetAsync(S.wS[0], 0, ws * 4, c->stream));
-    CK(c, cudaMemsetAsync(S.wS[1], 0, ws * 4, c->stream));
-    CK(c, cudaMemsetAsync(S.density, 0, hr * 4, c->stream));
-    CK(c, cudaMemsetAsync(S.r, 0, hr * 4, c->stream));
-    CK(c, cudaMemsetAsync(S.q, 0, hr * 4, c->stream));
-    CK(c, cudaMemsetAsync(S.p[0], 0, hr * 4, c->stream));
-    CK(c, cudaMemsetAsync(S.p[1], 0, hr * 4, c->stream));
-    CK(c, cudaMemsetAsync(c->umax, 0, 4, c->stream));
-  }
-  unsigned* umax = c->umax;
-  {
-    Control h{};
-    h.ring = c->ring;
-    h.cap = c->ring_cap;
-    CK(c, cudaMemcpyAsync(S.ctl, &h, sizeof(Control), cudaMemcpyHostToDevice, c->stream));
+    for (Part& P : c->parts) {
+      State& S = P.S;
+      CK(c, cudaMemsetAsync(S.wA, 0, lr * 4, c->stream));
+      CK(c, cudaMemsetAsync(S.wS[0], 0, ws * 4, c->stream));
+      CK(c, cudaMemsetAsync(S.wS[1], 0, ws * 4, c->stream));
+      CK(c, cudaMemsetAsync(S.density, 0, hr * 4, c->stream));
+      CK(c, cudaMemsetAsync(S.r, 0, hr * 4, c->stream));
+      CK(c, cudaMemsetAsync(S.q, 0, hr * 4, c->stream));
+      CK(c, cudaMemsetAsync(S.p[0], 0, hr * 4, c->stream));
+      CK(c, cudaMemsetAsync(S.p[1], 0, hr * 4, c->stream));
+    }
   }
   c->h_iter = 0;
-  CK(c, put2d(c, S.y, G.lps, lr_views, G.w, (size_t)G.n_views * G.h, mem));
-  CK(c, put2d(c, S.omega, G.ps, disparity, G.W, (size_t)G.H, mem));
+  unsigned* umax = c->umax;
+  for (Part& P : c->parts) {
+    Control h{};
+    h.ring = P.ring;
+    h.cap = kRingCap;
+    CK(c, cudaMemcpyAsync(P.S.ctl, &h, sizeof(Control), cudaMemcpyHostToDevice, c->stream));
+    CK(c, put2d(c, P.S.y, G.lps, lr_views, G.w, (size_t)G.n_views * G.h, mem));
+    CK(c, put2d(c, P.S.omega, G.ps, disparity, G.W, (size_t)G.H, mem));
+  }
+  State& S0 = c->parts[0].S;
 
   // halo sizes: S = ceil(max_k |dtheta_k| * max |omega|) per axis, in fp32 like the kernels
-  CK(c, launch_absmax(S.omega, hr, umax, c->stream));
+  CK(c, cudaMemsetAsync(umax, 0, 4, c->stream));
+  CK(c, launch_absmax(S0.omega, hr, umax, c->stream));
   unsigned ubits = 0;
   CK(c, cudaMemcpyAsync(&ubits, umax, 4, cudaMemcpyDeviceToHost, c->stream));
   CK(c, cudaStreamSynchronize(c->stream));
@@ -404,95 +547,320 @@ lfsr_status lfsr_set_observations(lfsr_ctx* c, const float* lr_views, const floa
     mx_rho = std::fmax(mx_rho, std::fabs(off[2 * k]));
     mx_tau = std::fmax(mx_tau, std::fabs(off[2 * k + 1]));
   }
-  G.SX = (int)std::ceil(mx_rho * om_max);
-  G.SY = (int)std::ceil(mx_tau * om_max);
-  if (G.SX > G.W || G.SY > G.H) {
-    G.SX = std::min(G.SX, G.W);
-    G.SY = std::min(G.SY, G.H);
-  }
+  G.SX = std::min((int)std::ceil(mx_rho * om_max), G.W);
+  G.SY = std::min((int)std::ceil(mx_tau * om_max), G.H);
   // fixed-point bounds: max |y| and the splat density max_z sum_k (W_k^T 1)(z)
-  CK(c, launch_density(G, c->V, S.omega, S.density, c->stream));
+  CK(c, launch_density(G, c->V, S0.omega, S0.density, c->stream));
   CK(c, cudaMemsetAsync(umax, 0, 4, c->stream));
-  CK(c, launch_absmax(S.density, hr, umax, c->stream));
+  CK(c, launch_absmax(S0.density, hr, umax, c->stream));
   CK(c, cudaMemcpyAsync(&ubits, umax, 4, cudaMemcpyDeviceToHost, c->stream));
   CK(c, cudaStreamSynchronize(c->stream));
   memcpy(&G.dmax, &ubits, 4);
   CK(c, cudaMemsetAsync(umax, 0, 4, c->stream));
-  CK(c, launch_absmax(S.y, lr, umax, c->stream));
+  CK(c, launch_absmax(S0.y, lr, umax, c->stream));
   CK(c, cudaMemcpyAsync(&ubits, umax, 4, cudaMemcpyDeviceToHost, c->stream));
   CK(c, cudaStreamSynchronize(c->stream));
   memcpy(&G.ymax, &ubits, 4);
   if (!std::isfinite(G.ymax)) G.ymax = 0.f;  // non-finite observations surface as DIVERGED
-  c->T = make_tile_geom(G, c->num_sms);
-  if (c->T.smem > 227 * 1024) {
-    FAIL(c, LFSR_ERR_UNSUPPORTED, "disparity range too large for the shared-memory tile (halo > ~60 px)");
-  }
-  CK(c, prepare_tile_kernels(G.scale, c->T.smem));
 
-  // a1: x0 (bicubic unless given), static w_o, weight map m from x0
-  if (x0) {
-    CK(c, put2d(c, S.x, G.ps, x0, G.W, (size_t)G.H, mem));
+  // strip plan and tile geometry per strip
+  std::vector<lfsr_strip> plan;
+  if (c->prm.n_ranks > 1) {
+    std::string why;
+    if ((st = make_plan(G, c->prm.n_ranks, G.SY, plan, why)) != LFSR_OK) FAIL(c, st, why);
   } else {
-    CK(c, launch_bicubic(G, S.y, S.x, c->stream));
+    plan.resize(1);
+    make_plan(G, 1, G.SY, plan, c->err);
   }
-  CK(c, launch_setup_wo(G, c->V, S.y, S.omega, S.wo, c->stream));
-  CK(c, launch_weights(G, S.x, S.wo, S.m, c->stream));
-  lfsr_status gs = build_graph(c);
+  for (int i = 0; i < nparts; ++i) {
+    Part& P = c->parts[i];
+    P.plan = plan[c->xmode == X_NCCL ? c->prm.rank : i];
+    P.T = make_tile_geom(G, c->num_sms, P.plan.tile_row0, P.plan.tile_row1);
+    if (P.T.smem > 227 * 1024) FAIL(c, LFSR_ERR_UNSUPPORTED, "disparity range too large for the shared-memory tile");
+    if (c->xmode == X_NCCL) {  // fold staging, sized by the halos
+      const size_t rows = (size_t)std::max(P.plan.halo_top, P.plan.halo_bottom) + 64;
+      if (P.stage_rows < rows) {
+        void* p = nullptr;
+        cudaError_t e;
+        if ((e = dalloc(c, &p, rows * G.ps * 4)) != cudaSuccess) return cuda_fail(c, e, "alloc");
+        P.stage[0] = (float*)p;
+        if ((e = dalloc(c, &p, rows * G.ps * 4)) != cudaSuccess) return cuda_fail(c, e, "alloc");
+        P.stage[1] = (float*)p;
+        P.stage_rows = rows;
+      }
+    }
+  }
+  c->Tfull = make_tile_geom(G, c->num_sms, -1, -1);
+  if (c->Tfull.smem > 227 * 1024) FAIL(c, LFSR_ERR_UNSUPPORTED, "disparity range too large for the shared-memory tile");
+  size_t smem_max = c->Tfull.smem;   // the kernels' dynamic smem limit must cover every strip's launch
+  for (const Part& P : c->parts) smem_max = std::max(smem_max, P.T.smem);
+  CK(c, prepare_tile_kernels(G.scale, smem_max));
+
+  // a1 (every strip, whole image): x0 (bicubic unless given), static w_o, m from x0, density
+  for (Part& P : c->parts) {
+    State& S = P.S;
+    if (x0) {
+      CK(c, put2d(c, S.x, G.ps, x0, G.W, (size_t)G.H, mem));
+    } else {
+      CK(c, launch_bicubic(G, S.y, S.x, c->stream));
+    }
+    CK(c, launch_setup_wo(G, c->V, S.y, S.omega, S.wo, c->stream));
+    CK(c, launch_weights(G, S.x, S.wo, S.m, c->stream));
+  }
+  lfsr_status gs = build_graphs(c);
   if (gs != LFSR_OK) return gs;
   CK(c, cudaStreamSynchronize(c->stream));
   c->ready = true;
   return LFSR_OK;
 }
 
-static TileIO base_io(lfsr_ctx* c) {
+static TileIO base_io(const Part& P) {
   TileIO io{};
-  io.omega = c->S.omega;
-  io.ctl = c->S.ctl;
-  io.m = c->S.m;
+  io.omega = P.S.omega;
+  io.ctl = P.S.ctl;
+  io.m = P.S.m;
   return io;
 }
 
-// One ADMM iteration = k_wz + K x (k_normal, k_cg_update), captured once.  In
-// profiling mode an external event-record node brackets every kernel so the
-// bench can read per-kernel device times of each replay.
-static lfsr_status enqueue_iteration(lfsr_ctx* c, cudaStream_t st) {
-  State& S = c->S;
+// ---------------------------------------------------------------------------
+// Halo exchange between strips.  Buffers are full size, so a
+// row has the same address offset in every strip.
+//   fill(buf):  rows [Y0 - top, Y0) <- previous strip, [Y1, Y1 + bot) <- next
+//   fold(buf):  rows [Y0 - top, Y0) -> added into the previous strip (its own
+//               rows), [Y1, Y1 + bot) -> into the next; then zeroed here.
+// planes/plane_stride: the same row ranges in each of `planes` planes (w_S).
+// ---------------------------------------------------------------------------
+struct Rows {
+  int a, b;  // [a, b)
+};
+
+static lfsr_status xfill(lfsr_ctx* c, cudaStream_t st, float* const* bufs, int top, int bot, int planes = 1,
+                         size_t plane_stride = 0) {
   const Geom& G = c->G;
-  int ev = 0;
-  auto mark = [&]() -> cudaError_t {
-    if (!c->profile) return cudaSuccess;
-    return cudaEventRecordWithFlags(c->prof_ev[ev++], st, cudaEventRecordExternal);
-  };
-  CK(c, mark());
-  TileIO io = base_io(c);
-  io.in_hr = S.x;
-  io.y = S.y;
-  io.wA = S.wA;
-  io.wS0 = S.wS[0];
-  io.wS1 = S.wS[1];
-  io.wo = S.wo;
-  io.out_hr = S.r;
-  io.reweight = c->prm.reweight_every_iter;
-  CK(c, launch_tile(MODE_WZ, G, c->V, c->T, io, st));
-  CK(c, mark());
-  for (int k = 1; k <= G.K; ++k) {
-    TileIO n = base_io(c);
-    n.in_hr = S.r;
-    n.in_hr2 = S.p[(k - 1) & 1];
-    n.p_out = S.p[k & 1];
-    n.out_hr = S.q;
-    n.cg_k = k;
-    n.do_nltv = 1;
-    CK(c, launch_tile(MODE_NORMAL, G, c->V, c->T, n, st));
-    CK(c, mark());
-    CK(c, launch_cg_update(G, S.x, S.r, S.p[k & 1], S.q, S.ctl, k, c->num_sms, st));
-    CK(c, mark());
+  const size_t rowf = (size_t)G.ps;
+  if (c->xmode == X_LOCAL) {
+    const int n = (int)c->parts.size();
+    for (int i = 0; i < n; ++i) {
+      const lfsr_strip& s = c->parts[i].plan;
+      Rows up{std::max(s.hr_row0 - top, 0), s.hr_row0}, dn{s.hr_row1, std::min(s.hr_row1 + bot, G.H)};
+      if (i > 0 && up.b > up.a)
+        CK(c, cudaMemcpy2DAsync(bufs[i] + up.a * rowf, plane_stride * 4, bufs[i - 1] + up.a * rowf, plane_stride * 4,
+                                (up.b - up.a) * rowf * 4, planes, cudaMemcpyDeviceToDevice, st));
+      if (i + 1 < n && dn.b > dn.a)
+        CK(c, cudaMemcpy2DAsync(bufs[i] + dn.a * rowf, plane_stride * 4, bufs[i + 1] + dn.a * rowf, plane_stride * 4,
+                                (dn.b - dn.a) * rowf * 4, planes, cudaMemcpyDeviceToDevice, st));
+    }
+    return LFSR_OK;
   }
-  c->launches_per_iter = 1 + 2 * G.K;
+  if (c->xmode == X_NCCL) {
+    const lfsr_strip& s = c->parts[0].plan;
+    const int r = s.rank, n = c->prm.n_ranks;
+    float* b = bufs[0];
+    NK(c, nccl_group_start());
+    for (int pl = 0; pl < planes; ++pl) {
+      float* bp = b + pl * plane_stride;
+      if (r > 0) {  // my first `bot` rows are the previous strip's lower halo; receive my upper halo
+        const int sa = s.hr_row0, sb = std::min(s.hr_row0 + bot, s.hr_row1);
+        NK(c, nccl_send_f32(bp + sa * rowf, (sb - sa) * rowf, r - 1, c->comm, st));
+        const int ra = std::max(s.hr_row0 - top, 0);
+        NK(c, nccl_recv_f32(bp + ra * rowf, (s.hr_row0 - ra) * rowf, r - 1, c->comm, st));
+      }
+      if (r + 1 < n) {
+        const int sa = std::max(s.hr_row1 - top, s.hr_row0), sb = s.hr_row1;
+        NK(c, nccl_send_f32(bp + sa * rowf, (sb - sa) * rowf, r + 1, c->comm, st));
+        const int rb = std::min(s.hr_row1 + bot, G.H);
+        NK(c, nccl_recv_f32(bp + s.hr_row1 * rowf, (rb - s.hr_row1) * rowf, r + 1, c->comm, st));
+      }
+    }
+    NK(c, nccl_group_end());
+  }
   return LFSR_OK;
 }
 
-static lfsr_status build_graph(lfsr_ctx* c) {
+static lfsr_status xfold(lfsr_ctx* c, cudaStream_t st, float* const* bufs, int top, int bot) {
+  const Geom& G = c->G;
+  const size_t rowf = (size_t)G.ps;
+  if (c->xmode == X_LOCAL) {
+    const int n = (int)c->parts.size();
+    for (int i = 0; i < n; ++i) {
+      const lfsr_strip& s = c->parts[i].plan;
+      if (i > 0) {
+        const int a = std::max(s.hr_row0 - top, 0);
+        CK(c, launch_fold_rows(bufs[i - 1] + a * rowf, bufs[i] + a * rowf, (s.hr_row0 - a) * rowf, 1, st));
+      }
+      if (i + 1 < n) {
+        const int b = std::min(s.hr_row1 + bot, G.H);
+        CK(c, launch_fold_rows(bufs[i + 1] + s.hr_row1 * rowf, bufs[i] + s.hr_row1 * rowf, (b - s.hr_row1) * rowf, 1,
+                               st));
+      }
+    }
+    return LFSR_OK;
+  }
+  if (c->xmode == X_NCCL) {
+    Part& P = c->parts[0];
+    const lfsr_strip& s = P.plan;
+    const int r = s.rank, n = c->prm.n_ranks;
+    float* b = bufs[0];
+    const int ua = std::max(s.hr_row0 - top, 0);          // my upper ring rows [ua, Y0)
+    const int db = std::min(s.hr_row1 + bot, G.H);        // my lower ring rows [Y1, db)
+    const int pa = s.hr_row0, pb = std::min(s.hr_row0 + bot, s.hr_row1);  // rows the previous strip folds into mine
+    const int na = std::max(s.hr_row1 - top, s.hr_row0), nb = s.hr_row1;  // rows the next strip folds into mine
+    NK(c, nccl_group_start());
+    if (r > 0) {
+      NK(c, nccl_send_f32(b + ua * rowf, (s.hr_row0 - ua) * rowf, r - 1, c->comm, st));
+      NK(c, nccl_recv_f32(P.stage[0], (pb - pa) * rowf, r - 1, c->comm, st));
+    }
+    if (r + 1 < n) {
+      NK(c, nccl_send_f32(b + s.hr_row1 * rowf, (db - s.hr_row1) * rowf, r + 1, c->comm, st));
+      NK(c, nccl_recv_f32(P.stage[1], (nb - na) * rowf, r + 1, c->comm, st));
+    }
+    NK(c, nccl_group_end());
+    if (r > 0) {
+      CK(c, launch_fold_rows(b + pa * rowf, P.stage[0], (pb - pa) * rowf, 0, st));
+      CK(c, cudaMemsetAsync(b + ua * rowf, 0, (s.hr_row0 - ua) * rowf * 4, st));
+    }
+    if (r + 1 < n) {
+      CK(c, launch_fold_rows(b + na * rowf, P.stage[1], (nb - na) * rowf, 0, st));
+      CK(c, cudaMemsetAsync(b + s.hr_row1 * rowf, 0, (db - s.hr_row1) * rowf * 4, st));
+    }
+  }
+  return LFSR_OK;
+}
+
+static lfsr_status xallreduce(lfsr_ctx* c, cudaStream_t st, int slot0, int count) {
+  if (c->xmode == X_LOCAL) {
+    CK(c, launch_allreduce_local(c->d_ctls, (int)c->parts.size(), slot0, count, st));
+  } else if (c->xmode == X_NCCL) {
+    NK(c, nccl_allreduce_sum_f64(c->parts[0].S.ctl->cur + slot0, count, c->comm, st));
+  }
+  return LFSR_OK;
+}
+
+// One ADMM iteration = k_wz + K x (k_normal, k_cg_update), captured once (per
+// parity of the iteration count: the w_S buffers alternate).  With several
+// strips the exchanges of DESIGN.md §10 sit between the kernels.  In profiling
+// mode (single strip) an external event-record node brackets every kernel.
+static lfsr_status enqueue_iteration(lfsr_ctx* c, cudaStream_t st, int parity) {
+  const Geom& G = c->G;
+  const int np = (int)c->parts.size();
+  const bool multi = c->xmode != X_NONE;
+  int ev = 0, launches = 0;
+  auto mark = [&]() -> cudaError_t {
+    if (!c->profile || multi) return cudaSuccess;
+    return cudaEventRecordWithFlags(c->prof_ev[ev++], st, cudaEventRecordExternal);
+  };
+  std::vector<float*> xs(np), rs(np), qs(np), ms(np), wsw(np), pk(np);
+  for (int i = 0; i < np; ++i) {
+    xs[i] = c->parts[i].S.x;
+    rs[i] = c->parts[i].S.r;
+    qs[i] = c->parts[i].S.q;
+    ms[i] = c->parts[i].S.m;
+    wsw[i] = c->parts[i].S.wS[parity ^ 1];   // written by this iteration's wz-step
+  }
+  const int top = multi ? c->parts[0].plan.halo_top + c->parts[0].plan.halo_bottom : 0;  // see below
+  (void)top;
+  // halo widths are the same for every strip boundary
+  int ht = 0, hb = 0;
+  for (const Part& P : c->parts) {
+    ht = std::max(ht, P.plan.halo_top);
+    hb = std::max(hb, P.plan.halo_bottom);
+  }
+  if (c->xmode == X_NCCL) {  // a single strip sees only its own halos; both directions have the plan widths
+    std::vector<lfsr_strip> plan;
+    std::string why;
+    make_plan(G, c->prm.n_ranks, G.SY, plan, why);
+    for (const lfsr_strip& s : plan) {
+      ht = std::max(ht, s.halo_top);
+      hb = std::max(hb, s.halo_bottom);
+    }
+  }
+  const int r = G.radius;
+  lfsr_status s_;
+#define XC(expr)                                 \
+  do {                                           \
+    if ((s_ = (expr)) != LFSR_OK) return s_;     \
+  } while (0)
+
+  if (multi) XC(xfill(c, st, xs.data(), ht, hb));   // x halo for the wz-step
+  CK(c, mark());
+  for (Part& P : c->parts) {
+    TileIO io = base_io(P);
+    io.in_hr = P.S.x;
+    io.y = P.S.y;
+    io.wA = P.S.wA;
+    io.wS0 = P.S.wS[0];
+    io.wS1 = P.S.wS[1];
+    io.wo = P.S.wo;
+    io.out_hr = P.S.r;
+    io.reweight = c->prm.reweight_every_iter;
+    CK(c, launch_tile(MODE_WZ, G, c->V, P.T, io, st));
+    ++launches;
+  }
+  CK(c, mark());
+  if (multi) {
+    XC(xfold(c, st, rs.data(), ht, hb));                                  // r = -v rings
+    XC(xfill(c, st, ms.data(), r, r));                                    // m for the NLTV normal term
+    XC(xfill(c, st, wsw.data(), r, r, G.s_d, (size_t)G.H * G.ps));        // new w_S for the next wz-step
+    XC(xallreduce(c, st, S_L1, 4));                                       // J terms, |dw|^2
+    XC(xfill(c, st, rs.data(), ht, hb));                                  // r_0 halo
+  }
+  for (int k = 1; k <= G.K; ++k) {
+    for (Part& P : c->parts) {
+      TileIO n = base_io(P);
+      n.in_hr = P.S.r;
+      n.in_hr2 = P.S.p[(k - 1) & 1];
+      n.p_out = P.S.p[k & 1];
+      n.out_hr = P.S.q;
+      n.cg_k = k;
+      n.do_nltv = 1;
+      CK(c, launch_tile(MODE_NORMAL, G, c->V, P.T, n, st));
+      ++launches;
+    }
+    CK(c, mark());
+    if (multi) {
+      XC(xfold(c, st, qs.data(), ht, hb));
+      XC(xallreduce(c, st, S_PQ + k, 1));
+      if (k == 1) XC(xallreduce(c, st, S_PI, 1));
+    }
+    for (Part& P : c->parts) {
+      const lfsr_strip& s = P.plan;
+      CK(c, launch_cg_update(G, P.S.x, P.S.r, P.S.p[k & 1], P.S.q, P.S.ctl, k, s.hr_row0, s.hr_row1 - s.hr_row0,
+                             multi ? 0 : 1, c->num_sms, st));
+      ++launches;
+    }
+    CK(c, mark());
+    if (multi) {
+      XC(xallreduce(c, st, S_PI + k, 1));
+      if (k == G.K) {
+        XC(xallreduce(c, st, S_NF, 1));
+        // the r halo rows hold filled neighbour values; the next wz-step accumulates
+        // its ring into them, so they must start at zero like the own rows
+        for (Part& P : c->parts) {
+          const lfsr_strip& s = P.plan;
+          const int a = std::max(s.hr_row0 - ht, 0), b = std::min(s.hr_row1 + hb, G.H);
+          if (s.hr_row0 > a) CK(c, cudaMemsetAsync(P.S.r + (size_t)a * G.ps, 0, (size_t)(s.hr_row0 - a) * G.ps * 4, st));
+          if (b > s.hr_row1)
+            CK(c, cudaMemsetAsync(P.S.r + (size_t)s.hr_row1 * G.ps, 0, (size_t)(b - s.hr_row1) * G.ps * 4, st));
+        }
+      } else {
+        for (int i = 0; i < np; ++i) pk[i] = c->parts[i].S.p[k & 1];
+        XC(xfill(c, st, rs.data(), ht, hb));
+        XC(xfill(c, st, pk.data(), ht, hb));
+      }
+    }
+  }
+  if (multi) {
+    for (Part& P : c->parts) {
+      CK(c, launch_close(G, P.S.ctl, st));
+      ++launches;
+    }
+  }
+#undef XC
+  c->launches_per_iter = launches;
+  return LFSR_OK;
+}
+
+static lfsr_status build_graphs(lfsr_ctx* c) {
   free_graph(c);
   if (c->profile) {
     size_t need = 2 + 2 * (size_t)c->G.K;
@@ -502,24 +870,27 @@ static lfsr_status build_graph(lfsr_ctx* c) {
       c->prof_ev.push_back(e);
     }
   }
-  CK(c, cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
-  lfsr_status st = enqueue_iteration(c, c->cap_stream);
-  cudaGraph_t g = nullptr;
-  cudaError_t e = cudaStreamEndCapture(c->cap_stream, &g);
-  if (st != LFSR_OK) {
-    if (g) cudaGraphDestroy(g);
-    return st;
+  const int ngraphs = c->xmode == X_NONE ? 1 : 2;  // the strip exchanges name the w_S buffer of each parity
+  for (int g = 0; g < ngraphs; ++g) {
+    CK(c, cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
+    lfsr_status st = enqueue_iteration(c, c->cap_stream, g);
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(c->cap_stream, &graph);
+    if (st != LFSR_OK) {
+      if (graph) cudaGraphDestroy(graph);
+      return st;
+    }
+    if (e != cudaSuccess) return cuda_fail(c, e, "cudaStreamEndCapture");
+    e = cudaGraphInstantiate(&c->graph[g], graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return cuda_fail(c, e, "cudaGraphInstantiate");
   }
-  if (e != cudaSuccess) return cuda_fail(c, e, "cudaStreamEndCapture");
-  e = cudaGraphInstantiate(&c->graph, g, 0);
-  cudaGraphDestroy(g);
-  if (e != cudaSuccess) return cuda_fail(c, e, "cudaGraphInstantiate");
   return LFSR_OK;
 }
 
 static lfsr_status check_run(lfsr_ctx* c) {
   if (!c) return LFSR_ERR_INVALID_ARG;
-  if (c->poisoned) FAIL(c, LFSR_ERR_STATE, "ctx is poisoned by an earlier CUDA error");
+  if (c->poisoned) FAIL(c, LFSR_ERR_STATE, "ctx is poisoned by an earlier CUDA/NCCL error");
   if (!c->ready) FAIL(c, LFSR_ERR_STATE, "ADMM call before lfsr_set_observations");
   return LFSR_OK;
 }
@@ -529,7 +900,10 @@ lfsr_status lfsr_admm_enqueue(lfsr_ctx* c, int32_t n_iters) {
   if (st != LFSR_OK) return st;
   if (n_iters < 0) FAIL(c, LFSR_ERR_INVALID_ARG, "n_iters must be >= 0");
   CK(c, cudaSetDevice(c->prm.device));
-  for (int n = 0; n < n_iters; ++n) CK(c, cudaGraphLaunch(c->graph, c->stream));
+  for (int n = 0; n < n_iters; ++n) {
+    cudaGraphExec_t g = c->graph[c->graph[1] ? (c->h_iter + n) & 1 : 0];
+    CK(c, cudaGraphLaunch(g, c->stream));
+  }
   c->h_iter += n_iters;
   return LFSR_OK;
 }
@@ -537,18 +911,17 @@ lfsr_status lfsr_admm_enqueue(lfsr_ctx* c, int32_t n_iters) {
 lfsr_status lfsr_admm_stats(lfsr_ctx* c, int32_t first_iter, int32_t n_iters, lfsr_iter_stats* stats) {
   lfsr_status st = check_run(c);
   if (st != LFSR_OK) return st;
-  if (n_iters < 0 || first_iter < 1 || first_iter + n_iters - 1 > c->h_iter ||
-      first_iter <= c->h_iter - c->ring_cap)
+  if (n_iters < 0 || first_iter < 1 || first_iter + n_iters - 1 > c->h_iter || first_iter <= c->h_iter - kRingCap)
     FAIL(c, LFSR_ERR_INVALID_ARG, "requested iterations are not in the stats window");
   if (n_iters == 0) return LFSR_OK;
   CK(c, cudaSetDevice(c->prm.device));
+  const double* ring = c->parts[0].ring;
   std::vector<double> rec((size_t)n_iters * T_COUNT);
-  // records [first-1, first-1+n) modulo the ring (at most two contiguous pieces)
   int done = 0;
-  while (done < n_iters) {
-    int slot = (first_iter - 1 + done) % c->ring_cap;
-    int cnt = std::min(n_iters - done, c->ring_cap - slot);
-    CK(c, cudaMemcpyAsync(rec.data() + (size_t)done * T_COUNT, c->ring + (size_t)slot * T_COUNT,
+  while (done < n_iters) {  // at most two contiguous pieces of the ring
+    int slot = (first_iter - 1 + done) % kRingCap;
+    int cnt = std::min(n_iters - done, kRingCap - slot);
+    CK(c, cudaMemcpyAsync(rec.data() + (size_t)done * T_COUNT, ring + (size_t)slot * T_COUNT,
                           (size_t)cnt * T_COUNT * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     done += cnt;
   }
@@ -583,8 +956,7 @@ lfsr_status lfsr_admm_run(lfsr_ctx* c, int32_t n_iters, lfsr_iter_stats* stats) 
   if (n_iters == 0) return LFSR_OK;
   const int first = c->h_iter + 1;
   if ((st = lfsr_admm_enqueue(c, n_iters)) != LFSR_OK) return st;
-  // divergence is checked over the whole run even when only the last ring window is readable
-  const int n_read = std::min(n_iters, c->ring_cap);
+  const int n_read = std::min(n_iters, kRingCap);
   if (stats && n_read < n_iters) FAIL(c, LFSR_ERR_INVALID_ARG, "stats requested for more than 4096 iterations");
   return lfsr_admm_stats(c, first + (n_iters - n_read), n_read, stats);
 }
@@ -593,11 +965,12 @@ lfsr_status lfsr_profile(lfsr_ctx* c, int32_t enable) {
   lfsr_status st = check_run(c);
   if (st != LFSR_OK) return st;
   for (int i = 0; i < 3; ++i) c->prof_ms[i] = 0.0, c->prof_n[i] = 0;
+  if (c->xmode != X_NONE) return LFSR_OK;  // per-kernel events only for a single strip
   if ((enable != 0) == c->profile) return LFSR_OK;
   CK(c, cudaSetDevice(c->prm.device));
   CK(c, cudaStreamSynchronize(c->stream));
   c->profile = enable != 0;
-  return build_graph(c);
+  return build_graphs(c);
 }
 
 lfsr_status lfsr_profile_read(lfsr_ctx* c, double* ms, int64_t* launches) {
@@ -623,40 +996,85 @@ lfsr_status lfsr_profile_read(lfsr_ctx* c, double* ms, int64_t* launches) {
   return LFSR_OK;
 }
 
+// Gather every strip's own rows of the solver state into strip 0's buffers
+// (virtual ranks: device copies; NCCL: broadcast from each rank).
+static lfsr_status gather(lfsr_ctx* c) {
+  if (c->xmode == X_NONE) return LFSR_OK;
+  const Geom& G = c->G;
+  const size_t rowf = G.ps, lrowf = G.lps, plane = (size_t)G.H * G.ps;
+  const int cur = c->h_iter & 1;
+  if (c->xmode == X_LOCAL) {
+    State& D = c->parts[0].S;
+    for (size_t i = 1; i < c->parts.size(); ++i) {
+      const State& S = c->parts[i].S;
+      const lfsr_strip& s = c->parts[i].plan;
+      const size_t a = s.hr_row0 * rowf, n = (size_t)(s.hr_row1 - s.hr_row0) * rowf;
+      CK(c, cudaMemcpyAsync(D.x + a, S.x + a, n * 4, cudaMemcpyDeviceToDevice, c->stream));
+      CK(c, cudaMemcpyAsync(D.m + a, S.m + a, n * 4, cudaMemcpyDeviceToDevice, c->stream));
+      CK(c, cudaMemcpy2DAsync(D.wS[cur] + a, plane * 4, S.wS[cur] + a, plane * 4, n * 4, G.s_d,
+                              cudaMemcpyDeviceToDevice, c->stream));
+      const size_t la = s.lr_row0 * lrowf, ln = (size_t)(s.lr_row1 - s.lr_row0) * lrowf;
+      CK(c, cudaMemcpy2DAsync(D.wA + la, (size_t)G.h * lrowf * 4, S.wA + la, (size_t)G.h * lrowf * 4, ln * 4,
+                              G.n_views, cudaMemcpyDeviceToDevice, c->stream));
+    }
+    return LFSR_OK;
+  }
+  // NCCL: every rank broadcasts its strip
+  std::vector<lfsr_strip> plan;
+  std::string why;
+  make_plan(G, c->prm.n_ranks, G.SY, plan, why);
+  State& D = c->parts[0].S;
+  NK(c, nccl_group_start());
+  for (const lfsr_strip& s : plan) {
+    const size_t a = s.hr_row0 * rowf, n = (size_t)(s.hr_row1 - s.hr_row0) * rowf;
+    NK(c, nccl_bcast_f32(D.x + a, n, s.rank, c->comm, c->stream));
+    NK(c, nccl_bcast_f32(D.m + a, n, s.rank, c->comm, c->stream));
+    for (int d = 0; d < G.s_d; ++d) NK(c, nccl_bcast_f32(D.wS[cur] + d * plane + a, n, s.rank, c->comm, c->stream));
+    const size_t la = s.lr_row0 * lrowf, ln = (size_t)(s.lr_row1 - s.lr_row0) * lrowf;
+    for (int k = 0; k < G.n_views; ++k)
+      NK(c, nccl_bcast_f32(D.wA + (size_t)k * G.h * lrowf + la, ln, s.rank, c->comm, c->stream));
+  }
+  NK(c, nccl_group_end());
+  return LFSR_OK;
+}
+
 lfsr_status lfsr_get_hr(lfsr_ctx* c, float* x_out, lfsr_mem mem) {
   if (!c) return LFSR_ERR_INVALID_ARG;
-  if (c->poisoned) FAIL(c, LFSR_ERR_STATE, "ctx is poisoned by an earlier CUDA error");
+  if (c->poisoned) FAIL(c, LFSR_ERR_STATE, "ctx is poisoned by an earlier CUDA/NCCL error");
   if (!c->ready) FAIL(c, LFSR_ERR_STATE, "lfsr_get_hr before lfsr_set_observations");
   lfsr_status st;
   if ((st = check_ptr(c, x_out, mem, "x_out")) != LFSR_OK) return st;
   CK(c, cudaSetDevice(c->prm.device));
-  CK(c, get2d(c, x_out, c->G.W, c->S.x, c->G.ps, (size_t)c->G.H, mem));
+  if ((st = gather(c)) != LFSR_OK) return st;
+  CK(c, get2d(c, x_out, c->G.W, c->parts[0].S.x, c->G.ps, (size_t)c->G.H, mem));
   if (mem == LFSR_MEM_HOST) CK(c, cudaStreamSynchronize(c->stream));
   return LFSR_OK;
 }
 
 lfsr_status lfsr_get_state(lfsr_ctx* c, float* w_A, float* w_S, float* x, float* m, lfsr_mem mem) {
   if (!c) return LFSR_ERR_INVALID_ARG;
-  if (c->poisoned) FAIL(c, LFSR_ERR_STATE, "ctx is poisoned by an earlier CUDA error");
+  if (c->poisoned) FAIL(c, LFSR_ERR_STATE, "ctx is poisoned by an earlier CUDA/NCCL error");
   if (!c->ready) FAIL(c, LFSR_ERR_STATE, "lfsr_get_state before lfsr_set_observations");
   const Geom& G = c->G;
   lfsr_status st;
   CK(c, cudaSetDevice(c->prm.device));
+  if ((st = gather(c)) != LFSR_OK) return st;
+  const State& S = c->parts[0].S;
   if (w_A) {
     if ((st = check_ptr(c, w_A, mem, "w_A")) != LFSR_OK) return st;
-    CK(c, get2d(c, w_A, G.w, c->S.wA, G.lps, (size_t)G.n_views * G.h, mem));
+    CK(c, get2d(c, w_A, G.w, S.wA, G.lps, (size_t)G.n_views * G.h, mem));
   }
   if (w_S) {
     if ((st = check_ptr(c, w_S, mem, "w_S")) != LFSR_OK) return st;
-    CK(c, get2d(c, w_S, G.W, c->S.wS[c->h_iter & 1], G.ps, (size_t)G.s_d * G.H, mem));
+    CK(c, get2d(c, w_S, G.W, S.wS[c->h_iter & 1], G.ps, (size_t)G.s_d * G.H, mem));
   }
   if (x) {
     if ((st = check_ptr(c, x, mem, "x")) != LFSR_OK) return st;
-    CK(c, get2d(c, x, G.W, c->S.x, G.ps, (size_t)G.H, mem));
+    CK(c, get2d(c, x, G.W, S.x, G.ps, (size_t)G.H, mem));
   }
   if (m) {
     if ((st = check_ptr(c, m, mem, "m")) != LFSR_OK) return st;
-    CK(c, get2d(c, m, G.W, c->S.m, G.ps, (size_t)G.H, mem));
+    CK(c, get2d(c, m, G.W, S.m, G.ps, (size_t)G.H, mem));
   }
   if (mem == LFSR_MEM_HOST) CK(c, cudaStreamSynchronize(c->stream));
   return LFSR_OK;
@@ -664,14 +1082,17 @@ lfsr_status lfsr_get_state(lfsr_ctx* c, float* w_A, float* w_S, float* x, float*
 
 lfsr_status lfsr_op_apply(lfsr_ctx* c, lfsr_op op, const float* in, float* out, lfsr_mem mem) {
   if (!c) return LFSR_ERR_INVALID_ARG;
-  if (c->poisoned) FAIL(c, LFSR_ERR_STATE, "ctx is poisoned by an earlier CUDA error");
+  if (c->poisoned) FAIL(c, LFSR_ERR_STATE, "ctx is poisoned by an earlier CUDA/NCCL error");
   if (!c->ready) FAIL(c, LFSR_ERR_STATE, "lfsr_op_apply before lfsr_set_observations");
   lfsr_status st;
   if ((st = check_ptr(c, in, mem, "in")) != LFSR_OK) return st;
   if ((st = check_ptr(c, out, mem, "out")) != LFSR_OK) return st;
   CK(c, cudaSetDevice(c->prm.device));
+  if ((st = gather(c)) != LFSR_OK) return st;   // the current weight map m on strip 0
   const Geom& G = c->G;
-  State& S = c->S;
+  Part& P0 = c->parts[0];
+  State& S = P0.S;
+  const TileGeom& T = c->Tfull;   // the operators act on the whole image
   const size_t hr = (size_t)G.H * G.ps;
   cudaStream_t s = c->stream;
   if ((op == LFSR_OP_S || op == LFSR_OP_ST) && !c->tmp_s) {
@@ -686,10 +1107,10 @@ lfsr_status lfsr_op_apply(lfsr_ctx* c, lfsr_op op, const float* in, float* out, 
   switch (op) {
     case LFSR_OP_A: {
       CK(c, put2d(c, S.tmp_hr, G.ps, in, G.W, (size_t)G.H, mem));
-      TileIO io = base_io(c);
+      TileIO io = base_io(P0);
       io.in_hr = S.tmp_hr;
       io.out_lr = S.tmp_lr;
-      CK(c, launch_tile(MODE_A, G, c->V, c->T, io, s));
+      CK(c, launch_tile(MODE_A, G, c->V, T, io, s));
       CK(c, get2d(c, out, G.w, S.tmp_lr, G.lps, (size_t)G.n_views * G.h, mem));
       break;
     }
@@ -701,22 +1122,22 @@ lfsr_status lfsr_op_apply(lfsr_ctx* c, lfsr_op op, const float* in, float* out, 
       unsigned ub = 0;
       CK(c, cudaMemcpyAsync(&ub, c->umax, 4, cudaMemcpyDeviceToHost, s));
       CK(c, cudaStreamSynchronize(s));
-      TileIO io = base_io(c);
+      TileIO io = base_io(P0);
       memcpy(&io.tmax_in, &ub, 4);
       io.in_lr = S.tmp_lr;
       io.out_hr = c->tmp_hr2;
-      CK(c, launch_tile(MODE_AT, G, c->V, c->T, io, s));
+      CK(c, launch_tile(MODE_AT, G, c->V, T, io, s));
       CK(c, get2d(c, out, G.W, c->tmp_hr2, G.ps, (size_t)G.H, mem));
       break;
     }
     case LFSR_OP_NORMAL: {
       CK(c, put2d(c, S.tmp_hr, G.ps, in, G.W, (size_t)G.H, mem));
       CK(c, cudaMemsetAsync(c->tmp_hr2, 0, hr * 4, s));
-      TileIO io = base_io(c);
+      TileIO io = base_io(P0);
       io.in_hr = S.tmp_hr;
       io.out_hr = c->tmp_hr2;
       io.do_nltv = 1;
-      CK(c, launch_tile(MODE_NORMAL, G, c->V, c->T, io, s));
+      CK(c, launch_tile(MODE_NORMAL, G, c->V, T, io, s));
       CK(c, get2d(c, out, G.W, c->tmp_hr2, G.ps, (size_t)G.H, mem));
       break;
     }

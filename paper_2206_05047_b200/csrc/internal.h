@@ -79,7 +79,8 @@ struct TileGeom {
   int32_t SYe, SXe;           // halo of the input tile around the E region (>= radius)
   int32_t PH, PW, PWZ;        // input tile rows, row pitch (= zeta * PWZ), phase pitch
   int32_t MH, MW;             // m tile (own + radius halo)
-  int32_t ntY, ntX;           // tiles per axis
+  int32_t ntY, ntX;           // tiles per axis (whole image)
+  int32_t tY0, ntYl;          // this strip's tile rows [tY0, tY0 + ntYl)
   int32_t groups;             // view groups (CTAs per tile)
   int32_t vpg;                // views per group
   int32_t nwarps;             // warps per CTA (views of a group are dealt round-robin)

@@ -38,6 +38,9 @@
 #define LFSR_CRING 0          // 1: the forward pass stores each sample's cells/fractions in a per-warp
                               //    shared ring, the adjoint pass reloads them instead of recomputing
 #endif
+#ifndef LFSR_BLOCK2
+#define LFSR_BLOCK2 1         // 1: zeta = 2 adjoint scatters the 2x2 positions of an LR step as one 3x3 patch
+#endif
 #ifndef LFSR_SMEM_DIET
 #define LFSR_SMEM_DIET 0      // 1: disparity and (NORMAL) weights read through L1 instead of shared tiles
 #endif
@@ -131,11 +134,10 @@ struct Tile {
   int ps;
   int4* CR;           // this warp's coordinate ring [NTAP][Z][32] (LFSR_CRING) or nullptr
 
-  // floor and fraction without the XU pipe: round(s - 1/2) by the 1.5*2^23 magic
-  // (|s| < 2^22).  At exact integers s = n this may return n - 1 with fraction 1,
-  // which selects the same bilinear value (the input tile has one spare row/column).
+  // floor and fraction without the XU pipe: s + 1.5*2^23 rounded toward -inf is
+  // 1.5*2^23 + floor(s) exactly (|s| < 2^22), so its bit pattern is the integer.
   __device__ __forceinline__ static void axis(float s, int org, int& n, float& f) {
-    const float r = (s - 0.5f) + 12582912.0f;
+    const float r = __fadd_rd(s, 12582912.0f);
     n = __float_as_int(r) - (0x4B400000 + org);
     f = s - (r - 12582912.0f);
   }
@@ -210,6 +212,80 @@ struct Tile {
       h = fmaf(taps[v], val, h);
     }
     return h;
+  }
+
+  // The Z rows of one LR step together (Z = 2): horizontal adjoint blur of both rows,
+  // then, when every lane's 2x2 positions hit a regular 3x3 patch of source cells
+  // (smooth disparity: vertically and horizontally adjacent samples share cells),
+  // 9 merged contributions instead of 16; otherwise the per-row path.
+  __device__ __forceinline__ void adj_rows2(int er, int lane, const float (&t1b)[2], float drho, float dtau,
+                                            const float* taps) const {
+    constexpr int NJ = 2 * TC<Z>::R / Z + 1;
+    int i00[2][2], i01[2][2];
+    float v00[2][2], v01[2][2], v10[2][2], v11[2][2];
+    bool reg = true;
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+      float tv[NJ];
+      tv[0] = t1b[rr];
+#pragma unroll
+      for (int j = 1; j < NJ; ++j) {
+        const float v = __shfl_up_sync(0xffffffffu, t1b[rr], j);
+        tv[j] = lane >= j ? v : 0.f;
+      }
+      float om[Z];
+      load_om(er + rr, lane, om);
+      const float Yf = (float)(YE0 + er + rr);
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        float t = 0.f;
+#pragma unroll
+        for (int j = 0; j < NJ; ++j)
+          if (Z * j + s <= 2 * TC<Z>::R) t = fmaf(taps[Z * j + s], tv[j], t);
+        float a, b;
+        sample(Yf, (float)(XE0 + Z * lane + s), om[s], drho, dtau, i00[rr][s], i01[rr][s], a, b);
+        const float ts = valid(er + rr, s) ? t * tscale : 0.f;
+        const float ta = ts * a, t1a = ts - ta;
+        v01[rr][s] = t1a * b;
+        v00[rr][s] = t1a - v01[rr][s];
+        v11[rr][s] = ta * b;
+        v10[rr][s] = ta - v11[rr][s];
+      }
+      reg = reg && (i00[rr][1] == i01[rr][0]);
+    }
+    reg = reg && (i00[1][0] == i00[0][0] + PW) && (i00[1][1] == i00[0][1] + PW);
+    if (__all_sync(0xffffffffu, reg)) {
+      const int c0 = i00[0][0], c1 = i00[0][1], c2 = i01[0][1];
+      acc_add(ACC, lo, c0, v00[0][0]);
+      acc_add(ACC, lo, c1, v01[0][0] + v00[0][1]);
+      acc_add(ACC, lo, c2, v01[0][1]);
+      acc_add(ACC, lo, c0 + PW, v10[0][0] + v00[1][0]);
+      acc_add(ACC, lo, c1 + PW, (v11[0][0] + v10[0][1]) + (v01[1][0] + v00[1][1]));
+      acc_add(ACC, lo, c2 + PW, v11[0][1] + v01[1][1]);
+      acc_add(ACC, lo, c0 + 2 * PW, v10[1][0]);
+      acc_add(ACC, lo, c1 + 2 * PW, v11[1][0] + v10[1][1]);
+      acc_add(ACC, lo, c2 + 2 * PW, v11[1][1]);
+    } else {
+#pragma unroll
+      for (int rr = 0; rr < 2; ++rr) {
+        if (i00[rr][1] == i01[rr][0]) {
+          acc_add(ACC, lo, i00[rr][0], v00[rr][0]);
+          acc_add(ACC, lo, i00[rr][0] + PW, v10[rr][0]);
+          acc_add(ACC, lo, i00[rr][1], v00[rr][1] + v01[rr][0]);
+          acc_add(ACC, lo, i00[rr][1] + PW, v10[rr][1] + v11[rr][0]);
+          acc_add(ACC, lo, i01[rr][1], v01[rr][1]);
+          acc_add(ACC, lo, i01[rr][1] + PW, v11[rr][1]);
+        } else {
+#pragma unroll
+          for (int s = 0; s < 2; ++s) {
+            acc_add(ACC, lo, i00[rr][s], v00[rr][s]);
+            acc_add(ACC, lo, i01[rr][s], v01[rr][s]);
+            acc_add(ACC, lo, i00[rr][s] + PW, v10[rr][s]);
+            acc_add(ACC, lo, i01[rr][s] + PW, v11[rr][s]);
+          }
+        }
+      }
+    }
   }
 
   // Horizontal adjoint blur of the row's LR-column values t1b and the exact bilinear
@@ -429,8 +505,13 @@ __device__ __forceinline__ void views(const Tile<Z, INT>& t, const Geom& G, cons
       if (kAdj) {
 #pragma unroll
         for (int u = 0; u < NTAP; ++u) br[u] = fmaf(taps[u], rho, br[u]);  // vertical adjoint (polyphase)
+        if constexpr (Z == 2 && LFSR_BLOCK2) {
+          const float tb[2] = {br[0], br[1]};
+          t.adj_rows2(Z * li, lane, tb, drho, dtau, taps);
+        } else {
 #pragma unroll
-        for (int u = 0; u < Z; ++u) t.adj_row(Z * li + u, lane, br[u], drho, dtau, taps);
+          for (int u = 0; u < Z; ++u) t.adj_row(Z * li + u, lane, br[u], drho, dtau, taps);
+        }
 #pragma unroll
         for (int u = 0; u < NTAP; ++u) br[u] = (u < KEEP) ? br[u + Z] : 0.f;
       }
@@ -447,17 +528,17 @@ __global__ void __launch_bounds__(LFSR_MAXW * 32, LFSR_MINB)
 k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
   using C = TC<Z>;
   constexpr int R = C::R, LX = C::LX, BL = C::BL, TY = C::TY, TX = C::TX;
-  constexpr int EY = C::EY, ECOL = C::ECOL, NTAP = C::NTAP, KEEP = C::KEEP;
+  constexpr int EY = C::EY, ECOL = C::ECOL;
   constexpr bool kFwd = (MODE != MODE_AT);
   constexpr bool kAdj = (MODE != MODE_A);
 
   extern __shared__ __align__(16) float smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int NT = blockDim.x, NW = NT >> 5;
-  const int ntiles = T.ntY * T.ntX;
+  const int ntiles = T.ntYl * T.ntX;                 // tiles of this strip (all tiles with one rank)
   const int tile = blockIdx.x % ntiles;
   const int grp = blockIdx.x / ntiles;
-  const int ti = tile / T.ntX, tj = tile % T.ntX;
+  const int ti = T.tY0 + tile / T.ntX, tj = tile % T.ntX;
   const int i0 = ti * BL, j0 = tj * LX;          // LR origin of the tile
   const int Y0 = i0 * Z, X0 = j0 * Z;             // HR origin of the own pixels
   const int YE0 = Y0 - R, XE0 = X0 - R;           // E-region origin
@@ -764,9 +845,18 @@ cudaError_t prepare_tile_kernels(int scale, size_t smem) {
   return e;
 }
 
+// Static tile constants for the strip planner (capi.cu).
+void tile_static(int scale, int& BL, int& LX, int& R, int& KEEP) {
+  switch (scale) {
+    case 2: BL = TC<2>::BL; LX = TC<2>::LX; R = TC<2>::R; KEEP = TC<2>::KEEP; break;
+    case 3: BL = TC<3>::BL; LX = TC<3>::LX; R = TC<3>::R; KEEP = TC<3>::KEEP; break;
+    default: BL = TC<4>::BL; LX = TC<4>::LX; R = TC<4>::R; KEEP = TC<4>::KEEP; break;
+  }
+}
+
 // Views per warp and warps per CTA: every warp of a group gets the same number of
 // views (or one less); view groups are added until the grid fills the GPU.
-TileGeom make_tile_geom(const Geom& G, int num_sms) {
+TileGeom make_tile_geom(const Geom& G, int num_sms, int tr0, int tr1) {
   TileGeom T{};
   switch (G.scale) {
     case 2: fill_static<2>(T); break;
@@ -783,7 +873,9 @@ TileGeom make_tile_geom(const Geom& G, int num_sms) {
   T.MW = T.TX + 2 * G.radius;
   T.ntY = (G.h + T.BL - 1) / T.BL;
   T.ntX = (G.w + T.LX - 1) / T.LX;
-  const int tiles = T.ntY * T.ntX;
+  T.tY0 = tr0 < 0 ? 0 : tr0;
+  T.ntYl = (tr1 < 0 ? T.ntY : tr1) - T.tY0;
+  const int tiles = T.ntYl * T.ntX;
   const int max_warps = LFSR_MAXW;
   T.smem = smem_bytes(T, max_warps);
   if (prepare_tile_kernels(G.scale, T.smem) != cudaSuccess) cudaGetLastError();
@@ -815,7 +907,7 @@ TileGeom make_tile_geom(const Geom& G, int num_sms) {
 
 template <int Z, int MODE>
 static cudaError_t launch_z(const Geom& G, const Views& V, const TileGeom& T, const TileIO& io, cudaStream_t st) {
-  dim3 grid(T.ntY * T.ntX * T.groups);
+  dim3 grid(T.ntYl * T.ntX * T.groups);
   k_tile<Z, MODE><<<grid, T.nwarps * 32, MODE == MODE_NORMAL ? T.smem_normal : T.smem, st>>>(G, V, T, io);
   return cudaGetLastError();
 }

@@ -31,7 +31,7 @@ OPS = {"A": OP_A, "AT": OP_AT, "S": OP_S, "ST": OP_ST, "NORMAL": OP_NORMAL, "WEI
 # every symbol include/lfsr.h declares (checked by tests/test_abi.py)
 EXPORTS = ("lfsr_create", "lfsr_set_observations", "lfsr_admm_run", "lfsr_admm_enqueue", "lfsr_admm_stats",
            "lfsr_get_hr", "lfsr_get_state", "lfsr_op_apply", "lfsr_launches_per_iter", "lfsr_profile",
-           "lfsr_profile_read", "lfsr_destroy", "lfsr_last_error", "lfsr_abi_version")
+           "lfsr_profile_read", "lfsr_strip_plan", "lfsr_destroy", "lfsr_last_error", "lfsr_abi_version")
 
 
 class LFSRError(RuntimeError):
@@ -60,6 +60,14 @@ class _CStats(ctypes.Structure):
 
 
 STAT_KEYS = [f[0] for f in _CStats._fields_]
+
+
+class _CStrip(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in ("rank", "tile_row0", "tile_row1", "lr_row0", "lr_row1", "hr_row0",
+                                               "hr_row1", "halo_top", "halo_bottom")]
+
+
+STRIP_KEYS = [f[0] for f in _CStrip._fields_]
 
 _lib = None
 
@@ -102,6 +110,8 @@ def load_library(path: str = LIB_PATH):
     lib.lfsr_destroy.restype = None
     lib.lfsr_last_error.argtypes = [vp]
     lib.lfsr_last_error.restype = ctypes.c_char_p
+    lib.lfsr_strip_plan.argtypes = [P(_CParams), ctypes.c_int32, P(_CStrip)]
+    lib.lfsr_strip_plan.restype = st
     lib.lfsr_abi_version.argtypes = []
     lib.lfsr_abi_version.restype = ctypes.c_int32
     _lib = lib
@@ -129,6 +139,9 @@ class Params:
     cg_tol: float = 0.0
     reweight_every_iter: int = 1
     device: int = 0
+    n_ranks: int = 1          # HR row strips
+    rank: int = 0             # this process's strip (NCCL mode) or -1: all strips in this ctx
+    nccl_unique_id: bytes | None = None
 
     @property
     def H(self):
@@ -145,8 +158,12 @@ class Params:
     def to_c(self, stream=None) -> _CParams:
         c = _CParams()
         for f in fields(self):
-            setattr(c, f.name, getattr(self, f.name))
-        c.rank, c.n_ranks, c.nccl_unique_id = 0, 1, None
+            if f.name != "nccl_unique_id":
+                setattr(c, f.name, getattr(self, f.name))
+        self._uid = None
+        if self.nccl_unique_id is not None:
+            self._uid = ctypes.create_string_buffer(bytes(self.nccl_unique_id), 128)
+            c.nccl_unique_id = ctypes.cast(self._uid, ctypes.c_void_p)
         c.stream = stream
         return c
 
@@ -293,6 +310,17 @@ class Solver:
     @property
     def launches_per_iter(self) -> int:
         return int(self.lib.lfsr_launches_per_iter(self._h))
+
+
+def strip_plan(params: Params, max_shift_rows: int):
+    """Row-strip plan of the multi-GPU decomposition (lfsr_strip_plan; no device needed)."""
+    lib = load_library()
+    out = (_CStrip * params.n_ranks)()
+    cp = params.to_c()
+    s = lib.lfsr_strip_plan(ctypes.byref(cp), int(max_shift_rows), out)
+    if s != LFSR_OK:
+        raise LFSRError(s, lib.lfsr_last_error(None).decode())
+    return [{k: getattr(out[i], k) for k in STRIP_KEYS} for i in range(params.n_ranks)]
 
 
 def params_for(lf_meta_or_cfg, defaults=None, **over) -> Params:
