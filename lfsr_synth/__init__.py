@@ -43,15 +43,17 @@ __all__ = ["CONFIGS", "LightField", "SolverDefaults", "make_lightfield", "grid_o
 
 @dataclass(frozen=True)
 class SolverDefaults:
-    """Solver constants for the bench/parity configs (reading A20; frozen before timing)."""
+    """Solver constants for the bench/parity configs (reading A20; frozen before timing).
+    Chosen by a PSNR sweep of the GPU solver over lambda2 x lambda_reg x theta x sigma_e on
+    C2/C3/C4 at N = 10 (tools/sweep.py, DESIGN.md §3 A20)."""
     lambda1: float = 1.0
-    lambda2: float = 10.0
-    lambda_reg: float = 0.05
+    lambda2: float = 0.1
+    lambda_reg: float = 0.5
     sigma_s: float = 3.0
-    sigma_e: float = 0.01
+    sigma_e: float = 0.2
     sigma_o1: float = 0.5
     sigma_o2: float = 0.2
-    theta: float = 1.0
+    theta: float = 4.0
     radius: int = 2          # 5x5 NLTV window (P:L1197)
     cg_max_iters: int = 5    # K = 5 (P:L1197)
     cg_tol: float = 0.0      # tau = 0: exactly K steps (reading A18)

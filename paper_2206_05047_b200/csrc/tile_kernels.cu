@@ -39,7 +39,10 @@
                               //    shared ring, the adjoint pass reloads them instead of recomputing
 #endif
 #ifndef LFSR_BLOCK2
-#define LFSR_BLOCK2 1         // 1: zeta = 2 adjoint scatters the 2x2 positions of an LR step as one 3x3 patch
+#define LFSR_BLOCK2 0         // 1: zeta = 2 adjoint scatters the 2x2 positions of an LR step as one 3x3 patch
+#endif
+#ifndef LFSR_VPAIR
+#define LFSR_VPAIR 1          // 2: a warp interleaves two views (ILP); 1: one view at a time
 #endif
 #ifndef LFSR_SMEM_DIET
 #define LFSR_SMEM_DIET 0      // 1: disparity and (NORMAL) weights read through L1 instead of shared tiles
@@ -48,7 +51,10 @@
 namespace lfsr {
 
 template <int Z> struct TileCfg;
-template <> struct TileCfg<2> { static constexpr int R = 2, LX = 30, BL = 16; };
+#ifndef LFSR_BL2
+#define LFSR_BL2 16           // LR rows per tile at zeta = 2
+#endif
+template <> struct TileCfg<2> { static constexpr int R = 2, LX = 30, BL = LFSR_BL2; };
 template <> struct TileCfg<3> { static constexpr int R = 3, LX = 30, BL = 11; };
 template <> struct TileCfg<4> { static constexpr int R = 3, LX = 31, BL = 8; };
 
@@ -432,57 +438,67 @@ __device__ __forceinline__ float nltv_pixel(const NltvCtx& c, const Geom& G, int
 }
 
 // Phase 2 of k_tile: every warp streams whole views through the tile (see header).
-template <int Z, int MODE, bool INT>
-__device__ __forceinline__ void views(const Tile<Z, INT>& t, const Geom& G, const Views& V, const TileGeom& T,
-                                      const TileIO& io, int grp, int lane, int warp, int NW, int i0, int j0,
-                                      double& red_a, double& red_b, double& red_c) {
+// NV views are processed interleaved row by row (independent dependency chains
+// for the scheduler); the last odd view of a warp takes the NV = 1 path.
+template <int Z, int MODE, bool INT, int NV>
+__device__ __forceinline__ void view_pass(const Tile<Z, INT>& t, const Geom& G, const Views& V, const TileIO& io,
+                                          const int (&ks)[NV], int lane, int i0, int j0, double& red_a,
+                                          double& red_b, double& red_c) {
   using C = TC<Z>;
   constexpr int LX = C::LX, BL = C::BL, NTAP = C::NTAP, KEEP = C::KEEP;
   constexpr bool kFwd = (MODE != MODE_AT);
   constexpr bool kAdj = (MODE != MODE_A);
-  const int kbeg = grp * T.vpg;
-  const int kend = min(G.n_views, kbeg + T.vpg);
   const float lam1 = G.lambda1, lam2 = G.lambda2, ith = G.inv_theta;
   const float* taps = G.taps;
   const int j = j0 + lane;
   const bool col_ok = lane < LX && j < G.w;
-  for (int k = kbeg + warp; k < kend; k += NW) {
-    const float drho = V.off[k].x, dtau = V.off[k].y;
-    float fr[NTAP], br[NTAP];
+  float drho[NV], dtau[NV], fr[NV][NTAP], br[NV][NTAP], y_nx[NV], wa_nx[NV];
+  size_t lrow0[NV];
 #pragma unroll
-    for (int u = 0; u < NTAP; ++u) { fr[u] = 0.f; br[u] = 0.f; }
-    if (kFwd) {
+  for (int v = 0; v < NV; ++v) {
+    drho[v] = V.off[ks[v]].x;
+    dtau[v] = V.off[ks[v]].y;
 #pragma unroll
-      for (int u = 0; u < KEEP; ++u) fr[u] = t.fwd_row(u, lane, drho, dtau, taps);
-    }
-    const size_t lrow0 = ((size_t)k * G.h) * G.lps + j;
+    for (int u = 0; u < NTAP; ++u) { fr[v][u] = 0.f; br[v][u] = 0.f; }
+    lrow0[v] = ((size_t)ks[v] * G.h) * G.lps + j;
+    y_nx[v] = 0.f;
+    wa_nx[v] = 0.f;
     // software prefetch of the next LR row's observation and dual (WZ)
-    float y_nx = 0.f, wa_nx = 0.f;
     if (MODE == MODE_WZ && col_ok && i0 < G.h) {
-      y_nx = io.y[lrow0 + (size_t)i0 * G.lps];
-      wa_nx = io.wA[lrow0 + (size_t)i0 * G.lps];
+      y_nx[v] = io.y[lrow0[v] + (size_t)i0 * G.lps];
+      wa_nx[v] = io.wA[lrow0[v] + (size_t)i0 * G.lps];
     }
-    for (int li = 0; li < BL; ++li) {
-      const int i = i0 + li;
-      const bool ok = col_ok && i < G.h;
-      const size_t lg = lrow0 + (size_t)i * G.lps;
-      float y_cur = y_nx, wa_cur = wa_nx;
+  }
+  if (kFwd) {
+#pragma unroll
+    for (int u = 0; u < KEEP; ++u)
+#pragma unroll
+      for (int v = 0; v < NV; ++v) fr[v][u] = t.fwd_row(u, lane, drho[v], dtau[v], taps);
+  }
+  for (int li = 0; li < BL; ++li) {
+    const int i = i0 + li;
+    const bool ok = col_ok && i < G.h;
+    float rho[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const size_t lg = lrow0[v] + (size_t)i * G.lps;
+      const float y_cur = y_nx[v], wa_cur = wa_nx[v];
       if (MODE == MODE_WZ && col_ok && li + 1 < BL && i + 1 < G.h) {
-        y_nx = io.y[lg + G.lps];
-        wa_nx = io.wA[lg + G.lps];
+        y_nx[v] = io.y[lg + G.lps];
+        wa_nx[v] = io.wA[lg + G.lps];
       }
-      float rho = 0.f;
+      rho[v] = 0.f;
       if (kFwd) {
 #pragma unroll
-        for (int u = 0; u < Z; ++u) fr[KEEP + u] = t.fwd_row(Z * li + KEEP + u, lane, drho, dtau, taps);
+        for (int u = 0; u < Z; ++u) fr[v][KEEP + u] = t.fwd_row(Z * li + KEEP + u, lane, drho[v], dtau[v], taps);
         float a = 0.f;
 #pragma unroll
-        for (int u = 0; u < NTAP; ++u) a = fmaf(taps[u], fr[u], a);   // A_k x at LR pixel (i, j)
+        for (int u = 0; u < NTAP; ++u) a = fmaf(taps[u], fr[v][u], a);   // A_k x at LR pixel (i, j)
         if (ok) {
           if (MODE == MODE_A) {
             io.out_lr[lg] = a;
           } else if (MODE == MODE_NORMAL) {
-            rho = G.cA * a;
+            rho[v] = G.cA * a;
             red_a += (double)G.cA * (double)a * (double)a;      // <p, c_A A^T A p> = c_A |A p|^2
           } else if (MODE == MODE_WZ) {
             const float e_ = a - y_cur;                         // e = A_k x - y_k (Alg.1 line 4)
@@ -490,7 +506,7 @@ __device__ __forceinline__ void views(const Tile<Z, INT>& t, const Geom& G, cons
             const float u = lam1 * e_ + wa;                     // u = F x - b' + w (line 5)
             const float wn = fminf(fmaxf(u, -ith), ith);        // w+ = u - prox(u) = clamp (A5/A6)
             const float f = 2.f * wn - wa;                      // f = 2w^n - w^{n-1} (line 8)
-            rho = lam2 * e_ + G.cS * lam1 * f;                  // A^T a + (th/2) F^T f, data rows
+            rho[v] = lam2 * e_ + G.cS * lam1 * f;               // A^T a + (th/2) F^T f, data rows
             io.wA[lg] = wn;
             red_a += fabs((double)e_);
             red_b += (double)e_ * e_;
@@ -498,28 +514,52 @@ __device__ __forceinline__ void views(const Tile<Z, INT>& t, const Geom& G, cons
           }
         }
 #pragma unroll
-        for (int u = 0; u < KEEP; ++u) fr[u] = fr[u + Z];
+        for (int u = 0; u < KEEP; ++u) fr[v][u] = fr[v][u + Z];
       } else {
-        rho = ok ? io.in_lr[lg] : 0.f;
-      }
-      if (kAdj) {
-#pragma unroll
-        for (int u = 0; u < NTAP; ++u) br[u] = fmaf(taps[u], rho, br[u]);  // vertical adjoint (polyphase)
-        if constexpr (Z == 2 && LFSR_BLOCK2) {
-          const float tb[2] = {br[0], br[1]};
-          t.adj_rows2(Z * li, lane, tb, drho, dtau, taps);
-        } else {
-#pragma unroll
-          for (int u = 0; u < Z; ++u) t.adj_row(Z * li + u, lane, br[u], drho, dtau, taps);
-        }
-#pragma unroll
-        for (int u = 0; u < NTAP; ++u) br[u] = (u < KEEP) ? br[u + Z] : 0.f;
+        rho[v] = ok ? io.in_lr[lg] : 0.f;
       }
     }
     if (kAdj) {
 #pragma unroll
-      for (int u = 0; u < KEEP; ++u) t.adj_row(Z * BL + u, lane, br[u], drho, dtau, taps);
+      for (int v = 0; v < NV; ++v) {
+#pragma unroll
+        for (int u = 0; u < NTAP; ++u) br[v][u] = fmaf(taps[u], rho[v], br[v][u]);  // vertical adjoint
+        if constexpr (Z == 2 && LFSR_BLOCK2) {
+          const float tb[2] = {br[v][0], br[v][1]};
+          t.adj_rows2(Z * li, lane, tb, drho[v], dtau[v], taps);
+        } else {
+#pragma unroll
+          for (int u = 0; u < Z; ++u) t.adj_row(Z * li + u, lane, br[v][u], drho[v], dtau[v], taps);
+        }
+#pragma unroll
+        for (int u = 0; u < NTAP; ++u) br[v][u] = (u < KEEP) ? br[v][u + Z] : 0.f;
+      }
     }
+  }
+  if (kAdj) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+#pragma unroll
+      for (int u = 0; u < KEEP; ++u) t.adj_row(Z * BL + u, lane, br[v][u], drho[v], dtau[v], taps);
+  }
+}
+
+template <int Z, int MODE, bool INT>
+__device__ __forceinline__ void views(const Tile<Z, INT>& t, const Geom& G, const Views& V, const TileGeom& T,
+                                      const TileIO& io, int grp, int lane, int warp, int NW, int i0, int j0,
+                                      double& red_a, double& red_b, double& red_c) {
+  const int kbeg = grp * T.vpg;
+  const int kend = min(G.n_views, kbeg + T.vpg);
+  int k = kbeg + warp;
+  if (LFSR_VPAIR > 1) {
+    for (; k + NW < kend; k += 2 * NW) {
+      const int ks[2] = {k, k + NW};
+      view_pass<Z, MODE, INT, 2>(t, G, V, io, ks, lane, i0, j0, red_a, red_b, red_c);
+    }
+  }
+  for (; k < kend; k += NW) {
+    const int ks[1] = {k};
+    view_pass<Z, MODE, INT, 1>(t, G, V, io, ks, lane, i0, j0, red_a, red_b, red_c);
   }
 }
 

@@ -120,7 +120,7 @@ def load_library(path: str = LIB_PATH):
 
 @dataclass
 class Params:
-    """lfsr_params (include/lfsr.h).  Defaults: reading A20 starting point, K=5, 5x5 window."""
+    """lfsr_params (include/lfsr.h).  Defaults: reading A20, K=5, 5x5 window."""
     n_views: int
     lr_height: int
     lr_width: int
@@ -128,13 +128,13 @@ class Params:
     ref_view: int = 0
     nltv_radius: int = 2
     lambda1: float = 1.0
-    lambda2: float = 10.0
-    lambda_reg: float = 0.05
+    lambda2: float = 0.1
+    lambda_reg: float = 0.5
     sigma_s: float = 3.0
-    sigma_e: float = 0.01
+    sigma_e: float = 0.2
     sigma_o1: float = 0.5
     sigma_o2: float = 0.2
-    theta: float = 1.0
+    theta: float = 4.0
     cg_max_iters: int = 5
     cg_tol: float = 0.0
     reweight_every_iter: int = 1

@@ -239,3 +239,46 @@ def test_divergence_guard(lfsr_mod):
         s.admm_run(2)
     assert ei.value.status == 6  # LFSR_ERR_DIVERGED
     assert ei.value.stats[0]["nonfinite"] == 1
+
+
+def test_full_size_C5_sampled(lfsr_mod):
+    """C5 (9x9 views, 512^2 -> 2048^2, zeta = 4) at full size in the bench launch configuration:
+    A and the normal operator are checked on interior crops the oracle can afford (an interior
+    pixel only sees its neighbourhood, so a crop with a margin wider than the operator's reach
+    gives the same values), plus the adjoint identity over the whole image."""
+    lf = S.make_lightfield("C5")
+    d = S.SolverDefaults()
+    c = S.CONFIGS["C5"]
+    p = lfsr_mod.params_for(c, d)
+    s = lfsr_mod.Solver(p)
+    s.set_observations(lf.y, lf.view_offsets, lf.omega)
+    g = np.random.default_rng(5)
+    x = g.uniform(-1, 1, (c.H, c.W)).astype(np.float32)
+    ax = s.op("A", x)
+    mx = s.op("NORMAL", x)
+    m = s.get_state()["m"]
+    z = c.scale
+    margin_lr = 16                                   # >= reach: (R + S_max + 1) / zeta, doubled for M
+    for (i0, j0) in [(100, 140), (300, 37), (470, 420)]:
+        h = w = 24
+        li0, lj0 = i0 - margin_lr, j0 - margin_lr
+        hh, ww = h + 2 * margin_lr, w + 2 * margin_lr
+        P = O.Params(n_views=c.n_views, lr_h=hh, lr_w=ww, scale=z, ref_view=c.ref_view, radius=d.radius,
+                     lambda1=d.lambda1, lambda2=d.lambda2, lambda_reg=d.lambda_reg, sigma_s=d.sigma_s,
+                     sigma_e=d.sigma_e, sigma_o1=d.sigma_o1, sigma_o2=d.sigma_o2, theta=d.theta)
+        sl = (slice(li0 * z, (li0 + hh) * z), slice(lj0 * z, (lj0 + ww) * z))
+        a_ora = O.apply_A(P, lf.view_offsets, lf.omega[sl], x[sl])
+        inner = (slice(None), slice(margin_lr, margin_lr + h), slice(margin_lr, margin_lr + w))
+        got = ax[:, i0:i0 + h, j0:j0 + w]
+        assert rel_l2(got, a_ora[inner]) < OP_TOL
+        m_ora = O.normal(P, lf.view_offsets, lf.omega[sl], m[sl], x[sl])
+        inner_hr = (slice(margin_lr * z, (margin_lr + h) * z), slice(margin_lr * z, (margin_lr + w) * z))
+        got_m = mx[i0 * z:(i0 + h) * z, j0 * z:(j0 + w) * z]
+        assert rel_l2(got_m, m_ora[inner_hr]) < OP_TOL
+    r = g.standard_normal((c.n_views, c.lr_h, c.lr_w)).astype(np.float32)
+    atr = s.op("AT", r).astype(np.float64)
+    lhs, rhs = float(np.vdot(ax.astype(np.float64), r)), float(np.vdot(x.astype(np.float64), atr))
+    assert abs(lhs - rhs) <= 1e-6 * np.linalg.norm(ax) * np.linalg.norm(r)
+    st = s.admm_run(1)
+    assert st[0]["cg_iters"] == d.cg_max_iters and not st[0]["nonfinite"]
+    s.close()

@@ -468,3 +468,22 @@ def test_oracle_deterministic_across_threads(oracle_lib):
         env = dict(os.environ, OMP_NUM_THREADS=nt, PYTHONPATH=root)
         outs.append(subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, check=True).stdout)
     assert outs[0] == outs[1] and len(outs[0]) > 0
+
+
+# ----------------------------------------------------------------------------- P15 usefulness
+@pytest.mark.slow
+def test_P15_admm_improves_psnr(oracle_lib):
+    """Sanity (not parity): the method recovers detail — N = 10 ADMM iterations on a 3x3 light
+    field with mixed noise (sigma = 10/255, 10 % impulses) raise PSNR over the bicubic x0 by
+    >= 3 dB (the desk-scale analogue of P:L900-908)."""
+    import lfsr_synth as S
+    cfg = S.Config("P15", 3, 32, 32, 2, 10.0 / 255.0, 10.0, 1.5, "hci", 10)
+    lf = S.make_lightfield(cfg, seed=77)
+    d = S.SolverDefaults()
+    P = O.Params(n_views=9, lr_h=32, lr_w=32, scale=2, ref_view=4, radius=d.radius, lambda1=d.lambda1,
+                 lambda2=d.lambda2, lambda_reg=d.lambda_reg, sigma_s=d.sigma_s, sigma_e=d.sigma_e,
+                 sigma_o1=d.sigma_o1, sigma_o2=d.sigma_o2, theta=d.theta, cg_max_iters=d.cg_max_iters)
+    res = O.admm(P, lf.y, lf.view_offsets, lf.omega, 10)
+    p0 = O.psnr(res.x_iters[0], lf.x_gt)
+    pN = O.psnr(res.x_iters[-1], lf.x_gt)
+    assert pN >= p0 + 3.0, (p0, pN)
