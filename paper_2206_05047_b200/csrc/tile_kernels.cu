@@ -142,9 +142,12 @@ struct Tile {
 
   // floor and fraction without the XU pipe: s + 1.5*2^23 rounded toward -inf is
   // 1.5*2^23 + floor(s) exactly (|s| < 2^22), so its bit pattern is the integer.
-  __device__ __forceinline__ static void axis(float s, int org, int& n, float& f) {
+  // The coordinates are tile-local (origin PY0/PX0, |s| < ~300), so the fraction
+  // keeps ~2^-15 absolute precision whatever the image size (an absolute HR
+  // coordinate near 2048 would leave only 2^-12).
+  __device__ __forceinline__ static void axis(float s, int& n, float& f) {
     const float r = __fadd_rd(s, 12582912.0f);
-    n = __float_as_int(r) - (0x4B400000 + org);
+    n = __float_as_int(r) - 0x4B400000;
     f = s - (r - 12582912.0f);
   }
 
@@ -158,8 +161,8 @@ struct Tile {
                                          int& i00, int& i01, float& a, float& b) const {
     const float sy = fmaf(dtau, om, Yf), sx = fmaf(drho, om, Xf);
     int iy, ix;
-    axis(sy, PY0, iy, a);
-    axis(sx, PX0, ix, b);
+    axis(sy, iy, a);
+    axis(sx, ix, b);
     const unsigned ux = (unsigned)ix, ph = ux % Z, q = ux / Z;
     i00 = iy * PW + (int)(ph * PWZ + q);
     i01 = (ph == Z - 1) ? i00 - (Z - 1) * PWZ + 1 : i00 + PWZ;
@@ -198,12 +201,12 @@ struct Tile {
   __device__ __forceinline__ float fwd_row(int er, int lane, float drho, float dtau, const float* taps) const {
     float om[Z], wp[Z];
     load_om(er, lane, om);
-    const float Yf = (float)(YE0 + er);
+    const float Yf = (float)(YE0 - PY0 + er);
 #pragma unroll
     for (int s = 0; s < Z; ++s) {
       int i00, i01;
       float a, b;
-      sample(Yf, (float)(XE0 + Z * lane + s), om[s], drho, dtau, i00, i01, a, b);
+      sample(Yf, (float)(XE0 - PX0 + Z * lane + s), om[s], drho, dtau, i00, i01, a, b);
       if (LFSR_CRING && CR)
         CR[((er % TC<Z>::NTAP) * Z + s) * 32 + lane] = make_int4(i00, i01, __float_as_int(a), __float_as_int(b));
       const float p00 = P[i00], p01 = P[i01], p10 = P[i00 + PW], p11 = P[i01 + PW];
@@ -241,7 +244,7 @@ struct Tile {
       }
       float om[Z];
       load_om(er + rr, lane, om);
-      const float Yf = (float)(YE0 + er + rr);
+      const float Yf = (float)(YE0 - PY0 + er + rr);
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
         float t = 0.f;
@@ -249,7 +252,7 @@ struct Tile {
         for (int j = 0; j < NJ; ++j)
           if (Z * j + s <= 2 * TC<Z>::R) t = fmaf(taps[Z * j + s], tv[j], t);
         float a, b;
-        sample(Yf, (float)(XE0 + Z * lane + s), om[s], drho, dtau, i00[rr][s], i01[rr][s], a, b);
+        sample(Yf, (float)(XE0 - PX0 + Z * lane + s), om[s], drho, dtau, i00[rr][s], i01[rr][s], a, b);
         const float ts = valid(er + rr, s) ? t * tscale : 0.f;
         const float ta = ts * a, t1a = ts - ta;
         v01[rr][s] = t1a * b;
@@ -311,7 +314,7 @@ struct Tile {
     float om[Z];
     const bool ring = LFSR_CRING && CR;
     if (!ring) load_om(er, lane, om);
-    const float Yf = (float)(YE0 + er);
+    const float Yf = (float)(YE0 - PY0 + er);
     const int4* slot = ring ? CR + (er % TC<Z>::NTAP) * Z * 32 + lane : nullptr;
     int i00[Z], i01[Z];
     float v00[Z], v01[Z], v10[Z], v11[Z];
@@ -330,7 +333,7 @@ struct Tile {
         a = __int_as_float(cr.z);
         b = __int_as_float(cr.w);
       } else {
-        sample(Yf, (float)(XE0 + Z * lane + s), om[s], drho, dtau, i00[s], i01[s], a, b);
+        sample(Yf, (float)(XE0 - PX0 + Z * lane + s), om[s], drho, dtau, i00[s], i01[s], a, b);
       }
       const float ts = valid(er, s) ? t * tscale : 0.f;
       const float ta = ts * a, t1a = ts - ta;
