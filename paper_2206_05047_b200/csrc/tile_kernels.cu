@@ -34,13 +34,6 @@
 #ifndef LFSR_MINB
 #define LFSR_MINB 1           // min CTAs per SM requested from ptxas
 #endif
-#ifndef LFSR_CRING
-#define LFSR_CRING 0          // 1: the forward pass stores each sample's cells/fractions in a per-warp
-                              //    shared ring, the adjoint pass reloads them instead of recomputing
-#endif
-#ifndef LFSR_BLOCK2
-#define LFSR_BLOCK2 0         // 1: zeta = 2 adjoint scatters the 2x2 positions of an LR step as one 3x3 patch
-#endif
 #ifndef LFSR_VPAIR
 #define LFSR_VPAIR 1          // 2: a warp interleaves two views (ILP); 1: one view at a time
 #endif
@@ -106,17 +99,6 @@ constexpr float kMagic = 12582912.0f;   // 1.5 * 2^23
 constexpr int kMagicBits = 0x4B400000;
 constexpr int kLoBits = 15;
 
-__device__ __forceinline__ int fix(float v) { return __float_as_int(v + kMagic) - kMagicBits; }
-
-__device__ __forceinline__ void acc_add(int* hi, int lo_off, int i, float v) {
-  const float t = v + kMagic;
-  const int q1 = __float_as_int(t) - kMagicBits;
-  const float r = v - (t - kMagic);
-  const int q2 = __float_as_int(fmaf(r, (float)(1 << kLoBits), kMagic)) - kMagicBits;
-  atomicAdd(hi + i, q1);
-  atomicAdd(hi + lo_off + i, q2);
-}
-
 // phase-split shared index of tile-local (py, px): columns of equal px % Z are
 // contiguous, so lanes zeta columns apart hit consecutive banks.
 template <int Z>
@@ -125,10 +107,33 @@ __device__ __forceinline__ int pidx(int py, int px, int PW, int PWZ) {
   return py * PW + (int)((ux % Z) * PWZ + ux / Z);
 }
 
+// Packed FP32 (sm_100 FFMA2/FADD2/FMUL2): two lanes of fp32 arithmetic per
+// issue slot.  Each packed op rounds every component exactly like its scalar
+// counterpart (x - y is computed as fma(y, -1, x), which rounds once), so the
+// pairing changes the instruction count, not the results.
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ float2 f2s(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 sub2(float2 x, float2 y) { return __ffma2_rn(y, f2s(-1.f), x); }
+
+// Two-word fixed-point accumulation of a pair of values into the cells i and j
+// (see kLoBits): the conversions run packed, the four ATOMS.ADD stay scalar.
+__device__ __forceinline__ void acc_add2(int* hi, int lo_off, int i, int j, float2 v) {
+  const float2 t = __fadd2_rn(v, f2s(kMagic));
+  const float2 r = sub2(v, __fadd2_rn(t, f2s(-kMagic)));
+  const float2 u = __ffma2_rn(r, f2s((float)(1 << kLoBits)), f2s(kMagic));
+  atomicAdd(hi + i, __float_as_int(t.x) - kMagicBits);
+  atomicAdd(hi + j, __float_as_int(t.y) - kMagicBits);
+  atomicAdd(hi + lo_off + i, __float_as_int(u.x) - kMagicBits);
+  atomicAdd(hi + lo_off + j, __float_as_int(u.y) - kMagicBits);
+}
+
 // Tile-local arithmetic of one CTA.  INT (interior tile): every E position and
 // every sample lies inside the image, so no clamping or validity test is needed.
+// A lane's zeta E columns are processed in pairs (s, s+1) with packed FP32; an
+// odd zeta leaves one scalar column.
 template <int Z, bool INT>
 struct Tile {
+  static constexpr int NP = Z / 2;     // column pairs per lane
   const float* P;
   int* ACC;
   const float* OM;
@@ -138,34 +143,52 @@ struct Tile {
   int lo;             // offset of the residual accumulator from ACC (ints)
   const float* omega; // global disparity (LFSR_SMEM_DIET)
   int ps;
-  int4* CR;           // this warp's coordinate ring [NTAP][Z][32] (LFSR_CRING) or nullptr
 
   // floor and fraction without the XU pipe: s + 1.5*2^23 rounded toward -inf is
   // 1.5*2^23 + floor(s) exactly (|s| < 2^22), so its bit pattern is the integer.
   // The coordinates are tile-local (origin PY0/PX0, |s| < ~300), so the fraction
   // keeps ~2^-15 absolute precision whatever the image size (an absolute HR
   // coordinate near 2048 would leave only 2^-12).
-  __device__ __forceinline__ static void axis(float s, int& n, float& f) {
-    const float r = __fadd_rd(s, 12582912.0f);
-    n = __float_as_int(r) - 0x4B400000;
-    f = s - (r - 12582912.0f);
+  __device__ __forceinline__ static void axis2(float2 s, int& n0, int& n1, float2& f) {
+    const float2 r = __fadd2_rd(s, f2s(kMagic));
+    n0 = __float_as_int(r.x) - kMagicBits;
+    n1 = __float_as_int(r.y) - kMagicBits;
+    f = sub2(s, __fadd2_rn(r, f2s(-kMagic)));
   }
-
-  // Tile-local phase-split indices of the sample's top-left / top-right cells and
-  // the bilinear fractions for the E position at HR (Yf, Xf) (A12/A13).
-  // No clamping: the input tile holds the image replicate-padded, and a bilinear
-  // sample of the replicate-padded image equals the sample at the clamped
-  // coordinate; the adjoint scatters into the padding and phase 4 folds it back
-  // onto the edge cells (the transpose of the padding).
-  __device__ __forceinline__ void sample(float Yf, float Xf, float om, float drho, float dtau,
-                                         int& i00, int& i01, float& a, float& b) const {
-    const float sy = fmaf(dtau, om, Yf), sx = fmaf(drho, om, Xf);
-    int iy, ix;
-    axis(sy, iy, a);
-    axis(sx, ix, b);
+  __device__ __forceinline__ static void axis(float s, int& n, float& f) {
+    const float r = __fadd_rd(s, kMagic);
+    n = __float_as_int(r) - kMagicBits;
+    f = s - (r - kMagic);
+  }
+  // phase-split indices of the top-left / top-right source cells of tile cell (iy, ix)
+  __device__ __forceinline__ void cells(int iy, int ix, int& i00, int& i01) const {
     const unsigned ux = (unsigned)ix, ph = ux % Z, q = ux / Z;
     i00 = iy * PW + (int)(ph * PWZ + q);
     i01 = (ph == Z - 1) ? i00 - (Z - 1) * PWZ + 1 : i00 + PWZ;
+  }
+
+  // Source cells and bilinear fractions of the E positions (Yf, Xf) and
+  // (Yf, Xf + 1) (A12/A13).  No clamping: the input tile holds the
+  // image replicate-padded, and a bilinear sample of the replicate-padded image
+  // equals the sample at the clamped coordinate; the adjoint scatters into the
+  // padding and phase 4 folds it back onto the edge cells (the transpose of the
+  // padding).
+  __device__ __forceinline__ void sample2(float Yf, float Xf, float2 om, float drho, float dtau,
+                                          int (&i00)[2], int (&i01)[2], float2& a, float2& b) const {
+    const float2 sy = __ffma2_rn(f2s(dtau), om, f2s(Yf));
+    const float2 sx = __ffma2_rn(f2s(drho), om, f2(Xf, Xf + 1.f));
+    int iy0, iy1, ix0, ix1;
+    axis2(sy, iy0, iy1, a);
+    axis2(sx, ix0, ix1, b);
+    cells(iy0, ix0, i00[0], i01[0]);
+    cells(iy1, ix1, i00[1], i01[1]);
+  }
+  __device__ __forceinline__ void sample(float Yf, float Xf, float om, float drho, float dtau,
+                                         int& i00, int& i01, float& a, float& b) const {
+    int iy, ix;
+    axis(fmaf(dtau, om, Yf), iy, a);
+    axis(fmaf(drho, om, Xf), ix, b);
+    cells(iy, ix, i00, i01);
   }
 
   // E positions outside the image carry zero (blur zero padding, A11): row test is
@@ -199,111 +222,55 @@ struct Tile {
 
   // W_k then the horizontal blur taps at this lane's LR column, for E row er.
   __device__ __forceinline__ float fwd_row(int er, int lane, float drho, float dtau, const float* taps) const {
+    constexpr int NTAP = TC<Z>::NTAP;
     float om[Z], wp[Z];
     load_om(er, lane, om);
     const float Yf = (float)(YE0 - PY0 + er);
+    const float X0 = (float)(XE0 - PX0 + Z * lane);
 #pragma unroll
-    for (int s = 0; s < Z; ++s) {
+    for (int k = 0; k < NP; ++k) {
+      const int s = 2 * k;
+      int i00[2], i01[2];
+      float2 a, b;
+      sample2(Yf, X0 + (float)s, f2(om[s], om[s + 1]), drho, dtau, i00, i01, a, b);
+      const float2 p00 = f2(P[i00[0]], P[i00[1]]), p01 = f2(P[i01[0]], P[i01[1]]);
+      const float2 p10 = f2(P[i00[0] + PW], P[i00[1] + PW]), p11 = f2(P[i01[0] + PW], P[i01[1] + PW]);
+      const float2 top = __ffma2_rn(b, sub2(p01, p00), p00), bot = __ffma2_rn(b, sub2(p11, p10), p10);
+      const float2 v = __ffma2_rn(a, sub2(bot, top), top);
+      wp[s] = valid(er, s) ? v.x : 0.f;
+      wp[s + 1] = valid(er, s + 1) ? v.y : 0.f;
+    }
+    if constexpr (Z & 1) {
+      constexpr int s = Z - 1;
       int i00, i01;
       float a, b;
-      sample(Yf, (float)(XE0 - PX0 + Z * lane + s), om[s], drho, dtau, i00, i01, a, b);
-      if (LFSR_CRING && CR)
-        CR[((er % TC<Z>::NTAP) * Z + s) * 32 + lane] = make_int4(i00, i01, __float_as_int(a), __float_as_int(b));
+      sample(Yf, X0 + (float)s, om[s], drho, dtau, i00, i01, a, b);
       const float p00 = P[i00], p01 = P[i01], p10 = P[i00 + PW], p11 = P[i01 + PW];
       const float top = fmaf(b, p01 - p00, p00), bot = fmaf(b, p11 - p10, p10);
       const float v = fmaf(a, bot - top, top);
       wp[s] = valid(er, s) ? v : 0.f;
     }
-    float h = 0.f;
+    float val[NTAP];
 #pragma unroll
-    for (int v = 0; v < TC<Z>::NTAP; ++v) {
-      const float val = (v < Z) ? wp[v % Z] : __shfl_down_sync(0xffffffffu, wp[v % Z], v / Z);
-      h = fmaf(taps[v], val, h);
-    }
+    for (int v = 0; v < NTAP; ++v)
+      val[v] = (v < Z) ? wp[v % Z] : __shfl_down_sync(0xffffffffu, wp[v % Z], v / Z);
+    float2 h2 = f2s(0.f);
+#pragma unroll
+    for (int v = 0; v + 1 < NTAP; v += 2) h2 = __ffma2_rn(f2(taps[v], taps[v + 1]), f2(val[v], val[v + 1]), h2);
+    float h = h2.x + h2.y;
+    if constexpr (NTAP & 1) h = fmaf(taps[NTAP - 1], val[NTAP - 1], h);
     return h;
-  }
-
-  // The Z rows of one LR step together (Z = 2): horizontal adjoint blur of both rows,
-  // then, when every lane's 2x2 positions hit a regular 3x3 patch of source cells
-  // (smooth disparity: vertically and horizontally adjacent samples share cells),
-  // 9 merged contributions instead of 16; otherwise the per-row path.
-  __device__ __forceinline__ void adj_rows2(int er, int lane, const float (&t1b)[2], float drho, float dtau,
-                                            const float* taps) const {
-    constexpr int NJ = 2 * TC<Z>::R / Z + 1;
-    int i00[2][2], i01[2][2];
-    float v00[2][2], v01[2][2], v10[2][2], v11[2][2];
-    bool reg = true;
-#pragma unroll
-    for (int rr = 0; rr < 2; ++rr) {
-      float tv[NJ];
-      tv[0] = t1b[rr];
-#pragma unroll
-      for (int j = 1; j < NJ; ++j) {
-        const float v = __shfl_up_sync(0xffffffffu, t1b[rr], j);
-        tv[j] = lane >= j ? v : 0.f;
-      }
-      float om[Z];
-      load_om(er + rr, lane, om);
-      const float Yf = (float)(YE0 - PY0 + er + rr);
-#pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        float t = 0.f;
-#pragma unroll
-        for (int j = 0; j < NJ; ++j)
-          if (Z * j + s <= 2 * TC<Z>::R) t = fmaf(taps[Z * j + s], tv[j], t);
-        float a, b;
-        sample(Yf, (float)(XE0 - PX0 + Z * lane + s), om[s], drho, dtau, i00[rr][s], i01[rr][s], a, b);
-        const float ts = valid(er + rr, s) ? t * tscale : 0.f;
-        const float ta = ts * a, t1a = ts - ta;
-        v01[rr][s] = t1a * b;
-        v00[rr][s] = t1a - v01[rr][s];
-        v11[rr][s] = ta * b;
-        v10[rr][s] = ta - v11[rr][s];
-      }
-      reg = reg && (i00[rr][1] == i01[rr][0]);
-    }
-    reg = reg && (i00[1][0] == i00[0][0] + PW) && (i00[1][1] == i00[0][1] + PW);
-    if (__all_sync(0xffffffffu, reg)) {
-      const int c0 = i00[0][0], c1 = i00[0][1], c2 = i01[0][1];
-      acc_add(ACC, lo, c0, v00[0][0]);
-      acc_add(ACC, lo, c1, v01[0][0] + v00[0][1]);
-      acc_add(ACC, lo, c2, v01[0][1]);
-      acc_add(ACC, lo, c0 + PW, v10[0][0] + v00[1][0]);
-      acc_add(ACC, lo, c1 + PW, (v11[0][0] + v10[0][1]) + (v01[1][0] + v00[1][1]));
-      acc_add(ACC, lo, c2 + PW, v11[0][1] + v01[1][1]);
-      acc_add(ACC, lo, c0 + 2 * PW, v10[1][0]);
-      acc_add(ACC, lo, c1 + 2 * PW, v11[1][0] + v10[1][1]);
-      acc_add(ACC, lo, c2 + 2 * PW, v11[1][1]);
-    } else {
-#pragma unroll
-      for (int rr = 0; rr < 2; ++rr) {
-        if (i00[rr][1] == i01[rr][0]) {
-          acc_add(ACC, lo, i00[rr][0], v00[rr][0]);
-          acc_add(ACC, lo, i00[rr][0] + PW, v10[rr][0]);
-          acc_add(ACC, lo, i00[rr][1], v00[rr][1] + v01[rr][0]);
-          acc_add(ACC, lo, i00[rr][1] + PW, v10[rr][1] + v11[rr][0]);
-          acc_add(ACC, lo, i01[rr][1], v01[rr][1]);
-          acc_add(ACC, lo, i01[rr][1] + PW, v11[rr][1]);
-        } else {
-#pragma unroll
-          for (int s = 0; s < 2; ++s) {
-            acc_add(ACC, lo, i00[rr][s], v00[rr][s]);
-            acc_add(ACC, lo, i01[rr][s], v01[rr][s]);
-            acc_add(ACC, lo, i00[rr][s] + PW, v10[rr][s]);
-            acc_add(ACC, lo, i01[rr][s] + PW, v11[rr][s]);
-          }
-        }
-      }
-    }
   }
 
   // Horizontal adjoint blur of the row's LR-column values t1b and the exact bilinear
   // scatter (W_k^T) of the lane's zeta positions into the fixed-point accumulator.
-  // When every lane's positions hit adjacent source columns (smooth disparity) the
-  // shared columns are merged first: 2 zeta + 2 atomics instead of 4 zeta.
+  // A position's four weights go out as two (row, row + 1) pairs; when every lane's
+  // positions hit adjacent source columns (smooth disparity) the shared columns are
+  // merged first: zeta + 1 pairs instead of 2 zeta.
   __device__ __forceinline__ void adj_row(int er, int lane, float t1b, float drho, float dtau,
                                           const float* taps) const {
     constexpr int NJ = 2 * TC<Z>::R / Z + 1;
+    constexpr int R2 = 2 * TC<Z>::R;
     float tv[NJ];
     tv[0] = t1b;
 #pragma unroll
@@ -312,54 +279,60 @@ struct Tile {
       tv[j] = lane >= j ? v : 0.f;
     }
     float om[Z];
-    const bool ring = LFSR_CRING && CR;
-    if (!ring) load_om(er, lane, om);
+    load_om(er, lane, om);
     const float Yf = (float)(YE0 - PY0 + er);
-    const int4* slot = ring ? CR + (er % TC<Z>::NTAP) * Z * 32 + lane : nullptr;
+    const float X0 = (float)(XE0 - PX0 + Z * lane);
     int i00[Z], i01[Z];
-    float v00[Z], v01[Z], v10[Z], v11[Z];
-    bool adj = true;
+    float2 w0[Z], w1[Z];   // (row, row + 1) weights times t on the left / right source column
 #pragma unroll
-    for (int s = 0; s < Z; ++s) {
+    for (int k = 0; k < NP; ++k) {
+      const int s = 2 * k;
+      float2 t = f2s(0.f);
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        if (Z * j + s + 1 <= R2) t = __ffma2_rn(f2(taps[Z * j + s], taps[Z * j + s + 1]), f2s(tv[j]), t);
+        else if (Z * j + s <= R2) t.x = fmaf(taps[Z * j + s], tv[j], t.x);
+      }
+      int c0[2], c1[2];
+      float2 a, b;
+      sample2(Yf, X0 + (float)s, f2(om[s], om[s + 1]), drho, dtau, c0, c1, a, b);
+      i00[s] = c0[0]; i01[s] = c1[0]; i00[s + 1] = c0[1]; i01[s + 1] = c1[1];
+      const float2 ts = __fmul2_rn(f2(valid(er, s) ? t.x : 0.f, valid(er, s + 1) ? t.y : 0.f), f2s(tscale));
+      const float2 ta = __fmul2_rn(ts, a), t1a = sub2(ts, ta);
+      // per position: (t1a, ta) = the two source rows' shares, split by b into columns
+      const float2 q0 = f2(t1a.x, ta.x), q1 = f2(t1a.y, ta.y);
+      w1[s] = __fmul2_rn(q0, f2s(b.x));
+      w0[s] = sub2(q0, w1[s]);
+      w1[s + 1] = __fmul2_rn(q1, f2s(b.y));
+      w0[s + 1] = sub2(q1, w1[s + 1]);
+    }
+    if constexpr (Z & 1) {
+      constexpr int s = Z - 1;
       float t = 0.f;
 #pragma unroll
       for (int j = 0; j < NJ; ++j)
-        if (Z * j + s <= 2 * TC<Z>::R) t = fmaf(taps[Z * j + s], tv[j], t);
+        if (Z * j + s <= R2) t = fmaf(taps[Z * j + s], tv[j], t);
       float a, b;
-      if (ring) {
-        const int4 cr = slot[s * 32];
-        i00[s] = cr.x;
-        i01[s] = cr.y;
-        a = __int_as_float(cr.z);
-        b = __int_as_float(cr.w);
-      } else {
-        sample(Yf, (float)(XE0 - PX0 + Z * lane + s), om[s], drho, dtau, i00[s], i01[s], a, b);
-      }
+      sample(Yf, X0 + (float)s, om[s], drho, dtau, i00[s], i01[s], a, b);
       const float ts = valid(er, s) ? t * tscale : 0.f;
-      const float ta = ts * a, t1a = ts - ta;
-      v01[s] = t1a * b;
-      v00[s] = t1a - v01[s];
-      v11[s] = ta * b;
-      v10[s] = ta - v11[s];
-      if (s > 0) adj = adj && (i00[s] == i01[s - 1]);
+      const float ta = ts * a;
+      const float2 q = f2(ts - ta, ta);
+      w1[s] = __fmul2_rn(q, f2s(b));
+      w0[s] = sub2(q, w1[s]);
     }
-    if (__all_sync(0xffffffffu, adj)) {
-      acc_add(ACC, lo, i00[0], v00[0]);
-      acc_add(ACC, lo, i00[0] + PW, v10[0]);
+    bool adj = true;
 #pragma unroll
-      for (int s = 1; s < Z; ++s) {
-        acc_add(ACC, lo, i00[s], v00[s] + v01[s - 1]);
-        acc_add(ACC, lo, i00[s] + PW, v10[s] + v11[s - 1]);
-      }
-      acc_add(ACC, lo, i01[Z - 1], v01[Z - 1]);
-      acc_add(ACC, lo, i01[Z - 1] + PW, v11[Z - 1]);
+    for (int s = 1; s < Z; ++s) adj = adj && (i00[s] == i01[s - 1]);
+    if (__all_sync(0xffffffffu, adj)) {
+      acc_add2(ACC, lo, i00[0], i00[0] + PW, w0[0]);
+#pragma unroll
+      for (int s = 1; s < Z; ++s) acc_add2(ACC, lo, i00[s], i00[s] + PW, __fadd2_rn(w0[s], w1[s - 1]));
+      acc_add2(ACC, lo, i01[Z - 1], i01[Z - 1] + PW, w1[Z - 1]);
     } else {
 #pragma unroll
       for (int s = 0; s < Z; ++s) {
-        acc_add(ACC, lo, i00[s], v00[s]);
-        acc_add(ACC, lo, i01[s], v01[s]);
-        acc_add(ACC, lo, i00[s] + PW, v10[s]);
-        acc_add(ACC, lo, i01[s] + PW, v11[s]);
+        acc_add2(ACC, lo, i00[s], i00[s] + PW, w0[s]);
+        acc_add2(ACC, lo, i01[s], i01[s] + PW, w1[s]);
       }
     }
   }
@@ -527,13 +500,8 @@ __device__ __forceinline__ void view_pass(const Tile<Z, INT>& t, const Geom& G, 
       for (int v = 0; v < NV; ++v) {
 #pragma unroll
         for (int u = 0; u < NTAP; ++u) br[v][u] = fmaf(taps[u], rho[v], br[v][u]);  // vertical adjoint
-        if constexpr (Z == 2 && LFSR_BLOCK2) {
-          const float tb[2] = {br[v][0], br[v][1]};
-          t.adj_rows2(Z * li, lane, tb, drho[v], dtau[v], taps);
-        } else {
 #pragma unroll
-          for (int u = 0; u < Z; ++u) t.adj_row(Z * li + u, lane, br[v][u], drho[v], dtau[v], taps);
-        }
+        for (int u = 0; u < Z; ++u) t.adj_row(Z * li + u, lane, br[v][u], drho[v], dtau[v], taps);
 #pragma unroll
         for (int u = 0; u < NTAP; ++u) br[v][u] = (u < KEEP) ? br[v][u + Z] : 0.f;
       }
@@ -599,12 +567,7 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
   float* OM = P + 3 * PH * PW;                               // EY*ECOL disparity on the E region
   float* M = OM + (kOMs ? EY * ECOL : 0);                    // MH*MW  weight map, own + radius
   float* NL = M + (kMs ? T.MH * T.MW : 0);                   // TY*TX  NLTV term of the own pixels
-  constexpr bool kRing = LFSR_CRING && kFwd && kAdj;
-  // per-warp coordinate rings, 16-byte aligned, after NL
-  const size_t ring_off = (((size_t)(NL - smem) + (size_t)TY * TX) + 3) & ~(size_t)3;
-  int4* RING = reinterpret_cast<int4*>(smem + ring_off);
-  const size_t ring_words = kRing ? (size_t)NW * C::NTAP * Z * 32 * 4 : 0;
-  const size_t red_off = (ring_off + ring_words + 1) & ~(size_t)1;
+  const size_t red_off = ((size_t)(NL - smem) + (size_t)TY * TX + 1) & ~(size_t)1;   // 8-byte aligned
   double* RED = reinterpret_cast<double*>(smem + red_off);
   __shared__ float s_max;
   __shared__ float s_scale[2];
@@ -747,12 +710,10 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
     // interior tile: every E position is inside the image (no masks needed)
     const bool interior = (YE0 >= 0) && (YE0 + EY <= H) && (XE0 >= 0) && (XE0 + C::EXv <= W);
     if (interior) {
-      Tile<Z, true> t{P, ACC, OM, PW, PWZ, PY0, PX0, YE0, XE0, H, W, colmask, s_scale[0], LO, io.omega, ps,
-                        kRing ? RING + (size_t)warp * C::NTAP * Z * 32 : nullptr};
+      Tile<Z, true> t{P, ACC, OM, PW, PWZ, PY0, PX0, YE0, XE0, H, W, colmask, s_scale[0], LO, io.omega, ps};
       views<Z, MODE, true>(t, G, V, T, io, grp, lane, warp, NW, i0, j0, red_a, red_b, red_c);
     } else {
-      Tile<Z, false> t{P, ACC, OM, PW, PWZ, PY0, PX0, YE0, XE0, H, W, colmask, s_scale[0], LO, io.omega, ps,
-                         kRing ? RING + (size_t)warp * C::NTAP * Z * 32 : nullptr};
+      Tile<Z, false> t{P, ACC, OM, PW, PWZ, PY0, PX0, YE0, XE0, H, W, colmask, s_scale[0], LO, io.omega, ps};
       views<Z, MODE, false>(t, G, V, T, io, grp, lane, warp, NW, i0, j0, red_a, red_b, red_c);
     }
   }
@@ -844,10 +805,8 @@ static void fill_static(TileGeom& T) {
 
 static size_t smem_bytes(const TileGeom& T, int nwarps, int mode = MODE_WZ) {
   const bool om = !LFSR_SMEM_DIET, m = (mode == MODE_WZ) || !LFSR_SMEM_DIET;
-  const int ntap = 2 * (int)std::ceil(3.0 * 0.25 * std::sqrt((double)T.ECOL * T.ECOL / 1024.0 - 1.0)) + 1;
-  const int z = T.ECOL / 32;
   size_t words = 3 * (size_t)T.PH * T.PW + (om ? (size_t)T.EY * T.ECOL : 0) + (m ? (size_t)T.MH * T.MW : 0) +
-                 (size_t)T.TY * T.TX + 8 + (LFSR_CRING ? (size_t)nwarps * ntap * z * 32 * 4 : 0);
+                 (size_t)T.TY * T.TX + 8;
   return words * 4 + (size_t)nwarps * 4 * sizeof(double);
 }
 
