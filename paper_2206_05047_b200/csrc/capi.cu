@@ -182,6 +182,11 @@ static void fill_geom(const lfsr_params& p, Geom& G) {
   double sum = 0.0, t[2 * kMaxTaps + 1];
   for (int u = -R; u <= R; ++u) sum += (t[u + R] = std::exp(-(double)u * u / (2.0 * sig * sig)));
   for (int u = 0; u <= 2 * R; ++u) G.taps[u] = (float)(t[u] / sum);
+  auto tap = [&](int u) { return u <= 2 * R ? G.taps[u] : 0.f; };
+  for (int v = 0; v <= kMaxTaps; ++v) {
+    G.tpe[v] = make_float2(tap(2 * v), tap(2 * v + 1));
+    G.tpo[v] = make_float2(tap(2 * v + 1), tap(2 * v + 2));
+  }
   double gmax = 0.0;
   for (int ph = 0; ph < p.scale; ++ph) {
     double sp = 0.0;

@@ -59,6 +59,8 @@ struct Geom {
   float gpoly2;               // (max polyphase tap sum)^2: |B^T D^T rho| <= gpoly2 max|rho|
   float cS;                   // theta / 2
   float taps[kMaxTaps * 2 + 1];
+  float2 tpe[kMaxTaps + 1];   // tap pairs (taps[2v], taps[2v+1]), zero past 2R (packed FP32 operands)
+  float2 tpo[kMaxTaps + 1];   // tap pairs (taps[2v+1], taps[2v+2])
   float wd[kMaxOffsets];      // spatial weights w_d
   int8_t ody[kMaxOffsets], odx[kMaxOffsets];
 };

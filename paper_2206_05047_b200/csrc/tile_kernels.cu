@@ -37,6 +37,12 @@
 #ifndef LFSR_VPAIR
 #define LFSR_VPAIR 1          // 2: a warp interleaves two views (ILP); 1: one view at a time
 #endif
+#ifndef LFSR_VPK
+#define LFSR_VPK 28           // bit zeta set: the vertical blur taps run as packed FP32 pairs
+#endif
+#ifndef LFSR_INTROWS
+#define LFSR_INTROWS 1        // 1: the fast tile path also requires every E row inside the image (0: measured slower)
+#endif
 #ifndef LFSR_SMEM_DIET
 #define LFSR_SMEM_DIET 0      // 1: disparity and (NORMAL) weights read through L1 instead of shared tiles
 #endif
@@ -114,6 +120,8 @@ __device__ __forceinline__ int pidx(int py, int px, int PW, int PWZ) {
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 __device__ __forceinline__ float2 f2s(float a) { return make_float2(a, a); }
 __device__ __forceinline__ float2 sub2(float2 x, float2 y) { return __ffma2_rn(y, f2s(-1.f), x); }
+// (taps[u], taps[u+1]) straight from the parameter block (u is a compile-time index)
+__device__ __forceinline__ float2 tap2(const Geom& G, int u) { return (u & 1) ? G.tpo[u >> 1] : G.tpe[u >> 1]; }
 
 // Two-word fixed-point accumulation of a pair of values into the cells i and j
 // (see kLoBits): the conversions run packed, the four ATOMS.ADD stay scalar.
@@ -127,32 +135,43 @@ __device__ __forceinline__ void acc_add2(int* hi, int lo_off, int i, int j, floa
   atomicAdd(hi + lo_off + j, __float_as_int(u.y) - kMagicBits);
 }
 
-// Tile-local arithmetic of one CTA.  INT (interior tile): every E position and
-// every sample lies inside the image, so no clamping or validity test is needed.
+// Tile-local arithmetic of one CTA.  INT: every E column of the tile lies inside
+// the image, so no column masks are applied (samples never need clamping: the
+// input tile is replicate-padded).
 // A lane's zeta E columns are processed in pairs (s, s+1) with packed FP32; an
 // odd zeta leaves one scalar column.
 template <int Z, bool INT>
 struct Tile {
   static constexpr int NP = Z / 2;     // column pairs per lane
+  static constexpr bool kInt = INT;
   const float* P;
   int* ACC;
   const float* OM;
   int PW, PWZ, PY0, PX0, YE0, XE0, H, W;
-  unsigned colmask;   // bit s: the lane's E column Z*lane+s is a real column inside the image
   float tscale;
   int lo;             // offset of the residual accumulator from ACC (ints)
   const float* omega; // global disparity (LFSR_SMEM_DIET)
   int ps;
+  unsigned koff;      // Z = 2: folded magic offsets of cells_bits()
+  unsigned colmask;   // bit s: the lane's E column Z*lane+s is a real image column (used when !INT)
+
+  bool rows_in;       // every row of the E region lies inside the image
+
+  // row er of the E region lies inside the image (warp uniform)
+  __device__ __forceinline__ bool row_in(int er) const {
+    return (LFSR_INTROWS && INT) || rows_in || (unsigned)(YE0 + er) < (unsigned)H;
+  }
 
   // floor and fraction without the XU pipe: s + 1.5*2^23 rounded toward -inf is
   // 1.5*2^23 + floor(s) exactly (|s| < 2^22), so its bit pattern is the integer.
   // The coordinates are tile-local (origin PY0/PX0, |s| < ~300), so the fraction
   // keeps ~2^-15 absolute precision whatever the image size (an absolute HR
   // coordinate near 2048 would leave only 2^-12).
+  // axis2 returns the raw bit patterns kMagicBits + floor(s).
   __device__ __forceinline__ static void axis2(float2 s, int& n0, int& n1, float2& f) {
     const float2 r = __fadd2_rd(s, f2s(kMagic));
-    n0 = __float_as_int(r.x) - kMagicBits;
-    n1 = __float_as_int(r.y) - kMagicBits;
+    n0 = __float_as_int(r.x);
+    n1 = __float_as_int(r.y);
     f = sub2(s, __fadd2_rn(r, f2s(-kMagic)));
   }
   __device__ __forceinline__ static void axis(float s, int& n, float& f) {
@@ -166,6 +185,18 @@ struct Tile {
     i00 = iy * PW + (int)(ph * PWZ + q);
     i01 = (ph == Z - 1) ? i00 - (Z - 1) * PWZ + 1 : i00 + PWZ;
   }
+  // The same from the raw bits b = kMagicBits + n.  kMagicBits is even, so for
+  // zeta = 2 the phase is b % 2 and the offsets fold into koff (mod 2^32); zeta = 4
+  // would fold the same way but measured longer code, zeta = 3 cannot.
+  __device__ __forceinline__ void cells_bits(int by, int bx, int& i00, int& i01) const {
+    if constexpr (Z == 2) {
+      const unsigned ux = (unsigned)bx, ph = ux % Z, q = ux / Z;
+      i00 = (int)((unsigned)by * (unsigned)PW + ph * (unsigned)PWZ + q + koff);
+      i01 = (ph == Z - 1) ? i00 - (Z - 1) * PWZ + 1 : i00 + PWZ;
+    } else {
+      cells(by - kMagicBits, bx - kMagicBits, i00, i01);
+    }
+  }
 
   // Source cells and bilinear fractions of the E positions (Yf, Xf) and
   // (Yf, Xf + 1) (A12/A13).  No clamping: the input tile holds the
@@ -177,11 +208,11 @@ struct Tile {
                                           int (&i00)[2], int (&i01)[2], float2& a, float2& b) const {
     const float2 sy = __ffma2_rn(f2s(dtau), om, f2s(Yf));
     const float2 sx = __ffma2_rn(f2s(drho), om, f2(Xf, Xf + 1.f));
-    int iy0, iy1, ix0, ix1;
-    axis2(sy, iy0, iy1, a);
-    axis2(sx, ix0, ix1, b);
-    cells(iy0, ix0, i00[0], i01[0]);
-    cells(iy1, ix1, i00[1], i01[1]);
+    int by0, by1, bx0, bx1;
+    axis2(sy, by0, by1, a);
+    axis2(sx, bx0, bx1, b);
+    cells_bits(by0, bx0, i00[0], i01[0]);
+    cells_bits(by1, bx1, i00[1], i01[1]);
   }
   __device__ __forceinline__ void sample(float Yf, float Xf, float om, float drho, float dtau,
                                          int& i00, int& i01, float& a, float& b) const {
@@ -191,12 +222,11 @@ struct Tile {
     cells(iy, ix, i00, i01);
   }
 
-  // E positions outside the image carry zero (blur zero padding, A11): row test is
-  // warp uniform, the column mask is per lane and fixed for the tile.
-  __device__ __forceinline__ bool valid(int er, int s) const {
-    if (INT) return true;
-    const int Y = YE0 + er;
-    return Y >= 0 && Y < H && ((colmask >> s) & 1u);
+  // E positions outside the image carry zero (blur zero padding, A11): rows by a
+  // warp-uniform test (row_in), columns by the per-lane mask (col_in).
+  __device__ __forceinline__ bool col_in(int s) const { return INT || ((colmask >> s) & 1u); }
+  __device__ __forceinline__ float2 colsel(float2 v, int s) const {
+    return INT ? v : f2(col_in(s) ? v.x : 0.f, col_in(s + 1) ? v.y : 0.f);
   }
 
   __device__ __forceinline__ void load_om(int er, int lane, float (&om)[Z]) const {
@@ -221,8 +251,9 @@ struct Tile {
   }
 
   // W_k then the horizontal blur taps at this lane's LR column, for E row er.
-  __device__ __forceinline__ float fwd_row(int er, int lane, float drho, float dtau, const float* taps) const {
+  __device__ __forceinline__ float fwd_row(int er, int lane, float drho, float dtau, const Geom& G) const {
     constexpr int NTAP = TC<Z>::NTAP;
+    if (!row_in(er)) return 0.f;    // blur zero padding (A11), warp uniform
     float om[Z], wp[Z];
     load_om(er, lane, om);
     const float Yf = (float)(YE0 - PY0 + er);
@@ -236,9 +267,9 @@ struct Tile {
       const float2 p00 = f2(P[i00[0]], P[i00[1]]), p01 = f2(P[i01[0]], P[i01[1]]);
       const float2 p10 = f2(P[i00[0] + PW], P[i00[1] + PW]), p11 = f2(P[i01[0] + PW], P[i01[1] + PW]);
       const float2 top = __ffma2_rn(b, sub2(p01, p00), p00), bot = __ffma2_rn(b, sub2(p11, p10), p10);
-      const float2 v = __ffma2_rn(a, sub2(bot, top), top);
-      wp[s] = valid(er, s) ? v.x : 0.f;
-      wp[s + 1] = valid(er, s + 1) ? v.y : 0.f;
+      const float2 v = colsel(__ffma2_rn(a, sub2(bot, top), top), s);
+      wp[s] = v.x;
+      wp[s + 1] = v.y;
     }
     if constexpr (Z & 1) {
       constexpr int s = Z - 1;
@@ -247,8 +278,7 @@ struct Tile {
       sample(Yf, X0 + (float)s, om[s], drho, dtau, i00, i01, a, b);
       const float p00 = P[i00], p01 = P[i01], p10 = P[i00 + PW], p11 = P[i01 + PW];
       const float top = fmaf(b, p01 - p00, p00), bot = fmaf(b, p11 - p10, p10);
-      const float v = fmaf(a, bot - top, top);
-      wp[s] = valid(er, s) ? v : 0.f;
+      wp[s] = col_in(s) ? fmaf(a, bot - top, top) : 0.f;
     }
     float val[NTAP];
 #pragma unroll
@@ -256,9 +286,9 @@ struct Tile {
       val[v] = (v < Z) ? wp[v % Z] : __shfl_down_sync(0xffffffffu, wp[v % Z], v / Z);
     float2 h2 = f2s(0.f);
 #pragma unroll
-    for (int v = 0; v + 1 < NTAP; v += 2) h2 = __ffma2_rn(f2(taps[v], taps[v + 1]), f2(val[v], val[v + 1]), h2);
+    for (int v = 0; v + 1 < NTAP; v += 2) h2 = __ffma2_rn(tap2(G, v), f2(val[v], val[v + 1]), h2);
     float h = h2.x + h2.y;
-    if constexpr (NTAP & 1) h = fmaf(taps[NTAP - 1], val[NTAP - 1], h);
+    if constexpr (NTAP & 1) h = fmaf(G.taps[NTAP - 1], val[NTAP - 1], h);
     return h;
   }
 
@@ -268,9 +298,10 @@ struct Tile {
   // positions hit adjacent source columns (smooth disparity) the shared columns are
   // merged first: zeta + 1 pairs instead of 2 zeta.
   __device__ __forceinline__ void adj_row(int er, int lane, float t1b, float drho, float dtau,
-                                          const float* taps) const {
+                                          const Geom& G) const {
     constexpr int NJ = 2 * TC<Z>::R / Z + 1;
     constexpr int R2 = 2 * TC<Z>::R;
+    if (!row_in(er)) return;        // E positions outside the image carry no adjoint (A11)
     float tv[NJ];
     tv[0] = t1b;
 #pragma unroll
@@ -290,14 +321,14 @@ struct Tile {
       float2 t = f2s(0.f);
 #pragma unroll
       for (int j = 0; j < NJ; ++j) {
-        if (Z * j + s + 1 <= R2) t = __ffma2_rn(f2(taps[Z * j + s], taps[Z * j + s + 1]), f2s(tv[j]), t);
-        else if (Z * j + s <= R2) t.x = fmaf(taps[Z * j + s], tv[j], t.x);
+        if (Z * j + s + 1 <= R2) t = __ffma2_rn(tap2(G, Z * j + s), f2s(tv[j]), t);
+        else if (Z * j + s <= R2) t.x = fmaf(G.taps[Z * j + s], tv[j], t.x);
       }
       int c0[2], c1[2];
       float2 a, b;
       sample2(Yf, X0 + (float)s, f2(om[s], om[s + 1]), drho, dtau, c0, c1, a, b);
       i00[s] = c0[0]; i01[s] = c1[0]; i00[s + 1] = c0[1]; i01[s + 1] = c1[1];
-      const float2 ts = __fmul2_rn(f2(valid(er, s) ? t.x : 0.f, valid(er, s + 1) ? t.y : 0.f), f2s(tscale));
+      const float2 ts = __fmul2_rn(colsel(t, s), f2s(tscale));
       const float2 ta = __fmul2_rn(ts, a), t1a = sub2(ts, ta);
       // per position: (t1a, ta) = the two source rows' shares, split by b into columns
       const float2 q0 = f2(t1a.x, ta.x), q1 = f2(t1a.y, ta.y);
@@ -311,10 +342,10 @@ struct Tile {
       float t = 0.f;
 #pragma unroll
       for (int j = 0; j < NJ; ++j)
-        if (Z * j + s <= R2) t = fmaf(taps[Z * j + s], tv[j], t);
+        if (Z * j + s <= R2) t = fmaf(G.taps[Z * j + s], tv[j], t);
       float a, b;
       sample(Yf, X0 + (float)s, om[s], drho, dtau, i00[s], i01[s], a, b);
-      const float ts = valid(er, s) ? t * tscale : 0.f;
+      const float ts = col_in(s) ? t * tscale : 0.f;
       const float ta = ts * a;
       const float2 q = f2(ts - ta, ta);
       w1[s] = __fmul2_rn(q, f2s(b));
@@ -425,7 +456,6 @@ __device__ __forceinline__ void view_pass(const Tile<Z, INT>& t, const Geom& G, 
   constexpr bool kFwd = (MODE != MODE_AT);
   constexpr bool kAdj = (MODE != MODE_A);
   const float lam1 = G.lambda1, lam2 = G.lambda2, ith = G.inv_theta;
-  const float* taps = G.taps;
   const int j = j0 + lane;
   const bool col_ok = lane < LX && j < G.w;
   float drho[NV], dtau[NV], fr[NV][NTAP], br[NV][NTAP], y_nx[NV], wa_nx[NV];
@@ -449,7 +479,7 @@ __device__ __forceinline__ void view_pass(const Tile<Z, INT>& t, const Geom& G, 
 #pragma unroll
     for (int u = 0; u < KEEP; ++u)
 #pragma unroll
-      for (int v = 0; v < NV; ++v) fr[v][u] = t.fwd_row(u, lane, drho[v], dtau[v], taps);
+      for (int v = 0; v < NV; ++v) fr[v][u] = t.fwd_row(u, lane, drho[v], dtau[v], G);
   }
   for (int li = 0; li < BL; ++li) {
     const int i = i0 + li;
@@ -466,10 +496,18 @@ __device__ __forceinline__ void view_pass(const Tile<Z, INT>& t, const Geom& G, 
       rho[v] = 0.f;
       if (kFwd) {
 #pragma unroll
-        for (int u = 0; u < Z; ++u) fr[v][KEEP + u] = t.fwd_row(Z * li + KEEP + u, lane, drho[v], dtau[v], taps);
-        float a = 0.f;
+        for (int u = 0; u < Z; ++u) fr[v][KEEP + u] = t.fwd_row(Z * li + KEEP + u, lane, drho[v], dtau[v], G);
+        float a = 0.f;                                                   // A_k x at LR pixel (i, j)
+        if constexpr ((LFSR_VPK >> Z) & 1) {
+          float2 a2 = f2s(0.f);
 #pragma unroll
-        for (int u = 0; u < NTAP; ++u) a = fmaf(taps[u], fr[v][u], a);   // A_k x at LR pixel (i, j)
+          for (int u = 0; u + 1 < NTAP; u += 2) a2 = __ffma2_rn(tap2(G, u), f2(fr[v][u], fr[v][u + 1]), a2);
+          a = a2.x + a2.y;
+          if constexpr (NTAP & 1) a = fmaf(G.taps[NTAP - 1], fr[v][NTAP - 1], a);
+        } else {
+#pragma unroll
+          for (int u = 0; u < NTAP; ++u) a = fmaf(G.taps[u], fr[v][u], a);
+        }
         if (ok) {
           if (MODE == MODE_A) {
             io.out_lr[lg] = a;
@@ -498,10 +536,20 @@ __device__ __forceinline__ void view_pass(const Tile<Z, INT>& t, const Geom& G, 
     if (kAdj) {
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
+        if constexpr ((LFSR_VPK >> Z) & 1) {                                             // vertical adjoint
 #pragma unroll
-        for (int u = 0; u < NTAP; ++u) br[v][u] = fmaf(taps[u], rho[v], br[v][u]);  // vertical adjoint
+          for (int u = 0; u + 1 < NTAP; u += 2) {
+            const float2 b2 = __ffma2_rn(tap2(G, u), f2s(rho[v]), f2(br[v][u], br[v][u + 1]));
+            br[v][u] = b2.x;
+            br[v][u + 1] = b2.y;
+          }
+          if constexpr (NTAP & 1) br[v][NTAP - 1] = fmaf(G.taps[NTAP - 1], rho[v], br[v][NTAP - 1]);
+        } else {
 #pragma unroll
-        for (int u = 0; u < Z; ++u) t.adj_row(Z * li + u, lane, br[v][u], drho[v], dtau[v], taps);
+          for (int u = 0; u < NTAP; ++u) br[v][u] = fmaf(G.taps[u], rho[v], br[v][u]);
+        }
+#pragma unroll
+        for (int u = 0; u < Z; ++u) t.adj_row(Z * li + u, lane, br[v][u], drho[v], dtau[v], G);
 #pragma unroll
         for (int u = 0; u < NTAP; ++u) br[v][u] = (u < KEEP) ? br[v][u + Z] : 0.f;
       }
@@ -511,7 +559,7 @@ __device__ __forceinline__ void view_pass(const Tile<Z, INT>& t, const Geom& G, 
 #pragma unroll
     for (int v = 0; v < NV; ++v)
 #pragma unroll
-      for (int u = 0; u < KEEP; ++u) t.adj_row(Z * BL + u, lane, br[v][u], drho[v], dtau[v], taps);
+      for (int u = 0; u < KEEP; ++u) t.adj_row(Z * BL + u, lane, br[v][u], drho[v], dtau[v], G);
   }
 }
 
@@ -700,22 +748,26 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
   // ---- phase 2: views (no barriers) ----------------------------------------
   double red_a = 0.0, red_b = 0.0, red_c = 0.0;
   {
-    // columns of this lane's E positions that are real image columns
+    // Column mask of this lane's E positions (bit s = a real image column); rows are
+    // tested per row (Tile::row_in) unless the whole E region is inside the image.
     unsigned colmask = 0;
 #pragma unroll
     for (int s2 = 0; s2 < Z; ++s2) {
       const int c = Z * lane + s2, X = XE0 + c;
       if (c < C::EXv && X >= 0 && X < W) colmask |= 1u << s2;
     }
-    // interior tile: every E position is inside the image (no masks needed)
-    const bool interior = (YE0 >= 0) && (YE0 + EY <= H) && (XE0 >= 0) && (XE0 + C::EXv <= W);
-    if (interior) {
-      Tile<Z, true> t{P, ACC, OM, PW, PWZ, PY0, PX0, YE0, XE0, H, W, colmask, s_scale[0], LO, io.omega, ps};
-      views<Z, MODE, true>(t, G, V, T, io, grp, lane, warp, NW, i0, j0, red_a, red_b, red_c);
-    } else {
-      Tile<Z, false> t{P, ACC, OM, PW, PWZ, PY0, PX0, YE0, XE0, H, W, colmask, s_scale[0], LO, io.omega, ps};
-      views<Z, MODE, false>(t, G, V, T, io, grp, lane, warp, NW, i0, j0, red_a, red_b, red_c);
-    }
+    const bool rows_in = (YE0 >= 0) && (YE0 + EY <= H);
+    const bool cols_in = (XE0 >= 0) && (XE0 + C::EXv <= W);
+    const unsigned koff = 0u - ((unsigned)kMagicBits * (unsigned)PW + (unsigned)kMagicBits / Z);
+    auto run = [&](auto tile) {
+      tile.colmask = colmask;
+      tile.P = P; tile.ACC = ACC; tile.OM = OM; tile.PW = PW; tile.PWZ = PWZ; tile.PY0 = PY0; tile.PX0 = PX0;
+      tile.YE0 = YE0; tile.XE0 = XE0; tile.H = H; tile.W = W; tile.tscale = s_scale[0]; tile.lo = LO;
+      tile.omega = io.omega; tile.ps = ps; tile.koff = koff; tile.rows_in = rows_in;
+      views<Z, MODE, decltype(tile)::kInt>(tile, G, V, T, io, grp, lane, warp, NW, i0, j0, red_a, red_b, red_c);
+    };
+    if (cols_in && (rows_in || !LFSR_INTROWS)) run(Tile<Z, true>{});
+    else run(Tile<Z, false>{});
   }
   if (MODE == MODE_A) return;
 
