@@ -28,11 +28,26 @@
 #include <cfloat>
 #include <cmath>
 
-#ifndef LFSR_MAXW
-#define LFSR_MAXW 12          // max warps per CTA
+// Launch bounds per zeta: max warps per CTA and min CTAs per SM requested from ptxas
+// (measured: zeta = 2, 3 prefer 12 fat warps, zeta = 4 (many tiles, several waves)
+// prefers two 10-warp CTAs per SM).
+#ifndef LFSR_MAXW2
+#define LFSR_MAXW2 12
 #endif
-#ifndef LFSR_MINB
-#define LFSR_MINB 1           // min CTAs per SM requested from ptxas
+#ifndef LFSR_MINB2
+#define LFSR_MINB2 1
+#endif
+#ifndef LFSR_MAXW3
+#define LFSR_MAXW3 12
+#endif
+#ifndef LFSR_MINB3
+#define LFSR_MINB3 1
+#endif
+#ifndef LFSR_MAXW4
+#define LFSR_MAXW4 10
+#endif
+#ifndef LFSR_MINB4
+#define LFSR_MINB4 2
 #endif
 #ifndef LFSR_VPAIR
 #define LFSR_VPAIR 1          // 2: a warp interleaves two views (ILP); 1: one view at a time
@@ -56,6 +71,11 @@ template <int Z> struct TileCfg;
 template <> struct TileCfg<2> { static constexpr int R = 2, LX = 30, BL = LFSR_BL2; };
 template <> struct TileCfg<3> { static constexpr int R = 3, LX = 30, BL = 11; };
 template <> struct TileCfg<4> { static constexpr int R = 3, LX = 31, BL = 8; };
+
+template <int Z> struct LaunchCfg;
+template <> struct LaunchCfg<2> { static constexpr int MAXW = LFSR_MAXW2, MINB = LFSR_MINB2; };
+template <> struct LaunchCfg<3> { static constexpr int MAXW = LFSR_MAXW3, MINB = LFSR_MINB3; };
+template <> struct LaunchCfg<4> { static constexpr int MAXW = LFSR_MAXW4, MINB = LFSR_MINB4; };
 
 template <int Z> struct TC {
   static constexpr int R = TileCfg<Z>::R, LX = TileCfg<Z>::LX, BL = TileCfg<Z>::BL;
@@ -329,9 +349,10 @@ struct Tile {
       sample2(Yf, X0 + (float)s, f2(om[s], om[s + 1]), drho, dtau, c0, c1, a, b);
       i00[s] = c0[0]; i01[s] = c1[0]; i00[s + 1] = c0[1]; i01[s + 1] = c1[1];
       const float2 ts = __fmul2_rn(colsel(t, s), f2s(tscale));
-      const float2 ta = __fmul2_rn(ts, a), t1a = sub2(ts, ta);
-      // per position: (t1a, ta) = the two source rows' shares, split by b into columns
-      const float2 q0 = f2(t1a.x, ta.x), q1 = f2(t1a.y, ta.y);
+      // per position: (ts (1 - a), ts a) = the two source rows' shares, split by b into
+      // columns (scalar here: the packed form would need the pairs transposed)
+      const float ta0 = ts.x * a.x, ta1 = ts.y * a.y;
+      const float2 q0 = f2(ts.x - ta0, ta0), q1 = f2(ts.y - ta1, ta1);
       w1[s] = __fmul2_rn(q0, f2s(b.x));
       w0[s] = sub2(q0, w1[s]);
       w1[s + 1] = __fmul2_rn(q1, f2s(b.y));
@@ -460,6 +481,7 @@ __device__ __forceinline__ void view_pass(const Tile<Z, INT>& t, const Geom& G, 
   const bool col_ok = lane < LX && j < G.w;
   float drho[NV], dtau[NV], fr[NV][NTAP], br[NV][NTAP], y_nx[NV], wa_nx[NV];
   size_t lrow0[NV];
+  float fa = 0.f, fb = 0.f, fc = 0.f;   // this pass's partial sums (<= BL * NV terms per lane), fp32
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
     drho[v] = V.off[ks[v]].x;
@@ -513,7 +535,7 @@ __device__ __forceinline__ void view_pass(const Tile<Z, INT>& t, const Geom& G, 
             io.out_lr[lg] = a;
           } else if (MODE == MODE_NORMAL) {
             rho[v] = G.cA * a;
-            red_a += (double)G.cA * (double)a * (double)a;      // <p, c_A A^T A p> = c_A |A p|^2
+            fa = fmaf(a, a, fa);                                // <p, c_A A^T A p> = c_A |A p|^2
           } else if (MODE == MODE_WZ) {
             const float e_ = a - y_cur;                         // e = A_k x - y_k (Alg.1 line 4)
             const float wa = wa_cur;
@@ -522,9 +544,9 @@ __device__ __forceinline__ void view_pass(const Tile<Z, INT>& t, const Geom& G, 
             const float f = 2.f * wn - wa;                      // f = 2w^n - w^{n-1} (line 8)
             rho[v] = lam2 * e_ + G.cS * lam1 * f;               // A^T a + (th/2) F^T f, data rows
             io.wA[lg] = wn;
-            red_a += fabs((double)e_);
-            red_b += (double)e_ * e_;
-            red_c += (double)(wn - wa) * (wn - wa);
+            fa += fabsf(e_);
+            fb = fmaf(e_, e_, fb);
+            fc = fmaf(wn - wa, wn - wa, fc);
           }
         }
 #pragma unroll
@@ -561,6 +583,12 @@ __device__ __forceinline__ void view_pass(const Tile<Z, INT>& t, const Geom& G, 
 #pragma unroll
       for (int u = 0; u < KEEP; ++u) t.adj_row(Z * BL + u, lane, br[v][u], drho[v], dtau[v], G);
   }
+  if (MODE == MODE_NORMAL) red_a += (double)G.cA * (double)fa;
+  if (MODE == MODE_WZ) {
+    red_a += (double)fa;
+    red_b += (double)fb;
+    red_c += (double)fc;
+  }
 }
 
 template <int Z, int MODE, bool INT>
@@ -583,7 +611,7 @@ __device__ __forceinline__ void views(const Tile<Z, INT>& t, const Geom& G, cons
 }
 
 template <int Z, int MODE>
-__global__ void __launch_bounds__(LFSR_MAXW * 32, LFSR_MINB)
+__global__ void __launch_bounds__(LaunchCfg<Z>::MAXW * 32, LaunchCfg<Z>::MINB)
 k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
   using C = TC<Z>;
   constexpr int R = C::R, LX = C::LX, BL = C::BL, TY = C::TY, TX = C::TX;
@@ -930,7 +958,7 @@ TileGeom make_tile_geom(const Geom& G, int num_sms, int tr0, int tr1) {
   T.tY0 = tr0 < 0 ? 0 : tr0;
   T.ntYl = (tr1 < 0 ? T.ntY : tr1) - T.tY0;
   const int tiles = T.ntYl * T.ntX;
-  const int max_warps = LFSR_MAXW;
+  const int max_warps = G.scale == 2 ? LaunchCfg<2>::MAXW : G.scale == 3 ? LaunchCfg<3>::MAXW : LaunchCfg<4>::MAXW;
   T.smem = smem_bytes(T, max_warps);
   if (prepare_tile_kernels(G.scale, T.smem) != cudaSuccess) cudaGetLastError();
   int best_g = 1, best_w = 1;
