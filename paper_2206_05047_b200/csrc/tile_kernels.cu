@@ -49,17 +49,11 @@
 #ifndef LFSR_MINB4
 #define LFSR_MINB4 2
 #endif
-#ifndef LFSR_VPAIR
-#define LFSR_VPAIR 1          // 2: a warp interleaves two views (ILP); 1: one view at a time
-#endif
 #ifndef LFSR_VPK
 #define LFSR_VPK 28           // bit zeta set: the vertical blur taps run as packed FP32 pairs
 #endif
 #ifndef LFSR_INTROWS
 #define LFSR_INTROWS 1        // 1: the fast tile path also requires every E row inside the image (0: measured slower)
-#endif
-#ifndef LFSR_SMEM_DIET
-#define LFSR_SMEM_DIET 0      // 1: disparity and (NORMAL) weights read through L1 instead of shared tiles
 #endif
 
 namespace lfsr {
@@ -170,8 +164,6 @@ struct Tile {
   int PW, PWZ, PY0, PX0, YE0, XE0, H, W;
   float tscale;
   int lo;             // offset of the residual accumulator from ACC (ints)
-  const float* omega; // global disparity (LFSR_SMEM_DIET)
-  int ps;
   unsigned koff;      // Z = 2: folded magic offsets of cells_bits()
   unsigned colmask;   // bit s: the lane's E column Z*lane+s is a real image column (used when !INT)
 
@@ -250,12 +242,6 @@ struct Tile {
   }
 
   __device__ __forceinline__ void load_om(int er, int lane, float (&om)[Z]) const {
-#if LFSR_SMEM_DIET
-    const int Y = min(max(YE0 + er, 0), H - 1);
-    const float* row = omega + (size_t)Y * ps;
-#pragma unroll
-    for (int s = 0; s < Z; ++s) om[s] = __ldg(row + min(max(XE0 + Z * lane + s, 0), W - 1));
-#else
     const float* src = OM + er * TC<Z>::ECOL + Z * lane;
     if constexpr (Z == 2) {
       float2 v = *reinterpret_cast<const float2*>(src);
@@ -267,7 +253,6 @@ struct Tile {
 #pragma unroll
       for (int s = 0; s < Z; ++s) om[s] = src[s];
     }
-#endif
   }
 
   // W_k then the horizontal blur taps at this lane's LR column, for E row er.
@@ -400,7 +385,6 @@ struct Tile {
 struct NltvCtx {
   const float* P;
   const float* M;
-  const float* __restrict__ mg;   // global weight map (LFSR_SMEM_DIET, NORMAL)
   const float* __restrict__ wSr;
   float* __restrict__ wSw;
   size_t plane;
@@ -412,8 +396,7 @@ template <int Z, int MODE, bool CHECK, int RAD>
 __device__ __forceinline__ float nltv_pixel(const NltvCtx& c, const Geom& G, int Y, int X, int py, int px, int mi,
                                             size_t gi, double& pq, double& reg, double& res) {
   const float xz = c.P[pidx<Z>(py, px, c.PW, c.PWZ)];
-  constexpr bool kMg = LFSR_SMEM_DIET && MODE == MODE_NORMAL;
-  const float mz = kMg ? __ldg(c.mg + gi) : c.M[mi];
+  const float mz = c.M[mi];
   float acc = 0.f;
   auto one = [&](int d, int dy, int dx) {
     const float wd = G.wd[d];
@@ -421,7 +404,7 @@ __device__ __forceinline__ float nltv_pixel(const NltvCtx& c, const Geom& G, int
     const bool bin = !CHECK || ((Y - dy >= 0) && (Y - dy < c.H) && (X - dx >= 0) && (X - dx < c.W));
     const float xf = c.P[pidx<Z>(py + dy, px + dx, c.PW, c.PWZ)];   // in the tile even when outside Omega
     const float xb = c.P[pidx<Z>(py - dy, px - dx, c.PW, c.PWZ)];
-    const float mb = kMg ? (bin ? __ldg(c.mg + gi - (size_t)dy * c.ps - dx) : 0.f) : c.M[mi - dy * c.MW - dx];
+    const float mb = c.M[mi - dy * c.MW - dx];
     if (MODE == MODE_NORMAL) {
       const float wz = wd * mz, wb = wd * mb;
       const float dp = xz - xf;
@@ -597,14 +580,7 @@ __device__ __forceinline__ void views(const Tile<Z, INT>& t, const Geom& G, cons
                                       double& red_a, double& red_b, double& red_c) {
   const int kbeg = grp * T.vpg;
   const int kend = min(G.n_views, kbeg + T.vpg);
-  int k = kbeg + warp;
-  if (LFSR_VPAIR > 1) {
-    for (; k + NW < kend; k += 2 * NW) {
-      const int ks[2] = {k, k + NW};
-      view_pass<Z, MODE, INT, 2>(t, G, V, io, ks, lane, i0, j0, red_a, red_b, red_c);
-    }
-  }
-  for (; k < kend; k += NW) {
+  for (int k = kbeg + warp; k < kend; k += NW) {
     const int ks[1] = {k};
     view_pass<Z, MODE, INT, 1>(t, G, V, io, ks, lane, i0, j0, red_a, red_b, red_c);
   }
@@ -638,11 +614,9 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
   float* P = smem;                                           // PH*PW  input tile (phase split)
   int* ACC = reinterpret_cast<int*>(P + PH * PW);            // 2*PH*PW fixed-point accumulator (hi, lo)
   const int LO = PH * PW;
-  constexpr bool kOMs = !LFSR_SMEM_DIET;                            // disparity tile in smem
-  constexpr bool kMs = (MODE == MODE_WZ) || !LFSR_SMEM_DIET;         // weight tile in smem
   float* OM = P + 3 * PH * PW;                               // EY*ECOL disparity on the E region
-  float* M = OM + (kOMs ? EY * ECOL : 0);                    // MH*MW  weight map, own + radius
-  float* NL = M + (kMs ? T.MH * T.MW : 0);                   // TY*TX  NLTV term of the own pixels
+  float* M = OM + EY * ECOL;                                 // MH*MW  weight map, own + radius
+  float* NL = M + T.MH * T.MW;                               // TY*TX  NLTV term of the own pixels
   const size_t red_off = ((size_t)(NL - smem) + (size_t)TY * TX + 1) & ~(size_t)1;   // 8-byte aligned
   double* RED = reinterpret_cast<double*>(smem + red_off);
   __shared__ float s_max;
@@ -711,13 +685,13 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
       ACC[LO + i] = 0;
     }
   }
-  for (int e = tid; kOMs && e < EY * ECOL; e += NT) {
+  for (int e = tid; e < EY * ECOL; e += NT) {
     const int er = e / ECOL, c = e - er * ECOL;
     const int Y = YE0 + er, X = XE0 + c;
     OM[e] = (Y >= 0 && Y < H && X >= 0 && X < W) ? io.omega[(size_t)Y * ps + X] : 0.f;
   }
   const int rr = G.radius, MW = T.MW;
-  if (MODE == MODE_NORMAL && io.do_nltv && kMs) {
+  if (MODE == MODE_NORMAL && io.do_nltv) {
     for (int e = tid; e < T.MH * MW; e += NT) {
       const int my = e / MW, mx = e - my * MW;
       const int gy = Y0 - rr + my, gx = X0 - rr + mx;
@@ -791,7 +765,7 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
       tile.colmask = colmask;
       tile.P = P; tile.ACC = ACC; tile.OM = OM; tile.PW = PW; tile.PWZ = PWZ; tile.PY0 = PY0; tile.PX0 = PX0;
       tile.YE0 = YE0; tile.XE0 = XE0; tile.H = H; tile.W = W; tile.tscale = s_scale[0]; tile.lo = LO;
-      tile.omega = io.omega; tile.ps = ps; tile.koff = koff; tile.rows_in = rows_in;
+      tile.koff = koff; tile.rows_in = rows_in;
       views<Z, MODE, decltype(tile)::kInt>(tile, G, V, T, io, grp, lane, warp, NW, i0, j0, red_a, red_b, red_c);
     };
     if (cols_in && (rows_in || !LFSR_INTROWS)) run(Tile<Z, true>{});
@@ -807,7 +781,7 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
   const bool nltv = (MODE == MODE_WZ) || (MODE == MODE_NORMAL && io.do_nltv);
   if (nltv) {
     NltvCtx c;
-    c.P = P; c.M = M; c.mg = io.m; c.PW = PW; c.PWZ = PWZ; c.MW = MW; c.H = H; c.W = W; c.ps = ps;
+    c.P = P; c.M = M; c.PW = PW; c.PWZ = PWZ; c.MW = MW; c.H = H; c.W = W; c.ps = ps;
     c.ith = G.inv_theta;
     const int rd = ctl->iter & 1;
     c.wSr = rd ? io.wS1 : io.wS0;
@@ -883,10 +857,8 @@ static void fill_static(TileGeom& T) {
   T.EY = C::EY; T.ECOL = C::ECOL; T.EXv = C::EXv;
 }
 
-static size_t smem_bytes(const TileGeom& T, int nwarps, int mode = MODE_WZ) {
-  const bool om = !LFSR_SMEM_DIET, m = (mode == MODE_WZ) || !LFSR_SMEM_DIET;
-  size_t words = 3 * (size_t)T.PH * T.PW + (om ? (size_t)T.EY * T.ECOL : 0) + (m ? (size_t)T.MH * T.MW : 0) +
-                 (size_t)T.TY * T.TX + 8;
+static size_t smem_bytes(const TileGeom& T, int nwarps) {
+  size_t words = 3 * (size_t)T.PH * T.PW + (size_t)T.EY * T.ECOL + (size_t)T.MH * T.MW + (size_t)T.TY * T.TX + 8;
   return words * 4 + (size_t)nwarps * 4 * sizeof(double);
 }
 
@@ -973,7 +945,7 @@ TileGeom make_tile_geom(const Geom& G, int num_sms, int tr0, int tr1) {
         if (waste < bestw) { bestw = waste; nw = w; }
       }
     }
-    const int occ = occupancy_for(G.scale, nw * 32, smem_bytes(T, nw, MODE_NORMAL));
+    const int occ = occupancy_for(G.scale, nw * 32, smem_bytes(T, nw));
     const double waves = (double)tiles * g / ((double)num_sms * occ);
     double cost = std::ceil(waves) * ((vpg + nw - 1) / nw) * (1.0 + 0.02 * g);  // flush cost grows with g
     if (waves < 0.9) cost *= 1.0 + (0.9 - waves);
@@ -983,7 +955,7 @@ TileGeom make_tile_geom(const Geom& G, int num_sms, int tr0, int tr1) {
   T.vpg = (G.n_views + best_g - 1) / best_g;
   T.groups = (G.n_views + T.vpg - 1) / T.vpg;
   T.smem = smem_bytes(T, T.nwarps);
-  T.smem_normal = smem_bytes(T, T.nwarps, MODE_NORMAL);
+  T.smem_normal = T.smem;
   return T;
 }
 
