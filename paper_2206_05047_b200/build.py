@@ -30,7 +30,8 @@ def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = sources() + glob.glob(os.path.join(CSRC, "*.h")) + [os.path.join(ROOT, "include", "lfsr.h"), __file__]
+    deps = (sources() + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) +
+            [os.path.join(ROOT, "include", "lfsr.h"), __file__])
     return any(os.path.getmtime(d) > t for d in deps)
 
 
@@ -38,15 +39,21 @@ def build(force: bool = False, verbose: bool = False) -> str:
     """Compile every .cu under csrc/ into liblfsr.so (static cudart)."""
     if not force and not _stale():
         return LIB
-    objs = []
-    for src in sources():
+    objs, procs = [], []
+    for src in sources():   # one nvcc per translation unit, in parallel (the tile kernel is split per zeta)
         obj = os.path.join(CSRC, os.path.basename(src)[:-3] + ".%d.o" % os.getpid())
         cmd = [NVCC, *ARCH, *FLAGS, *VARIANT, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
         if verbose:
             cmd += ["-Xptxas", "-v"]
             print(" ".join(cmd), file=sys.stderr)
-        subprocess.check_call(cmd)
+        procs.append((subprocess.Popen(cmd), cmd))
         objs.append(obj)
+    failed = [cmd for pr, cmd in procs if pr.wait() != 0]
+    if failed:
+        for o in objs:
+            if os.path.exists(o):
+                os.remove(o)
+        raise subprocess.CalledProcessError(1, failed[0])
     tmp = LIB + ".tmp%d" % os.getpid()
     subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-cudart", "static"])
     os.replace(tmp, LIB)

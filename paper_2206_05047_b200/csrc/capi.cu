@@ -8,7 +8,10 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -16,6 +19,7 @@
 namespace lfsr {
 TileGeom make_tile_geom(const Geom& G, int num_sms, int tr0, int tr1);
 void tile_static(int scale, int& BL, int& LX, int& R, int& KEEP);
+int tile_bl_candidates(int scale, int* out, int cap);
 cudaError_t prepare_tile_kernels(int scale, size_t smem);
 cudaError_t launch_tile(int mode, const Geom& G, const Views& V, const TileGeom& T, const TileIO& io,
                         cudaStream_t st);
@@ -76,6 +80,7 @@ struct lfsr_ctx {
   float* tmp_hr2 = nullptr;
   float* tmp_s = nullptr;
   unsigned* umax = nullptr;
+  Control* tune_ctl = nullptr;   // scratch control block for the tile-height timing
   int h_iter = 0;                // iterations enqueued since set_observations
   size_t alloc_key[6] = {0, 0, 0, 0, 0, 0};
   bool profile = false;          // event-record nodes around every kernel (single strip)
@@ -212,6 +217,7 @@ static lfsr_status make_plan(const Geom& G, int n_ranks, int max_shift_rows, std
                              std::string& err) {
   int BL, LX, R, KEEP;
   tile_static(G.scale, BL, LX, R, KEEP);
+  if (G.tile_bl > 0) BL = G.tile_bl;
   const int ntY = (G.h + BL - 1) / BL;
   const int sye = std::max(max_shift_rows, G.radius);
   const int top = R + sye + 1;          // input-tile rows above the own rows (see k_tile)
@@ -463,6 +469,133 @@ static lfsr_status alloc_part(lfsr_ctx* c, Part& P) {
   return LFSR_OK;
 }
 
+static TileIO base_io(const Part& P);
+
+// Strip plan and tile geometry of every part for the current G.tile_bl.
+static lfsr_status setup_tiles(lfsr_ctx* c) {
+  const Geom& G = c->G;
+  const int nparts = (int)c->parts.size();
+  lfsr_status st;
+  std::vector<lfsr_strip> plan;
+  if (c->prm.n_ranks > 1) {
+    std::string why;
+    if ((st = make_plan(G, c->prm.n_ranks, G.SY, plan, why)) != LFSR_OK) FAIL(c, st, why);
+  } else {
+    plan.resize(1);
+    make_plan(G, 1, G.SY, plan, c->err);
+  }
+  for (int i = 0; i < nparts; ++i) {
+    Part& P = c->parts[i];
+    P.plan = plan[c->xmode == X_NCCL ? c->prm.rank : i];
+    P.T = make_tile_geom(G, c->num_sms, P.plan.tile_row0, P.plan.tile_row1);
+    if (P.T.smem > 227 * 1024) FAIL(c, LFSR_ERR_UNSUPPORTED, "disparity range too large for the shared-memory tile");
+    if (c->xmode == X_NCCL) {  // fold staging, sized by the halos
+      const size_t rows = (size_t)std::max(P.plan.halo_top, P.plan.halo_bottom) + 64;
+      if (P.stage_rows < rows) {
+        void* p = nullptr;
+        cudaError_t e;
+        if ((e = dalloc(c, &p, rows * G.ps * 4)) != cudaSuccess) return cuda_fail(c, e, "alloc");
+        P.stage[0] = (float*)p;
+        if ((e = dalloc(c, &p, rows * G.ps * 4)) != cudaSuccess) return cuda_fail(c, e, "alloc");
+        P.stage[1] = (float*)p;
+        P.stage_rows = rows;
+      }
+    }
+  }
+  c->Tfull = make_tile_geom(G, c->num_sms, -1, -1);
+  if (c->Tfull.smem > 227 * 1024) FAIL(c, LFSR_ERR_UNSUPPORTED, "disparity range too large for the shared-memory tile");
+  size_t smem_max = c->Tfull.smem;   // the kernels' dynamic smem limit must cover every strip's launch
+  for (const Part& P : c->parts) smem_max = std::max(smem_max, P.T.smem);
+  CK(c, prepare_tile_kernels(G.scale, smem_max));
+
+  return LFSR_OK;
+}
+
+// Tile height (LR rows per tile).  Wave quantisation and the shared-memory
+// footprint make the best value depend on the problem and the GPU, so a single
+// strip times the CG normal-operator kernel for a few candidates on the first
+// set_observations of a geometry and remembers the winner for the process
+// (same geometry => same tiling => bit-identical reruns).  LFSR_TILE_BL=<n>
+// forces a height; strip decompositions use the zeta default (their plan must
+// match lfsr_strip_plan, which has no observations to tune on).
+static std::mutex g_tune_mu;
+static std::map<std::string, int> g_tuned_bl;
+
+static std::string tune_key(const lfsr_ctx* c) {
+  const Geom& G = c->G;
+  char k[256];
+  snprintf(k, sizeof k, "%d/%d/%d/%d/%d/%d/%d/%d/%d", c->prm.device, G.scale, G.h, G.w, G.n_views, G.SX, G.SY,
+           G.radius, c->num_sms);
+  return k;
+}
+
+static int initial_tile_bl(lfsr_ctx* c, bool* tune) {
+  *tune = false;
+  if (const char* e = getenv("LFSR_TILE_BL")) {
+    const int v = atoi(e);
+    if (v > 0) return v;
+  }
+  if (c->xmode != X_NONE) return 0;
+  std::lock_guard<std::mutex> lk(g_tune_mu);
+  auto it = g_tuned_bl.find(tune_key(c));
+  if (it != g_tuned_bl.end()) return it->second;
+  *tune = true;
+  return 0;
+}
+
+static lfsr_status tune_tile_bl(lfsr_ctx* c) {
+  Geom& G = c->G;
+  Part& P = c->parts[0];
+  if (!c->tune_ctl) {
+    void* p = nullptr;
+    cudaError_t e;
+    if ((e = dalloc(c, &p, sizeof(Control))) != cudaSuccess) return cuda_fail(c, e, "alloc");
+    c->tune_ctl = (Control*)p;
+  }
+  int cand[8];
+  const int n = tile_bl_candidates(G.scale, cand, 8);
+  cudaEvent_t e0, e1;
+  CK(c, cudaEventCreate(&e0));
+  CK(c, cudaEventCreate(&e1));
+  int best_bl = 0;
+  float best_ms = 1e30f;
+  for (int i = 0; i < n; ++i) {
+    if (cand[i] > G.h && i > 0) continue;
+    G.tile_bl = cand[i];
+    TileGeom T = make_tile_geom(G, c->num_sms, -1, -1);
+    if (T.smem > 227 * 1024) continue;
+    CK(c, prepare_tile_kernels(G.scale, T.smem));
+    TileIO io = base_io(P);
+    io.ctl = c->tune_ctl;
+    io.in_hr = P.S.x;
+    io.out_hr = P.S.tmp_hr;
+    io.cg_k = 0;
+    io.do_nltv = 1;
+    CK(c, cudaMemsetAsync(c->tune_ctl, 0, sizeof(Control), c->stream));
+    CK(c, launch_tile(MODE_NORMAL, G, c->V, T, io, c->stream));     // warm
+    CK(c, cudaEventRecord(e0, c->stream));
+    for (int r = 0; r < 3; ++r) CK(c, launch_tile(MODE_NORMAL, G, c->V, T, io, c->stream));
+    CK(c, cudaEventRecord(e1, c->stream));
+    CK(c, cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CK(c, cudaEventElapsedTime(&ms, e0, e1));
+    if (getenv("LFSR_TUNE_VERBOSE")) fprintf(stderr, "lfsr tile tuning: BL %d  %.1f us\n", cand[i], ms * 1000.f / 3);
+    if (ms < best_ms * 0.98f) {   // prefer the earlier (smaller) candidate within 2 %
+      best_ms = ms;
+      best_bl = cand[i];
+    }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  CK(c, cudaMemsetAsync(P.S.tmp_hr, 0, (size_t)G.H * G.ps * 4, c->stream));
+  G.tile_bl = best_bl;
+  {
+    std::lock_guard<std::mutex> lk(g_tune_mu);
+    g_tuned_bl[tune_key(c)] = best_bl;
+  }
+  return setup_tiles(c);
+}
+
 lfsr_status lfsr_set_observations(lfsr_ctx* c, const float* lr_views, const float* view_offsets,
                                   const float* disparity, lfsr_disp_mode disp_mode, const float* x0, lfsr_mem mem) {
   if (!c) return LFSR_ERR_INVALID_ARG;
@@ -568,38 +701,10 @@ lfsr_status lfsr_set_observations(lfsr_ctx* c, const float* lr_views, const floa
   memcpy(&G.ymax, &ubits, 4);
   if (!std::isfinite(G.ymax)) G.ymax = 0.f;  // non-finite observations surface as DIVERGED
 
-  // strip plan and tile geometry per strip
-  std::vector<lfsr_strip> plan;
-  if (c->prm.n_ranks > 1) {
-    std::string why;
-    if ((st = make_plan(G, c->prm.n_ranks, G.SY, plan, why)) != LFSR_OK) FAIL(c, st, why);
-  } else {
-    plan.resize(1);
-    make_plan(G, 1, G.SY, plan, c->err);
-  }
-  for (int i = 0; i < nparts; ++i) {
-    Part& P = c->parts[i];
-    P.plan = plan[c->xmode == X_NCCL ? c->prm.rank : i];
-    P.T = make_tile_geom(G, c->num_sms, P.plan.tile_row0, P.plan.tile_row1);
-    if (P.T.smem > 227 * 1024) FAIL(c, LFSR_ERR_UNSUPPORTED, "disparity range too large for the shared-memory tile");
-    if (c->xmode == X_NCCL) {  // fold staging, sized by the halos
-      const size_t rows = (size_t)std::max(P.plan.halo_top, P.plan.halo_bottom) + 64;
-      if (P.stage_rows < rows) {
-        void* p = nullptr;
-        cudaError_t e;
-        if ((e = dalloc(c, &p, rows * G.ps * 4)) != cudaSuccess) return cuda_fail(c, e, "alloc");
-        P.stage[0] = (float*)p;
-        if ((e = dalloc(c, &p, rows * G.ps * 4)) != cudaSuccess) return cuda_fail(c, e, "alloc");
-        P.stage[1] = (float*)p;
-        P.stage_rows = rows;
-      }
-    }
-  }
-  c->Tfull = make_tile_geom(G, c->num_sms, -1, -1);
-  if (c->Tfull.smem > 227 * 1024) FAIL(c, LFSR_ERR_UNSUPPORTED, "disparity range too large for the shared-memory tile");
-  size_t smem_max = c->Tfull.smem;   // the kernels' dynamic smem limit must cover every strip's launch
-  for (const Part& P : c->parts) smem_max = std::max(smem_max, P.T.smem);
-  CK(c, prepare_tile_kernels(G.scale, smem_max));
+  // tile height and the strip plan / tile geometry of every part
+  bool tune = false;
+  G.tile_bl = initial_tile_bl(c, &tune);
+  if ((st = setup_tiles(c)) != LFSR_OK) return st;
 
   // a1 (every strip, whole image): x0 (bicubic unless given), static w_o, m from x0, density
   for (Part& P : c->parts) {
@@ -612,6 +717,7 @@ lfsr_status lfsr_set_observations(lfsr_ctx* c, const float* lr_views, const floa
     CK(c, launch_setup_wo(G, c->V, S.y, S.omega, S.wo, c->stream));
     CK(c, launch_weights(G, S.x, S.wo, S.m, c->stream));
   }
+  if (tune && (st = tune_tile_bl(c)) != LFSR_OK) return st;
   lfsr_status gs = build_graphs(c);
   if (gs != LFSR_OK) return gs;
   CK(c, cudaStreamSynchronize(c->stream));

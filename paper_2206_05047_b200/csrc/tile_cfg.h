@@ -1,0 +1,58 @@
+// tile_cfg.h — compile-time constants of the tile kernel (shared by the per-zeta
+// kernel translation units and the host-side geometry code).
+#pragma once
+#include "internal.h"
+
+// Launch bounds per zeta: max warps per CTA and min CTAs per SM requested from ptxas
+// (measured: zeta = 2, 3 prefer 12 fat warps, zeta = 4 (many tiles, several waves)
+// prefers two 10-warp CTAs per SM).
+#ifndef LFSR_MAXW2
+#define LFSR_MAXW2 12
+#endif
+#ifndef LFSR_MINB2
+#define LFSR_MINB2 1
+#endif
+#ifndef LFSR_MAXW3
+#define LFSR_MAXW3 12
+#endif
+#ifndef LFSR_MINB3
+#define LFSR_MINB3 1
+#endif
+#ifndef LFSR_MAXW4
+#define LFSR_MAXW4 10
+#endif
+#ifndef LFSR_MINB4
+#define LFSR_MINB4 2
+#endif
+#ifndef LFSR_VPK
+#define LFSR_VPK 28           // bit zeta set: the vertical blur taps run as packed FP32 pairs
+#endif
+#ifndef LFSR_INTROWS
+#define LFSR_INTROWS 1        // 1: the fast tile path also requires every E row inside the image (0: measured slower)
+#endif
+
+namespace lfsr {
+
+template <int Z> struct TileCfg;
+// BL (LR rows per tile) is a runtime parameter (TileGeom::BL, tuned per problem at
+// set_observations); BL here is the default / fallback.
+template <> struct TileCfg<2> { static constexpr int R = 2, LX = 30, BL = 16; };
+template <> struct TileCfg<3> { static constexpr int R = 3, LX = 30, BL = 11; };
+template <> struct TileCfg<4> { static constexpr int R = 3, LX = 31, BL = 6; };
+
+template <int Z> struct LaunchCfg;
+template <> struct LaunchCfg<2> { static constexpr int MAXW = LFSR_MAXW2, MINB = LFSR_MINB2; };
+template <> struct LaunchCfg<3> { static constexpr int MAXW = LFSR_MAXW3, MINB = LFSR_MINB3; };
+template <> struct LaunchCfg<4> { static constexpr int MAXW = LFSR_MAXW4, MINB = LFSR_MINB4; };
+
+template <int Z> struct TC {
+  static constexpr int R = TileCfg<Z>::R, LX = TileCfg<Z>::LX, BL = TileCfg<Z>::BL;
+  static constexpr int NTAP = 2 * R + 1;
+  static constexpr int KEEP = NTAP - Z;           // forward-ring rows carried between LR rows
+  static constexpr int TX = Z * LX;              // tile rows TY = Z BL, E rows EY = Z BL + KEEP (runtime)
+  static constexpr int ECOL = 32 * Z;
+  static constexpr int EXv = Z * (LX - 1) + NTAP;
+  static_assert(EXv <= ECOL, "strip too wide for one warp");
+};
+
+}  // namespace lfsr

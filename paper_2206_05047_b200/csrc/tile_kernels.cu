@@ -1,851 +1,10 @@
-// tile_kernels.cu — the fused observation-operator tile kernel of liblfsr (v2).
-//
-// One CTA owns a tile = a band of BL LR rows x a strip of LX LR columns, and a
-// group of views.  Every warp of the CTA takes whole views (round robin) and
-// streams the tile's "E region" (the HR positions whose blurred warped value
-// reaches an own LR pixel) row by row, lane = LR column, each lane holding the
-// zeta HR columns under its LR column:
-//   W_k    bilinear gather at z + dtheta_k * omega(z) from the shared input tile
-//          (replicate-clamped coordinate)                       P:L580-583, A12/A13
-//   B, D   Gaussian blur evaluated at LR positions only: horizontal taps by warp
-//          shuffles, vertical taps in a register ring (decimation is free) P:L577-579
-//   epilogue per LR pixel: (WZ) e = A_k x - y_k, clamp-form prox + scaled dual
-//          (Alg.1 lines 4-8, A5/A6) -> rho; (NORMAL) rho = c_A A_k p
-//   D^T B^T polyphase adjoint blur (register ring + shuffles)           A11/A14
-//   W_k^T  exact bilinear scatter into a shared int32 fixed-point accumulator
-//          (native ATOMS.ADD, order-independent -> deterministic per CTA)  A12
-// No barrier inside the view loop.  Then the weighted NLTV term in gather form
-// for the own pixels (the CTA's view group takes every G-th offset),
-// and one RED.ADD flush of accumulator + NLTV term (tile + halo) to global so
-// neighbouring tiles and view groups sum.
-//
-// Fixed-point scale: every CTA bounds |t| (the blurred adjoint value of one
-// source) by tb (c_A max|p| for NORMAL; l2 (max|x| + max|y|) + (th/2) l1 3/th for
-// WZ) and the accumulated weight per cell by the splat density max_z sum_k
-// (W_k^T 1)(z) (computed once at setup), and picks 2^s with |w t 2^s| < 2^21 and
-// |acc| < 2^30: the per-contribution rounding is <= 2^-22 tb.
-#include "internal.h"
-#include <cfloat>
+// tile_kernels.cu — host side of the tile kernel: tile geometry (tile height,
+// view groups, warps per CTA, shared-memory footprint) and the per-zeta dispatch.
+// The kernel itself is in tile_impl.cuh (instantiated in tile_z2/3/4.cu).
+#include "tile_cfg.h"
 #include <cmath>
 
-// Launch bounds per zeta: max warps per CTA and min CTAs per SM requested from ptxas
-// (measured: zeta = 2, 3 prefer 12 fat warps, zeta = 4 (many tiles, several waves)
-// prefers two 10-warp CTAs per SM).
-#ifndef LFSR_MAXW2
-#define LFSR_MAXW2 12
-#endif
-#ifndef LFSR_MINB2
-#define LFSR_MINB2 1
-#endif
-#ifndef LFSR_MAXW3
-#define LFSR_MAXW3 12
-#endif
-#ifndef LFSR_MINB3
-#define LFSR_MINB3 1
-#endif
-#ifndef LFSR_MAXW4
-#define LFSR_MAXW4 10
-#endif
-#ifndef LFSR_MINB4
-#define LFSR_MINB4 2
-#endif
-#ifndef LFSR_VPK
-#define LFSR_VPK 28           // bit zeta set: the vertical blur taps run as packed FP32 pairs
-#endif
-#ifndef LFSR_INTROWS
-#define LFSR_INTROWS 1        // 1: the fast tile path also requires every E row inside the image (0: measured slower)
-#endif
-
 namespace lfsr {
-
-template <int Z> struct TileCfg;
-#ifndef LFSR_BL2
-#define LFSR_BL2 16           // LR rows per tile at zeta = 2
-#endif
-template <> struct TileCfg<2> { static constexpr int R = 2, LX = 30, BL = LFSR_BL2; };
-template <> struct TileCfg<3> { static constexpr int R = 3, LX = 30, BL = 11; };
-template <> struct TileCfg<4> { static constexpr int R = 3, LX = 31, BL = 8; };
-
-template <int Z> struct LaunchCfg;
-template <> struct LaunchCfg<2> { static constexpr int MAXW = LFSR_MAXW2, MINB = LFSR_MINB2; };
-template <> struct LaunchCfg<3> { static constexpr int MAXW = LFSR_MAXW3, MINB = LFSR_MINB3; };
-template <> struct LaunchCfg<4> { static constexpr int MAXW = LFSR_MAXW4, MINB = LFSR_MINB4; };
-
-template <int Z> struct TC {
-  static constexpr int R = TileCfg<Z>::R, LX = TileCfg<Z>::LX, BL = TileCfg<Z>::BL;
-  static constexpr int NTAP = 2 * R + 1;
-  static constexpr int KEEP = NTAP - Z;           // forward-ring rows carried between LR rows
-  static constexpr int TY = Z * BL, TX = Z * LX;
-  static constexpr int EY = Z * BL + KEEP;        // = Z (BL - 1) + 2R + 1
-  static constexpr int ECOL = 32 * Z;
-  static constexpr int EXv = Z * (LX - 1) + NTAP;
-  static_assert(EXv <= ECOL, "strip too wide for one warp");
-};
-
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
-// Block-wide sum of NV doubles, then one atomicAdd per value into dst[slot[i]].
-template <int NV>
-__device__ __forceinline__ void block_reduce_add(double (&v)[NV], double* red, double* dst,
-                                                 const int (&slot)[NV]) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-#pragma unroll
-  for (int i = 0; i < NV; ++i) v[i] = warp_sum(v[i]);
-  __syncthreads();
-  if (lane == 0) {
-#pragma unroll
-    for (int i = 0; i < NV; ++i) red[warp * NV + i] = v[i];
-  }
-  __syncthreads();
-  if (threadIdx.x < NV) {
-    double s = 0.0;
-    for (int w = 0; w < nw; ++w) s += red[w * NV + threadIdx.x];
-    if (s != 0.0) atomicAdd(dst + slot[threadIdx.x], s);
-  }
-}
-
-// Two-word fixed-point accumulation: v (already scaled by 2^s,
-// |v| < 2^22) is split into its rounded integer part q1 and the residual
-// r = v - q1 in [-1/2, 1/2], which goes to a second accumulator in units of 2^-15
-// (|q2| <= 2^14, so 2^17 contributions per cell cannot overflow).  Both rounding
-// steps use the 1.5*2^23 magic (FADD + IADD, no XU-pipe conversion); integer
-// atomics are native (ATOMS.ADD) and associative, so the result does not depend
-// on the order of the atomics.  Resolution 2^-(s+15) ~ 2^-37 of the per-CTA bound.
-constexpr float kMagic = 12582912.0f;   // 1.5 * 2^23
-constexpr int kMagicBits = 0x4B400000;
-constexpr int kLoBits = 15;
-
-// phase-split shared index of tile-local (py, px): columns of equal px % Z are
-// contiguous, so lanes zeta columns apart hit consecutive banks.
-template <int Z>
-__device__ __forceinline__ int pidx(int py, int px, int PW, int PWZ) {
-  const unsigned ux = (unsigned)px;
-  return py * PW + (int)((ux % Z) * PWZ + ux / Z);
-}
-
-// Packed FP32 (sm_100 FFMA2/FADD2/FMUL2): two lanes of fp32 arithmetic per
-// issue slot.  Each packed op rounds every component exactly like its scalar
-// counterpart (x - y is computed as fma(y, -1, x), which rounds once), so the
-// pairing changes the instruction count, not the results.
-__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
-__device__ __forceinline__ float2 f2s(float a) { return make_float2(a, a); }
-__device__ __forceinline__ float2 sub2(float2 x, float2 y) { return __ffma2_rn(y, f2s(-1.f), x); }
-// (taps[u], taps[u+1]) straight from the parameter block (u is a compile-time index)
-__device__ __forceinline__ float2 tap2(const Geom& G, int u) { return (u & 1) ? G.tpo[u >> 1] : G.tpe[u >> 1]; }
-
-// Two-word fixed-point accumulation of a pair of values into the cells i and j
-// (see kLoBits): the conversions run packed, the four ATOMS.ADD stay scalar.
-__device__ __forceinline__ void acc_add2(int* hi, int lo_off, int i, int j, float2 v) {
-  const float2 t = __fadd2_rn(v, f2s(kMagic));
-  const float2 r = sub2(v, __fadd2_rn(t, f2s(-kMagic)));
-  const float2 u = __ffma2_rn(r, f2s((float)(1 << kLoBits)), f2s(kMagic));
-  atomicAdd(hi + i, __float_as_int(t.x) - kMagicBits);
-  atomicAdd(hi + j, __float_as_int(t.y) - kMagicBits);
-  atomicAdd(hi + lo_off + i, __float_as_int(u.x) - kMagicBits);
-  atomicAdd(hi + lo_off + j, __float_as_int(u.y) - kMagicBits);
-}
-
-// Tile-local arithmetic of one CTA.  INT: every E column of the tile lies inside
-// the image, so no column masks are applied (samples never need clamping: the
-// input tile is replicate-padded).
-// A lane's zeta E columns are processed in pairs (s, s+1) with packed FP32; an
-// odd zeta leaves one scalar column.
-template <int Z, bool INT>
-struct Tile {
-  static constexpr int NP = Z / 2;     // column pairs per lane
-  static constexpr bool kInt = INT;
-  const float* P;
-  int* ACC;
-  const float* OM;
-  int PW, PWZ, PY0, PX0, YE0, XE0, H, W;
-  float tscale;
-  int lo;             // offset of the residual accumulator from ACC (ints)
-  unsigned koff;      // Z = 2: folded magic offsets of cells_bits()
-  unsigned colmask;   // bit s: the lane's E column Z*lane+s is a real image column (used when !INT)
-
-  bool rows_in;       // every row of the E region lies inside the image
-
-  // row er of the E region lies inside the image (warp uniform)
-  __device__ __forceinline__ bool row_in(int er) const {
-    return (LFSR_INTROWS && INT) || rows_in || (unsigned)(YE0 + er) < (unsigned)H;
-  }
-
-  // floor and fraction without the XU pipe: s + 1.5*2^23 rounded toward -inf is
-  // 1.5*2^23 + floor(s) exactly (|s| < 2^22), so its bit pattern is the integer.
-  // The coordinates are tile-local (origin PY0/PX0, |s| < ~300), so the fraction
-  // keeps ~2^-15 absolute precision whatever the image size (an absolute HR
-  // coordinate near 2048 would leave only 2^-12).
-  // axis2 returns the raw bit patterns kMagicBits + floor(s).
-  __device__ __forceinline__ static void axis2(float2 s, int& n0, int& n1, float2& f) {
-    const float2 r = __fadd2_rd(s, f2s(kMagic));
-    n0 = __float_as_int(r.x);
-    n1 = __float_as_int(r.y);
-    f = sub2(s, __fadd2_rn(r, f2s(-kMagic)));
-  }
-  __device__ __forceinline__ static void axis(float s, int& n, float& f) {
-    const float r = __fadd_rd(s, kMagic);
-    n = __float_as_int(r) - kMagicBits;
-    f = s - (r - kMagic);
-  }
-  // phase-split indices of the top-left / top-right source cells of tile cell (iy, ix)
-  __device__ __forceinline__ void cells(int iy, int ix, int& i00, int& i01) const {
-    const unsigned ux = (unsigned)ix, ph = ux % Z, q = ux / Z;
-    i00 = iy * PW + (int)(ph * PWZ + q);
-    i01 = (ph == Z - 1) ? i00 - (Z - 1) * PWZ + 1 : i00 + PWZ;
-  }
-  // The same from the raw bits b = kMagicBits + n.  kMagicBits is even, so for
-  // zeta = 2 the phase is b % 2 and the offsets fold into koff (mod 2^32); zeta = 4
-  // would fold the same way but measured longer code, zeta = 3 cannot.
-  __device__ __forceinline__ void cells_bits(int by, int bx, int& i00, int& i01) const {
-    if constexpr (Z == 2) {
-      const unsigned ux = (unsigned)bx, ph = ux % Z, q = ux / Z;
-      i00 = (int)((unsigned)by * (unsigned)PW + ph * (unsigned)PWZ + q + koff);
-      i01 = (ph == Z - 1) ? i00 - (Z - 1) * PWZ + 1 : i00 + PWZ;
-    } else {
-      cells(by - kMagicBits, bx - kMagicBits, i00, i01);
-    }
-  }
-
-  // Source cells and bilinear fractions of the E positions (Yf, Xf) and
-  // (Yf, Xf + 1) (A12/A13).  No clamping: the input tile holds the
-  // image replicate-padded, and a bilinear sample of the replicate-padded image
-  // equals the sample at the clamped coordinate; the adjoint scatters into the
-  // padding and phase 4 folds it back onto the edge cells (the transpose of the
-  // padding).
-  __device__ __forceinline__ void sample2(float Yf, float Xf, float2 om, float drho, float dtau,
-                                          int (&i00)[2], int (&i01)[2], float2& a, float2& b) const {
-    const float2 sy = __ffma2_rn(f2s(dtau), om, f2s(Yf));
-    const float2 sx = __ffma2_rn(f2s(drho), om, f2(Xf, Xf + 1.f));
-    int by0, by1, bx0, bx1;
-    axis2(sy, by0, by1, a);
-    axis2(sx, bx0, bx1, b);
-    cells_bits(by0, bx0, i00[0], i01[0]);
-    cells_bits(by1, bx1, i00[1], i01[1]);
-  }
-  __device__ __forceinline__ void sample(float Yf, float Xf, float om, float drho, float dtau,
-                                         int& i00, int& i01, float& a, float& b) const {
-    int iy, ix;
-    axis(fmaf(dtau, om, Yf), iy, a);
-    axis(fmaf(drho, om, Xf), ix, b);
-    cells(iy, ix, i00, i01);
-  }
-
-  // E positions outside the image carry zero (blur zero padding, A11): rows by a
-  // warp-uniform test (row_in), columns by the per-lane mask (col_in).
-  __device__ __forceinline__ bool col_in(int s) const { return INT || ((colmask >> s) & 1u); }
-  __device__ __forceinline__ float2 colsel(float2 v, int s) const {
-    return INT ? v : f2(col_in(s) ? v.x : 0.f, col_in(s + 1) ? v.y : 0.f);
-  }
-
-  __device__ __forceinline__ void load_om(int er, int lane, float (&om)[Z]) const {
-    const float* src = OM + er * TC<Z>::ECOL + Z * lane;
-    if constexpr (Z == 2) {
-      float2 v = *reinterpret_cast<const float2*>(src);
-      om[0] = v.x; om[1] = v.y;
-    } else if constexpr (Z == 4) {
-      float4 v = *reinterpret_cast<const float4*>(src);
-      om[0] = v.x; om[1] = v.y; om[2] = v.z; om[3] = v.w;
-    } else {
-#pragma unroll
-      for (int s = 0; s < Z; ++s) om[s] = src[s];
-    }
-  }
-
-  // W_k then the horizontal blur taps at this lane's LR column, for E row er.
-  __device__ __forceinline__ float fwd_row(int er, int lane, float drho, float dtau, const Geom& G) const {
-    constexpr int NTAP = TC<Z>::NTAP;
-    if (!row_in(er)) return 0.f;    // blur zero padding (A11), warp uniform
-    float om[Z], wp[Z];
-    load_om(er, lane, om);
-    const float Yf = (float)(YE0 - PY0 + er);
-    const float X0 = (float)(XE0 - PX0 + Z * lane);
-#pragma unroll
-    for (int k = 0; k < NP; ++k) {
-      const int s = 2 * k;
-      int i00[2], i01[2];
-      float2 a, b;
-      sample2(Yf, X0 + (float)s, f2(om[s], om[s + 1]), drho, dtau, i00, i01, a, b);
-      const float2 p00 = f2(P[i00[0]], P[i00[1]]), p01 = f2(P[i01[0]], P[i01[1]]);
-      const float2 p10 = f2(P[i00[0] + PW], P[i00[1] + PW]), p11 = f2(P[i01[0] + PW], P[i01[1] + PW]);
-      const float2 top = __ffma2_rn(b, sub2(p01, p00), p00), bot = __ffma2_rn(b, sub2(p11, p10), p10);
-      const float2 v = colsel(__ffma2_rn(a, sub2(bot, top), top), s);
-      wp[s] = v.x;
-      wp[s + 1] = v.y;
-    }
-    if constexpr (Z & 1) {
-      constexpr int s = Z - 1;
-      int i00, i01;
-      float a, b;
-      sample(Yf, X0 + (float)s, om[s], drho, dtau, i00, i01, a, b);
-      const float p00 = P[i00], p01 = P[i01], p10 = P[i00 + PW], p11 = P[i01 + PW];
-      const float top = fmaf(b, p01 - p00, p00), bot = fmaf(b, p11 - p10, p10);
-      wp[s] = col_in(s) ? fmaf(a, bot - top, top) : 0.f;
-    }
-    float val[NTAP];
-#pragma unroll
-    for (int v = 0; v < NTAP; ++v)
-      val[v] = (v < Z) ? wp[v % Z] : __shfl_down_sync(0xffffffffu, wp[v % Z], v / Z);
-    float2 h2 = f2s(0.f);
-#pragma unroll
-    for (int v = 0; v + 1 < NTAP; v += 2) h2 = __ffma2_rn(tap2(G, v), f2(val[v], val[v + 1]), h2);
-    float h = h2.x + h2.y;
-    if constexpr (NTAP & 1) h = fmaf(G.taps[NTAP - 1], val[NTAP - 1], h);
-    return h;
-  }
-
-  // Horizontal adjoint blur of the row's LR-column values t1b and the exact bilinear
-  // scatter (W_k^T) of the lane's zeta positions into the fixed-point accumulator.
-  // A position's four weights go out as two (row, row + 1) pairs; when every lane's
-  // positions hit adjacent source columns (smooth disparity) the shared columns are
-  // merged first: zeta + 1 pairs instead of 2 zeta.
-  __device__ __forceinline__ void adj_row(int er, int lane, float t1b, float drho, float dtau,
-                                          const Geom& G) const {
-    constexpr int NJ = 2 * TC<Z>::R / Z + 1;
-    constexpr int R2 = 2 * TC<Z>::R;
-    if (!row_in(er)) return;        // E positions outside the image carry no adjoint (A11)
-    float tv[NJ];
-    tv[0] = t1b;
-#pragma unroll
-    for (int j = 1; j < NJ; ++j) {
-      const float v = __shfl_up_sync(0xffffffffu, t1b, j);
-      tv[j] = lane >= j ? v : 0.f;
-    }
-    float om[Z];
-    load_om(er, lane, om);
-    const float Yf = (float)(YE0 - PY0 + er);
-    const float X0 = (float)(XE0 - PX0 + Z * lane);
-    int i00[Z], i01[Z];
-    float2 w0[Z], w1[Z];   // (row, row + 1) weights times t on the left / right source column
-#pragma unroll
-    for (int k = 0; k < NP; ++k) {
-      const int s = 2 * k;
-      float2 t = f2s(0.f);
-#pragma unroll
-      for (int j = 0; j < NJ; ++j) {
-        if (Z * j + s + 1 <= R2) t = __ffma2_rn(tap2(G, Z * j + s), f2s(tv[j]), t);
-        else if (Z * j + s <= R2) t.x = fmaf(G.taps[Z * j + s], tv[j], t.x);
-      }
-      int c0[2], c1[2];
-      float2 a, b;
-      sample2(Yf, X0 + (float)s, f2(om[s], om[s + 1]), drho, dtau, c0, c1, a, b);
-      i00[s] = c0[0]; i01[s] = c1[0]; i00[s + 1] = c0[1]; i01[s + 1] = c1[1];
-      const float2 ts = __fmul2_rn(colsel(t, s), f2s(tscale));
-      // per position: (ts (1 - a), ts a) = the two source rows' shares, split by b into
-      // columns (scalar here: the packed form would need the pairs transposed)
-      const float ta0 = ts.x * a.x, ta1 = ts.y * a.y;
-      const float2 q0 = f2(ts.x - ta0, ta0), q1 = f2(ts.y - ta1, ta1);
-      w1[s] = __fmul2_rn(q0, f2s(b.x));
-      w0[s] = sub2(q0, w1[s]);
-      w1[s + 1] = __fmul2_rn(q1, f2s(b.y));
-      w0[s + 1] = sub2(q1, w1[s + 1]);
-    }
-    if constexpr (Z & 1) {
-      constexpr int s = Z - 1;
-      float t = 0.f;
-#pragma unroll
-      for (int j = 0; j < NJ; ++j)
-        if (Z * j + s <= R2) t = fmaf(G.taps[Z * j + s], tv[j], t);
-      float a, b;
-      sample(Yf, X0 + (float)s, om[s], drho, dtau, i00[s], i01[s], a, b);
-      const float ts = col_in(s) ? t * tscale : 0.f;
-      const float ta = ts * a;
-      const float2 q = f2(ts - ta, ta);
-      w1[s] = __fmul2_rn(q, f2s(b));
-      w0[s] = sub2(q, w1[s]);
-    }
-    bool adj = true;
-#pragma unroll
-    for (int s = 1; s < Z; ++s) adj = adj && (i00[s] == i01[s - 1]);
-    if (__all_sync(0xffffffffu, adj)) {
-      acc_add2(ACC, lo, i00[0], i00[0] + PW, w0[0]);
-#pragma unroll
-      for (int s = 1; s < Z; ++s) acc_add2(ACC, lo, i00[s], i00[s] + PW, __fadd2_rn(w0[s], w1[s - 1]));
-      acc_add2(ACC, lo, i01[Z - 1], i01[Z - 1] + PW, w1[Z - 1]);
-    } else {
-#pragma unroll
-      for (int s = 0; s < Z; ++s) {
-        acc_add2(ACC, lo, i00[s], i00[s] + PW, w0[s]);
-        acc_add2(ACC, lo, i01[s], i01[s] + PW, w1[s]);
-      }
-    }
-  }
-};
-
-// Weighted NLTV term of one own pixel z (readings A9/A10):
-//   NORMAL: sum_d Delta_d^T (W_d^2 Delta_d p)(z) and its <p, .> share (W_d = w_d m)
-//   WZ:     z/w steps of the NLTV rows (Alg.1 lines 5-8, clamp form A5/A6) for the
-//           pairs (z, z+d), written to the other w_S buffer, and
-//           sum_d Delta_d^T (W_d f_d)(z) with the backward neighbour's f_d
-//           recomputed from the old duals (gather form: no atomics, no race).
-// RAD > 0: offsets unrolled at compile time (paper's 5x5 window: RAD = 2).
-struct NltvCtx {
-  const float* P;
-  const float* M;
-  const float* __restrict__ wSr;
-  float* __restrict__ wSw;
-  size_t plane;
-  int PW, PWZ, MW, H, W, ps;
-  float ith;
-};
-
-template <int Z, int MODE, bool CHECK, int RAD>
-__device__ __forceinline__ float nltv_pixel(const NltvCtx& c, const Geom& G, int Y, int X, int py, int px, int mi,
-                                            size_t gi, double& pq, double& reg, double& res) {
-  const float xz = c.P[pidx<Z>(py, px, c.PW, c.PWZ)];
-  const float mz = c.M[mi];
-  float acc = 0.f;
-  auto one = [&](int d, int dy, int dx) {
-    const float wd = G.wd[d];
-    const bool fin = !CHECK || ((Y + dy >= 0) && (Y + dy < c.H) && (X + dx >= 0) && (X + dx < c.W));
-    const bool bin = !CHECK || ((Y - dy >= 0) && (Y - dy < c.H) && (X - dx >= 0) && (X - dx < c.W));
-    const float xf = c.P[pidx<Z>(py + dy, px + dx, c.PW, c.PWZ)];   // in the tile even when outside Omega
-    const float xb = c.P[pidx<Z>(py - dy, px - dx, c.PW, c.PWZ)];
-    const float mb = c.M[mi - dy * c.MW - dx];
-    if (MODE == MODE_NORMAL) {
-      const float wz = wd * mz, wb = wd * mb;
-      const float dp = xz - xf;
-      const float f2 = fin ? wz * wz : 0.f;
-      acc = fmaf(f2, dp, acc);
-      pq += (double)(f2 * dp) * dp;
-      const float b2 = bin ? wb * wb : 0.f;
-      acc = fmaf(-b2, xb - xz, acc);
-    } else {
-      const size_t pl = (size_t)d * c.plane;
-      const float wz = wd * mz;
-      const float g = fin ? wz * (xz - xf) : 0.f;             // W_d (.) Delta_d x
-      const float wso = __ldg(c.wSr + pl + gi);
-      const float wn = fminf(fmaxf(g + wso, -c.ith), c.ith);
-      c.wSw[pl + gi] = wn;
-      reg += fabs((double)g);
-      res += (double)(wn - wso) * (wn - wso);
-      if (fin) acc = fmaf(wz, 2.f * wn - wso, acc);
-      if (bin) {
-        const float wb = wd * mb;
-        const float wsb = __ldg(c.wSr + pl + gi - (size_t)dy * c.ps - dx);
-        const float wnb = fminf(fmaxf(fmaf(wb, xb - xz, wsb), -c.ith), c.ith);
-        acc = fmaf(-wb, 2.f * wnb - wsb, acc);
-      }
-    }
-  };
-  if constexpr (RAD > 0) {
-#pragma unroll
-    for (int dy = -RAD; dy <= RAD; ++dy) {
-#pragma unroll
-      for (int dx = -RAD; dx <= RAD; ++dx) {
-        if (dy == 0 && dx == 0) continue;
-        const int lin = (dy + RAD) * (2 * RAD + 1) + (dx + RAD);
-        const int d = lin > (2 * RAD + 1) * RAD + RAD ? lin - 1 : lin;   // row-major order, centre skipped (A9)
-        one(d, dy, dx);
-      }
-    }
-  } else {
-    for (int d = 0; d < G.s_d; ++d) one(d, G.ody[d], G.odx[d]);
-  }
-  return acc;
-}
-
-// Phase 2 of k_tile: every warp streams whole views through the tile (see header).
-// NV views are processed interleaved row by row (independent dependency chains
-// for the scheduler); the last odd view of a warp takes the NV = 1 path.
-template <int Z, int MODE, bool INT, int NV>
-__device__ __forceinline__ void view_pass(const Tile<Z, INT>& t, const Geom& G, const Views& V, const TileIO& io,
-                                          const int (&ks)[NV], int lane, int i0, int j0, double& red_a,
-                                          double& red_b, double& red_c) {
-  using C = TC<Z>;
-  constexpr int LX = C::LX, BL = C::BL, NTAP = C::NTAP, KEEP = C::KEEP;
-  constexpr bool kFwd = (MODE != MODE_AT);
-  constexpr bool kAdj = (MODE != MODE_A);
-  const float lam1 = G.lambda1, lam2 = G.lambda2, ith = G.inv_theta;
-  const int j = j0 + lane;
-  const bool col_ok = lane < LX && j < G.w;
-  float drho[NV], dtau[NV], fr[NV][NTAP], br[NV][NTAP], y_nx[NV], wa_nx[NV];
-  size_t lrow0[NV];
-  float fa = 0.f, fb = 0.f, fc = 0.f;   // this pass's partial sums (<= BL * NV terms per lane), fp32
-#pragma unroll
-  for (int v = 0; v < NV; ++v) {
-    drho[v] = V.off[ks[v]].x;
-    dtau[v] = V.off[ks[v]].y;
-#pragma unroll
-    for (int u = 0; u < NTAP; ++u) { fr[v][u] = 0.f; br[v][u] = 0.f; }
-    lrow0[v] = ((size_t)ks[v] * G.h) * G.lps + j;
-    y_nx[v] = 0.f;
-    wa_nx[v] = 0.f;
-    // software prefetch of the next LR row's observation and dual (WZ)
-    if (MODE == MODE_WZ && col_ok && i0 < G.h) {
-      y_nx[v] = io.y[lrow0[v] + (size_t)i0 * G.lps];
-      wa_nx[v] = io.wA[lrow0[v] + (size_t)i0 * G.lps];
-    }
-  }
-  if (kFwd) {
-#pragma unroll
-    for (int u = 0; u < KEEP; ++u)
-#pragma unroll
-      for (int v = 0; v < NV; ++v) fr[v][u] = t.fwd_row(u, lane, drho[v], dtau[v], G);
-  }
-  for (int li = 0; li < BL; ++li) {
-    const int i = i0 + li;
-    const bool ok = col_ok && i < G.h;
-    float rho[NV];
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      const size_t lg = lrow0[v] + (size_t)i * G.lps;
-      const float y_cur = y_nx[v], wa_cur = wa_nx[v];
-      if (MODE == MODE_WZ && col_ok && li + 1 < BL && i + 1 < G.h) {
-        y_nx[v] = io.y[lg + G.lps];
-        wa_nx[v] = io.wA[lg + G.lps];
-      }
-      rho[v] = 0.f;
-      if (kFwd) {
-#pragma unroll
-        for (int u = 0; u < Z; ++u) fr[v][KEEP + u] = t.fwd_row(Z * li + KEEP + u, lane, drho[v], dtau[v], G);
-        float a = 0.f;                                                   // A_k x at LR pixel (i, j)
-        if constexpr ((LFSR_VPK >> Z) & 1) {
-          float2 a2 = f2s(0.f);
-#pragma unroll
-          for (int u = 0; u + 1 < NTAP; u += 2) a2 = __ffma2_rn(tap2(G, u), f2(fr[v][u], fr[v][u + 1]), a2);
-          a = a2.x + a2.y;
-          if constexpr (NTAP & 1) a = fmaf(G.taps[NTAP - 1], fr[v][NTAP - 1], a);
-        } else {
-#pragma unroll
-          for (int u = 0; u < NTAP; ++u) a = fmaf(G.taps[u], fr[v][u], a);
-        }
-        if (ok) {
-          if (MODE == MODE_A) {
-            io.out_lr[lg] = a;
-          } else if (MODE == MODE_NORMAL) {
-            rho[v] = G.cA * a;
-            fa = fmaf(a, a, fa);                                // <p, c_A A^T A p> = c_A |A p|^2
-          } else if (MODE == MODE_WZ) {
-            const float e_ = a - y_cur;                         // e = A_k x - y_k (Alg.1 line 4)
-            const float wa = wa_cur;
-            const float u = lam1 * e_ + wa;                     // u = F x - b' + w (line 5)
-            const float wn = fminf(fmaxf(u, -ith), ith);        // w+ = u - prox(u) = clamp (A5/A6)
-            const float f = 2.f * wn - wa;                      // f = 2w^n - w^{n-1} (line 8)
-            rho[v] = lam2 * e_ + G.cS * lam1 * f;               // A^T a + (th/2) F^T f, data rows
-            io.wA[lg] = wn;
-            fa += fabsf(e_);
-            fb = fmaf(e_, e_, fb);
-            fc = fmaf(wn - wa, wn - wa, fc);
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < KEEP; ++u) fr[v][u] = fr[v][u + Z];
-      } else {
-        rho[v] = ok ? io.in_lr[lg] : 0.f;
-      }
-    }
-    if (kAdj) {
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        if constexpr ((LFSR_VPK >> Z) & 1) {                                             // vertical adjoint
-#pragma unroll
-          for (int u = 0; u + 1 < NTAP; u += 2) {
-            const float2 b2 = __ffma2_rn(tap2(G, u), f2s(rho[v]), f2(br[v][u], br[v][u + 1]));
-            br[v][u] = b2.x;
-            br[v][u + 1] = b2.y;
-          }
-          if constexpr (NTAP & 1) br[v][NTAP - 1] = fmaf(G.taps[NTAP - 1], rho[v], br[v][NTAP - 1]);
-        } else {
-#pragma unroll
-          for (int u = 0; u < NTAP; ++u) br[v][u] = fmaf(G.taps[u], rho[v], br[v][u]);
-        }
-#pragma unroll
-        for (int u = 0; u < Z; ++u) t.adj_row(Z * li + u, lane, br[v][u], drho[v], dtau[v], G);
-#pragma unroll
-        for (int u = 0; u < NTAP; ++u) br[v][u] = (u < KEEP) ? br[v][u + Z] : 0.f;
-      }
-    }
-  }
-  if (kAdj) {
-#pragma unroll
-    for (int v = 0; v < NV; ++v)
-#pragma unroll
-      for (int u = 0; u < KEEP; ++u) t.adj_row(Z * BL + u, lane, br[v][u], drho[v], dtau[v], G);
-  }
-  if (MODE == MODE_NORMAL) red_a += (double)G.cA * (double)fa;
-  if (MODE == MODE_WZ) {
-    red_a += (double)fa;
-    red_b += (double)fb;
-    red_c += (double)fc;
-  }
-}
-
-template <int Z, int MODE, bool INT>
-__device__ __forceinline__ void views(const Tile<Z, INT>& t, const Geom& G, const Views& V, const TileGeom& T,
-                                      const TileIO& io, int grp, int lane, int warp, int NW, int i0, int j0,
-                                      double& red_a, double& red_b, double& red_c) {
-  const int kbeg = grp * T.vpg;
-  const int kend = min(G.n_views, kbeg + T.vpg);
-  for (int k = kbeg + warp; k < kend; k += NW) {
-    const int ks[1] = {k};
-    view_pass<Z, MODE, INT, 1>(t, G, V, io, ks, lane, i0, j0, red_a, red_b, red_c);
-  }
-}
-
-template <int Z, int MODE>
-__global__ void __launch_bounds__(LaunchCfg<Z>::MAXW * 32, LaunchCfg<Z>::MINB)
-k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
-  using C = TC<Z>;
-  constexpr int R = C::R, LX = C::LX, BL = C::BL, TY = C::TY, TX = C::TX;
-  constexpr int EY = C::EY, ECOL = C::ECOL;
-  constexpr bool kFwd = (MODE != MODE_AT);
-  constexpr bool kAdj = (MODE != MODE_A);
-
-  extern __shared__ __align__(16) float smem[];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int NT = blockDim.x, NW = NT >> 5;
-  const int ntiles = T.ntYl * T.ntX;                 // tiles of this strip (all tiles with one rank)
-  const int tile = blockIdx.x % ntiles;
-  const int grp = blockIdx.x / ntiles;
-  const int ti = T.tY0 + tile / T.ntX, tj = tile % T.ntX;
-  const int i0 = ti * BL, j0 = tj * LX;          // LR origin of the tile
-  const int Y0 = i0 * Z, X0 = j0 * Z;             // HR origin of the own pixels
-  const int YE0 = Y0 - R, XE0 = X0 - R;           // E-region origin
-  const int PY0 = YE0 - T.SYe - 1, PX0 = XE0 - T.SXe - 1;  // input-tile origin (+1 spare, see axis())
-  const int PH = T.PH, PW = T.PW, PWn = ECOL + 2 * T.SXe + 2;
-  const int H = G.H, W = G.W, ps = G.ps;
-  Control* ctl = io.ctl;
-  if (MODE == MODE_NORMAL && io.cg_k >= 2 && ctl->cur[S_STOP] != 0.0) return;  // CG stopped
-
-  float* P = smem;                                           // PH*PW  input tile (phase split)
-  int* ACC = reinterpret_cast<int*>(P + PH * PW);            // 2*PH*PW fixed-point accumulator (hi, lo)
-  const int LO = PH * PW;
-  float* OM = P + 3 * PH * PW;                               // EY*ECOL disparity on the E region
-  float* M = OM + EY * ECOL;                                 // MH*MW  weight map, own + radius
-  float* NL = M + T.MH * T.MW;                               // TY*TX  NLTV term of the own pixels
-  const size_t red_off = ((size_t)(NL - smem) + (size_t)TY * TX + 1) & ~(size_t)1;   // 8-byte aligned
-  double* RED = reinterpret_cast<double*>(smem + red_off);
-  __shared__ float s_max;
-  __shared__ float s_scale[2];
-  __shared__ int s_nl_next;
-
-  const int PWZ = T.PWZ;
-
-  // ---- phase 1: input tile (+ CG direction update), disparity, m -----------
-  double pi0_part = 0.0;
-  float beta = 0.f, pmax = 0.f;
-  if (MODE == MODE_NORMAL && io.cg_k >= 2) {
-    double pim1 = ctl->cur[S_PI + io.cg_k - 1], pim2 = ctl->cur[S_PI + io.cg_k - 2];
-    beta = (float)(pim1 / pim2);    // Alg.2 line 10 (reading A2): p_k = r_k + beta p_{k-1}
-  }
-  if (tid == 0) {
-    s_max = 0.f;
-    s_nl_next = 0;
-  }
-  {
-    // 4 independent loads in flight per thread (the tile load is latency bound)
-    constexpr int U = 4;
-    const int n = PH * PWn;
-    for (int e0 = tid; e0 < n; e0 += U * NT) {
-      float v[U], v2[U];
-      size_t gi[U];
-      bool own[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int e = e0 + u * NT;
-        const int py = e / PWn, px = e - py * PWn;
-        const int gy = PY0 + py, gx = PX0 + px;
-        // replicate padding outside the image (see Tile::sample)
-        const int cy = min(max(gy, 0), H - 1), cx = min(max(gx, 0), W - 1);
-        gi[u] = (size_t)cy * ps + cx;
-        own[u] = e < n && gy == cy && gx == cx && gy >= Y0 && gy < Y0 + TY && gx >= X0 && gx < X0 + TX;
-        v[u] = (kFwd && e < n) ? __ldg(io.in_hr + gi[u]) : 0.f;
-        v2[u] = (MODE == MODE_NORMAL && io.cg_k >= 2 && e < n) ? __ldg(io.in_hr2 + gi[u]) : 0.f;
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int e = e0 + u * NT;
-        if (e >= n) break;
-        float val = v[u];
-        if (MODE == MODE_NORMAL && io.cg_k >= 1) {
-          if (io.cg_k == 1) {
-            if (own[u] && grp == 0) pi0_part += (double)val * val;   // pi_0 = <r_0, r_0> (Alg.2 line 3)
-          } else {
-            val = val + beta * v2[u];
-          }
-          if (own[u] && grp == 0) io.p_out[gi[u]] = val;
-        }
-        pmax = fmaxf(pmax, fabsf(val));
-        const int py = e / PWn, px = e - py * PWn;
-        const int i = pidx<Z>(py, px, PW, PWZ);
-        if (kFwd) P[i] = val;
-        if (kAdj) { ACC[i] = 0; ACC[LO + i] = 0; }
-      }
-    }
-  }
-  if (kAdj && PW > PWn) {  // phase-split padding cells of the accumulator
-    for (int e = tid; e < PH * (PW - PWn); e += NT) {
-      const int py = e / (PW - PWn), px = PWn + e - py * (PW - PWn);
-      const int i = pidx<Z>(py, px, PW, PWZ);
-      ACC[i] = 0;
-      ACC[LO + i] = 0;
-    }
-  }
-  for (int e = tid; e < EY * ECOL; e += NT) {
-    const int er = e / ECOL, c = e - er * ECOL;
-    const int Y = YE0 + er, X = XE0 + c;
-    OM[e] = (Y >= 0 && Y < H && X >= 0 && X < W) ? io.omega[(size_t)Y * ps + X] : 0.f;
-  }
-  const int rr = G.radius, MW = T.MW;
-  if (MODE == MODE_NORMAL && io.do_nltv) {
-    for (int e = tid; e < T.MH * MW; e += NT) {
-      const int my = e / MW, mx = e - my * MW;
-      const int gy = Y0 - rr + my, gx = X0 - rr + mx;
-      M[e] = (gy >= 0 && gy < H && gx >= 0 && gx < W) ? io.m[(size_t)gy * ps + gx] : 0.f;
-    }
-  }
-  // block max of |input| -> fixed-point scale
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) pmax = fmaxf(pmax, __shfl_xor_sync(0xffffffffu, pmax, o));
-  __syncthreads();
-  if (lane == 0 && pmax > 0.f) atomicMax(reinterpret_cast<unsigned*>(&s_max), __float_as_uint(pmax));
-  __syncthreads();
-  if (tid == 0) {
-    float tb = 0.f;
-    if (MODE == MODE_NORMAL) tb = G.cA * s_max;
-    if (MODE == MODE_WZ) tb = G.lambda2 * (s_max + G.ymax) + G.cS * G.lambda1 * 3.f * G.inv_theta;
-    if (MODE == MODE_AT) tb = io.tmax_in;
-    tb *= G.gpoly2;   // the polyphase adjoint blur shrinks max|rho|
-    float sc = 0.f, isc = 0.f;
-    if (tb > 0.f && isfinite(tb)) {
-      int e1, e2;
-      frexpf(tb, &e1);
-      frexpf(tb * fmaxf(G.dmax, 1.f) * 1.02f, &e2);
-      const int s = min(21 - e1, 30 - e2);
-      sc = ldexpf(1.f, s);
-      isc = ldexpf(1.f, -s);
-    }
-    s_scale[0] = sc;
-    s_scale[1] = isc;
-  }
-  if (MODE == MODE_WZ) {  // m over own + radius from x (A8/A17/A19)
-    __syncthreads();      // P complete
-    for (int e = tid; e < T.MH * MW; e += NT) {
-      const int my = e / MW, mx = e - my * MW;
-      const int gy = Y0 - rr + my, gx = X0 - rr + mx;
-      float mz = 0.f;
-      if (gy >= 0 && gy < H && gx >= 0 && gx < W) {
-        const size_t gi = (size_t)gy * ps + gx;
-        if (io.reweight) {
-          const int py = gy - PY0, px = gx - PX0;
-          const float xr = P[pidx<Z>(py, min(gx + 1, W - 1) - PX0, PW, PWZ)], xl = P[pidx<Z>(py, max(gx - 1, 0) - PX0, PW, PWZ)];
-          const float xd = P[pidx<Z>(min(gy + 1, H - 1) - PY0, px, PW, PWZ)], xu = P[pidx<Z>(max(gy - 1, 0) - PY0, px, PW, PWZ)];
-          const float gxv = 0.5f * (xr - xl), gyv = 0.5f * (xd - xu);
-          mz = G.lambda_reg * io.wo[gi] * expf(-(gxv * gxv + gyv * gyv) * G.inv_sigma_e);
-          const bool own = gy >= Y0 && gy < Y0 + TY && gx >= X0 && gx < X0 + TX;
-          if (own && grp == 0) io.m[gi] = mz;
-        } else {
-          mz = io.m[gi];
-        }
-      }
-      M[e] = mz;
-    }
-  }
-  __syncthreads();
-
-  // ---- phase 2: views (no barriers) ----------------------------------------
-  double red_a = 0.0, red_b = 0.0, red_c = 0.0;
-  {
-    // Column mask of this lane's E positions (bit s = a real image column); rows are
-    // tested per row (Tile::row_in) unless the whole E region is inside the image.
-    unsigned colmask = 0;
-#pragma unroll
-    for (int s2 = 0; s2 < Z; ++s2) {
-      const int c = Z * lane + s2, X = XE0 + c;
-      if (c < C::EXv && X >= 0 && X < W) colmask |= 1u << s2;
-    }
-    const bool rows_in = (YE0 >= 0) && (YE0 + EY <= H);
-    const bool cols_in = (XE0 >= 0) && (XE0 + C::EXv <= W);
-    const unsigned koff = 0u - ((unsigned)kMagicBits * (unsigned)PW + (unsigned)kMagicBits / Z);
-    auto run = [&](auto tile) {
-      tile.colmask = colmask;
-      tile.P = P; tile.ACC = ACC; tile.OM = OM; tile.PW = PW; tile.PWZ = PWZ; tile.PY0 = PY0; tile.PX0 = PX0;
-      tile.YE0 = YE0; tile.XE0 = XE0; tile.H = H; tile.W = W; tile.tscale = s_scale[0]; tile.lo = LO;
-      tile.koff = koff; tile.rows_in = rows_in;
-      views<Z, MODE, decltype(tile)::kInt>(tile, G, V, T, io, grp, lane, warp, NW, i0, j0, red_a, red_b, red_c);
-    };
-    if (cols_in && (rows_in || !LFSR_INTROWS)) run(Tile<Z, true>{});
-    else run(Tile<Z, false>{});
-  }
-  if (MODE == MODE_A) return;
-
-  // ---- phase 3: NLTV term of the own pixels (view group g takes own rows g, g+G, ...);
-  // warps that finish their views early pull rows from a shared counter, so the NLTV
-  // work (the w_S stream in WZ) fills the wait for the slowest warp.
-  double red_reg = 0.0;
-  const int ng = T.groups;
-  const bool nltv = (MODE == MODE_WZ) || (MODE == MODE_NORMAL && io.do_nltv);
-  if (nltv) {
-    NltvCtx c;
-    c.P = P; c.M = M; c.PW = PW; c.PWZ = PWZ; c.MW = MW; c.H = H; c.W = W; c.ps = ps;
-    c.ith = G.inv_theta;
-    const int rd = ctl->iter & 1;
-    c.wSr = rd ? io.wS1 : io.wS0;
-    c.wSw = rd ? io.wS0 : io.wS1;
-    c.plane = (size_t)H * ps;
-    const int my_rows = TY > grp ? (TY - grp + ng - 1) / ng : 0;
-    for (;;) {
-      int row = 0;
-      if (lane == 0) row = atomicAdd(&s_nl_next, 1);
-      row = __shfl_sync(0xffffffffu, row, 0);
-      if (row >= my_rows) break;
-      const int oy = grp + ng * row;
-      for (int ox = lane; ox < TX; ox += 32) {
-        const int Y = Y0 + oy, X = X0 + ox;
-        float acc = 0.f;
-        if (Y < H && X < W) {
-          const int py = Y - PY0, px = X - PX0;
-          const int mi = (oy + rr) * MW + (ox + rr);
-          const size_t gi = (size_t)Y * ps + X;
-          double pq = 0.0;
-          const bool inner = Y >= rr && Y < H - rr && X >= rr && X < W - rr;
-          if (rr == 2) {
-            acc = inner ? nltv_pixel<Z, MODE, false, 2>(c, G, Y, X, py, px, mi, gi, pq, red_reg, red_c)
-                        : nltv_pixel<Z, MODE, true, 2>(c, G, Y, X, py, px, mi, gi, pq, red_reg, red_c);
-          } else {
-            acc = nltv_pixel<Z, MODE, true, 0>(c, G, Y, X, py, px, mi, gi, pq, red_reg, red_c);
-          }
-          acc *= G.cS;
-          red_b += (double)G.cS * pq;
-        }
-        NL[oy * TX + ox] = acc;
-      }
-    }
-  }
-  __syncthreads();   // views and NLTV done: ACC and NL complete
-
-  // ---- phase 4: flush accumulator + NLTV (tile + halo) with RED.ADD ----------
-  {
-    const float isc = s_scale[1];
-    const float sign = (MODE == MODE_WZ) ? -1.f : 1.f;   // WZ writes r = -v (reading A3)
-    for (int e = tid; e < PH * PWn; e += NT) {
-      const int py = e / PWn, px = e - py * PWn;
-      const int gy = PY0 + py, gx = PX0 + px;
-      const int ia = pidx<Z>(py, px, PW, PWZ);
-      float v = fmaf((float)ACC[LO + ia], 1.f / (float)(1 << kLoBits), (float)ACC[ia]) * isc;
-      const int oy = gy - Y0, ox = gx - X0;
-      if (nltv && gy < H && gx < W && oy >= 0 && oy < TY && ox >= 0 && ox < TX && (oy % ng) == grp)
-        v += NL[oy * TX + ox];
-      // padding cells fold onto their replicate source (transpose of the padding)
-      const int cy = min(max(gy, 0), H - 1), cx = min(max(gx, 0), W - 1);
-      if (v != 0.f) atomicAdd(&io.out_hr[(size_t)cy * ps + cx], sign * v);
-    }
-  }
-  // ---- reductions ----------------------------------------------------------------
-  if (MODE == MODE_WZ) {
-    double v[4] = {red_a, red_b, red_reg, red_c};
-    const int slot[4] = {S_L1, S_L2, S_REG, S_RES2};
-    block_reduce_add<4>(v, RED, ctl->cur, slot);
-  } else if (MODE == MODE_NORMAL && io.cg_k >= 1) {
-    double v[2] = {red_a + red_b, pi0_part};
-    const int slot[2] = {S_PQ + io.cg_k, S_PI + 0};
-    block_reduce_add<2>(v, RED, ctl->cur, slot);
-  }
-}
 
 // --------------------------------------------------------------------------------
 // Host-side geometry and launchers
@@ -853,8 +12,9 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
 template <int Z>
 static void fill_static(TileGeom& T) {
   using C = TC<Z>;
-  T.BL = C::BL; T.LX = C::LX; T.TY = C::TY; T.TX = C::TX;
-  T.EY = C::EY; T.ECOL = C::ECOL; T.EXv = C::EXv;
+  if (T.BL <= 0) T.BL = C::BL;
+  T.LX = C::LX; T.TY = Z * T.BL; T.TX = C::TX;
+  T.EY = Z * T.BL + C::KEEP; T.ECOL = C::ECOL; T.EXv = C::EXv;
 }
 
 static size_t smem_bytes(const TileGeom& T, int nwarps) {
@@ -862,44 +22,34 @@ static size_t smem_bytes(const TileGeom& T, int nwarps) {
   return words * 4 + (size_t)nwarps * 4 * sizeof(double);
 }
 
-template <int Z, int MODE>
-static int occupancy(int threads, size_t smem) {
-  int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_tile<Z, MODE>, threads, smem) != cudaSuccess) {
-    cudaGetLastError();
-    return 1;
-  }
-  return n > 0 ? n : 1;
-}
+cudaError_t tile_launch_z2(int, const Geom&, const Views&, const TileGeom&, const TileIO&, cudaStream_t);
+cudaError_t tile_launch_z3(int, const Geom&, const Views&, const TileGeom&, const TileIO&, cudaStream_t);
+cudaError_t tile_launch_z4(int, const Geom&, const Views&, const TileGeom&, const TileIO&, cudaStream_t);
+cudaError_t tile_prepare_z2(size_t);
+cudaError_t tile_prepare_z3(size_t);
+cudaError_t tile_prepare_z4(size_t);
+int tile_occupancy_z2(int, size_t);
+int tile_occupancy_z3(int, size_t);
+int tile_occupancy_z4(int, size_t);
 
 static int occupancy_for(int scale, int threads, size_t smem) {
   switch (scale) {
-    case 2: return occupancy<2, MODE_NORMAL>(threads, smem);
-    case 3: return occupancy<3, MODE_NORMAL>(threads, smem);
-    default: return occupancy<4, MODE_NORMAL>(threads, smem);
+    case 2: return tile_occupancy_z2(threads, smem);
+    case 3: return tile_occupancy_z3(threads, smem);
+    default: return tile_occupancy_z4(threads, smem);
   }
-}
-
-template <int Z, int MODE>
-static cudaError_t prepare_z(size_t smem) {
-  return cudaFuncSetAttribute(k_tile<Z, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
 cudaError_t prepare_tile_kernels(int scale, size_t smem) {
-  cudaError_t e = cudaSuccess;
-#define PREP(Z)                                                        \
-  if (scale == Z) {                                                    \
-    if ((e = prepare_z<Z, MODE_WZ>(smem)) != cudaSuccess) return e;     \
-    if ((e = prepare_z<Z, MODE_NORMAL>(smem)) != cudaSuccess) return e; \
-    if ((e = prepare_z<Z, MODE_A>(smem)) != cudaSuccess) return e;      \
-    if ((e = prepare_z<Z, MODE_AT>(smem)) != cudaSuccess) return e;     \
+  switch (scale) {
+    case 2: return tile_prepare_z2(smem);
+    case 3: return tile_prepare_z3(smem);
+    case 4: return tile_prepare_z4(smem);
   }
-  PREP(2) PREP(3) PREP(4)
-#undef PREP
-  return e;
+  return cudaErrorInvalidValue;
 }
 
-// Static tile constants for the strip planner (capi.cu).
+// Static tile constants for the strip planner (capi.cu); BL is the default.
 void tile_static(int scale, int& BL, int& LX, int& R, int& KEEP) {
   switch (scale) {
     case 2: BL = TC<2>::BL; LX = TC<2>::LX; R = TC<2>::R; KEEP = TC<2>::KEEP; break;
@@ -908,10 +58,20 @@ void tile_static(int scale, int& BL, int& LX, int& R, int& KEEP) {
   }
 }
 
+// Candidate tile heights (LR rows) for the per-problem tuning in capi.cu.
+int tile_bl_candidates(int scale, int* out, int cap) {
+  static const int c2[] = {8, 12, 16, 20, 24, 32}, c3[] = {6, 8, 11, 14, 16, 22}, c4[] = {4, 6, 8, 10, 12, 16};
+  const int* c = scale == 2 ? c2 : scale == 3 ? c3 : c4;
+  int n = 0;
+  for (int i = 0; i < 6 && n < cap; ++i) out[n++] = c[i];
+  return n;
+}
+
 // Views per warp and warps per CTA: every warp of a group gets the same number of
 // views (or one less); view groups are added until the grid fills the GPU.
 TileGeom make_tile_geom(const Geom& G, int num_sms, int tr0, int tr1) {
   TileGeom T{};
+  T.BL = G.tile_bl;
   switch (G.scale) {
     case 2: fill_static<2>(T); break;
     case 3: fill_static<3>(T); break;
@@ -959,30 +119,12 @@ TileGeom make_tile_geom(const Geom& G, int num_sms, int tr0, int tr1) {
   return T;
 }
 
-template <int Z, int MODE>
-static cudaError_t launch_z(const Geom& G, const Views& V, const TileGeom& T, const TileIO& io, cudaStream_t st) {
-  dim3 grid(T.ntYl * T.ntX * T.groups);
-  k_tile<Z, MODE><<<grid, T.nwarps * 32, MODE == MODE_NORMAL ? T.smem_normal : T.smem, st>>>(G, V, T, io);
-  return cudaGetLastError();
-}
-
-template <int MODE>
-static cudaError_t launch_mode(const Geom& G, const Views& V, const TileGeom& T, const TileIO& io, cudaStream_t st) {
-  switch (G.scale) {
-    case 2: return launch_z<2, MODE>(G, V, T, io, st);
-    case 3: return launch_z<3, MODE>(G, V, T, io, st);
-    case 4: return launch_z<4, MODE>(G, V, T, io, st);
-  }
-  return cudaErrorInvalidValue;
-}
-
 cudaError_t launch_tile(int mode, const Geom& G, const Views& V, const TileGeom& T, const TileIO& io,
                         cudaStream_t st) {
-  switch (mode) {
-    case MODE_WZ: return launch_mode<MODE_WZ>(G, V, T, io, st);
-    case MODE_NORMAL: return launch_mode<MODE_NORMAL>(G, V, T, io, st);
-    case MODE_A: return launch_mode<MODE_A>(G, V, T, io, st);
-    case MODE_AT: return launch_mode<MODE_AT>(G, V, T, io, st);
+  switch (G.scale) {
+    case 2: return tile_launch_z2(mode, G, V, T, io, st);
+    case 3: return tile_launch_z3(mode, G, V, T, io, st);
+    case 4: return tile_launch_z4(mode, G, V, T, io, st);
   }
   return cudaErrorInvalidValue;
 }

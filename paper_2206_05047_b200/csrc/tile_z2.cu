@@ -1,0 +1,13 @@
+// tile_z2.cu — the tile kernel instantiated for zeta = 2 (see tile_impl.cuh).
+#include "tile_impl.cuh"
+
+namespace lfsr {
+
+cudaError_t tile_launch_z2(int mode, const Geom& G, const Views& V, const TileGeom& T, const TileIO& io,
+                           cudaStream_t st) {
+  return TileZ<2>::launch(mode, G, V, T, io, st);
+}
+cudaError_t tile_prepare_z2(size_t smem) { return TileZ<2>::prepare(smem); }
+int tile_occupancy_z2(int threads, size_t smem) { return TileZ<2>::occupancy(threads, smem); }
+
+}  // namespace lfsr

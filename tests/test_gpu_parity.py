@@ -161,6 +161,17 @@ def test_admm_parity_C1_variants(lfsr_mod):
         check_iterates(p, ora, xs, stats, st, lf.x_gt)
 
 
+@pytest.mark.parametrize("cfg,bl", [("C1", 1), ("C1", 5), ("C2", 8), ("C4", 22)])
+def test_admm_parity_forced_tile_height(lfsr_mod, monkeypatch, cfg, bl):
+    """Every tile height the per-problem tuning may pick (set_observations times a few and keeps
+    the fastest) gives the same iterates: LFSR_TILE_BL forces one, including degenerate 1-row
+    tiles and heights that leave a ragged last band."""
+    monkeypatch.setenv("LFSR_TILE_BL", str(bl))
+    lf = S.make_lightfield(cfg)
+    p, ora, xs, stats, st = run_pair(lfsr_mod, lf, 2)
+    check_iterates(p, ora, xs, stats, st, lf.x_gt)
+
+
 @pytest.mark.parametrize("cfg,n", [("C2", 4), ("C3", 2), ("C4", 2)])
 def test_admm_parity_full_size(lfsr_mod, cfg, n):
     """BASELINE configs at full size, in the launch configuration bench.py times."""
