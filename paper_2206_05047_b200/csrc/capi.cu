@@ -20,6 +20,7 @@ namespace lfsr {
 TileGeom make_tile_geom(const Geom& G, int num_sms, int tr0, int tr1);
 void tile_static(int scale, int& BL, int& LX, int& R, int& KEEP);
 int tile_bl_candidates(int scale, int* out, int cap);
+int tile_max_warps(int scale);
 cudaError_t prepare_tile_kernels(int scale, size_t smem);
 cudaError_t launch_tile(int mode, const Geom& G, const Views& V, const TileGeom& T, const TileIO& io,
                         cudaStream_t st);
@@ -519,7 +520,10 @@ static lfsr_status setup_tiles(lfsr_ctx* c) {
 // forces a height; strip decompositions use the zeta default (their plan must
 // match lfsr_strip_plan, which has no observations to tune on).
 static std::mutex g_tune_mu;
-static std::map<std::string, int> g_tuned_bl;
+struct TileChoice {
+  int bl, g, nw;
+};
+static std::map<std::string, TileChoice> g_tuned;
 
 static std::string tune_key(const lfsr_ctx* c) {
   const Geom& G = c->G;
@@ -529,18 +533,28 @@ static std::string tune_key(const lfsr_ctx* c) {
   return k;
 }
 
-static int initial_tile_bl(lfsr_ctx* c, bool* tune) {
+static void initial_tiles(lfsr_ctx* c, bool* tune) {
+  Geom& G = c->G;
   *tune = false;
+  G.tile_bl = G.tile_g = G.tile_nw = 0;
   if (const char* e = getenv("LFSR_TILE_BL")) {
     const int v = atoi(e);
-    if (v > 0) return v;
+    if (v > 0) G.tile_bl = v;
   }
-  if (c->xmode != X_NONE) return 0;
+  if (const char* e = getenv("LFSR_TILE_GNW")) {   // "groups,warps"
+    int g = 0, w = 0;
+    if (sscanf(e, "%d,%d", &g, &w) == 2 && g > 0 && w > 0) { G.tile_g = g; G.tile_nw = w; }
+  }
+  if (G.tile_bl || G.tile_g || c->xmode != X_NONE) return;
   std::lock_guard<std::mutex> lk(g_tune_mu);
-  auto it = g_tuned_bl.find(tune_key(c));
-  if (it != g_tuned_bl.end()) return it->second;
+  auto it = g_tuned.find(tune_key(c));
+  if (it != g_tuned.end()) {
+    G.tile_bl = it->second.bl;
+    G.tile_g = it->second.g;
+    G.tile_nw = it->second.nw;
+    return;
+  }
   *tune = true;
-  return 0;
 }
 
 static lfsr_status tune_tile_bl(lfsr_ctx* c) {
@@ -554,44 +568,62 @@ static lfsr_status tune_tile_bl(lfsr_ctx* c) {
   }
   int cand[8];
   const int n = tile_bl_candidates(G.scale, cand, 8);
+  const int maxw = tile_max_warps(G.scale);
   cudaEvent_t e0, e1;
   CK(c, cudaEventCreate(&e0));
   CK(c, cudaEventCreate(&e1));
-  int best_bl = 0;
+  TileChoice best{0, 0, 0};
   float best_ms = 1e30f;
   for (int i = 0; i < n; ++i) {
     if (cand[i] > G.h && i > 0) continue;
-    G.tile_bl = cand[i];
-    TileGeom T = make_tile_geom(G, c->num_sms, -1, -1);
-    if (T.smem > 227 * 1024) continue;
-    CK(c, prepare_tile_kernels(G.scale, T.smem));
-    TileIO io = base_io(P);
-    io.ctl = c->tune_ctl;
-    io.in_hr = P.S.x;
-    io.out_hr = P.S.tmp_hr;
-    io.cg_k = 0;
-    io.do_nltv = 1;
-    CK(c, cudaMemsetAsync(c->tune_ctl, 0, sizeof(Control), c->stream));
-    CK(c, launch_tile(MODE_NORMAL, G, c->V, T, io, c->stream));     // warm
-    CK(c, cudaEventRecord(e0, c->stream));
-    for (int r = 0; r < 3; ++r) CK(c, launch_tile(MODE_NORMAL, G, c->V, T, io, c->stream));
-    CK(c, cudaEventRecord(e1, c->stream));
-    CK(c, cudaEventSynchronize(e1));
-    float ms = 0.f;
-    CK(c, cudaEventElapsedTime(&ms, e0, e1));
-    if (getenv("LFSR_TUNE_VERBOSE")) fprintf(stderr, "lfsr tile tuning: BL %d  %.1f us\n", cand[i], ms * 1000.f / 3);
-    if (ms < best_ms * 0.98f) {   // prefer the earlier (smaller) candidate within 2 %
-      best_ms = ms;
-      best_bl = cand[i];
+    // per height: the cost model's groups/warps, and 1-3 groups of maximal CTAs
+    const int gnw[4][2] = {{0, 0}, {1, maxw}, {2, maxw}, {3, maxw}};
+    int model_g = 0, model_w = 0;
+    for (int j = 0; j < 4; ++j) {
+      G.tile_bl = cand[i];
+      G.tile_g = gnw[j][0];
+      G.tile_nw = gnw[j][1];
+      TileGeom T = make_tile_geom(G, c->num_sms, -1, -1);
+      if (T.smem > 227 * 1024) continue;
+      if (j == 0) {
+        model_g = T.groups;
+        model_w = T.nwarps;
+      } else if (T.groups == model_g && T.nwarps == model_w) {
+        continue;
+      }
+      CK(c, prepare_tile_kernels(G.scale, T.smem));
+      TileIO io = base_io(P);
+      io.ctl = c->tune_ctl;
+      io.in_hr = P.S.x;
+      io.out_hr = P.S.tmp_hr;
+      io.cg_k = 0;
+      io.do_nltv = 1;
+      CK(c, cudaMemsetAsync(c->tune_ctl, 0, sizeof(Control), c->stream));
+      CK(c, launch_tile(MODE_NORMAL, G, c->V, T, io, c->stream));     // warm
+      CK(c, cudaEventRecord(e0, c->stream));
+      for (int r = 0; r < 3; ++r) CK(c, launch_tile(MODE_NORMAL, G, c->V, T, io, c->stream));
+      CK(c, cudaEventRecord(e1, c->stream));
+      CK(c, cudaEventSynchronize(e1));
+      float ms = 0.f;
+      CK(c, cudaEventElapsedTime(&ms, e0, e1));
+      if (getenv("LFSR_TUNE_VERBOSE"))
+        fprintf(stderr, "lfsr tile tuning: BL %d groups %d warps %d  %.1f us\n", cand[i], T.groups, T.nwarps,
+                ms * 1000.f / 3);
+      if (ms < best_ms * 0.98f) {   // a later candidate must win by 2 % (stable choice)
+        best_ms = ms;
+        best = TileChoice{cand[i], T.groups, T.nwarps};
+      }
     }
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   CK(c, cudaMemsetAsync(P.S.tmp_hr, 0, (size_t)G.H * G.ps * 4, c->stream));
-  G.tile_bl = best_bl;
+  G.tile_bl = best.bl;
+  G.tile_g = best.g;
+  G.tile_nw = best.nw;
   {
     std::lock_guard<std::mutex> lk(g_tune_mu);
-    g_tuned_bl[tune_key(c)] = best_bl;
+    g_tuned[tune_key(c)] = best;
   }
   return setup_tiles(c);
 }
@@ -703,7 +735,7 @@ lfsr_status lfsr_set_observations(lfsr_ctx* c, const float* lr_views, const floa
 
   // tile height and the strip plan / tile geometry of every part
   bool tune = false;
-  G.tile_bl = initial_tile_bl(c, &tune);
+  initial_tiles(c, &tune);
   if ((st = setup_tiles(c)) != LFSR_OK) return st;
 
   // a1 (every strip, whole image): x0 (bicubic unless given), static w_o, m from x0, density

@@ -59,6 +59,7 @@ struct Geom {
   float gpoly2;               // (max polyphase tap sum)^2: |B^T D^T rho| <= gpoly2 max|rho|
   float cS;                   // theta / 2
   int32_t tile_bl;            // LR rows per tile (host-chosen, 0 = the zeta default; see make_tile_geom)
+  int32_t tile_g, tile_nw;    // view groups and warps per CTA (host-chosen, 0 = the cost model's choice)
   float taps[kMaxTaps * 2 + 1];
   float2 tpe[kMaxTaps + 1];   // tap pairs (taps[2v], taps[2v+1]), zero past 2R (packed FP32 operands)
   float2 tpo[kMaxTaps + 1];   // tap pairs (taps[2v+1], taps[2v+2])

@@ -2,6 +2,7 @@
 // view groups, warps per CTA, shared-memory footprint) and the per-zeta dispatch.
 // The kernel itself is in tile_impl.cuh (instantiated in tile_z2/3/4.cu).
 #include "tile_cfg.h"
+#include <algorithm>
 #include <cmath>
 
 namespace lfsr {
@@ -67,6 +68,10 @@ int tile_bl_candidates(int scale, int* out, int cap) {
   return n;
 }
 
+int tile_max_warps(int scale) {
+  return scale == 2 ? LaunchCfg<2>::MAXW : scale == 3 ? LaunchCfg<3>::MAXW : LaunchCfg<4>::MAXW;
+}
+
 // Views per warp and warps per CTA: every warp of a group gets the same number of
 // views (or one less); view groups are added until the grid fills the GPU.
 TileGeom make_tile_geom(const Geom& G, int num_sms, int tr0, int tr1) {
@@ -110,6 +115,10 @@ TileGeom make_tile_geom(const Geom& G, int num_sms, int tr0, int tr1) {
     double cost = std::ceil(waves) * ((vpg + nw - 1) / nw) * (1.0 + 0.02 * g);  // flush cost grows with g
     if (waves < 0.9) cost *= 1.0 + (0.9 - waves);
     if (cost < best) { best = cost; best_g = g; best_w = nw; }
+  }
+  if (G.tile_g > 0 && G.tile_nw > 0 && G.tile_nw <= max_warps) {   // tuned (capi.cu) or forced choice
+    best_g = std::min(G.tile_g, G.n_views);
+    best_w = G.tile_nw;
   }
   T.nwarps = best_w;
   T.vpg = (G.n_views + best_g - 1) / best_g;

@@ -161,12 +161,16 @@ def test_admm_parity_C1_variants(lfsr_mod):
         check_iterates(p, ora, xs, stats, st, lf.x_gt)
 
 
-@pytest.mark.parametrize("cfg,bl", [("C1", 1), ("C1", 5), ("C2", 8), ("C4", 22)])
-def test_admm_parity_forced_tile_height(lfsr_mod, monkeypatch, cfg, bl):
-    """Every tile height the per-problem tuning may pick (set_observations times a few and keeps
-    the fastest) gives the same iterates: LFSR_TILE_BL forces one, including degenerate 1-row
-    tiles and heights that leave a ragged last band."""
+@pytest.mark.parametrize("cfg,bl,gnw", [("C1", 1, None), ("C1", 5, "3,7"), ("C2", 8, "1,12"), ("C4", 22, "2,12"),
+                                        ("C2", 12, "25,1")])
+def test_admm_parity_forced_tile_height(lfsr_mod, monkeypatch, cfg, bl, gnw):
+    """Every tiling the per-problem tuning may pick (set_observations times a few tile heights x
+    view-group / warp splits and keeps the fastest) gives the same iterates: LFSR_TILE_BL and
+    LFSR_TILE_GNW force one, including degenerate 1-row tiles, heights that leave a ragged last
+    band, and one view per CTA."""
     monkeypatch.setenv("LFSR_TILE_BL", str(bl))
+    if gnw:
+        monkeypatch.setenv("LFSR_TILE_GNW", gnw)
     lf = S.make_lightfield(cfg)
     p, ora, xs, stats, st = run_pair(lfsr_mod, lf, 2)
     check_iterates(p, ora, xs, stats, st, lf.x_gt)
