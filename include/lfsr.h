@@ -193,6 +193,15 @@ LFSR_API lfsr_status lfsr_op_apply(lfsr_ctx* ctx, lfsr_op op, const float* in, f
  * gpu_launches count).  Valid after set_observations; 0 otherwise. */
 LFSR_API int32_t lfsr_launches_per_iter(const lfsr_ctx* ctx);
 
+/* Tiling of the fused operator kernel chosen for this context:
+ * LR rows per tile, view groups (CTAs per tile) and warps per CTA.  A single
+ * strip picks them at its first lfsr_set_observations of a geometry by timing
+ * the CG normal-operator kernel for a few candidates (cached per process;
+ * environment LFSR_TILE_BL / LFSR_TILE_GNW="groups,warps" force them).  Any
+ * out pointer may be NULL.  LFSR_ERR_STATE before set_observations. */
+LFSR_API lfsr_status lfsr_tile_config(const lfsr_ctx* ctx, int32_t* tile_rows, int32_t* view_groups,
+                                      int32_t* warps_per_cta);
+
 /* Row-strip plan of the multi-GPU decomposition (DESIGN 10): rank r
  * owns tile rows [tile_row0, tile_row1) = LR rows [lr_row0, lr_row1) = HR rows
  * [hr_row0, hr_row1); before every operator pass it needs halo_top HR rows above

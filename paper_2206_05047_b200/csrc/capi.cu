@@ -390,6 +390,16 @@ const char* lfsr_last_error(const lfsr_ctx* c) { return c ? c->err.c_str() : g_c
 
 int32_t lfsr_launches_per_iter(const lfsr_ctx* c) { return (c && c->ready) ? c->launches_per_iter : 0; }
 
+lfsr_status lfsr_tile_config(const lfsr_ctx* c, int32_t* tile_rows, int32_t* view_groups, int32_t* warps_per_cta) {
+  if (!c) return LFSR_ERR_INVALID_ARG;
+  if (!c->ready || c->parts.empty()) return LFSR_ERR_STATE;
+  const TileGeom& T = c->parts[0].T;
+  if (tile_rows) *tile_rows = T.BL;
+  if (view_groups) *view_groups = T.groups;
+  if (warps_per_cta) *warps_per_cta = T.nwarps;
+  return LFSR_OK;
+}
+
 static cudaError_t dalloc(lfsr_ctx* c, void** p, size_t bytes) {
   cudaError_t e = cudaMalloc(p, bytes);
   if (e == cudaSuccess) {

@@ -30,7 +30,7 @@ OPS = {"A": OP_A, "AT": OP_AT, "S": OP_S, "ST": OP_ST, "NORMAL": OP_NORMAL, "WEI
 
 # every symbol include/lfsr.h declares (checked by tests/test_abi.py)
 EXPORTS = ("lfsr_create", "lfsr_set_observations", "lfsr_admm_run", "lfsr_admm_enqueue", "lfsr_admm_stats",
-           "lfsr_get_hr", "lfsr_get_state", "lfsr_op_apply", "lfsr_launches_per_iter", "lfsr_profile",
+           "lfsr_get_hr", "lfsr_get_state", "lfsr_op_apply", "lfsr_launches_per_iter", "lfsr_tile_config", "lfsr_profile",
            "lfsr_profile_read", "lfsr_strip_plan", "lfsr_destroy", "lfsr_last_error", "lfsr_abi_version")
 
 
@@ -106,6 +106,9 @@ def load_library(path: str = LIB_PATH):
     lib.lfsr_op_apply.restype = st
     lib.lfsr_launches_per_iter.argtypes = [vp]
     lib.lfsr_launches_per_iter.restype = ctypes.c_int32
+    i32p = ctypes.POINTER(ctypes.c_int32)
+    lib.lfsr_tile_config.argtypes = [vp, i32p, i32p, i32p]
+    lib.lfsr_tile_config.restype = st
     lib.lfsr_destroy.argtypes = [vp]
     lib.lfsr_destroy.restype = None
     lib.lfsr_last_error.argtypes = [vp]
@@ -310,6 +313,13 @@ class Solver:
     @property
     def launches_per_iter(self) -> int:
         return int(self.lib.lfsr_launches_per_iter(self._h))
+
+    @property
+    def tile_config(self) -> dict:
+        """lfsr_tile_config: the fused kernel's tiling (tile rows, view groups, warps per CTA)."""
+        b, g, w = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        self._check(self.lib.lfsr_tile_config(self._h, ctypes.byref(b), ctypes.byref(g), ctypes.byref(w)))
+        return {"tile_rows": b.value, "view_groups": g.value, "warps_per_cta": w.value}
 
 
 def strip_plan(params: Params, max_shift_rows: int):

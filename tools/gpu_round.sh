@@ -12,10 +12,12 @@ if [ "$TESTS" = "tests" ]; then
 fi
 timeout 900 python bench.py --config $CFG --steps 20 --warmup 5 > gpurun_out/bench_${TAG}_${CFG}.json 2> gpurun_out/bench_${TAG}_${CFG}.err; tail -c 400 gpurun_out/bench_${TAG}_${CFG}.json
 timeout 600 python bench.py --impl reference --config $CFG --steps 3 --warmup 1 > gpurun_out/bench_ref_${TAG}_${CFG}.json 2>&1; tail -c 300 gpurun_out/bench_ref_${TAG}_${CFG}.json
+# profile the tiling the bench runs (the tuned one), without the tuning launches
+export $(python tools/tuned_env.py $CFG 2>/dev/null | tail -1); echo "tiling: $LFSR_TILE_BL $LFSR_TILE_GNW"
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_${TAG}_${CFG}.csv \
    python bench.py --config $CFG --steps 2 --warmup 1 --e2e-steps 0 --no-cpu-baseline --no-flush > /dev/null 2>&1
 for m in 1 0; do
-  timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:k_tile<.*${m}>" -s 3 -c 1 \
+  timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:k_tile<[0-9], ${m}," -s 3 -c 1 \
      -o gpurun_out/prof_${TAG}_${CFG}_m${m} -f python tools/quick_time.py $CFG 2 > gpurun_out/ncu_${TAG}_${CFG}_m${m}.log 2>&1
 done
 timeout 900 ncu --set full --clock-control none --kernel-name-base demangled -k "regex:k_cg_update" -s 3 -c 1 \
