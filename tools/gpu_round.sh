@@ -17,7 +17,7 @@ export $(python tools/tuned_env.py $CFG 2>/dev/null | tail -1); echo "tiling: $L
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_${TAG}_${CFG}.csv \
    python bench.py --config $CFG --steps 2 --warmup 1 --e2e-steps 0 --no-cpu-baseline --no-flush > /dev/null 2>&1
 for m in 1 0; do
-  timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:k_tile<[0-9], ${m}," -s 3 -c 1 \
+  timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:\(int\)${m}, \(bool\)" -s 3 -c 1 \
      -o gpurun_out/prof_${TAG}_${CFG}_m${m} -f python tools/quick_time.py $CFG 2 > gpurun_out/ncu_${TAG}_${CFG}_m${m}.log 2>&1
 done
 timeout 900 ncu --set full --clock-control none --kernel-name-base demangled -k "regex:k_cg_update" -s 3 -c 1 \
