@@ -27,6 +27,9 @@
 #ifndef LFSR_VPK
 #define LFSR_VPK 28           // bit zeta set: the vertical blur taps run as packed FP32 pairs
 #endif
+#ifndef LFSR_DUMMY_MASK
+#define LFSR_DUMMY_MASK 12    // bit zeta set: zero-row routing for edge tiles (TC::DUMMY)
+#endif
 #ifndef LFSR_INTROWS
 #define LFSR_INTROWS 1        // 1: the fast tile path also requires every E row inside the image (0: measured slower)
 #endif
@@ -52,6 +55,10 @@ template <int Z> struct TC {
   static constexpr int TX = Z * LX;              // tile rows TY = Z BL, E rows EY = Z BL + KEEP (runtime)
   static constexpr int ECOL = 32 * Z;
   static constexpr int EXv = Z * (LX - 1) + NTAP;
+  // edge tiles send E positions outside the image to two zero rows past the input tile
+  // instead of masking them (measured +4 % at C3/C4; at zeta = 4 the 2 extra rows cost
+  // occupancy, so masks stay there)
+  static constexpr bool DUMMY = LFSR_DUMMY_MASK & (1 << Z);
   static_assert(EXv <= ECOL, "strip too wide for one warp");
 };
 

@@ -30,6 +30,7 @@
 #include <cfloat>
 #include <cmath>
 
+
 namespace lfsr {
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -104,8 +105,18 @@ __device__ __forceinline__ void acc_add2(int* hi, int lo_off, int i, int j, floa
 // input tile is replicate-padded).
 // A lane's zeta E columns are processed in pairs (s, s+1) with packed FP32; an
 // odd zeta leaves one scalar column.
+// Edge-tile routing data (TC::DUMMY): Yp = Yrow * ymul + yadd per column pair sends
+// an E position outside the image to the zero rows at PHd.  Empty otherwise.
+template <bool D, int NP>
+struct YRoute {
+  float2 ymul[NP + 1], yadd[NP + 1];
+  float PHd;
+};
+template <int NP>
+struct YRoute<false, NP> {};
+
 template <int Z, bool INT>
-struct Tile {
+struct Tile : YRoute<!INT && TC<Z>::DUMMY, Z / 2> {
   static constexpr int NP = Z / 2;     // column pairs per lane
   static constexpr bool kInt = INT;
   const float* P;
@@ -166,9 +177,9 @@ struct Tile {
   // equals the sample at the clamped coordinate; the adjoint scatters into the
   // padding and phase 4 folds it back onto the edge cells (the transpose of the
   // padding).
-  __device__ __forceinline__ void sample2(float Yf, float Xf, float2 om, float drho, float dtau,
+  __device__ __forceinline__ void sample2(float2 Yp, float Xf, float2 om, float drho, float dtau,
                                           int (&i00)[2], int (&i01)[2], float2& a, float2& b) const {
-    const float2 sy = __ffma2_rn(f2s(dtau), om, f2s(Yf));
+    const float2 sy = __ffma2_rn(f2s(dtau), om, Yp);
     const float2 sx = __ffma2_rn(f2s(drho), om, f2(Xf, Xf + 1.f));
     int by0, by1, bx0, bx1;
     axis2(sy, by0, by1, a);
@@ -186,9 +197,24 @@ struct Tile {
 
   // E positions outside the image carry zero (blur zero padding, A11): rows by a
   // warp-uniform test (row_in), columns by the per-lane mask (col_in).
-  __device__ __forceinline__ bool col_in(int s) const { return INT || ((colmask >> s) & 1u); }
+  __device__ __forceinline__ bool col_in(int s) const { return INT || TC<Z>::DUMMY || ((colmask >> s) & 1u); }
   __device__ __forceinline__ float2 colsel(float2 v, int s) const {
-    return INT ? v : f2(col_in(s) ? v.x : 0.f, col_in(s + 1) ? v.y : 0.f);
+    return (INT || TC<Z>::DUMMY) ? v : f2(col_in(s) ? v.x : 0.f, col_in(s + 1) ? v.y : 0.f);
+  }
+  static constexpr bool kDummy = !INT && TC<Z>::DUMMY;
+  // E row of the samples: the row itself, or the dummy zero rows when it is outside the image
+  __device__ __forceinline__ float yrow(int er) const {
+    const float Yf = (float)(YE0 - PY0 + er);
+    if constexpr (kDummy) return (unsigned)(YE0 + er) >= (unsigned)H ? this->PHd : Yf;
+    return Yf;
+  }
+  __device__ __forceinline__ float yone(float Yrow) const {   // the odd column of an odd zeta
+    if constexpr (kDummy) return fmaf(Yrow, this->ymul[NP].x, this->yadd[NP].x);
+    return Yrow;
+  }
+  __device__ __forceinline__ float2 ypair(float Yrow, int k) const {
+    if constexpr (kDummy) return __ffma2_rn(f2s(Yrow), this->ymul[k], this->yadd[k]);
+    return f2s(Yrow);
   }
 
   __device__ __forceinline__ void load_om(int er, int lane, float (&om)[Z]) const {
@@ -208,17 +234,17 @@ struct Tile {
   // W_k then the horizontal blur taps at this lane's LR column, for E row er.
   __device__ __forceinline__ float fwd_row(int er, int lane, float drho, float dtau, const Geom& G) const {
     constexpr int NTAP = TC<Z>::NTAP;
-    if (!row_in(er)) return 0.f;    // blur zero padding (A11), warp uniform
+    if (!kDummy && !row_in(er)) return 0.f;    // blur zero padding (A11), warp uniform
     float om[Z], wp[Z];
     load_om(er, lane, om);
-    const float Yf = (float)(YE0 - PY0 + er);
+    const float Yf = yrow(er);
     const float X0 = (float)(XE0 - PX0 + Z * lane);
 #pragma unroll
     for (int k = 0; k < NP; ++k) {
       const int s = 2 * k;
       int i00[2], i01[2];
       float2 a, b;
-      sample2(Yf, X0 + (float)s, f2(om[s], om[s + 1]), drho, dtau, i00, i01, a, b);
+      sample2(ypair(Yf, k), X0 + (float)s, f2(om[s], om[s + 1]), drho, dtau, i00, i01, a, b);
       const float2 p00 = f2(P[i00[0]], P[i00[1]]), p01 = f2(P[i01[0]], P[i01[1]]);
       const float2 p10 = f2(P[i00[0] + PW], P[i00[1] + PW]), p11 = f2(P[i01[0] + PW], P[i01[1] + PW]);
       const float2 top = __ffma2_rn(b, sub2(p01, p00), p00), bot = __ffma2_rn(b, sub2(p11, p10), p10);
@@ -230,7 +256,7 @@ struct Tile {
       constexpr int s = Z - 1;
       int i00, i01;
       float a, b;
-      sample(Yf, X0 + (float)s, om[s], drho, dtau, i00, i01, a, b);
+      sample(yone(Yf), X0 + (float)s, om[s], drho, dtau, i00, i01, a, b);
       const float p00 = P[i00], p01 = P[i01], p10 = P[i00 + PW], p11 = P[i01 + PW];
       const float top = fmaf(b, p01 - p00, p00), bot = fmaf(b, p11 - p10, p10);
       wp[s] = col_in(s) ? fmaf(a, bot - top, top) : 0.f;
@@ -256,7 +282,7 @@ struct Tile {
                                           const Geom& G) const {
     constexpr int NJ = 2 * TC<Z>::R / Z + 1;
     constexpr int R2 = 2 * TC<Z>::R;
-    if (!row_in(er)) return;        // E positions outside the image carry no adjoint (A11)
+    if (!kDummy && !row_in(er)) return;        // E positions outside the image carry no adjoint (A11)
     float tv[NJ];
     tv[0] = t1b;
 #pragma unroll
@@ -266,7 +292,7 @@ struct Tile {
     }
     float om[Z];
     load_om(er, lane, om);
-    const float Yf = (float)(YE0 - PY0 + er);
+    const float Yf = yrow(er);
     const float X0 = (float)(XE0 - PX0 + Z * lane);
     int i00[Z], i01[Z];
     float2 w0[Z], w1[Z];   // (row, row + 1) weights times t on the left / right source column
@@ -281,7 +307,7 @@ struct Tile {
       }
       int c0[2], c1[2];
       float2 a, b;
-      sample2(Yf, X0 + (float)s, f2(om[s], om[s + 1]), drho, dtau, c0, c1, a, b);
+      sample2(ypair(Yf, k), X0 + (float)s, f2(om[s], om[s + 1]), drho, dtau, c0, c1, a, b);
       i00[s] = c0[0]; i01[s] = c1[0]; i00[s + 1] = c0[1]; i01[s + 1] = c1[1];
       const float2 ts = __fmul2_rn(colsel(t, s), f2s(tscale));
       // per position: (ts (1 - a), ts a) = the two source rows' shares, split by b into
@@ -300,7 +326,7 @@ struct Tile {
       for (int j = 0; j < NJ; ++j)
         if (Z * j + s <= R2) t = fmaf(G.taps[Z * j + s], tv[j], t);
       float a, b;
-      sample(Yf, X0 + (float)s, om[s], drho, dtau, i00[s], i01[s], a, b);
+      sample(yone(Yf), X0 + (float)s, om[s], drho, dtau, i00[s], i01[s], a, b);
       const float ts = col_in(s) ? t * tscale : 0.f;
       const float ta = ts * a;
       const float2 q = f2(ts - ta, ta);
@@ -569,9 +595,10 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
   if (MODE == MODE_NORMAL && io.cg_k >= 2 && ctl->cur[S_STOP] != 0.0) return;  // CG stopped
 
   float* P = smem;                                           // PH*PW  input tile (phase split)
-  int* ACC = reinterpret_cast<int*>(P + PH * PW);            // 2*PH*PW fixed-point accumulator (hi, lo)
-  const int LO = PH * PW;
-  float* OM = P + 3 * PH * PW;                               // EY*ECOL disparity on the E region
+  const int PHA = PH + (C::DUMMY ? 2 : 0);                   // + 2 zero rows (TC::DUMMY, Tile::yrow)
+  int* ACC = reinterpret_cast<int*>(P + PHA * PW);           // 2*PHA*PW fixed-point accumulator (hi, lo)
+  const int LO = PHA * PW;
+  float* OM = P + 3 * PHA * PW;                              // EY*ECOL disparity on the E region
   float* M = OM + EY * ECOL;                                 // MH*MW  weight map, own + radius
   float* NL = M + T.MH * T.MW;                               // TY*TX  NLTV term of the own pixels
   const size_t red_off = ((size_t)(NL - smem) + (size_t)TY * TX + 1) & ~(size_t)1;   // 8-byte aligned
@@ -642,11 +669,17 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
       ACC[LO + i] = 0;
     }
   }
-  for (int e = tid; e < EY * ECOL; e += NT) {
+  for (int e = tid; e < EY * ECOL; e += NT) {   // 0 outside the image (the dummy rows rely on it)
     const int er = e / ECOL, c = e - er * ECOL;
     const int Y = YE0 + er, X = XE0 + c;
     OM[e] = (Y >= 0 && Y < H && X >= 0 && X < W) ? io.omega[(size_t)Y * ps + X] : 0.f;
   }
+  if (C::DUMMY)   // the two zero rows past the input tile (and their accumulator cells)
+    for (int e = tid; e < 2 * PW; e += NT) {
+      P[PH * PW + e] = 0.f;
+      ACC[PH * PW + e] = 0;
+      ACC[LO + PH * PW + e] = 0;
+    }
   const int rr = G.radius, MW = T.MW;
   if (MODE == MODE_NORMAL && io.do_nltv) {
     for (int e = tid; e < T.MH * MW; e += NT) {
@@ -713,13 +746,25 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
 #pragma unroll
     for (int s2 = 0; s2 < Z; ++s2) {
       const int c = Z * lane + s2, X = XE0 + c;
-      if (c < C::EXv && X >= 0 && X < W) colmask |= 1u << s2;
+      // (E columns past EXv feed no own LR column and receive a zero adjoint: left as they are,
+      // so their real disparity keeps the warp's adjacency test of adj_row true)
+      if (X >= 0 && X < W) colmask |= 1u << s2;
     }
     const bool rows_in = (YE0 >= 0) && (YE0 + EY <= H);
     const bool cols_in = (XE0 >= 0) && (XE0 + C::EXv <= W);
     const unsigned koff = 0u - ((unsigned)kMagicBits * (unsigned)PW + (unsigned)kMagicBits / Z);
     auto run = [&](auto tile) {
       tile.colmask = colmask;
+      if constexpr (decltype(tile)::kDummy) {
+        tile.PHd = (float)PH;
+#pragma unroll
+        for (int k = 0; k <= decltype(tile)::NP; ++k) {
+          const float m0 = ((colmask >> (2 * k)) & 1u) ? 1.f : 0.f;
+          const float m1 = (2 * k + 1 < Z && ((colmask >> (2 * k + 1)) & 1u)) ? 1.f : 0.f;
+          tile.ymul[k] = f2(m0, m1);
+          tile.yadd[k] = f2((1.f - m0) * (float)PH, (1.f - m1) * (float)PH);
+        }
+      }
       tile.P = P; tile.ACC = ACC; tile.OM = OM; tile.PW = PW; tile.PWZ = PWZ; tile.PY0 = PY0; tile.PX0 = PX0;
       tile.YE0 = YE0; tile.XE0 = XE0; tile.H = H; tile.W = W; tile.tscale = s_scale[0]; tile.lo = LO;
       tile.koff = koff; tile.rows_in = rows_in;

@@ -19,7 +19,9 @@ static void fill_static(TileGeom& T) {
 }
 
 static size_t smem_bytes(const TileGeom& T, int nwarps) {
-  size_t words = 3 * (size_t)T.PH * T.PW + (size_t)T.EY * T.ECOL + (size_t)T.MH * T.MW + (size_t)T.TY * T.TX + 8;
+  const bool dummy = LFSR_DUMMY_MASK & (1 << (T.ECOL / 32));   // TC<zeta>::DUMMY
+  size_t words = 3 * (size_t)(T.PH + (dummy ? 2 : 0)) * T.PW + (size_t)T.EY * T.ECOL + (size_t)T.MH * T.MW +
+                 (size_t)T.TY * T.TX + 8;
   return words * 4 + (size_t)nwarps * 4 * sizeof(double);
 }
 
