@@ -374,6 +374,7 @@ __device__ __forceinline__ float nltv_pixel(const NltvCtx& c, const Geom& G, int
   const float xz = c.P[pidx<Z>(py, px, c.PW, c.PWZ)];
   const float mz = c.M[mi];
   float acc = 0.f;
+  float fpq = 0.f, freg = 0.f, fres = 0.f;   // this pixel's reduction terms (<= s_d each), fp32
   auto one = [&](int d, int dy, int dx) {
     const float wd = G.wd[d];
     const bool fin = !CHECK || ((Y + dy >= 0) && (Y + dy < c.H) && (X + dx >= 0) && (X + dx < c.W));
@@ -386,7 +387,7 @@ __device__ __forceinline__ float nltv_pixel(const NltvCtx& c, const Geom& G, int
       const float dp = xz - xf;
       const float f2 = fin ? wz * wz : 0.f;
       acc = fmaf(f2, dp, acc);
-      pq += (double)(f2 * dp) * dp;
+      fpq = fmaf(f2 * dp, dp, fpq);
       const float b2 = bin ? wb * wb : 0.f;
       acc = fmaf(-b2, xb - xz, acc);
     } else {
@@ -396,8 +397,8 @@ __device__ __forceinline__ float nltv_pixel(const NltvCtx& c, const Geom& G, int
       const float wso = __ldg(c.wSr + pl + gi);
       const float wn = fminf(fmaxf(g + wso, -c.ith), c.ith);
       c.wSw[pl + gi] = wn;
-      reg += fabs((double)g);
-      res += (double)(wn - wso) * (wn - wso);
+      freg += fabsf(g);
+      fres = fmaf(wn - wso, wn - wso, fres);
       if (fin) acc = fmaf(wz, 2.f * wn - wso, acc);
       if (bin) {
         const float wb = wd * mb;
@@ -420,6 +421,11 @@ __device__ __forceinline__ float nltv_pixel(const NltvCtx& c, const Geom& G, int
     }
   } else {
     for (int d = 0; d < G.s_d; ++d) one(d, G.ody[d], G.odx[d]);
+  }
+  if (MODE == MODE_NORMAL) pq += (double)fpq;
+  if (MODE == MODE_WZ) {
+    reg += (double)freg;
+    res += (double)fres;
   }
   return acc;
 }
