@@ -143,7 +143,8 @@ def oracle_params(cfg, d):
     return O.Params(n_views=cfg.n_views, lr_h=cfg.lr_h, lr_w=cfg.lr_w, scale=cfg.scale, ref_view=cfg.ref_view,
                     radius=d.radius, lambda1=d.lambda1, lambda2=d.lambda2, lambda_reg=d.lambda_reg,
                     sigma_s=d.sigma_s, sigma_e=d.sigma_e, sigma_o1=d.sigma_o1, sigma_o2=d.sigma_o2, theta=d.theta,
-                    cg_max_iters=d.cg_max_iters, cg_tol=d.cg_tol)
+                    cg_max_iters=d.cg_max_iters, cg_tol=d.cg_tol,
+                    offset_weights=getattr(d, "offset_weights", None))
 
 
 def time_oracle(lf, cfg, d, iters=1):
@@ -189,7 +190,7 @@ def main():
     args = parse()
     import lfsr_synth as S
     cfg = S.CONFIGS[args.config]
-    d = S.SolverDefaults()
+    d = S.defaults_for(cfg)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))

@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define LFSR_ABI_VERSION 1
+#define LFSR_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define LFSR_API __attribute__((visibility("default")))
@@ -96,6 +96,11 @@ typedef struct {
                                  e.g. broadcast over a torch.distributed group; else NULL */
   void* stream;         /* cudaStream_t to run on (e.g. torch.cuda.current_stream()
                            .cuda_stream), or NULL for a ctx-owned stream             */
+  const float* offset_weights; /* NULL: w_d = exp(-|d|^2/sigma_s) (A8).  Else s_d finite
+                           weights >= 0 in the offset order of reading A9 (row-major dy,
+                           dx over the window, centre skipped), copied at lfsr_create --
+                           e.g. BTV's alpha^(|dx|+|dy|) for the MISR use (P:L404-412,
+                           P:L1110-1116).  Host memory.              */
 } lfsr_params;
 
 /* Per-ADMM-iteration record.  J terms refer to x^{n-1} and the

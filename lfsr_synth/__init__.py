@@ -59,6 +59,37 @@ class SolverDefaults:
     cg_tol: float = 0.0      # tau = 0: exactly K steps (reading A18)
 
 
+@dataclass
+class MisrDefaults:
+    """Solver constants for the MISR use of the method:
+    l1 data term only (lambda2 = 0), BTV regulariser -- offset weights alpha^(|dx|+|dy|)
+    with no edge or occlusion weighting (sigma_e, sigma_o -> inf) -- on frames
+    with global sub-pixel shifts (constant disparity)."""
+    lambda1: float = 1.0
+    lambda2: float = 0.0
+    lambda_reg: float = 0.1       # M1 oracle sweep (lambda_reg x theta x alpha): 19.4 dB bicubic -> 24.6 dB at N = 20
+    sigma_s: float = 3.0          # unused: offset_weights override w_d
+    sigma_e: float = math.inf
+    sigma_o1: float = math.inf
+    sigma_o2: float = math.inf
+    theta: float = 4.0
+    radius: int = 2
+    cg_max_iters: int = 5
+    cg_tol: float = 0.0
+    btv_alpha: float = 0.7
+
+    @property
+    def offset_weights(self):
+        return btv_weights(self.radius, self.btv_alpha)
+
+
+def btv_weights(radius: int, alpha: float) -> list:
+    """BTV offset weights alpha^(|dx|+|dy|) in the offset order of reading A9 (row-major dy, dx
+    over the (2r+1)^2 window, centre skipped) -- the lfsr_params.offset_weights layout."""
+    return [float(alpha) ** (abs(dx) + abs(dy)) for dy in range(-radius, radius + 1)
+            for dx in range(-radius, radius + 1) if (dy, dx) != (0, 0)]
+
+
 @dataclass(frozen=True)
 class Config:
     name: str
@@ -79,7 +110,7 @@ class Config:
 
     @property
     def ref_view(self):
-        return self.n_views // 2
+        return 0 if self.kind == "misr" else self.n_views // 2
 
     @property
     def H(self):
@@ -97,11 +128,33 @@ CONFIGS = {
     "C3": Config("C3", 9, 256, 256, 2, 0.05, 20.0, 1.5, "hci", 10, "9x9 views, 256x256 LR -> x2 (512x512 HR), sigma=0.05 + 20% impulse"),
     "C4": Config("C4", 9, 171, 171, 3, 0.05, 20.0, 1.5, "hci", 10, "9x9 views, 171x171 LR -> x3 (513x513 HR)"),
     "C5": Config("C5", 9, 512, 512, 4, 0.02, 5.0, 1.0, "natural", 10, "9x9 views, 512x512 LR -> x4 (2048x2048 HR)"),
+    # MISR (SURVEY 8f NEXT-1): grid x grid frames with global shifts of 1/zeta LR px (= 1 HR px),
+    # constant disparity 1, natural-image texture (DIV8K-shaped; tab:mfsr, P:L1125-1165)
+    "M1": Config("M1", 2, 32, 32, 2, 0.02, 5.0, 1.0, "misr", 20, "MISR 4 frames x2, 32x32 LR -> 64x64 HR"),
+    "M2": Config("M2", 2, 1024, 1024, 2, 0.02, 5.0, 1.0, "misr", 10, "MISR 4 frames x2 (1/2-px shifts), 1024^2 LR -> 2048^2 HR"),
+    "M3": Config("M3", 3, 512, 512, 3, 0.02, 5.0, 1.0, "misr", 10, "MISR 9 frames x3 (1/3-px shifts), 512^2 LR -> 1536^2 HR"),
 }
+
+
+def misr_offsets(grid: int) -> np.ndarray:
+    """[grid*grid][2] = (drho, dtau) = (b, a) HR px for a, b in [0, grid): the MISR frame
+    shifts (1/zeta LR px steps at zeta = grid), frame 0 unshifted (the reference)."""
+    out = np.zeros((grid * grid, 2), dtype=np.float32)
+    for a in range(grid):
+        for b in range(grid):
+            out[a * grid + b] = (b, a)
+    return out
 
 
 def get_config(name: str) -> Config:
     return CONFIGS[name]
+
+
+def defaults_for(cfg) -> "SolverDefaults | MisrDefaults":
+    """The frozen solver constants of a config: MisrDefaults for the MISR configs."""
+    if isinstance(cfg, str):
+        cfg = CONFIGS[cfg]
+    return MisrDefaults() if cfg.kind == "misr" else SolverDefaults()
 
 
 def grid_offsets(grid: int) -> np.ndarray:
@@ -222,6 +275,9 @@ def _natural_texture(rng, H, W):
 
 def _build_scene(kind, H, W, omega_max, rng, n_objects):
     layers = []
+    if kind == "misr":   # one textured plane at constant disparity omega_max: frames are global shifts
+        layers.append(_Layer("plane", None, float(omega_max), _natural_texture(rng, H, W)))
+        return layers
     if kind == "natural":
         # smooth disparity plane over the whole frame within [-omega_max, omega_max]
         d0 = rng.uniform(-0.3, 0.3) * omega_max
@@ -291,7 +347,10 @@ def make_lightfield(cfg: Config | str, seed: int | None = None, ss: int = 2,
     rng = np.random.Generator(np.random.Philox(scene_seed))
     H, W, z = cfg.H, cfg.W, cfg.scale
     layers = _build_scene(cfg.kind, H, W, cfg.omega_max, rng, n_objects=8)
-    vo = grid_offsets(cfg.grid) if views is None else np.asarray(views, dtype=np.float32)
+    if views is not None:
+        vo = np.asarray(views, dtype=np.float32)
+    else:
+        vo = misr_offsets(cfg.grid) if cfg.kind == "misr" else grid_offsets(cfg.grid)
     ref = int(np.argmin(np.abs(vo).sum(axis=1)))
 
     # reference view at HR (area average over each HR pixel) and its disparity map

@@ -20,6 +20,7 @@ import subprocess
 from dataclasses import dataclass, field
 
 import numpy as np
+from typing import Optional, Sequence
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.c")
@@ -44,7 +45,8 @@ class _Params(ctypes.Structure):
                 ("sigma_e", ctypes.c_double), ("sigma_o1", ctypes.c_double),
                 ("sigma_o2", ctypes.c_double), ("theta", ctypes.c_double),
                 ("cg_max_iters", ctypes.c_int32), ("cg_tol", ctypes.c_double),
-                ("reweight_every_iter", ctypes.c_int32)]
+                ("reweight_every_iter", ctypes.c_int32),
+                ("offset_weights", ctypes.POINTER(ctypes.c_double))]
 
 
 class _Stats(ctypes.Structure):
@@ -77,6 +79,8 @@ def lib():
             "or_offsets": (I, [I, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),
             "or_apply_S": (None, [I, I, I, ctypes.c_double, D, D, D]),
             "or_apply_ST": (None, [I, I, I, ctypes.c_double, D, D, D]),
+            "or_apply_Sw": (None, [I, I, I, D, D, D, D]),
+            "or_apply_STw": (None, [I, I, I, D, D, D, D]),
             "or_weights_m": (None, [I, I, ctypes.c_double, ctypes.c_double, D, D, D]),
             "or_setup_wo": (None, [P, D, D, D, D, D, D]),
             "or_bicubic": (None, [I, I, I, D, D]),
@@ -124,6 +128,7 @@ class Params:
     cg_max_iters: int = 5
     cg_tol: float = 0.0
     reweight_every_iter: int = 1
+    offset_weights: Optional[Sequence[float]] = None   # s_d weights overriding exp(-|d|^2/sigma_s)
 
     @property
     def H(self):
@@ -138,10 +143,15 @@ class Params:
         return (2 * self.radius + 1) ** 2 - 1
 
     def c(self):
+        ow = None
+        if self.offset_weights is not None:
+            self._ow = np.ascontiguousarray(self.offset_weights, dtype=np.float64)   # kept alive with self
+            assert self._ow.shape == (self.s_d,), "offset_weights must have s_d entries"
+            ow = _ptr(self._ow)
         return _Params(self.n_views, self.lr_h, self.lr_w, self.scale, self.ref_view, self.radius,
                        self.lambda1, self.lambda2, self.lambda_reg, self.sigma_s, self.sigma_e,
                        self.sigma_o1, self.sigma_o2, self.theta, self.cg_max_iters, self.cg_tol,
-                       self.reweight_every_iter)
+                       self.reweight_every_iter, ow)
 
 
 def blur_taps(scale: int) -> np.ndarray:
@@ -213,20 +223,30 @@ def apply_AT(P: Params, view_offsets, omega, r):
     return out
 
 
-def apply_S(x, m, radius, sigma_s):
+def apply_S(x, m, radius, sigma_s, weights=None):
+    """S; weights: optional s_d offset weights replacing exp(-|d|^2/sigma_s)."""
     x, m = _d(x), _d(m)
     H, W = x.shape
     sd = (2 * radius + 1) ** 2 - 1
     out = np.zeros((sd, H, W))
-    lib().or_apply_S(H, W, radius, float(sigma_s), _ptr(m), _ptr(x), _ptr(out))
+    if weights is None:
+        lib().or_apply_S(H, W, radius, float(sigma_s), _ptr(m), _ptr(x), _ptr(out))
+    else:
+        wv = _d(weights)
+        lib().or_apply_Sw(H, W, radius, _ptr(wv), _ptr(m), _ptr(x), _ptr(out))
     return out
 
 
-def apply_ST(h, m, radius, sigma_s):
+def apply_ST(h, m, radius, sigma_s, weights=None):
+    """S^T (P:L596-601); weights as in apply_S."""
     h, m = _d(h), _d(m)
     _, H, W = h.shape
     out = np.zeros((H, W))
-    lib().or_apply_ST(H, W, radius, float(sigma_s), _ptr(m), _ptr(h), _ptr(out))
+    if weights is None:
+        lib().or_apply_ST(H, W, radius, float(sigma_s), _ptr(m), _ptr(h), _ptr(out))
+    else:
+        wv = _d(weights)
+        lib().or_apply_STw(H, W, radius, _ptr(wv), _ptr(m), _ptr(h), _ptr(out))
     return out
 
 

@@ -51,6 +51,8 @@ typedef struct {
   int32_t cg_max_iters;                         /* K */
   double cg_tol;                                /* tau on <r,r> (reading A18) */
   int32_t reweight_every_iter;                  /* 1 = paper */
+  const double* offset_weights;                 /* NULL: w_d = exp(-|d|^2/sigma_s); else s_d
+                                                   user weights in the U order (BTV, NEXT-1) */
 } or_params;
 
 typedef struct {
@@ -223,16 +225,25 @@ static double spatial_weight(int dy, int dx, double sigma_s) {
   return exp(-(double)(dy * dy + dx * dx) / sigma_s);
 }
 
+/* The s_d offset weights w_d: Gaussian in |d| (above), or the caller's list --
+ * e.g. BTV's alpha^(|dx|+|dy|) (the regulariser family is fixed by
+ * the choice of N(u) and w; MISR use with l1 + BTV). */
+static void offset_weights(int radius, double sigma_s, const double* user, double* wd) {
+  int dys[1024], dxs[1024];
+  int sd = or_offsets(radius, dys, dxs);
+  for (int d = 0; d < sd; ++d) wd[d] = user ? user[d] : spatial_weight(dys[d], dxs[d], sigma_s);
+}
+
 /* Weighted directional gradient nabla^{U,V}, reading A10:
  *   g_d(z) = W_d(z) (x(z) - x(z+d)) if z+d in Omega, else 0,
- * W_d(z) = w_d * m(z).  out: [s_d][H][W]. */
-void or_apply_S(int H, int W, int radius, double sigma_s, const double* m, const double* x,
-                double* out) {
+ * W_d(z) = w_d * m(z).  out: [s_d][H][W].  wd: the s_d offset weights. */
+void or_apply_Sw(int H, int W, int radius, const double* wds, const double* m, const double* x,
+                 double* out) {
   int dys[1024], dxs[1024];
   int sd = or_offsets(radius, dys, dxs);
   size_t p = (size_t)H * W;
   for (int d = 0; d < sd; ++d) {
-    double wd = spatial_weight(dys[d], dxs[d], sigma_s);
+    double wd = wds[d];
 #pragma omp parallel for schedule(static)
     for (int Y = 0; Y < H; ++Y)
       for (int X = 0; X < W; ++X) {
@@ -248,8 +259,8 @@ void or_apply_S(int H, int W, int radius, double sigma_s, const double* m, const
 /* Weighted directional divergence div^{U,V} taken as the exact
  * transpose of or_apply_S:
  *   (S^T h)(z) = sum_d [ 1{z+d in Omega} W_d(z) h_d(z) - 1{z-d in Omega} W_d(z-d) h_d(z-d) ]. */
-void or_apply_ST(int H, int W, int radius, double sigma_s, const double* m, const double* h,
-                 double* out) {
+void or_apply_STw(int H, int W, int radius, const double* wds, const double* m, const double* h,
+                  double* out) {
   int dys[1024], dxs[1024];
   int sd = or_offsets(radius, dys, dxs);
   size_t p = (size_t)H * W;
@@ -258,7 +269,7 @@ void or_apply_ST(int H, int W, int radius, double sigma_s, const double* m, cons
     for (int X = 0; X < W; ++X) {
       double s = 0.0;
       for (int d = 0; d < sd; ++d) {
-        double wd = spatial_weight(dys[d], dxs[d], sigma_s);
+        double wd = wds[d];
         int yf = Y + dys[d], xf = X + dxs[d];
         if (yf >= 0 && yf < H && xf >= 0 && xf < W)
           s += wd * m[(size_t)Y * W + X] * h[d * p + (size_t)Y * W + X];
@@ -268,6 +279,18 @@ void or_apply_ST(int H, int W, int radius, double sigma_s, const double* m, cons
       }
       out[(size_t)Y * W + X] = s;
     }
+}
+
+/* The same with the Gaussian offset weights exp(-|d|^2 / sigma_s) (reading A8). */
+void or_apply_S(int H, int W, int radius, double sigma_s, const double* m, const double* x, double* out) {
+  double wd[1024];
+  offset_weights(radius, sigma_s, NULL, wd);
+  or_apply_Sw(H, W, radius, wd, m, x, out);
+}
+void or_apply_ST(int H, int W, int radius, double sigma_s, const double* m, const double* h, double* out) {
+  double wd[1024];
+  offset_weights(radius, sigma_s, NULL, wd);
+  or_apply_STw(H, W, radius, wd, m, h, out);
 }
 
 /* Per-pixel weight map m = lambda_R * w_o * w_e (W_d = w_d * m),
@@ -391,8 +414,10 @@ void or_normal(const or_params* P, const double* view_offsets, const double* ome
   double* stsp = (double*)malloc(sizeof(double) * p);
   or_apply_A(P, view_offsets, omega, pvec, ap);
   or_apply_AT(P, view_offsets, omega, ap, atap);
-  or_apply_S(H, W, P->radius, P->sigma_s, m, pvec, sp);
-  or_apply_ST(H, W, P->radius, P->sigma_s, m, sp, stsp);
+  double wds[1024];
+  offset_weights(P->radius, P->sigma_s, P->offset_weights, wds);
+  or_apply_Sw(H, W, P->radius, wds, m, pvec, sp);
+  or_apply_STw(H, W, P->radius, wds, m, sp, stsp);
   double cA = P->lambda2 + 0.5 * P->theta * P->lambda1 * P->lambda1;
   for (size_t i = 0; i < p; ++i) out[i] = cA * atap[i] + 0.5 * P->theta * stsp[i];
   free(ap);
@@ -407,6 +432,11 @@ static int validate(const or_params* P) {
   if (!(P->theta > 0) || P->lambda1 < 0 || P->lambda2 < 0 || P->lambda_reg < 0) return OR_ERR_ARG;
   if (P->lambda1 + P->lambda2 <= 0 || P->cg_max_iters < 1 || P->cg_tol < 0) return OR_ERR_ARG;
   if (!(P->sigma_s > 0) || !(P->sigma_e > 0) || !(P->sigma_o1 > 0) || !(P->sigma_o2 > 0)) return OR_ERR_ARG;
+  if (P->offset_weights) {
+    int sd = (2 * P->radius + 1) * (2 * P->radius + 1) - 1;
+    for (int d = 0; d < sd; ++d)
+      if (!(P->offset_weights[d] >= 0) || isinf(P->offset_weights[d])) return OR_ERR_ARG;
+  }
   return OR_OK;
 }
 
@@ -437,6 +467,8 @@ int or_admm(const or_params* P, const double* y, const double* view_offsets,
   int sd = or_offsets(P->radius, dys, dxs);
   size_t ns = p * sd;
   double th = P->theta, l1 = P->lambda1, l2 = P->lambda2, inv_th = 1.0 / th;
+  double wds[1024];
+  offset_weights(P->radius, P->sigma_s, P->offset_weights, wds);
 
   double* x = (double*)malloc(sizeof(double) * p);
   double* wo = (double*)malloc(sizeof(double) * p);
@@ -482,7 +514,7 @@ int or_admm(const or_params* P, const double* y, const double* view_offsets,
       dl2 += e[i] * e[i];
     }
     /* NLTV part */
-    or_apply_S(H, W, P->radius, P->sigma_s, m, x, g);
+    or_apply_Sw(H, W, P->radius, wds, m, x, g);
     double reg = 0.0;
     for (size_t i = 0; i < ns; ++i) {
       double uS = g[i] + wS[i];
@@ -500,7 +532,7 @@ int or_admm(const or_params* P, const double* y, const double* view_offsets,
 
     /* v = A^T rho + (th/2) S^T f_S */
     or_apply_AT(P, view_offsets, omega, rho, v);
-    or_apply_ST(H, W, P->radius, P->sigma_s, m, fS, t);
+    or_apply_STw(H, W, P->radius, wds, m, fS, t);
     for (size_t i = 0; i < p; ++i) v[i] += 0.5 * th * t[i];
 
     /* x-step: textbook CG (readings A1-A4, A18) */
@@ -549,7 +581,9 @@ double or_cost(const or_params* P, const double* y, const double* view_offsets,
   or_apply_A(P, view_offsets, omega, x, e);
   double l1 = 0, l2 = 0, reg = 0;
   for (size_t i = 0; i < nq; ++i) { double d = e[i] - y[i]; l1 += fabs(d); l2 += d * d; }
-  or_apply_S(H, W, P->radius, P->sigma_s, m, x, g);
+  double wds[1024];
+  offset_weights(P->radius, P->sigma_s, P->offset_weights, wds);
+  or_apply_Sw(H, W, P->radius, wds, m, x, g);
   for (size_t i = 0; i < p * sd; ++i) reg += fabs(g[i]);
   free(e);
   free(g);

@@ -145,6 +145,12 @@ static const char* validate(const lfsr_params* p) {
   if (p->cg_max_iters < 1 || p->cg_max_iters > kMaxK) return "cg_max_iters must be in [1, 64]";
   if (!(p->cg_tol >= 0.f)) return "cg_tol must be >= 0";
   if (p->reweight_every_iter != 0 && p->reweight_every_iter != 1) return "reweight_every_iter must be 0 or 1";
+  if (p->offset_weights) {
+    const int sd = (2 * p->nltv_radius + 1) * (2 * p->nltv_radius + 1) - 1;
+    for (int d = 0; d < sd; ++d)
+      if (!(p->offset_weights[d] >= 0.f) || !std::isfinite(p->offset_weights[d]))
+        return "offset_weights must be finite and >= 0";
+  }
   if (p->device < 0) return "device must be >= 0";
   if (p->n_ranks < 1 || p->n_ranks > 1024) return "n_ranks must be in [1, 1024]";
   if (p->n_ranks == 1 && p->rank != 0) return "rank must be 0 when n_ranks == 1";
@@ -207,7 +213,8 @@ static void fill_geom(const lfsr_params& p, Geom& G) {
       if (!dy && !dx) continue;
       G.ody[n] = (int8_t)dy;
       G.odx[n] = (int8_t)dx;
-      G.wd[n] = std::isinf(p.sigma_s) ? 1.f : (float)std::exp(-(double)(dy * dy + dx * dx) / p.sigma_s);
+      G.wd[n] = p.offset_weights ? p.offset_weights[n]
+                : std::isinf(p.sigma_s) ? 1.f : (float)std::exp(-(double)(dy * dy + dx * dx) / p.sigma_s);
       ++n;
     }
   G.s_d = n;

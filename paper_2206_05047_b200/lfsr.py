@@ -49,7 +49,7 @@ class _CParams(ctypes.Structure):
                 ("sigma_o2", ctypes.c_float), ("theta", ctypes.c_float), ("cg_max_iters", ctypes.c_int32),
                 ("cg_tol", ctypes.c_float), ("reweight_every_iter", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("rank", ctypes.c_int32), ("n_ranks", ctypes.c_int32), ("nccl_unique_id", ctypes.c_void_p),
-                ("stream", ctypes.c_void_p)]
+                ("stream", ctypes.c_void_p), ("offset_weights", ctypes.POINTER(ctypes.c_float))]
 
 
 class _CStats(ctypes.Structure):
@@ -145,6 +145,7 @@ class Params:
     n_ranks: int = 1          # HR row strips
     rank: int = 0             # this process's strip (NCCL mode) or -1: all strips in this ctx
     nccl_unique_id: bytes | None = None
+    offset_weights: object = None   # s_d floats (e.g. BTV alpha^(|dx|+|dy|)) replacing exp(-|d|^2/sigma_s)
 
     @property
     def H(self):
@@ -161,8 +162,15 @@ class Params:
     def to_c(self, stream=None) -> _CParams:
         c = _CParams()
         for f in fields(self):
-            if f.name != "nccl_unique_id":
+            if f.name not in ("nccl_unique_id", "offset_weights"):
                 setattr(c, f.name, getattr(self, f.name))
+        self._ow = None
+        if self.offset_weights is not None:
+            ow = [float(v) for v in self.offset_weights]
+            if len(ow) != self.s_d:
+                raise LFSRError(1, "offset_weights must have s_d = %d entries" % self.s_d)
+            self._ow = (ctypes.c_float * len(ow))(*ow)   # copied by lfsr_create
+            c.offset_weights = ctypes.cast(self._ow, ctypes.POINTER(ctypes.c_float))
         self._uid = None
         if self.nccl_unique_id is not None:
             self._uid = ctypes.create_string_buffer(bytes(self.nccl_unique_id), 128)
@@ -341,6 +349,8 @@ def params_for(lf_meta_or_cfg, defaults=None, **over) -> Params:
                                        "sigma_o2", "theta", "cg_max_iters", "cg_tol")}
     if defaults is not None:
         d["nltv_radius"] = defaults.radius
+        if getattr(defaults, "offset_weights", None) is not None:
+            d["offset_weights"] = list(defaults.offset_weights)
     d.update(n_views=cfg.n_views, lr_height=cfg.lr_h, lr_width=cfg.lr_w, scale=cfg.scale, ref_view=cfg.ref_view)
     d.update(over)
     return Params(**d)

@@ -28,7 +28,7 @@ def oparams(gp):
                     radius=gp.nltv_radius, lambda1=gp.lambda1, lambda2=gp.lambda2, lambda_reg=gp.lambda_reg,
                     sigma_s=gp.sigma_s, sigma_e=gp.sigma_e, sigma_o1=gp.sigma_o1, sigma_o2=gp.sigma_o2,
                     theta=gp.theta, cg_max_iters=gp.cg_max_iters, cg_tol=gp.cg_tol,
-                    reweight_every_iter=gp.reweight_every_iter)
+                    reweight_every_iter=gp.reweight_every_iter, offset_weights=gp.offset_weights)
 
 
 def f32(a):
@@ -104,14 +104,15 @@ def test_gpu_adjoint_identities(lfsr_mod, case):
     s.close()
 
 
-def run_pair(lfsr_mod, lf, n_iters, **over):
-    cfg_defaults = S.SolverDefaults()
+def run_pair(lfsr_mod, lf, n_iters, defaults=None, **over):
+    cfg_defaults = defaults or S.SolverDefaults()
     p = lfsr_mod.Params(n_views=lf.n_views, lr_height=lf.y.shape[1], lr_width=lf.y.shape[2], scale=lf.scale,
                         ref_view=lf.ref_view, nltv_radius=cfg_defaults.radius, lambda1=cfg_defaults.lambda1,
                         lambda2=cfg_defaults.lambda2, lambda_reg=cfg_defaults.lambda_reg,
                         sigma_s=cfg_defaults.sigma_s, sigma_e=cfg_defaults.sigma_e, sigma_o1=cfg_defaults.sigma_o1,
                         sigma_o2=cfg_defaults.sigma_o2, theta=cfg_defaults.theta,
-                        cg_max_iters=cfg_defaults.cg_max_iters, cg_tol=cfg_defaults.cg_tol)
+                        cg_max_iters=cfg_defaults.cg_max_iters, cg_tol=cfg_defaults.cg_tol,
+                        offset_weights=getattr(cfg_defaults, "offset_weights", None))
     for k, v in over.items():
         setattr(p, k, v)
     ora = O.admm(oparams(p), lf.y, lf.view_offsets, lf.omega, n_iters)
@@ -297,3 +298,31 @@ def test_full_size_C5_sampled(lfsr_mod):
     st = s.admm_run(1)
     assert st[0]["cg_iters"] == d.cg_max_iters and not st[0]["nonfinite"]
     s.close()
+
+
+# ----------------------------------------------------------------------------- MISR (NEXT-1)
+def test_misr_operator_parity_btv_weights(lfsr_mod):
+    """S / S^T / M with user offset weights (BTV alpha^(|dx|+|dy|)) and global-shift frames."""
+    lf = S.make_lightfield("M1")
+    d = S.MisrDefaults()
+    p = lfsr_mod.params_for(S.CONFIGS["M1"], d)
+    s = lfsr_mod.Solver(p)
+    s.set_observations(lf.y, lf.view_offsets, lf.omega)
+    P = oparams(p)
+    g = np.random.default_rng(17)
+    xin = g.uniform(-1, 1, (p.H, p.W)).astype(np.float32)
+    hin = g.uniform(-1, 1, (p.s_d, p.H, p.W)).astype(np.float32)
+    m = s.get_state()["m"]
+    assert np.allclose(m, d.lambda_reg)          # sigma_e = sigma_o = inf: m = lambda_R (S:L305)
+    w = d.offset_weights
+    assert rel_l2(s.op("S", xin), O.apply_S(xin, m, p.nltv_radius, p.sigma_s, weights=w)) < OP_TOL
+    assert rel_l2(s.op("ST", hin), O.apply_ST(hin, m, p.nltv_radius, p.sigma_s, weights=w)) < OP_TOL
+    assert rel_l2(s.op("NORMAL", xin), O.normal(P, lf.view_offsets, lf.omega, m, xin)) < OP_TOL
+    s.close()
+
+
+def test_misr_admm_parity(lfsr_mod):
+    """The MISR use: l1 + BTV, lambda2 = 0, 4 frames x2 with global shifts."""
+    lf = S.make_lightfield("M1")
+    p, ora, xs, stats, st = run_pair(lfsr_mod, lf, 10, defaults=S.MisrDefaults())
+    check_iterates(p, ora, xs, stats, st, lf.x_gt)

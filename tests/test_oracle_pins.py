@@ -487,3 +487,52 @@ def test_P15_admm_improves_psnr(oracle_lib):
     p0 = O.psnr(res.x_iters[0], lf.x_gt)
     pN = O.psnr(res.x_iters[-1], lf.x_gt)
     assert pN >= p0 + 3.0, (p0, pN)
+
+
+# ----------------------------------------------------------------------------- P16/P17 MISR (NEXT-1)
+def test_P16_btv_offset_weights(oracle_lib):
+    """User offset weights (BTV): with m = 1, sum |S x| over all offsets equals the
+    bilateral-TV value sum_{0 < |l|,|k| <= r} alpha^(|l|+|k|) sum_z |x(z) - x(z + (l, k))| over
+    pairs inside the image, computed here by array slicing; and S^T is S's transpose."""
+    import lfsr_synth as S
+    g = np.random.default_rng(16)
+    H, W, r, alpha = 13, 17, 2, 0.6
+    x = g.standard_normal((H, W))
+    wts = S.btv_weights(r, alpha)
+    m = np.ones((H, W))
+    sx = O.apply_S(x, m, r, 3.0, weights=wts)
+    btv = 0.0
+    for l in range(-r, r + 1):
+        for k in range(-r, r + 1):
+            if (l, k) == (0, 0):
+                continue
+            a = x[max(0, -l):H - max(0, l), max(0, -k):W - max(0, k)]
+            b = x[max(0, l):H + min(0, l), max(0, k):W + min(0, k)]
+            btv += alpha ** (abs(l) + abs(k)) * np.abs(a - b).sum()
+    assert abs(np.abs(sx).sum() - btv) <= 1e-12 * btv
+    hv = g.standard_normal(sx.shape)
+    lhs = float(np.vdot(sx, hv))
+    rhs = float(np.vdot(x, O.apply_ST(hv, m, r, 3.0, weights=wts)))
+    assert abs(lhs - rhs) <= 1e-12 * (np.linalg.norm(sx) * np.linalg.norm(hv))
+    # the Gaussian default is the same as passing its weights explicitly
+    gw = [np.exp(-(dy * dy + dx * dx) / 3.0) for dy in range(-r, r + 1) for dx in range(-r, r + 1)
+          if (dy, dx) != (0, 0)]
+    assert np.array_equal(O.apply_S(x, m, r, 3.0), O.apply_S(x, m, r, 3.0, weights=gw))
+
+
+@pytest.mark.slow
+def test_P17_misr_improves_psnr(oracle_lib):
+    """Sanity (not parity) for the MISR use: 4 frames x2 with 1/2-LR-px global
+    shifts, l1 data term + BTV (MisrDefaults); N = 20 ADMM iterations raise PSNR over the
+    bicubic x0 of frame 0 by >= 3 dB."""
+    import lfsr_synth as S
+    lf = S.make_lightfield("M1")
+    d = S.MisrDefaults()
+    P = O.Params(n_views=4, lr_h=32, lr_w=32, scale=2, ref_view=0, radius=d.radius, lambda1=d.lambda1,
+                 lambda2=d.lambda2, lambda_reg=d.lambda_reg, sigma_s=d.sigma_s, sigma_e=d.sigma_e,
+                 sigma_o1=d.sigma_o1, sigma_o2=d.sigma_o2, theta=d.theta, cg_max_iters=d.cg_max_iters,
+                 offset_weights=d.offset_weights)
+    res = O.admm(P, lf.y, lf.view_offsets, lf.omega, 20)
+    p0 = O.psnr(res.x_iters[0], lf.x_gt)
+    pN = O.psnr(res.x_iters[-1], lf.x_gt)
+    assert pN >= p0 + 3.0, (p0, pN)

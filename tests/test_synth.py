@@ -37,3 +37,14 @@ def test_grid_offsets_axis_convention():
     o = S.grid_offsets(3)
     # row-major over the angular grid: row = tau, column = rho (reading A13)
     assert np.array_equal(o[0], [-1, -1]) and np.array_equal(o[1], [0, -1]) and np.array_equal(o[3], [-1, 0])
+
+
+def test_misr_frames():
+    """MISR configs (NEXT-1): frame 0 unshifted and the reference, 1/zeta-LR-px (1 HR px) shifts,
+    constant disparity; BTV weights in the A9 offset order."""
+    lf = S.make_lightfield("M1")
+    assert lf.ref_view == S.CONFIGS["M1"].ref_view == 0
+    assert lf.view_offsets.tolist() == [[0, 0], [1, 0], [0, 1], [1, 1]]
+    assert np.all(lf.omega == 1.0)
+    w = S.btv_weights(1, 0.5)
+    assert w == [0.25, 0.5, 0.25, 0.5, 0.5, 0.25, 0.5, 0.25]

@@ -11,7 +11,7 @@ t0 = time.time()
 lf = S.make_lightfield(cfgname)
 print("gen %.1fs" % (time.time() - t0), flush=True)
 cfg = S.CONFIGS[cfgname]
-p = L.params_for(cfg, S.SolverDefaults())
+p = L.params_for(cfg, S.defaults_for(cfg))
 stream = torch.cuda.Stream()
 torch.cuda.set_stream(stream)
 s = L.Solver(p, stream=stream.cuda_stream)

@@ -11,7 +11,7 @@ import paper_2206_05047_b200 as L
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C3"
 lf = S.make_lightfield(cfg)
-s = L.Solver(L.params_for(S.CONFIGS[cfg], S.SolverDefaults()))
+s = L.Solver(L.params_for(S.CONFIGS[cfg], S.defaults_for(cfg)))
 s.set_observations(lf.y, lf.view_offsets, lf.omega)
 t = s.tile_config
 print("LFSR_TILE_BL=%d LFSR_TILE_GNW=%d,%d" % (t["tile_rows"], t["view_groups"], t["warps_per_cta"]))
