@@ -24,14 +24,8 @@
 #ifndef LFSR_MINB4
 #define LFSR_MINB4 2
 #endif
-#ifndef LFSR_VPK
-#define LFSR_VPK 28           // bit zeta set: the vertical blur taps run as packed FP32 pairs
-#endif
 #ifndef LFSR_DUMMY_MASK
 #define LFSR_DUMMY_MASK 12    // bit zeta set: zero-row routing for edge tiles (TC::DUMMY)
-#endif
-#ifndef LFSR_INTROWS
-#define LFSR_INTROWS 1        // 1: the fast tile path also requires every E row inside the image (0: measured slower)
 #endif
 
 namespace lfsr {

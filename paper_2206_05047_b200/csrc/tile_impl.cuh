@@ -16,9 +16,12 @@
 //   W_k^T  exact bilinear scatter into a shared int32 fixed-point accumulator
 //          (native ATOMS.ADD, order-independent -> deterministic per CTA)  A12
 // No barrier inside the view loop.  Then the weighted NLTV term in gather form
-// for the own pixels (the CTA's view group takes every G-th offset),
-// and one RED.ADD flush of accumulator + NLTV term (tile + halo) to global so
-// neighbouring tiles and view groups sum.
+// for the own pixels (view group g takes every G-th own row, warps
+// pull rows from a shared counter), and one RED.ADD flush of accumulator + NLTV
+// term (tile + halo) to global so neighbouring tiles and view groups sum.
+// Arithmetic is packed FP32 (FFMA2/FADD2/FMUL2) over a lane's column pairs; the
+// tiling (BL, view groups, warps) is chosen per problem by tile_kernels.cu /
+// capi.cu.
 //
 // Fixed-point scale: every CTA bounds |t| (the blurred adjoint value of one
 // source) by tb (c_A max|p| for NORMAL; l2 (max|x| + max|y|) + (th/2) l1 3/th for
@@ -132,7 +135,7 @@ struct Tile : YRoute<!INT && TC<Z>::DUMMY, Z / 2> {
 
   // row er of the E region lies inside the image (warp uniform)
   __device__ __forceinline__ bool row_in(int er) const {
-    return (LFSR_INTROWS && INT) || rows_in || (unsigned)(YE0 + er) < (unsigned)H;
+    return INT || rows_in || (unsigned)(YE0 + er) < (unsigned)H;
   }
 
   // floor and fraction without the XU pipe: s + 1.5*2^23 rounded toward -inf is
@@ -468,11 +471,6 @@ __device__ __forceinline__ void view_pass(const Tile<Z, INT>& t, const Geom& G, 
 #pragma unroll
       for (int v = 0; v < NV; ++v) fr[v][u] = t.fwd_row(u, lane, drho[v], dtau[v], G);
   }
-#if defined(LFSR_LI_UNROLL) && LFSR_LI_UNROLL == 2
-#pragma unroll 2
-#elif defined(LFSR_LI_UNROLL) && LFSR_LI_UNROLL == 1
-#pragma unroll 1
-#endif
   for (int li = 0; li < BL; ++li) {
     const int i = i0 + li;
     const bool ok = col_ok && i < G.h;
@@ -489,17 +487,11 @@ __device__ __forceinline__ void view_pass(const Tile<Z, INT>& t, const Geom& G, 
       if (kFwd) {
 #pragma unroll
         for (int u = 0; u < Z; ++u) fr[v][KEEP + u] = t.fwd_row(Z * li + KEEP + u, lane, drho[v], dtau[v], G);
-        float a = 0.f;                                                   // A_k x at LR pixel (i, j)
-        if constexpr ((LFSR_VPK >> Z) & 1) {
-          float2 a2 = f2s(0.f);
+        float2 a2 = f2s(0.f);                                            // A_k x at LR pixel (i, j)
 #pragma unroll
-          for (int u = 0; u + 1 < NTAP; u += 2) a2 = __ffma2_rn(tap2(G, u), f2(fr[v][u], fr[v][u + 1]), a2);
-          a = a2.x + a2.y;
-          if constexpr (NTAP & 1) a = fmaf(G.taps[NTAP - 1], fr[v][NTAP - 1], a);
-        } else {
-#pragma unroll
-          for (int u = 0; u < NTAP; ++u) a = fmaf(G.taps[u], fr[v][u], a);
-        }
+        for (int u = 0; u + 1 < NTAP; u += 2) a2 = __ffma2_rn(tap2(G, u), f2(fr[v][u], fr[v][u + 1]), a2);
+        float a = a2.x + a2.y;
+        if constexpr (NTAP & 1) a = fmaf(G.taps[NTAP - 1], fr[v][NTAP - 1], a);
         if (ok) {
           if (MODE == MODE_A) {
             io.out_lr[lg] = a;
@@ -528,18 +520,13 @@ __device__ __forceinline__ void view_pass(const Tile<Z, INT>& t, const Geom& G, 
     if (kAdj) {
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
-        if constexpr ((LFSR_VPK >> Z) & 1) {                                             // vertical adjoint
 #pragma unroll
-          for (int u = 0; u + 1 < NTAP; u += 2) {
-            const float2 b2 = __ffma2_rn(tap2(G, u), f2s(rho[v]), f2(br[v][u], br[v][u + 1]));
-            br[v][u] = b2.x;
-            br[v][u + 1] = b2.y;
-          }
-          if constexpr (NTAP & 1) br[v][NTAP - 1] = fmaf(G.taps[NTAP - 1], rho[v], br[v][NTAP - 1]);
-        } else {
-#pragma unroll
-          for (int u = 0; u < NTAP; ++u) br[v][u] = fmaf(G.taps[u], rho[v], br[v][u]);
+        for (int u = 0; u + 1 < NTAP; u += 2) {                                          // vertical adjoint
+          const float2 b2 = __ffma2_rn(tap2(G, u), f2s(rho[v]), f2(br[v][u], br[v][u + 1]));
+          br[v][u] = b2.x;
+          br[v][u + 1] = b2.y;
         }
+        if constexpr (NTAP & 1) br[v][NTAP - 1] = fmaf(G.taps[NTAP - 1], rho[v], br[v][NTAP - 1]);
 #pragma unroll
         for (int u = 0; u < Z; ++u) t.adj_row(Z * li + u, lane, br[v][u], drho[v], dtau[v], G);
 #pragma unroll
@@ -776,7 +763,7 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
       tile.koff = koff; tile.rows_in = rows_in;
       views<Z, MODE, decltype(tile)::kInt>(tile, G, V, T, io, grp, lane, warp, NW, i0, j0, BL, red_a, red_b, red_c);
     };
-    if (cols_in && (rows_in || !LFSR_INTROWS)) run(Tile<Z, true>{});
+    if (cols_in && rows_in) run(Tile<Z, true>{});   // (columns-only interior: measured slower)
     else run(Tile<Z, false>{});
   }
   if (MODE == MODE_A) return;
