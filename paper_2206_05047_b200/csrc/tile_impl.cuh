@@ -278,9 +278,10 @@ struct Tile : YRoute<!INT && TC<Z>::DUMMY, Z / 2> {
 
   // Horizontal adjoint blur of the row's LR-column values t1b and the exact bilinear
   // scatter (W_k^T) of the lane's zeta positions into the fixed-point accumulator.
-  // A position's four weights go out as two (row, row + 1) pairs; when every lane's
-  // positions hit adjacent source columns (smooth disparity) the shared columns are
-  // merged first: zeta + 1 pairs instead of 2 zeta.
+  // A position's four weights go out as two (row, row + 1) pairs; adjacent positions
+  // whose source columns coincide (smooth disparity) are merged first: zeta + 1 pairs
+  // instead of 2 zeta (per lane and boundary; the all-or-nothing warp test it replaces
+  // cost 4 % at C4/C5).
   __device__ __forceinline__ void adj_row(int er, int lane, float t1b, float drho, float dtau,
                                           const Geom& G) const {
     constexpr int NJ = 2 * TC<Z>::R / Z + 1;
@@ -336,21 +337,17 @@ struct Tile : YRoute<!INT && TC<Z>::DUMMY, Z / 2> {
       w1[s] = __fmul2_rn(q, f2s(b));
       w0[s] = sub2(q, w1[s]);
     }
-    bool adj = true;
+    // per lane and per column boundary: merge when the two positions share the column
+    // (i00[s] == i01[s-1]); the lanes that do not, add the left position's right column
+    // separately (a warp-uniform skip when no lane needs it)
+    acc_add2(ACC, lo, i00[0], i00[0] + PW, w0[0]);
 #pragma unroll
-    for (int s = 1; s < Z; ++s) adj = adj && (i00[s] == i01[s - 1]);
-    if (__all_sync(0xffffffffu, adj)) {
-      acc_add2(ACC, lo, i00[0], i00[0] + PW, w0[0]);
-#pragma unroll
-      for (int s = 1; s < Z; ++s) acc_add2(ACC, lo, i00[s], i00[s] + PW, __fadd2_rn(w0[s], w1[s - 1]));
-      acc_add2(ACC, lo, i01[Z - 1], i01[Z - 1] + PW, w1[Z - 1]);
-    } else {
-#pragma unroll
-      for (int s = 0; s < Z; ++s) {
-        acc_add2(ACC, lo, i00[s], i00[s] + PW, w0[s]);
-        acc_add2(ACC, lo, i01[s], i01[s] + PW, w1[s]);
-      }
+    for (int s = 1; s < Z; ++s) {
+      const bool adj = i00[s] == i01[s - 1];
+      acc_add2(ACC, lo, i00[s], i00[s] + PW, adj ? __fadd2_rn(w0[s], w1[s - 1]) : w0[s]);
+      if (__any_sync(0xffffffffu, !adj) && !adj) acc_add2(ACC, lo, i01[s - 1], i01[s - 1] + PW, w1[s - 1]);
     }
+    acc_add2(ACC, lo, i01[Z - 1], i01[Z - 1] + PW, w1[Z - 1]);
   }
 };
 
