@@ -6,6 +6,7 @@
 #include "nccl_shim.h"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -657,6 +658,7 @@ lfsr_status lfsr_set_observations(lfsr_ctx* c, const float* lr_views, const floa
   if ((st = check_ptr(c, disparity, mem, "disparity")) != LFSR_OK) return st;
   if (x0 && (st = check_ptr(c, x0, mem, "x0")) != LFSR_OK) return st;
   CK(c, cudaSetDevice(c->prm.device));
+  const auto ts0 = std::chrono::steady_clock::now();
 
   // view offsets to the host (needed for halo sizing) and validation
   const int nv = c->prm.n_views;
@@ -684,7 +686,7 @@ lfsr_status lfsr_set_observations(lfsr_ctx* c, const float* lr_views, const floa
     cudaError_t e;
     if ((e = dalloc(c, &p, hr * 4)) != cudaSuccess) return cuda_fail(c, e, "alloc");
     c->tmp_hr2 = (float*)p;
-    if ((e = dalloc(c, &p, sizeof(unsigned))) != cudaSuccess) return cuda_fail(c, e, "alloc");
+    if ((e = dalloc(c, &p, 3 * sizeof(unsigned))) != cudaSuccess) return cuda_fail(c, e, "alloc");
     c->umax = (unsigned*)p;
     if (nparts > 1) {
       if ((e = dalloc(c, &p, sizeof(Control*) * nparts)) != cudaSuccess) return cuda_fail(c, e, "alloc");
@@ -719,35 +721,30 @@ lfsr_status lfsr_set_observations(lfsr_ctx* c, const float* lr_views, const floa
   }
   State& S0 = c->parts[0].S;
 
-  // halo sizes: S = ceil(max_k |dtheta_k| * max |omega|) per axis, in fp32 like the kernels
-  CK(c, cudaMemsetAsync(umax, 0, 4, c->stream));
+  // three maxima with one round trip: max|omega| (halo sizes S = ceil(max_k |dtheta_k|
+  // max|omega|) per axis, in fp32 like the kernels), and the fixed-point bounds max|y| and
+  // the splat density max_z sum_k (W_k^T 1)(z)
+  for (int k = 0; k < nv; ++k) c->V.off[k] = make_float2(off[2 * k], off[2 * k + 1]);
+  CK(c, cudaMemsetAsync(umax, 0, 3 * sizeof(unsigned), c->stream));
   CK(c, launch_absmax(S0.omega, hr, umax, c->stream));
-  unsigned ubits = 0;
-  CK(c, cudaMemcpyAsync(&ubits, umax, 4, cudaMemcpyDeviceToHost, c->stream));
+  CK(c, launch_density(G, c->V, S0.omega, S0.density, c->stream));
+  CK(c, launch_absmax(S0.density, hr, umax + 1, c->stream));
+  CK(c, launch_absmax(S0.y, lr, umax + 2, c->stream));
+  unsigned ubits[3] = {0, 0, 0};
+  CK(c, cudaMemcpyAsync(ubits, umax, sizeof ubits, cudaMemcpyDeviceToHost, c->stream));
   CK(c, cudaStreamSynchronize(c->stream));
   float om_max;
-  memcpy(&om_max, &ubits, 4);
+  memcpy(&om_max, &ubits[0], 4);
   if (!std::isfinite(om_max)) FAIL(c, LFSR_ERR_INVALID_ARG, "disparity must be finite");
   float mx_rho = 0.f, mx_tau = 0.f;
   for (int k = 0; k < nv; ++k) {
-    c->V.off[k] = make_float2(off[2 * k], off[2 * k + 1]);
     mx_rho = std::fmax(mx_rho, std::fabs(off[2 * k]));
     mx_tau = std::fmax(mx_tau, std::fabs(off[2 * k + 1]));
   }
   G.SX = std::min((int)std::ceil(mx_rho * om_max), G.W);
   G.SY = std::min((int)std::ceil(mx_tau * om_max), G.H);
-  // fixed-point bounds: max |y| and the splat density max_z sum_k (W_k^T 1)(z)
-  CK(c, launch_density(G, c->V, S0.omega, S0.density, c->stream));
-  CK(c, cudaMemsetAsync(umax, 0, 4, c->stream));
-  CK(c, launch_absmax(S0.density, hr, umax, c->stream));
-  CK(c, cudaMemcpyAsync(&ubits, umax, 4, cudaMemcpyDeviceToHost, c->stream));
-  CK(c, cudaStreamSynchronize(c->stream));
-  memcpy(&G.dmax, &ubits, 4);
-  CK(c, cudaMemsetAsync(umax, 0, 4, c->stream));
-  CK(c, launch_absmax(S0.y, lr, umax, c->stream));
-  CK(c, cudaMemcpyAsync(&ubits, umax, 4, cudaMemcpyDeviceToHost, c->stream));
-  CK(c, cudaStreamSynchronize(c->stream));
-  memcpy(&G.ymax, &ubits, 4);
+  memcpy(&G.dmax, &ubits[1], 4);
+  memcpy(&G.ymax, &ubits[2], 4);
   if (!std::isfinite(G.ymax)) G.ymax = 0.f;  // non-finite observations surface as DIVERGED
 
   // tile height and the strip plan / tile geometry of every part
@@ -767,9 +764,15 @@ lfsr_status lfsr_set_observations(lfsr_ctx* c, const float* lr_views, const floa
     CK(c, launch_weights(G, S.x, S.wo, S.m, c->stream));
   }
   if (tune && (st = tune_tile_bl(c)) != LFSR_OK) return st;
+  const auto tg0 = std::chrono::steady_clock::now();
   lfsr_status gs = build_graphs(c);
   if (gs != LFSR_OK) return gs;
+  const auto tg1 = std::chrono::steady_clock::now();
   CK(c, cudaStreamSynchronize(c->stream));
+  if (getenv("LFSR_TRACE_SETUP"))
+    fprintf(stderr, "lfsr set_observations: graph build %.3f ms, total %.3f ms\n",
+            std::chrono::duration<double, std::milli>(tg1 - tg0).count(),
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ts0).count());
   c->ready = true;
   return LFSR_OK;
 }
