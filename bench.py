@@ -88,7 +88,7 @@ def peaks():
         except Exception:
             pass
     fp32 = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
-    return hbm, fp32, src
+    return hbm, fp32, src, sm_mhz * 1e6
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -202,9 +202,17 @@ def main():
     import torch.distributed as dist
     import paper_2206_05047_b200 as L
 
+    # development only: LFSR_BENCH_SHARE_GPU=1 runs all ranks on the visible GPUs round-robin with a
+    # gloo group (exercises the multi-rank replica path on a 1-GPU box); the product launch is nccl
+    share = os.environ.get("LFSR_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     def barrier():
         if world > 1:
@@ -313,7 +321,7 @@ def main():
 
     # ---- roofline of the dominant kernel (the CG normal-operator tile kernel)
     alg = algorithmic(cfg, d)
-    hbm_peak, fp32_peak, peak_src = peaks()
+    hbm_peak, fp32_peak, peak_src, clk_hz = peaks()
     if kn[1] == 0:   # strips: per-kernel events are not recorded; use the step time split evenly
         kms, kn = [t_ms * 0.2, t_ms * 0.75, t_ms * 0.05], [args.steps, args.steps * d.cg_max_iters,
                                                           args.steps * d.cg_max_iters]
@@ -321,13 +329,15 @@ def main():
     k_wz_ms = kms[0] / max(kn[0], 1)
     k_upd_ms = kms[2] / max(kn[2], 1)
     achieved = alg["normal_flops"] / (k_normal_ms / 1000.0) / 1e12
-    traffic = None
+    traffic, winst = None, None
     tr_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tr_path):
         try:
-            traffic = json.load(open(tr_path)).get(cfg.name, {}).get("k_tile_normal_dram_bytes")
+            rec = json.load(open(tr_path)).get(cfg.name, {})
+            traffic = rec.get("k_tile_normal_dram_bytes")
+            winst = rec.get("k_tile_normal_warp_instr")
         except Exception:
-            traffic = None
+            traffic, winst = None, None
     roofline = {"bound": "alu", "kernel": "k_tile<NORMAL> (CG normal operator q = M p, a8)",
                 "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s", "frac": achieved / fp32_peak,
                 "traffic": traffic, "peak_source": "FP32 CUDA cores, 148 SM x 128 lanes x 2 x sm_max_mhz (%s)" % peak_src,
@@ -344,6 +354,13 @@ def main():
                 "iteration_hbm_gbs": alg["iter_bytes"] * total_iters / (t_max / 1000.0) / 1e9 / world,
                 "iteration_hbm_frac": alg["iter_bytes"] * total_iters / (t_max / 1000.0) / 1e9 / world / hbm_peak,
                 "hbm_peak_gbs": hbm_peak}
+    if winst:   # the binding ceiling: instruction issue (1 warp instruction / scheduler / clock)
+        issue_peak = 148 * 4 * clk_hz / 1e12
+        roofline["issue"] = {"achieved": winst / (k_normal_ms / 1000.0) / 1e12, "peak": issue_peak,
+                             "unit": "T warp-instr/s", "frac": winst / (k_normal_ms / 1000.0) / 1e12 / issue_peak,
+                             "warp_instr_per_launch": winst,
+                             "source": "ncu smsp__inst_executed.sum per launch (profiles/ncu_traffic.json) / live "
+                                       "launch time; peak = 148 SM x 4 schedulers x sm_max_mhz"}
 
     # ---- CPU baseline: the oracle as it stands, on a bounded sample, rank 0 at N = 1 only
     cpu = None
