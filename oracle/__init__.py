@@ -57,6 +57,13 @@ class _Stats(ctypes.Structure):
                 ("cg_pi0", ctypes.c_double), ("cg_pi_last", ctypes.c_double)]
 
 
+class _GdStats(ctypes.Structure):
+    _fields_ = [("iter", ctypes.c_int32), ("ls_evals", ctypes.c_int32),
+                ("ls_failed", ctypes.c_int32), ("nonfinite", ctypes.c_int32),
+                ("J", ctypes.c_double), ("data_l1", ctypes.c_double), ("data_l2", ctypes.c_double),
+                ("reg_l1", ctypes.c_double), ("step", ctypes.c_double), ("grad_sq", ctypes.c_double)]
+
+
 _lib = None
 
 
@@ -87,6 +94,9 @@ def lib():
             "or_normal": (None, [P, D, D, D, D, D]),
             "or_admm": (I, [P, D, D, D, D, I, D, D, D, D, ctypes.POINTER(_Stats)]),
             "or_cost": (ctypes.c_double, [P, D, D, D, D, D, D]),
+            "or_gradient": (ctypes.c_double, [P, D, D, D, D, D, D, D]),
+            "or_gd": (I, [P, D, D, D, D, I, ctypes.c_double, I, I, ctypes.c_double, D, D,
+                          ctypes.POINTER(_GdStats)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(_lib, name)
@@ -321,6 +331,44 @@ def admm(P: Params, y, view_offsets, omega, n_iters: int, x0=None) -> AdmmResult
         raise ValueError("oracle: invalid parameters")
     stats = [{k: getattr(st[i], k) for k in STAT_KEYS} for i in range(n_iters)]
     return AdmmResult(xs, wA, wS, stats, rc)
+
+
+def gradient(P: Params, y, view_offsets, omega, m, x):
+    """J(x) and its subgradient sum_k A_k^T (l1 sgn(e_k) + 2 l2 e_k) + S_w^T sgn(S_w x) for the
+    weight map m (reading A30).  Returns (J, terms3, g)."""
+    y, vo, om, m, x = _d(y), _d(view_offsets), _d(omega), _d(m), _d(x)
+    g = np.zeros((P.H, P.W))
+    t = np.zeros(3)
+    pc = P.c()
+    J = lib().or_gradient(ctypes.byref(pc), _ptr(y), _ptr(vo), _ptr(om), _ptr(m), _ptr(x), _ptr(g), _ptr(t))
+    return J, t, g
+
+
+GD_STAT_KEYS = ("iter", "ls_evals", "ls_failed", "nonfinite", "J", "data_l1", "data_l2", "reg_l1",
+                "step", "grad_sq")
+
+
+@dataclass
+class GdResult:
+    x_iters: np.ndarray          # [N+1][H][W], x^0 .. x^N
+    stats: list = field(default_factory=list)
+    status: int = 0
+
+
+def gd(P: Params, y, view_offsets, omega, n_iters: int, step: float, line_search: bool = False,
+       max_halvings: int = 30, armijo_c: float = 1e-4, x0=None) -> GdResult:
+    """gd / gd-ls baselines of the solver comparison (readings A30-A33); see
+    oracle.c or_gd.  CU of iteration n: 2 + stats[n]["ls_evals"] (A33)."""
+    y, vo, om, x0 = _d(y), _d(view_offsets), _d(omega), _d(x0)
+    xs = np.zeros((n_iters + 1, P.H, P.W))
+    st = (_GdStats * max(n_iters, 1))()
+    pc = P.c()
+    rc = lib().or_gd(ctypes.byref(pc), _ptr(y), _ptr(vo), _ptr(om), _ptr(x0), int(n_iters), float(step),
+                     int(bool(line_search)), int(max_halvings), float(armijo_c), _ptr(xs), None, st)
+    if rc == 1:
+        raise ValueError("oracle: invalid parameters")
+    stats = [{k: getattr(st[i], k) for k in GD_STAT_KEYS} for i in range(n_iters)]
+    return GdResult(xs, stats, rc)
 
 
 def psnr(x, gt, crop: int = 8) -> float:

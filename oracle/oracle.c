@@ -33,6 +33,10 @@
  *   or_normal         pinned: equals dense c_A A^T A + (th/2) S_W^T S_W, SPD
  *   or_admm           pinned: l2-only == lstsq (P10), == textbook scaled ADMM with exact
  *                     x-step (P11), convergence to an independent minimiser (P12)
+ *   or_gradient       pinned: central finite differences of J (P18), J == or_cost
+ *   or_gd             pinned: smooth case with step 1/L decreases J monotonically and reaches the
+ *                     lstsq solution (P19); Armijo acceptance checked against or_cost and
+ *                     maximality of the step (P20); ADMM below gd at equal CU (P21)
  */
 #include <math.h>
 #include <stdlib.h>
@@ -589,4 +593,132 @@ double or_cost(const or_params* P, const double* y, const double* view_offsets,
   free(g);
   if (terms3) { terms3[0] = l1; terms3[1] = l2; terms3[2] = reg; }
   return P->lambda1 * l1 + P->lambda2 * l2 + reg;
+}
+
+/* ---------------------------------------------------------------------------
+ * Gradient-descent baselines of the paper's solver comparison (P:L910-933:
+ * "gradient descent solver (GD) without and with line search denoted as gd
+ * and gd-ls"), with the readings A30-A33 of DESIGN.md §3:
+ *   A30  the subgradient of |.| is sgn, with sgn(0) = 0;
+ *   A31  the weight map m is re-estimated from x^{n-1} at the start of every
+ *        iteration (as for ADMM, A16) and frozen through that
+ *        iteration's line search;
+ *   A32  line search = Armijo backtracking (c = 1e-4, halving):
+ *        eta_t = eta0 * 2^-t for t = 0..L-1, the first t with
+ *        J(x - eta_t g) <= J(x) - c * eta_t * |g|^2 is taken; if none is,
+ *        no step is taken (x unchanged) and ls_failed = 1;
+ *   A33  CU accounting: the cost J (A and S) is one CU, the
+ *        gradient (A^T and S^T) one CU, every line-search trial one CU;
+ *        an ADMM iteration counts 2(K+1).
+ * ------------------------------------------------------------------------- */
+static double sgn(double v) { return v > 0.0 ? 1.0 : (v < 0.0 ? -1.0 : 0.0); }
+
+/* Cost terms and subgradient of J (Eq. sr_fin) at x for a given
+ * weight map m (W_d = w_d m):
+ *   e_k = A_k x - y_k ,  G = S_w x  (G_d(z) = W_d(z) (x(z) - x(z+d)))
+ *   terms3 = (sum|e|, sum e^2, sum|G|)
+ *   g = sum_k A_k^T (l1 sgn(e_k) + 2 l2 e_k) + S_w^T sgn(G)           (A30)
+ * Returns J = l1 terms3[0] + l2 terms3[1] + terms3[2].  g may be NULL. */
+double or_gradient(const or_params* P, const double* y, const double* view_offsets,
+                   const double* omega, const double* m, const double* x, double* g,
+                   double* terms3) {
+  int z = P->scale, H = P->lr_h * z, W = P->lr_w * z;
+  size_t p = (size_t)H * W, nq = (size_t)P->lr_h * P->lr_w * P->n_views;
+  int dys[1024], dxs[1024];
+  int sd = or_offsets(P->radius, dys, dxs);
+  size_t ns = p * sd;
+  double wds[1024];
+  offset_weights(P->radius, P->sigma_s, P->offset_weights, wds);
+  double* e = (double*)malloc(sizeof(double) * nq);
+  double* G = (double*)malloc(sizeof(double) * ns);
+  or_apply_A(P, view_offsets, omega, x, e);
+  double l1 = 0.0, l2 = 0.0, reg = 0.0;
+  for (size_t i = 0; i < nq; ++i) {
+    e[i] -= y[i];
+    l1 += fabs(e[i]);
+    l2 += e[i] * e[i];
+  }
+  or_apply_Sw(H, W, P->radius, wds, m, x, G);
+  for (size_t i = 0; i < ns; ++i) reg += fabs(G[i]);
+  if (g) {
+    double* t = (double*)malloc(sizeof(double) * p);
+    for (size_t i = 0; i < nq; ++i) e[i] = P->lambda1 * sgn(e[i]) + 2.0 * P->lambda2 * e[i];
+    for (size_t i = 0; i < ns; ++i) G[i] = sgn(G[i]);
+    or_apply_AT(P, view_offsets, omega, e, g);
+    or_apply_STw(H, W, P->radius, wds, m, G, t);
+    for (size_t i = 0; i < p; ++i) g[i] += t[i];
+    free(t);
+  }
+  free(e);
+  free(G);
+  if (terms3) { terms3[0] = l1; terms3[1] = l2; terms3[2] = reg; }
+  return P->lambda1 * l1 + P->lambda2 * l2 + reg;
+}
+
+typedef struct {
+  int32_t iter, ls_evals, ls_failed, nonfinite;
+  double J, data_l1, data_l2, reg_l1, step, grad_sq;
+} or_gd_stats;
+
+/* gd / gd-ls (A30-A33).  Per iteration n, from x = x^{n-1}:
+ *   m = weights(x) (A31) ; J0, g = or_gradient(x, m) ; gsq = <g, g>
+ *   fixed step:  x := x - eta0 g
+ *   line search: for t = 0..L-1: eta = eta0 2^-t ; if J(x - eta g; m) <= J0 - c eta gsq:
+ *                x := x - eta g, stop  (A32)
+ * stats[n-1] = (n, trials evaluated, failed, nonfinite, J0 and its terms, eta taken, gsq).
+ * x_iters [(N+1)][H][W] (may be NULL), x_out [H][W] (may be NULL); x0 NULL => bicubic. */
+int or_gd(const or_params* P, const double* y, const double* view_offsets, const double* omega,
+          const double* x0, int N, double step0, int line_search, int max_halvings, double armijo_c,
+          double* x_iters, double* x_out, or_gd_stats* stats) {
+  if (validate(P) != OR_OK || N < 0 || !(step0 > 0) || max_halvings < 1 || armijo_c < 0) return OR_ERR_ARG;
+  int z = P->scale, h = P->lr_h, w = P->lr_w, H = h * z, W = w * z;
+  size_t p = (size_t)H * W, q = (size_t)h * w;
+  double* x = (double*)malloc(sizeof(double) * p);
+  double* xt = (double*)malloc(sizeof(double) * p);
+  double* g = (double*)malloc(sizeof(double) * p);
+  double* wo = (double*)malloc(sizeof(double) * p);
+  double* m = (double*)malloc(sizeof(double) * p);
+  if (x0) memcpy(x, x0, sizeof(double) * p);
+  else or_bicubic(h, w, z, y + (size_t)P->ref_view * q, x);
+  or_setup_wo(P, y, view_offsets, omega, wo, NULL, NULL);
+  or_weights_m(H, W, P->lambda_reg, P->sigma_e, wo, x, m);
+  if (x_iters) memcpy(x_iters, x, sizeof(double) * p);
+  int status = OR_OK;
+  for (int n = 1; n <= N; ++n) {
+    or_gd_stats st;
+    memset(&st, 0, sizeof(st));
+    st.iter = n;
+    if (P->reweight_every_iter) or_weights_m(H, W, P->lambda_reg, P->sigma_e, wo, x, m);
+    double t3[3];
+    double J0 = or_gradient(P, y, view_offsets, omega, m, x, g, t3);
+    double gsq = dot(p, g, g, H);
+    st.J = J0;
+    st.data_l1 = t3[0];
+    st.data_l2 = t3[1];
+    st.reg_l1 = t3[2];
+    st.grad_sq = gsq;
+    double eta = step0;
+    if (line_search) {
+      int ok = 0;
+      for (int t = 0; t < max_halvings; ++t) {
+        double et = ldexp(step0, -t);
+        for (size_t i = 0; i < p; ++i) xt[i] = x[i] - et * g[i];
+        double Jt = or_gradient(P, y, view_offsets, omega, m, xt, NULL, NULL);
+        st.ls_evals = t + 1;
+        if (Jt <= J0 - armijo_c * et * gsq) { eta = et; ok = 1; break; }
+      }
+      if (!ok) { eta = 0.0; st.ls_failed = 1; }
+    }
+    st.step = eta;
+    for (size_t i = 0; i < p; ++i) x[i] -= eta * g[i];
+    int bad = !isfinite(J0);
+    for (size_t i = 0; i < p && !bad; ++i) bad = !isfinite(x[i]);
+    st.nonfinite = bad;
+    if (stats) stats[n - 1] = st;
+    if (x_iters) memcpy(x_iters + (size_t)n * p, x, sizeof(double) * p);
+    if (bad) { status = OR_ERR_DIVERGED; break; }
+  }
+  if (x_out) memcpy(x_out, x, sizeof(double) * p);
+  free(x); free(xt); free(g); free(wo); free(m);
+  return status;
 }
