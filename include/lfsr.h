@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define LFSR_ABI_VERSION 2
+#define LFSR_ABI_VERSION 3
 
 #if defined(__GNUC__)
 #define LFSR_API __attribute__((visibility("default")))
@@ -142,8 +142,8 @@ LFSR_API lfsr_status lfsr_set_observations(lfsr_ctx* ctx, const float* lr_views,
 /* Run n_iters >= 0 ADMM iterations (Alg.1 lines 3-10) continuing from the
  * current (x, w_A, w_S): run(a); run(b) == run(a+b).  Each iteration is one
  * CUDA-graph launch on the ctx stream.  Blocks until done.  stats: NULL or an
- * array of n_iters records.  Errors: STATE (before set_observations),
- * DIVERGED (non-finite x/J; the state is kept for inspection), CUDA. */
+ * array of n_iters records.  Errors: STATE (before set_observations, or after
+ * lfsr_gd_run iterations since it), DIVERGED (non-finite x/J; the state is kept for inspection), CUDA. */
 LFSR_API lfsr_status lfsr_admm_run(lfsr_ctx* ctx, int32_t n_iters, lfsr_iter_stats* stats);
 
 /* Enqueue n_iters >= 0 ADMM iterations (graph launches) on the ctx stream and
@@ -183,16 +183,62 @@ LFSR_API lfsr_status lfsr_get_state(lfsr_ctx* ctx, float* w_A, float* w_S, float
  *   ST      : in [s_d][H][W]          -> out HR                div^{U,V}
  *   NORMAL  : in HR                   -> out HR                M x (A7)
  *   WEIGHTS : in HR x                 -> out HR m(x) = lambda_reg w_o w_e(x)
- * NORMAL/A/AT run the same tile kernels as lfsr_admm_run.  Blocks for HOST. */
+ * NORMAL/A/AT run the same tile kernels as lfsr_admm_run, GRAD the one of lfsr_gd_run.
+ * Blocks for HOST. */
 typedef enum {
   LFSR_OP_A = 0,
   LFSR_OP_AT = 1,
   LFSR_OP_S = 2,
   LFSR_OP_ST = 3,
   LFSR_OP_NORMAL = 4,
-  LFSR_OP_WEIGHTS = 5
+  LFSR_OP_WEIGHTS = 5,
+  LFSR_OP_GRAD = 6     /* in HR x -> out HR subgradient of J at x with the current m:
+                          sum_k A_k^T (l1 sgn(e_k) + 2 l2 e_k) + S_w^T sgn(S_w x) (A30) */
 } lfsr_op;
 LFSR_API lfsr_status lfsr_op_apply(lfsr_ctx* ctx, lfsr_op op, const float* in, float* out, lfsr_mem mem);
+
+/* Gradient-descent baselines of the paper's solver comparison (P:L910-933:
+ * "gradient descent solver (GD) without and with line search denoted as gd and
+ * gd-ls"; readings A30-A33 of DESIGN.md §3).  Per iteration,
+ * from x = x^{n-1}: m = weights(x) (if reweight_every_iter; A31), cost J(x) and
+ * its subgradient g = sum_k A_k^T (l1 sgn(e_k) + 2 l2 e_k) + S_w^T sgn(S_w x)
+ * (A30), then
+ *   gd    : x := x - step g
+ *   gd-ls : Armijo backtracking (A32): the first t < max_trials with
+ *           J(x - step 2^-t g) <= J(x) - armijo_c step 2^-t |g|^2 is taken; none
+ *           => x unchanged and ls_failed = 1.
+ * The same fused tile kernel as the ADMM path computes e, the adjoint and the
+ * NLTV term; every step runs on the device (one CUDA graph per iteration, no
+ * host round trip inside it). */
+typedef struct {
+  float step;           /* > 0: the fixed step (gd) or the first trial (gd-ls)        */
+  int32_t line_search;  /* 0: gd, 1: gd-ls                                            */
+  int32_t max_trials;   /* gd-ls: L in [1, 32] trials step * 2^-t, t < L              */
+  float armijo_c;       /* >= 0, Armijo constant (1e-4)                        */
+} lfsr_gd_params;
+
+/* Per-gd-iteration record.  J terms at x^{n-1} with m(x^{n-1}) (as lfsr_iter_stats). */
+typedef struct {
+  int32_t iter;         /* 1-based, counted since set_observations                    */
+  int32_t ls_evals;     /* line-search trials evaluated (0 for gd)                     */
+  int32_t ls_failed;    /* 1: no trial met the Armijo condition (x unchanged)          */
+  int32_t nonfinite;    /* 1: x or J became non-finite                                 */
+  int32_t cu;           /* computation units of this iteration: 2 + ls_evals (A33)     */
+  int32_t pad;
+  double J, data_l1, data_l2, reg_l1;
+  double step;          /* step taken (0 if ls_failed)                                 */
+  double grad_sq;       /* |g|^2                                                       */
+} lfsr_gd_stats;
+
+/* Run n_iters >= 0 gd / gd-ls iterations continuing from the current x (run(a);
+ * run(b) == run(a+b)); blocks until done.  One solver per set_observations: after
+ * ADMM iterations this returns STATE (and lfsr_admm_run after gd iterations).
+ * stats: NULL or n_iters records.  Errors: INVALID_ARG (params), STATE,
+ * UNSUPPORTED (strip decompositions, n_ranks > 1), DIVERGED, OOM, CUDA. */
+LFSR_API lfsr_status lfsr_gd_run(lfsr_ctx* ctx, const lfsr_gd_params* gd, int32_t n_iters, lfsr_gd_stats* stats);
+
+/* Kernel launches of one gd iteration graph (valid after lfsr_gd_run; 0 before). */
+LFSR_API int32_t lfsr_gd_launches_per_iter(const lfsr_ctx* ctx);
 
 /* Number of kernel launches one ADMM iteration issues (for the bench's
  * gpu_launches count).  Valid after set_observations; 0 otherwise. */

@@ -236,6 +236,117 @@ __global__ void __launch_bounds__(256) k_cg_update(const Geom G, float* __restri
 }
 
 // ---------------------------------------------------------------------------
+// gd / gd-ls (the baselines of the paper's solver comparison, P:L910-933;
+// readings A30-A33).  One iteration = k_tile<GRAD> (cost terms of x and the
+// subgradient g, accumulated into a zeroed buffer) [+ k_gd_gnorm and L trial
+// launches of k_tile<J> for the line search] + k_gd_update.
+// ---------------------------------------------------------------------------
+template <int NV>
+__device__ __forceinline__ void block_sum_to(double (&v)[NV], double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i < NV; ++i)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
+  if (lane == 0)
+#pragma unroll
+    for (int i = 0; i < NV; ++i) red[warp * NV + i] = v[i];
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int i = 0; i < NV; ++i) {
+      double a = 0.0;
+      for (int w = 0; w < (int)(blockDim.x / 32); ++w) a += red[w * NV + i];
+      v[i] = a;
+    }
+}
+
+// |g|^2 -> cur[S_GN] (the Armijo right-hand side needs it before the trials)
+__global__ void __launch_bounds__(256) k_gd_gnorm(const Geom G, const float* __restrict__ g, Control* ctl) {
+  __shared__ double red[8];
+  const size_t n4 = (size_t)G.H * G.ps / 4;
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  double v[1] = {0.0};
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
+    const float4 a = g4[i];
+    v[0] += (double)a.x * a.x + (double)a.y * a.y + (double)a.z * a.z + (double)a.w * a.w;
+  }
+  block_sum_to<1>(v, red);
+  if (threadIdx.x == 0 && v[0] != 0.0) atomicAdd(&ctl->cur[S_GN], v[0]);
+}
+
+// Step choice (A32; every block computes the same from the fp64 sums), x -= eta g
+// (fmaf: the rounding the J trial applied to the same x and g), non-finite count,
+// and in the last block the iteration record: T_CGIT = trials evaluated, T_BREAK =
+// ls_failed, T_RES = eta, T_PI0 = |g|^2 (lfsr_gd_stats).
+__global__ void __launch_bounds__(256) k_gd_update(const Geom G, float* __restrict__ x, const float* __restrict__ g,
+                                                   Control* ctl, const GdCfg cfg) {
+  __shared__ double red[8 * 2];
+  __shared__ bool am_last;
+  const double* cur = ctl->cur;
+  const double J0 = (double)G.lambda1 * cur[S_L1] + (double)G.lambda2 * cur[S_L2] + cur[S_REG];
+  float eta = cfg.eta0;
+  int evals = 0, failed = 0;
+  if (cfg.ls) {
+    eta = 0.f;
+    failed = 1;
+    evals = cfg.L;
+    for (int t = 0; t < cfg.L; ++t) {
+      const double et = ldexp((double)cfg.eta0, -t);
+      const double* jt = cur + S_TJ + 3 * t;
+      const double Jt = (double)G.lambda1 * jt[0] + (double)G.lambda2 * jt[1] + jt[2];
+      if (Jt <= J0 - (double)cfg.armijo_c * et * cur[S_GN]) {
+        eta = ldexpf(cfg.eta0, -t);
+        evals = t + 1;
+        failed = 0;
+        break;
+      }
+    }
+  }
+  const float beta = -eta;
+  const size_t n4 = (size_t)G.H * G.ps / 4;
+  float4* x4 = reinterpret_cast<float4*>(x);
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  double v[2] = {0.0, 0.0};   // |g|^2 (fixed step), non-finite count
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
+    const float4 gv = g4[i];
+    float4 xv = x4[i];
+    xv.x = fmaf(beta, gv.x, xv.x); xv.y = fmaf(beta, gv.y, xv.y);
+    xv.z = fmaf(beta, gv.z, xv.z); xv.w = fmaf(beta, gv.w, xv.w);
+    x4[i] = xv;
+    if (!cfg.ls) v[0] += (double)gv.x * gv.x + (double)gv.y * gv.y + (double)gv.z * gv.z + (double)gv.w * gv.w;
+    v[1] += (double)(!isfinite(xv.x)) + (!isfinite(xv.y)) + (!isfinite(xv.z)) + (!isfinite(xv.w));
+  }
+  block_sum_to<2>(v, red);
+  if (threadIdx.x == 0) {
+    if (v[0] != 0.0) atomicAdd(&ctl->cur[S_GN], v[0]);
+    if (v[1] != 0.0) atomicAdd(&ctl->cur[S_NF], v[1]);
+    __threadfence();
+    const unsigned prev = atomicAdd(&ctl->done, 1u);
+    am_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!am_last || threadIdx.x != 0) return;
+  __threadfence();
+  volatile double* vc = ctl->cur;
+  double* rec = ctl->ring + (size_t)(ctl->iter % ctl->cap) * T_COUNT;
+  rec[T_ITER] = (double)(ctl->iter + 1);
+  rec[T_CGIT] = (double)evals;
+  rec[T_BREAK] = (double)failed;
+  rec[T_NF] = (vc[S_NF] > 0.0 || !isfinite(J0)) ? 1.0 : 0.0;
+  rec[T_J] = J0;
+  rec[T_L1] = vc[S_L1];
+  rec[T_L2] = vc[S_L2];
+  rec[T_REG] = vc[S_REG];
+  rec[T_RES] = (double)eta;
+  rec[T_PI0] = vc[S_GN];
+  rec[T_PILAST] = 0.0;
+  for (int s = 0; s < S_COUNT; ++s) vc[s] = 0.0;
+  ctl->iter = ctl->iter + 1;
+  __threadfence();
+  ctl->done = 0u;
+}
+
+// ---------------------------------------------------------------------------
 // Test operators S / S^T (weighted directional gradient / divergence,
 // P:L585-601, reading A10) on dense [s_d][H][ps] stacks.
 // ---------------------------------------------------------------------------
@@ -304,6 +415,19 @@ cudaError_t launch_cg_update(const Geom& G, float* x, float* r, const float* p, 
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   k_cg_update<<<blocks, 256, 0, st>>>(G, x, r, p, q, ctl, k, row0, nrows, close_here);
+  return cudaGetLastError();
+}
+cudaError_t launch_gd_gnorm(const Geom& G, const float* g, Control* ctl, int num_sms, cudaStream_t st) {
+  k_gd_gnorm<<<num_sms * 2, 256, 0, st>>>(G, g, ctl);
+  return cudaGetLastError();
+}
+cudaError_t launch_gd_update(const Geom& G, float* x, const float* g, Control* ctl, const GdCfg& cfg, int num_sms,
+                             cudaStream_t st) {
+  size_t n4 = (size_t)G.H * G.ps / 4;
+  int blocks = (int)((n4 + 255) / 256);
+  if (blocks > num_sms * 4) blocks = num_sms * 4;
+  if (blocks < 1) blocks = 1;
+  k_gd_update<<<blocks, 256, 0, st>>>(G, x, g, ctl, cfg);
   return cudaGetLastError();
 }
 cudaError_t launch_close(const Geom& G, Control* ctl, cudaStream_t st) {

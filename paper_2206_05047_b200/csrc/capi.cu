@@ -38,6 +38,9 @@ cudaError_t launch_apply_S(const Geom& G, const float* x, const float* m, float*
 cudaError_t launch_apply_ST(const Geom& G, const float* h, const float* m, float* out, cudaStream_t st);
 cudaError_t launch_fold_rows(float* dst, float* src, size_t n, int zero_src, cudaStream_t st);
 cudaError_t launch_allreduce_local(Control* const* ctls, int nparts, int slot0, int count, cudaStream_t st);
+cudaError_t launch_gd_gnorm(const Geom& G, const float* g, Control* ctl, int num_sms, cudaStream_t st);
+cudaError_t launch_gd_update(const Geom& G, float* x, const float* g, Control* ctl, const GdCfg& cfg, int num_sms,
+                             cudaStream_t st);
 }  // namespace lfsr
 
 using namespace lfsr;
@@ -84,6 +87,12 @@ struct lfsr_ctx {
   unsigned* umax = nullptr;
   Control* tune_ctl = nullptr;   // scratch control block for the tile-height timing
   int h_iter = 0;                // iterations enqueued since set_observations
+  int solver = 0;                // 0: none yet, 1: ADMM, 2: gd (one solver per set_observations)
+  cudaGraphExec_t gd_graph = nullptr;   // one gd / gd-ls iteration (built for gd_cfg)
+  GdCfg gd_cfg{};
+  int gd_launches = 0;
+  float* gd_g = nullptr;         // gd subgradient buffer [H][ps]
+  Control* op_ctl = nullptr;     // scratch control block of lfsr_op_apply (keeps the solver sums clean)
   size_t alloc_key[6] = {0, 0, 0, 0, 0, 0};
   bool profile = false;          // event-record nodes around every kernel (single strip)
   std::vector<cudaEvent_t> prof_ev;
@@ -364,6 +373,10 @@ static void free_graph(lfsr_ctx* c) {
       cudaGraphExecDestroy(g);
       g = nullptr;
     }
+  if (c->gd_graph) {
+    cudaGraphExecDestroy(c->gd_graph);
+    c->gd_graph = nullptr;
+  }
 }
 
 static void free_state(lfsr_ctx* c) {
@@ -373,6 +386,8 @@ static void free_state(lfsr_ctx* c) {
   c->parts.clear();
   c->tmp_hr2 = nullptr;
   c->tmp_s = nullptr;
+  c->gd_g = nullptr;
+  c->op_ctl = nullptr;
   c->umax = nullptr;
   c->d_ctls = nullptr;
   for (auto& k : c->alloc_key) k = 0;
@@ -710,6 +725,7 @@ lfsr_status lfsr_set_observations(lfsr_ctx* c, const float* lr_views, const floa
     }
   }
   c->h_iter = 0;
+  c->solver = 0;
   unsigned* umax = c->umax;
   for (Part& P : c->parts) {
     Control h{};
@@ -1062,6 +1078,8 @@ lfsr_status lfsr_admm_enqueue(lfsr_ctx* c, int32_t n_iters) {
   lfsr_status st = check_run(c);
   if (st != LFSR_OK) return st;
   if (n_iters < 0) FAIL(c, LFSR_ERR_INVALID_ARG, "n_iters must be >= 0");
+  if (c->solver == 2) FAIL(c, LFSR_ERR_STATE, "gd iterations ran since lfsr_set_observations (one solver per solve)");
+  c->solver = 1;
   CK(c, cudaSetDevice(c->prm.device));
   for (int n = 0; n < n_iters; ++n) {
     cudaGraphExec_t g = c->graph[c->graph[1] ? (c->h_iter + n) & 1 : 0];
@@ -1071,15 +1089,11 @@ lfsr_status lfsr_admm_enqueue(lfsr_ctx* c, int32_t n_iters) {
   return LFSR_OK;
 }
 
-lfsr_status lfsr_admm_stats(lfsr_ctx* c, int32_t first_iter, int32_t n_iters, lfsr_iter_stats* stats) {
-  lfsr_status st = check_run(c);
-  if (st != LFSR_OK) return st;
-  if (n_iters < 0 || first_iter < 1 || first_iter + n_iters - 1 > c->h_iter || first_iter <= c->h_iter - kRingCap)
-    FAIL(c, LFSR_ERR_INVALID_ARG, "requested iterations are not in the stats window");
-  if (n_iters == 0) return LFSR_OK;
+// Blocking read of the device records of iterations [first, first + n) (1-based).
+static lfsr_status read_records(lfsr_ctx* c, int first_iter, int n_iters, std::vector<double>& rec) {
   CK(c, cudaSetDevice(c->prm.device));
   const double* ring = c->parts[0].ring;
-  std::vector<double> rec((size_t)n_iters * T_COUNT);
+  rec.assign((size_t)n_iters * T_COUNT, 0.0);
   int done = 0;
   while (done < n_iters) {  // at most two contiguous pieces of the ring
     int slot = (first_iter - 1 + done) % kRingCap;
@@ -1089,6 +1103,17 @@ lfsr_status lfsr_admm_stats(lfsr_ctx* c, int32_t first_iter, int32_t n_iters, lf
     done += cnt;
   }
   CK(c, cudaStreamSynchronize(c->stream));
+  return LFSR_OK;
+}
+
+lfsr_status lfsr_admm_stats(lfsr_ctx* c, int32_t first_iter, int32_t n_iters, lfsr_iter_stats* stats) {
+  lfsr_status st = check_run(c);
+  if (st != LFSR_OK) return st;
+  if (n_iters < 0 || first_iter < 1 || first_iter + n_iters - 1 > c->h_iter || first_iter <= c->h_iter - kRingCap)
+    FAIL(c, LFSR_ERR_INVALID_ARG, "requested iterations are not in the stats window");
+  if (n_iters == 0) return LFSR_OK;
+  std::vector<double> rec;
+  if ((st = read_records(c, first_iter, n_iters, rec)) != LFSR_OK) return st;
   bool bad = false;
   for (int n = 0; n < n_iters; ++n) {
     const double* r = rec.data() + (size_t)n * T_COUNT;
@@ -1123,6 +1148,124 @@ lfsr_status lfsr_admm_run(lfsr_ctx* c, int32_t n_iters, lfsr_iter_stats* stats) 
   if (stats && n_read < n_iters) FAIL(c, LFSR_ERR_INVALID_ARG, "stats requested for more than 4096 iterations");
   return lfsr_admm_stats(c, first + (n_iters - n_read), n_read, stats);
 }
+
+// ---------------------------------------------------------------------------
+// gd / gd-ls (readings A30-A33).  One iteration is
+// one graph: zero g -> k_tile<GRAD> (m from x, cost terms, g) [-> |g|^2 -> L
+// trial launches of k_tile<J>, each a no-op once an earlier trial met Armijo]
+// -> k_gd_update (step choice, x -= eta g, record).
+// ---------------------------------------------------------------------------
+static lfsr_status enqueue_gd(lfsr_ctx* c, cudaStream_t st, const GdCfg& cfg) {
+  const Geom& G = c->G;
+  Part& P = c->parts[0];
+  int launches = 0;
+  CK(c, cudaMemsetAsync(c->gd_g, 0, (size_t)G.H * G.ps * 4, st));
+  TileIO io = base_io(P);
+  io.in_hr = P.S.x;
+  io.y = P.S.y;
+  io.wo = P.S.wo;
+  io.out_hr = c->gd_g;
+  io.reweight = c->prm.reweight_every_iter;
+  CK(c, launch_tile(MODE_GRAD, G, c->V, P.T, io, st));
+  ++launches;
+  if (cfg.ls) {
+    CK(c, launch_gd_gnorm(G, c->gd_g, P.S.ctl, c->num_sms, st));
+    ++launches;
+    for (int t = 0; t < cfg.L; ++t) {
+      TileIO j = base_io(P);
+      j.in_hr = P.S.x;
+      j.in_hr2 = c->gd_g;
+      j.y = P.S.y;
+      j.ls_t = t;
+      j.eta0 = cfg.eta0;
+      j.armijo_c = cfg.armijo_c;
+      CK(c, launch_tile(MODE_J, G, c->V, P.T, j, st));
+      ++launches;
+    }
+  }
+  CK(c, launch_gd_update(G, P.S.x, c->gd_g, P.S.ctl, cfg, c->num_sms, st));
+  ++launches;
+  c->gd_launches = launches;
+  return LFSR_OK;
+}
+
+lfsr_status lfsr_gd_run(lfsr_ctx* c, const lfsr_gd_params* gp, int32_t n_iters, lfsr_gd_stats* stats) {
+  lfsr_status st = check_run(c);
+  if (st != LFSR_OK) return st;
+  if (!gp) FAIL(c, LFSR_ERR_INVALID_ARG, "gd params must not be NULL");
+  if (n_iters < 0) FAIL(c, LFSR_ERR_INVALID_ARG, "n_iters must be >= 0");
+  if (!(gp->step > 0.f) || !std::isfinite(gp->step)) FAIL(c, LFSR_ERR_INVALID_ARG, "step must be finite and > 0");
+  if (gp->line_search && (gp->max_trials < 1 || gp->max_trials > kMaxLs))
+    FAIL(c, LFSR_ERR_INVALID_ARG, "max_trials must be in [1, 32]");
+  if (!(gp->armijo_c >= 0.f) || !std::isfinite(gp->armijo_c)) FAIL(c, LFSR_ERR_INVALID_ARG, "armijo_c must be >= 0");
+  if (c->xmode != X_NONE) FAIL(c, LFSR_ERR_UNSUPPORTED, "gd runs on a single strip");
+  if (n_iters > kRingCap && stats) FAIL(c, LFSR_ERR_INVALID_ARG, "stats requested for more than 4096 iterations");
+  if (c->solver == 1) FAIL(c, LFSR_ERR_STATE, "ADMM iterations ran since lfsr_set_observations (one solver per solve)");
+  c->solver = 2;
+  if (n_iters == 0) return LFSR_OK;
+  CK(c, cudaSetDevice(c->prm.device));
+  const Geom& G = c->G;
+  if (!c->gd_g) {
+    void* p = nullptr;
+    cudaError_t e = dalloc(c, &p, (size_t)G.H * G.ps * 4);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      FAIL(c, LFSR_ERR_OOM, "device allocation failed");
+    }
+    c->gd_g = (float*)p;
+  }
+  GdCfg cfg{gp->step, gp->armijo_c, gp->line_search ? 1 : 0, gp->line_search ? gp->max_trials : 0};
+  if (!c->gd_graph || memcmp(&cfg, &c->gd_cfg, sizeof cfg) != 0) {
+    if (c->gd_graph) {
+      CK(c, cudaStreamSynchronize(c->stream));
+      cudaGraphExecDestroy(c->gd_graph);
+      c->gd_graph = nullptr;
+    }
+    CK(c, cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
+    lfsr_status es = enqueue_gd(c, c->cap_stream, cfg);
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(c->cap_stream, &graph);
+    if (es != LFSR_OK) {
+      if (graph) cudaGraphDestroy(graph);
+      return es;
+    }
+    if (e != cudaSuccess) return cuda_fail(c, e, "cudaStreamEndCapture");
+    e = cudaGraphInstantiate(&c->gd_graph, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return cuda_fail(c, e, "cudaGraphInstantiate");
+    c->gd_cfg = cfg;
+  }
+  const int first = c->h_iter + 1;
+  for (int n = 0; n < n_iters; ++n) CK(c, cudaGraphLaunch(c->gd_graph, c->stream));
+  c->h_iter += n_iters;
+  const int n_read = std::min(n_iters, kRingCap);
+  std::vector<double> rec;
+  if ((st = read_records(c, first + (n_iters - n_read), n_read, rec)) != LFSR_OK) return st;
+  bool bad = false;
+  for (int n = 0; n < n_read; ++n) {
+    const double* r = rec.data() + (size_t)n * T_COUNT;
+    if (r[T_NF] != 0.0) bad = true;
+    if (stats) {
+      lfsr_gd_stats& s = stats[n];
+      s.iter = (int32_t)r[T_ITER];
+      s.ls_evals = (int32_t)r[T_CGIT];
+      s.ls_failed = (int32_t)r[T_BREAK];
+      s.nonfinite = (int32_t)r[T_NF];
+      s.cu = 2 + s.ls_evals;
+      s.pad = 0;
+      s.J = r[T_J];
+      s.data_l1 = r[T_L1];
+      s.data_l2 = r[T_L2];
+      s.reg_l1 = r[T_REG];
+      s.step = r[T_RES];
+      s.grad_sq = r[T_PI0];
+    }
+  }
+  if (bad) FAIL(c, LFSR_ERR_DIVERGED, "non-finite x or cost during the gd iterations");
+  return LFSR_OK;
+}
+
+int32_t lfsr_gd_launches_per_iter(const lfsr_ctx* c) { return (c && c->gd_graph) ? c->gd_launches : 0; }
 
 lfsr_status lfsr_profile(lfsr_ctx* c, int32_t enable) {
   lfsr_status st = check_run(c);
@@ -1313,6 +1456,30 @@ lfsr_status lfsr_op_apply(lfsr_ctx* c, lfsr_op op, const float* in, float* out, 
     case LFSR_OP_ST: {
       CK(c, put2d(c, c->tmp_s, G.ps, in, G.W, (size_t)G.s_d * G.H, mem));
       CK(c, launch_apply_ST(G, c->tmp_s, S.m, c->tmp_hr2, s));
+      CK(c, get2d(c, out, G.W, c->tmp_hr2, G.ps, (size_t)G.H, mem));
+      break;
+    }
+    case LFSR_OP_GRAD: {
+      if (!c->op_ctl) {
+        void* p = nullptr;
+        cudaError_t e = dalloc(c, &p, sizeof(Control));
+        if (e != cudaSuccess) {
+          cudaGetLastError();
+          FAIL(c, LFSR_ERR_OOM, "device allocation failed");
+        }
+        c->op_ctl = (Control*)p;
+      }
+      CK(c, cudaMemsetAsync(c->op_ctl, 0, sizeof(Control), s));
+      CK(c, put2d(c, S.tmp_hr, G.ps, in, G.W, (size_t)G.H, mem));
+      CK(c, cudaMemsetAsync(c->tmp_hr2, 0, hr * 4, s));
+      TileIO io = base_io(P0);
+      io.ctl = c->op_ctl;
+      io.in_hr = S.tmp_hr;
+      io.y = S.y;
+      io.wo = S.wo;
+      io.out_hr = c->tmp_hr2;
+      io.reweight = 0;   // the current weight map m
+      CK(c, launch_tile(MODE_GRAD, G, c->V, T, io, s));
       CK(c, get2d(c, out, G.W, c->tmp_hr2, G.ps, (size_t)G.H, mem));
       break;
     }

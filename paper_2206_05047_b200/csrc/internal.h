@@ -11,6 +11,7 @@ constexpr int kMaxTaps = 8;      // blur radius R <= 3 for zeta <= 4 (Appendix B
 constexpr int kMaxOffsets = 80;  // s_d for r <= 4
 constexpr int kMaxK = 64;        // CG steps per ADMM iteration
 constexpr int kThreads = 256;    // threads per tile CTA
+constexpr int kMaxLs = 32;       // gd-ls: Armijo trials per iteration (reading A32)
 
 // Scalar slots of the current ADMM iteration (doubles in Control::cur).
 enum Slot : int {
@@ -24,7 +25,9 @@ enum Slot : int {
   S_STOP = 7,   // CG stopped flag (pi < tau, pi == 0 or breakdown)
   S_PI = 8,     // pi_k = <r_k, r_k>, k = 0..K      at S_PI + k
   S_PQ = S_PI + kMaxK + 1,  // <p_k, M p_k>, k = 1..K at S_PQ + k
-  S_COUNT = S_PQ + kMaxK + 1
+  S_GN = S_PQ + kMaxK + 1,  // gd: |g|^2
+  S_TJ = S_GN + 1,          // gd-ls: cost terms (sum|e|, sum e^2, sum|G|) of trial t at S_TJ + 3t
+  S_COUNT = S_TJ + 3 * kMaxLs
 };
 
 // Stats record layout in the ring (doubles).
@@ -112,9 +115,22 @@ struct TileIO {
   int32_t cg_k;          // NORMAL-CG: step index k >= 1; 0 = plain operator
   int32_t reweight;      // WZ: recompute m from x
   int32_t do_nltv;       // NORMAL: include the (th/2) S^T S term
+  int32_t ls_t;          // J: line-search trial index t (input tile = x - eta0 2^-t g, in_hr2 = g)
+  float eta0;            // J: initial step of the line search
+  float armijo_c;        // J: Armijo constant c (reading A32)
 };
 
-enum TileMode : int { MODE_WZ = 0, MODE_NORMAL = 1, MODE_A = 2, MODE_AT = 3 };
+// WZ: ADMM wz-step; NORMAL: CG normal operator; A / AT: test operators;
+// GRAD: cost terms and subgradient of J for gd (A30); J: cost terms of one gd-ls trial.
+enum TileMode : int { MODE_WZ = 0, MODE_NORMAL = 1, MODE_A = 2, MODE_AT = 3, MODE_GRAD = 4, MODE_J = 5 };
+
+// gd / gd-ls configuration of one iteration graph (readings A30-A33).
+struct GdCfg {
+  float eta0;        // (initial) step
+  float armijo_c;    // Armijo constant
+  int32_t ls;        // 1: Armijo backtracking over L trials
+  int32_t L;         // trials (<= kMaxLs)
+};
 
 struct State {
   // persistent solver state (pitched)

@@ -11,7 +11,8 @@
 //   B, D   Gaussian blur evaluated at LR positions only: horizontal taps by warp
 //          shuffles, vertical taps in a register ring (decimation is free) P:L577-579
 //   epilogue per LR pixel: (WZ) e = A_k x - y_k, clamp-form prox + scaled dual
-//          (Alg.1 lines 4-8, A5/A6) -> rho; (NORMAL) rho = c_A A_k p
+//          (Alg.1 lines 4-8, A5/A6) -> rho; (NORMAL) rho = c_A A_k p;
+//          (GRAD, gd) rho = l1 sgn(e) + 2 l2 e (A30); (J, gd-ls trial) cost terms only
 //   D^T B^T polyphase adjoint blur (register ring + shuffles)           A11/A14
 //   W_k^T  exact bilinear scatter into a shared int32 fixed-point accumulator
 //          (native ATOMS.ADD, order-independent -> deterministic per CTA)  A12
@@ -358,6 +359,8 @@ struct Tile : YRoute<!INT && TC<Z>::DUMMY, Z / 2> {
 //           sum_d Delta_d^T (W_d f_d)(z) with the backward neighbour's f_d
 //           recomputed from the old duals (gather form: no atomics, no race).
 // RAD > 0: offsets unrolled at compile time (paper's 5x5 window: RAD = 2).
+__device__ __forceinline__ float sgnf(float v) { return v > 0.f ? 1.f : (v < 0.f ? -1.f : 0.f); }   // A30
+
 struct NltvCtx {
   const float* P;
   const float* M;
@@ -382,7 +385,19 @@ __device__ __forceinline__ float nltv_pixel(const NltvCtx& c, const Geom& G, int
     const float xf = c.P[pidx<Z>(py + dy, px + dx, c.PW, c.PWZ)];   // in the tile even when outside Omega
     const float xb = c.P[pidx<Z>(py - dy, px - dx, c.PW, c.PWZ)];
     const float mb = c.M[mi - dy * c.MW - dx];
-    if (MODE == MODE_NORMAL) {
+    if (MODE == MODE_GRAD || MODE == MODE_J) {
+      // G_d = W_d (.) Delta_d x and the subgradient S_w^T sgn(G) in gather form (A30)
+      const float wz = wd * mz;
+      const float g = fin ? wz * (xz - xf) : 0.f;
+      freg += fabsf(g);
+      if (MODE == MODE_GRAD) {
+        acc = fmaf(wz, sgnf(g), acc);
+        if (bin) {
+          const float wb = wd * mb;
+          acc = fmaf(-wb, sgnf(wb * (xb - xz)), acc);
+        }
+      }
+    } else if (MODE == MODE_NORMAL) {
       const float wz = wd * mz, wb = wd * mb;
       const float dp = xz - xf;
       const float f2 = fin ? wz * wz : 0.f;
@@ -427,6 +442,7 @@ __device__ __forceinline__ float nltv_pixel(const NltvCtx& c, const Geom& G, int
     reg += (double)freg;
     res += (double)fres;
   }
+  if (MODE == MODE_GRAD || MODE == MODE_J) reg += (double)freg;
   return acc;
 }
 
@@ -440,7 +456,8 @@ __device__ __forceinline__ void view_pass(const Tile<Z, INT>& t, const Geom& G, 
   using C = TC<Z>;
   constexpr int LX = C::LX, NTAP = C::NTAP, KEEP = C::KEEP;
   constexpr bool kFwd = (MODE != MODE_AT);
-  constexpr bool kAdj = (MODE != MODE_A);
+  constexpr bool kAdj = (MODE != MODE_A && MODE != MODE_J);
+  constexpr bool kY = (MODE == MODE_WZ || MODE == MODE_GRAD || MODE == MODE_J);   // reads y_k
   const float lam1 = G.lambda1, lam2 = G.lambda2, ith = G.inv_theta;
   const int j = j0 + lane;
   const bool col_ok = lane < LX && j < G.w;
@@ -457,9 +474,9 @@ __device__ __forceinline__ void view_pass(const Tile<Z, INT>& t, const Geom& G, 
     y_nx[v] = 0.f;
     wa_nx[v] = 0.f;
     // software prefetch of the next LR row's observation and dual (WZ)
-    if (MODE == MODE_WZ && col_ok && i0 < G.h) {
+    if (kY && col_ok && i0 < G.h) {
       y_nx[v] = io.y[lrow0[v] + (size_t)i0 * G.lps];
-      wa_nx[v] = io.wA[lrow0[v] + (size_t)i0 * G.lps];
+      if (MODE == MODE_WZ) wa_nx[v] = io.wA[lrow0[v] + (size_t)i0 * G.lps];
     }
   }
   if (kFwd) {
@@ -476,9 +493,9 @@ __device__ __forceinline__ void view_pass(const Tile<Z, INT>& t, const Geom& G, 
     for (int v = 0; v < NV; ++v) {
       const size_t lg = lrow0[v] + (size_t)i * G.lps;
       const float y_cur = y_nx[v], wa_cur = wa_nx[v];
-      if (MODE == MODE_WZ && col_ok && li + 1 < BL && i + 1 < G.h) {
+      if (kY && col_ok && li + 1 < BL && i + 1 < G.h) {
         y_nx[v] = io.y[lg + G.lps];
-        wa_nx[v] = io.wA[lg + G.lps];
+        if (MODE == MODE_WZ) wa_nx[v] = io.wA[lg + G.lps];
       }
       rho[v] = 0.f;
       if (kFwd) {
@@ -506,6 +523,11 @@ __device__ __forceinline__ void view_pass(const Tile<Z, INT>& t, const Geom& G, 
             fa += fabsf(e_);
             fb = fmaf(e_, e_, fb);
             fc = fmaf(wn - wa, wn - wa, fc);
+          } else if (MODE == MODE_GRAD || MODE == MODE_J) {
+            const float e_ = a - y_cur;                         // e = A_k x - y_k
+            if (MODE == MODE_GRAD) rho[v] = fmaf(2.f * lam2, e_, lam1 * sgnf(e_));   // l1 sgn(e) + 2 l2 e (A30)
+            fa += fabsf(e_);
+            fb = fmaf(e_, e_, fb);
           }
         }
 #pragma unroll
@@ -538,6 +560,10 @@ __device__ __forceinline__ void view_pass(const Tile<Z, INT>& t, const Geom& G, 
       for (int u = 0; u < KEEP; ++u) t.adj_row(Z * BL + u, lane, br[v][u], drho[v], dtau[v], G);
   }
   if (MODE == MODE_NORMAL) red_a += (double)G.cA * (double)fa;
+  if (MODE == MODE_GRAD || MODE == MODE_J) {
+    red_a += (double)fa;
+    red_b += (double)fb;
+  }
   if (MODE == MODE_WZ) {
     red_a += (double)fa;
     red_b += (double)fb;
@@ -566,7 +592,8 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
   constexpr int R = C::R, LX = C::LX, TX = C::TX, ECOL = C::ECOL;
   const int BL = FIXBL ? C::BL : T.BL, TY = Z * BL, EY = Z * BL + C::KEEP;
   constexpr bool kFwd = (MODE != MODE_AT);
-  constexpr bool kAdj = (MODE != MODE_A);
+  constexpr bool kAdj = (MODE != MODE_A && MODE != MODE_J);
+  constexpr bool kWeights = (MODE == MODE_WZ || MODE == MODE_GRAD);   // m from x in the tile (A16, A31)
 
   extern __shared__ __align__(16) float smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -583,6 +610,20 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
   const int H = G.H, W = G.W, ps = G.ps;
   Control* ctl = io.ctl;
   if (MODE == MODE_NORMAL && io.cg_k >= 2 && ctl->cur[S_STOP] != 0.0) return;  // CG stopped
+  // gd-ls trial t runs only while no earlier trial met the Armijo condition (A32); every
+  // CTA reads the same fp64 sums, so all take the same decision
+  float ls_beta = 0.f;
+  if (MODE == MODE_J) {
+    const double* cur = ctl->cur;
+    const double J0 = (double)G.lambda1 * cur[S_L1] + (double)G.lambda2 * cur[S_L2] + cur[S_REG];
+    for (int t = 0; t < io.ls_t; ++t) {
+      const double et = ldexp((double)io.eta0, -t);
+      const double* jt = cur + S_TJ + 3 * t;
+      const double Jt = (double)G.lambda1 * jt[0] + (double)G.lambda2 * jt[1] + jt[2];
+      if (Jt <= J0 - (double)io.armijo_c * et * cur[S_GN]) return;
+    }
+    ls_beta = -ldexpf(io.eta0, -io.ls_t);
+  }
 
   float* P = smem;                                           // PH*PW  input tile (phase split)
   const int PHA = PH + (C::DUMMY ? 2 : 0);                   // + 2 zero rows (TC::DUMMY, Tile::yrow)
@@ -606,6 +647,8 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
     double pim1 = ctl->cur[S_PI + io.cg_k - 1], pim2 = ctl->cur[S_PI + io.cg_k - 2];
     beta = (float)(pim1 / pim2);    // Alg.2 line 10 (reading A2): p_k = r_k + beta p_{k-1}
   }
+  if (MODE == MODE_J) beta = ls_beta;   // trial point x - eta_t g
+  const bool two_in = (MODE == MODE_NORMAL && io.cg_k >= 2) || MODE == MODE_J;
   if (tid == 0) {
     s_max = 0.f;
     s_nl_next = 0;
@@ -628,7 +671,7 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
         gi[u] = (size_t)cy * ps + cx;
         own[u] = e < n && gy == cy && gx == cx && gy >= Y0 && gy < Y0 + TY && gx >= X0 && gx < X0 + TX;
         v[u] = (kFwd && e < n) ? __ldg(io.in_hr + gi[u]) : 0.f;
-        v2[u] = (MODE == MODE_NORMAL && io.cg_k >= 2 && e < n) ? __ldg(io.in_hr2 + gi[u]) : 0.f;
+        v2[u] = (two_in && e < n) ? __ldg(io.in_hr2 + gi[u]) : 0.f;
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -643,6 +686,7 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
           }
           if (own[u] && grp == 0) io.p_out[gi[u]] = val;
         }
+        if (MODE == MODE_J) val = fmaf(beta, v2[u], val);   // the same rounding as k_gd_update
         pmax = fmaxf(pmax, fabsf(val));
         const int py = e / PWn, px = e - py * PWn;
         const int i = pidx<Z>(py, px, PW, PWZ);
@@ -671,7 +715,7 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
       ACC[LO + PH * PW + e] = 0;
     }
   const int rr = G.radius, MW = T.MW;
-  if (MODE == MODE_NORMAL && io.do_nltv) {
+  if ((MODE == MODE_NORMAL && io.do_nltv) || MODE == MODE_J) {   // frozen m (J: of this gd iteration)
     for (int e = tid; e < T.MH * MW; e += NT) {
       const int my = e / MW, mx = e - my * MW;
       const int gy = Y0 - rr + my, gx = X0 - rr + mx;
@@ -689,6 +733,7 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
     if (MODE == MODE_NORMAL) tb = G.cA * s_max;
     if (MODE == MODE_WZ) tb = G.lambda2 * (s_max + G.ymax) + G.cS * G.lambda1 * 3.f * G.inv_theta;
     if (MODE == MODE_AT) tb = io.tmax_in;
+    if (MODE == MODE_GRAD) tb = G.lambda1 + 2.f * G.lambda2 * (s_max + G.ymax);   // |l1 sgn(e) + 2 l2 e|
     tb *= G.gpoly2;   // the polyphase adjoint blur shrinks max|rho|
     float sc = 0.f, isc = 0.f;
     if (tb > 0.f && isfinite(tb)) {
@@ -702,7 +747,7 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
     s_scale[0] = sc;
     s_scale[1] = isc;
   }
-  if (MODE == MODE_WZ) {  // m over own + radius from x (A8/A17/A19)
+  if (kWeights) {  // m over own + radius from x (A8/A17/A19)
     __syncthreads();      // P complete
     for (int e = tid; e < T.MH * MW; e += NT) {
       const int my = e / MW, mx = e - my * MW;
@@ -770,7 +815,7 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
   // work (the w_S stream in WZ) fills the wait for the slowest warp.
   double red_reg = 0.0;
   const int ng = T.groups;
-  const bool nltv = (MODE == MODE_WZ) || (MODE == MODE_NORMAL && io.do_nltv);
+  const bool nltv = (MODE == MODE_WZ || MODE == MODE_GRAD || MODE == MODE_J) || (MODE == MODE_NORMAL && io.do_nltv);
   if (nltv) {
     NltvCtx c;
     c.P = P; c.M = M; c.PW = PW; c.PWZ = PWZ; c.MW = MW; c.H = H; c.W = W; c.ps = ps;
@@ -801,12 +846,18 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
           } else {
             acc = nltv_pixel<Z, MODE, true, 0>(c, G, Y, X, py, px, mi, gi, pq, red_reg, red_c);
           }
-          acc *= G.cS;
+          if (MODE == MODE_WZ || MODE == MODE_NORMAL) acc *= G.cS;
           red_b += (double)G.cS * pq;
         }
         NL[oy * TX + ox] = acc;
       }
     }
+  }
+  if (MODE == MODE_J) {   // cost terms of trial t only (no output image)
+    double v[3] = {red_a, red_b, red_reg};
+    const int slot[3] = {S_TJ + 3 * io.ls_t, S_TJ + 3 * io.ls_t + 1, S_TJ + 3 * io.ls_t + 2};
+    block_reduce_add<3>(v, RED, ctl->cur, slot);
+    return;
   }
   __syncthreads();   // views and NLTV done: ACC and NL complete
 
@@ -832,6 +883,10 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
     double v[4] = {red_a, red_b, red_reg, red_c};
     const int slot[4] = {S_L1, S_L2, S_REG, S_RES2};
     block_reduce_add<4>(v, RED, ctl->cur, slot);
+  } else if (MODE == MODE_GRAD) {
+    double v[3] = {red_a, red_b, red_reg};
+    const int slot[3] = {S_L1, S_L2, S_REG};
+    block_reduce_add<3>(v, RED, ctl->cur, slot);
   } else if (MODE == MODE_NORMAL && io.cg_k >= 1) {
     double v[2] = {red_a + red_b, pi0_part};
     const int slot[2] = {S_PQ + io.cg_k, S_PI + 0};
@@ -858,6 +913,8 @@ struct TileZ {
       case MODE_NORMAL: return launchm<MODE_NORMAL>(G, V, T, io, st);
       case MODE_A: return launchm<MODE_A>(G, V, T, io, st);
       case MODE_AT: return launchm<MODE_AT>(G, V, T, io, st);
+      case MODE_GRAD: return launch1<MODE_GRAD, false>(G, V, T, io, st);   // gd: no fixed-height instance
+      case MODE_J: return launch1<MODE_J, false>(G, V, T, io, st);
     }
     return cudaErrorInvalidValue;
   }
@@ -874,6 +931,8 @@ struct TileZ {
     if ((e = prep1<MODE_A, true>(smem)) != cudaSuccess) return e;
     if ((e = prep1<MODE_A, false>(smem)) != cudaSuccess) return e;
     if ((e = prep1<MODE_AT, true>(smem)) != cudaSuccess) return e;
+    if ((e = prep1<MODE_GRAD, false>(smem)) != cudaSuccess) return e;
+    if ((e = prep1<MODE_J, false>(smem)) != cudaSuccess) return e;
     return prep1<MODE_AT, false>(smem);
   }
   static int occupancy(int threads, size_t smem) {

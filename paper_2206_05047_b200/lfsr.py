@@ -25,13 +25,14 @@ LFSR_OK, LFSR_ERR_INVALID_ARG, LFSR_ERR_STATE, LFSR_ERR_OOM, LFSR_ERR_CUDA, LFSR
     LFSR_ERR_DIVERGED, LFSR_ERR_UNSUPPORTED = range(8)
 STATUS_NAMES = ["OK", "INVALID_ARG", "STATE", "OOM", "CUDA", "NCCL", "DIVERGED", "UNSUPPORTED"]
 MEM_HOST, MEM_DEVICE = 0, 1
-OP_A, OP_AT, OP_S, OP_ST, OP_NORMAL, OP_WEIGHTS = range(6)
-OPS = {"A": OP_A, "AT": OP_AT, "S": OP_S, "ST": OP_ST, "NORMAL": OP_NORMAL, "WEIGHTS": OP_WEIGHTS}
+OP_A, OP_AT, OP_S, OP_ST, OP_NORMAL, OP_WEIGHTS, OP_GRAD = range(7)
+OPS = {"A": OP_A, "AT": OP_AT, "S": OP_S, "ST": OP_ST, "NORMAL": OP_NORMAL, "WEIGHTS": OP_WEIGHTS, "GRAD": OP_GRAD}
 
 # every symbol include/lfsr.h declares (checked by tests/test_abi.py)
 EXPORTS = ("lfsr_create", "lfsr_set_observations", "lfsr_admm_run", "lfsr_admm_enqueue", "lfsr_admm_stats",
            "lfsr_get_hr", "lfsr_get_state", "lfsr_op_apply", "lfsr_launches_per_iter", "lfsr_tile_config", "lfsr_profile",
-           "lfsr_profile_read", "lfsr_strip_plan", "lfsr_destroy", "lfsr_last_error", "lfsr_abi_version")
+           "lfsr_profile_read", "lfsr_strip_plan", "lfsr_destroy", "lfsr_last_error", "lfsr_abi_version",
+           "lfsr_gd_run", "lfsr_gd_launches_per_iter")
 
 
 class LFSRError(RuntimeError):
@@ -60,6 +61,21 @@ class _CStats(ctypes.Structure):
 
 
 STAT_KEYS = [f[0] for f in _CStats._fields_]
+
+
+class _CGdParams(ctypes.Structure):
+    _fields_ = [("step", ctypes.c_float), ("line_search", ctypes.c_int32), ("max_trials", ctypes.c_int32),
+                ("armijo_c", ctypes.c_float)]
+
+
+class _CGdStats(ctypes.Structure):
+    _fields_ = [("iter", ctypes.c_int32), ("ls_evals", ctypes.c_int32), ("ls_failed", ctypes.c_int32),
+                ("nonfinite", ctypes.c_int32), ("cu", ctypes.c_int32), ("pad", ctypes.c_int32),
+                ("J", ctypes.c_double), ("data_l1", ctypes.c_double), ("data_l2", ctypes.c_double),
+                ("reg_l1", ctypes.c_double), ("step", ctypes.c_double), ("grad_sq", ctypes.c_double)]
+
+
+GD_STAT_KEYS = [f[0] for f in _CGdStats._fields_ if f[0] != "pad"]
 
 
 class _CStrip(ctypes.Structure):
@@ -115,6 +131,10 @@ def load_library(path: str = LIB_PATH):
     lib.lfsr_last_error.restype = ctypes.c_char_p
     lib.lfsr_strip_plan.argtypes = [P(_CParams), ctypes.c_int32, P(_CStrip)]
     lib.lfsr_strip_plan.restype = st
+    lib.lfsr_gd_run.argtypes = [vp, P(_CGdParams), ctypes.c_int32, P(_CGdStats)]
+    lib.lfsr_gd_run.restype = st
+    lib.lfsr_gd_launches_per_iter.argtypes = [vp]
+    lib.lfsr_gd_launches_per_iter.restype = ctypes.c_int32
     lib.lfsr_abi_version.argtypes = []
     lib.lfsr_abi_version.restype = ctypes.c_int32
     _lib = lib
@@ -270,6 +290,23 @@ class Solver:
         self._check(s)
         return stats
 
+    def gd_run(self, n_iters: int, step: float, line_search: bool = False, max_trials: int = 30,
+               armijo_c: float = 1e-4, want_stats: bool = True):
+        """gd / gd-ls iterations (lfsr_gd_run, readings A30-A33)."""
+        gp = _CGdParams(float(step), 1 if line_search else 0, int(max_trials), float(armijo_c))
+        st = (_CGdStats * max(int(n_iters), 1))() if want_stats else None
+        s = self.lib.lfsr_gd_run(self._h, ctypes.byref(gp), int(n_iters), st)
+        stats = [{k: getattr(st[i], k) for k in GD_STAT_KEYS} for i in range(n_iters)] if want_stats else None
+        if s == LFSR_ERR_DIVERGED:
+            err = LFSRError(s, self.lib.lfsr_last_error(self._h).decode())
+            err.stats = stats
+            raise err
+        self._check(s)
+        return stats
+
+    def gd_launches_per_iter(self) -> int:
+        return int(self.lib.lfsr_gd_launches_per_iter(self._h))
+
     def profile(self, enable: bool = True):
         self._check(self.lib.lfsr_profile(self._h, 1 if enable else 0))
 
@@ -307,7 +344,7 @@ class Solver:
         op = OPS[name]
         out_shape = {OP_A: (p.n_views, p.lr_height, p.lr_width), OP_AT: (p.H, p.W),
                      OP_S: (p.s_d, p.H, p.W), OP_ST: (p.H, p.W), OP_NORMAL: (p.H, p.W),
-                     OP_WEIGHTS: (p.H, p.W)}[op]
+                     OP_WEIGHTS: (p.H, p.W), OP_GRAD: (p.H, p.W)}[op]
         ptr, mem, keep = self._ptr_in(inp)
         if mem == MEM_DEVICE:
             import torch

@@ -35,7 +35,7 @@ def test_exports_every_declared_symbol(lib):
     exported = set(re.findall(r" T (lfsr_\w+)", out))
     assert set(header_symbols()) <= exported
     assert set(lfsr.EXPORTS) == set(header_symbols())
-    assert lib.lfsr_abi_version() == 2
+    assert lib.lfsr_abi_version() == 3
 
 
 def test_built_for_sm100a(lib):
