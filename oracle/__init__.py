@@ -46,7 +46,7 @@ class _Params(ctypes.Structure):
                 ("sigma_o2", ctypes.c_double), ("theta", ctypes.c_double),
                 ("cg_max_iters", ctypes.c_int32), ("cg_tol", ctypes.c_double),
                 ("reweight_every_iter", ctypes.c_int32),
-                ("offset_weights", ctypes.POINTER(ctypes.c_double))]
+                ("offset_weights", ctypes.POINTER(ctypes.c_double)), ("disp_per_view", ctypes.c_int32)]
 
 
 class _Stats(ctypes.Structure):
@@ -139,6 +139,7 @@ class Params:
     cg_tol: float = 0.0
     reweight_every_iter: int = 1
     offset_weights: Optional[Sequence[float]] = None   # s_d weights overriding exp(-|d|^2/sigma_s)
+    disp_per_view: int = 0      # 1: omega is [n_views][H][W] (view k warped with omega_k, A34)
 
     @property
     def H(self):
@@ -161,7 +162,7 @@ class Params:
         return _Params(self.n_views, self.lr_h, self.lr_w, self.scale, self.ref_view, self.radius,
                        self.lambda1, self.lambda2, self.lambda_reg, self.sigma_s, self.sigma_e,
                        self.sigma_o1, self.sigma_o2, self.theta, self.cg_max_iters, self.cg_tol,
-                       self.reweight_every_iter, ow)
+                       self.reweight_every_iter, ow, int(self.disp_per_view))
 
 
 def blur_taps(scale: int) -> np.ndarray:

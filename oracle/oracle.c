@@ -34,6 +34,8 @@
  *   or_admm           pinned: l2-only == lstsq (P10), == textbook scaled ADMM with exact
  *                     x-step (P11), convergence to an independent minimiser (P12)
  *   or_gradient       pinned: central finite differences of J (P18), J == or_cost
+ *   per-view omega    pinned: equal maps == shared mode, view k == shared mode with omega_k,
+ *                     adjoint identity (P22)
  *   or_gd             pinned: smooth case with step 1/L decreases J monotonically and reaches the
  *                     lstsq solution (P19); Armijo acceptance checked against or_cost and
  *                     maximality of the step (P20); ADMM below gd at equal CU (P21)
@@ -57,7 +59,17 @@ typedef struct {
   int32_t reweight_every_iter;                  /* 1 = paper */
   const double* offset_weights;                 /* NULL: w_d = exp(-|d|^2/sigma_s); else s_d
                                                    user weights in the U order (BTV, NEXT-1) */
+  int32_t disp_per_view;                        /* 0: one omega [H][W] on theta_0's grid for every
+                                                   view (A12); 1: omega [n_views][H][W], view k
+                                                   warped with its own omega_k (P:L580-582,
+                                                   NEXT-2, reading A34) */
 } or_params;
+
+/* The disparity map view k is warped with ("for each perspective theta_k, we
+ * need to find the disparity map omega_k"): omega_k in per-view mode, else the shared map. */
+static const double* omega_of(const or_params* P, const double* omega, int k) {
+  return P->disp_per_view ? omega + (size_t)k * P->lr_h * P->scale * P->lr_w * P->scale : omega;
+}
 
 typedef struct {
   int32_t iter, cg_iters, breakdown, nonfinite;
@@ -179,7 +191,7 @@ void or_apply_A(const or_params* P, const double* view_offsets, const double* om
   double* t1 = (double*)malloc(sizeof(double) * p);
   double* t2 = (double*)malloc(sizeof(double) * p);
   for (int k = 0; k < P->n_views; ++k) {
-    or_apply_W(H, W, x, omega, view_offsets[2 * k], view_offsets[2 * k + 1], t1);
+    or_apply_W(H, W, x, omega_of(P, omega, k), view_offsets[2 * k], view_offsets[2 * k + 1], t1);
     or_apply_B(H, W, R, taps, t1, t2);
     or_apply_D(H, W, z, t2, out + k * q);
   }
@@ -201,7 +213,7 @@ void or_apply_AT(const or_params* P, const double* view_offsets, const double* o
   for (int k = 0; k < P->n_views; ++k) {
     or_apply_DT(H, W, z, r + k * q, t1);
     or_apply_B(H, W, R, taps, t1, t2);
-    or_apply_WT(H, W, t2, omega, view_offsets[2 * k], view_offsets[2 * k + 1], t3);
+    or_apply_WT(H, W, t2, omega_of(P, omega, k), view_offsets[2 * k], view_offsets[2 * k + 1], t3);
     for (size_t i = 0; i < p; ++i) out[i] += t3[i];
   }
   free(t1);
@@ -323,7 +335,8 @@ static double bilin_lr(int h, int w, const double* img, double r, double c) {
          a * (1 - b) * img[(size_t)r1 * w + c0] + a * b * img[(size_t)r1 * w + c1];
 }
 
-/* Static occlusion weight (Eq. weight_occ), readings A16/A17:
+/* Static occlusion weight (Eq. weight_occ), readings A16/A17 (per-view
+ * disparity: the reference view's omega_0, the map on theta_0's grid, A34):
  *   b(z) = min(0, d_X omega + d_Y omega), forward differences, 0 on last col/row;
  *   p(z) = mean_{k != ref} | y_ref(z/zeta) - y_k((z - dtheta_k omega(z))/zeta) |;
  *   w_o  = exp(-b^2 / (2 s1^2)) exp(-p^2 / (2 s2^2)).
@@ -333,6 +346,7 @@ void or_setup_wo(const or_params* P, const double* y, const double* view_offsets
   int z = P->scale, h = P->lr_h, w = P->lr_w, H = h * z, W = w * z;
   size_t q = (size_t)h * w;
   const double* yref = y + (size_t)P->ref_view * q;
+  omega = omega_of(P, omega, P->ref_view);
 #pragma omp parallel for schedule(static)
   for (int Y = 0; Y < H; ++Y)
     for (int X = 0; X < W; ++X) {
