@@ -63,8 +63,11 @@ typedef enum {
 typedef enum { LFSR_MEM_HOST = 0, LFSR_MEM_DEVICE = 1 } lfsr_mem;
 
 /* Disparity layout.  SHARED: one HR map omega on theta_0's grid used by every
- * view (reading A12).  PER_VIEW (the paper's omega_k): not in
- * this build (LFSR_ERR_UNSUPPORTED). */
+ * view (reading A12).  PER_VIEW (the paper's omega_k, P:L580-582;
+ * reading A34): [n_views][H][W], view k is warped with its own map omega_k on
+ * theta_0's grid (W_k x (z) = x(z + dtheta_k omega_k(z)), exact transpose kept);
+ * the occlusion weight uses omega_{ref_view}.  Costs one extra global read of
+ * omega_k per E row and view in the fused kernel. */
 typedef enum { LFSR_DISP_SHARED = 0, LFSR_DISP_PER_VIEW = 1 } lfsr_disp_mode;
 
 typedef struct {
@@ -127,14 +130,16 @@ LFSR_API lfsr_status lfsr_create(const lfsr_params* params, lfsr_ctx** out);
  *   lr_views     [n_views][lr_height][lr_width]  y_k
  *   view_offsets [n_views][2] = (drho_k, dtau_k) = theta_k - theta_0 in angular
  *                steps; drho shifts along X (columns), dtau along Y (rows) (A13)
- *   disparity    [H][W] omega on theta_0's HR grid, HR px per angular step
+ *   disparity    [H][W] omega on theta_0's HR grid, HR px per angular step (SHARED),
+ *                or [n_views][H][W] omega_k (PER_VIEW)
  *   x0           [H][W] initial guess, or NULL => bicubic (Catmull-Rom a=-0.5)
  *                up-sampling of the reference view (A15)
  * Also computes the static occlusion weight w_o (Eq. weight_occ, P:L424-444,
  * A16/A17) and the weight map from x0.  Synchronises the ctx stream (it needs
  * max|omega| and the view offsets on the host to size the kernel halos).
- * Errors: INVALID_ARG (NULL arrays, non-finite offsets), UNSUPPORTED
- * (PER_VIEW), OOM, CUDA, STATE. */
+ * Errors: INVALID_ARG (NULL arrays, non-finite offsets or disparity, unknown
+ * disp_mode), UNSUPPORTED (disparity range too large for the shared-memory
+ * tile), OOM, CUDA, STATE. */
 LFSR_API lfsr_status lfsr_set_observations(lfsr_ctx* ctx, const float* lr_views, const float* view_offsets,
                                   const float* disparity, lfsr_disp_mode disp_mode,
                                   const float* x0, lfsr_mem mem);

@@ -432,3 +432,19 @@ def random_instance(seed: int, n_views: int, lr_h: int, lr_w: int, scale: int,
 
 def config_dict(cfg: Config) -> dict:
     return asdict(cfg)
+
+
+def per_view_disparity(omega: np.ndarray, n_views: int, amp: float = 0.2, seed: int = 0) -> np.ndarray:
+    """[n_views][H][W] fp32 per-view disparity maps omega_k on theta_0's grid (LFSR_DISP_PER_VIEW,
+    reading A34): the shared map plus a smooth per-view perturbation of amplitude `amp` (a
+    low-frequency sinusoid with a random phase and direction per view), e.g. the per-view
+    estimates a disparity estimator would return.  Input generator only; no method arithmetic."""
+    g = np.random.Generator(np.random.Philox(seed))
+    H, W = omega.shape
+    Y, X = np.meshgrid(np.arange(H, dtype=np.float64), np.arange(W, dtype=np.float64), indexing="ij")
+    out = np.empty((n_views, H, W), np.float32)
+    for k in range(n_views):
+        fy, fx = g.uniform(0.5, 2.0, size=2) / np.array([max(H, 2), max(W, 2)])
+        ph = g.uniform(0.0, 2.0 * np.pi)
+        out[k] = (omega + amp * np.sin(2.0 * np.pi * (fy * Y + fx * X) + ph)).astype(np.float32)
+    return out

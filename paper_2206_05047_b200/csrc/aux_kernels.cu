@@ -55,8 +55,9 @@ __global__ void k_density(const Geom G, const Views V, const float* __restrict__
   int X = blockIdx.x * blockDim.x + threadIdx.x, Y = blockIdx.y;
   if (X >= G.W || Y >= G.H) return;
   const int ps = G.ps;
-  const float om = omega[(size_t)Y * ps + X];
+  const size_t pv_stride = G.per_view ? (size_t)G.H * ps : 0;   // omega_k (A34)
   for (int k = 0; k < G.n_views; ++k) {
+    const float om = omega[k * pv_stride + (size_t)Y * ps + X];
     const float2 o = V.off[k];
     const float sy = fminf(fmaxf((float)Y + o.y * om, 0.f), (float)(G.H - 1));
     const float sx = fminf(fmaxf((float)X + o.x * om, 0.f), (float)(G.W - 1));

@@ -93,7 +93,7 @@ struct lfsr_ctx {
   int gd_launches = 0;
   float* gd_g = nullptr;         // gd subgradient buffer [H][ps]
   Control* op_ctl = nullptr;     // scratch control block of lfsr_op_apply (keeps the solver sums clean)
-  size_t alloc_key[6] = {0, 0, 0, 0, 0, 0};
+  size_t alloc_key[7] = {0, 0, 0, 0, 0, 0, 0};
   bool profile = false;          // event-record nodes around every kernel (single strip)
   std::vector<cudaEvent_t> prof_ev;
   double prof_ms[3] = {0, 0, 0}; // accumulated wz / normal / update milliseconds
@@ -488,7 +488,7 @@ static lfsr_status alloc_part(lfsr_ctx* c, Part& P) {
   ALLOC(S.wS[0], ws * 4);
   ALLOC(S.wS[1], ws * 4);
   ALLOC(S.density, hr * 4);
-  ALLOC(S.omega, hr * 4);
+  ALLOC(S.omega, hr * 4 * (G.per_view ? (size_t)G.n_views : 1));
   ALLOC(S.wo, hr * 4);
   ALLOC(S.m, hr * 4);
   ALLOC(S.r, hr * 4);
@@ -665,8 +665,7 @@ lfsr_status lfsr_set_observations(lfsr_ctx* c, const float* lr_views, const floa
                                   const float* disparity, lfsr_disp_mode disp_mode, const float* x0, lfsr_mem mem) {
   if (!c) return LFSR_ERR_INVALID_ARG;
   if (c->poisoned) FAIL(c, LFSR_ERR_STATE, "ctx is poisoned by an earlier CUDA/NCCL error");
-  if (disp_mode == LFSR_DISP_PER_VIEW) FAIL(c, LFSR_ERR_UNSUPPORTED, "per-view disparity maps are not in this build");
-  if (disp_mode != LFSR_DISP_SHARED) FAIL(c, LFSR_ERR_INVALID_ARG, "unknown disp_mode");
+  if (disp_mode != LFSR_DISP_SHARED && disp_mode != LFSR_DISP_PER_VIEW) FAIL(c, LFSR_ERR_INVALID_ARG, "unknown disp_mode");
   lfsr_status st;
   if ((st = check_ptr(c, lr_views, mem, "lr_views")) != LFSR_OK) return st;
   if ((st = check_ptr(c, view_offsets, mem, "view_offsets")) != LFSR_OK) return st;
@@ -688,8 +687,10 @@ lfsr_status lfsr_set_observations(lfsr_ctx* c, const float* lr_views, const floa
   const size_t hr = (size_t)G.H * G.ps, lr = (size_t)G.n_views * G.h * G.lps;
   const size_t ws = (size_t)G.s_d * hr;
   const int nparts = c->xmode == X_LOCAL ? c->prm.n_ranks : 1;
-  const size_t key[6] = {(size_t)G.n_views, (size_t)G.h, (size_t)G.w, (size_t)G.scale, (size_t)G.s_d,
-                         (size_t)nparts};
+  G.per_view = disp_mode == LFSR_DISP_PER_VIEW ? 1 : 0;
+  const size_t n_om = G.per_view ? (size_t)G.n_views : 1;   // disparity maps
+  const size_t key[7] = {(size_t)G.n_views, (size_t)G.h, (size_t)G.w, (size_t)G.scale, (size_t)G.s_d,
+                         (size_t)nparts, n_om};
   c->ready = false;
   free_graph(c);
   if (memcmp(key, c->alloc_key, sizeof key) != 0) {
@@ -733,7 +734,7 @@ lfsr_status lfsr_set_observations(lfsr_ctx* c, const float* lr_views, const floa
     h.cap = kRingCap;
     CK(c, cudaMemcpyAsync(P.S.ctl, &h, sizeof(Control), cudaMemcpyHostToDevice, c->stream));
     CK(c, put2d(c, P.S.y, G.lps, lr_views, G.w, (size_t)G.n_views * G.h, mem));
-    CK(c, put2d(c, P.S.omega, G.ps, disparity, G.W, (size_t)G.H, mem));
+    CK(c, put2d(c, P.S.omega, G.ps, disparity, G.W, (size_t)G.H * n_om, mem));
   }
   State& S0 = c->parts[0].S;
 
@@ -742,7 +743,7 @@ lfsr_status lfsr_set_observations(lfsr_ctx* c, const float* lr_views, const floa
   // the splat density max_z sum_k (W_k^T 1)(z)
   for (int k = 0; k < nv; ++k) c->V.off[k] = make_float2(off[2 * k], off[2 * k + 1]);
   CK(c, cudaMemsetAsync(umax, 0, 3 * sizeof(unsigned), c->stream));
-  CK(c, launch_absmax(S0.omega, hr, umax, c->stream));
+  CK(c, launch_absmax(S0.omega, hr * n_om, umax, c->stream));
   CK(c, launch_density(G, c->V, S0.omega, S0.density, c->stream));
   CK(c, launch_absmax(S0.density, hr, umax + 1, c->stream));
   CK(c, launch_absmax(S0.y, lr, umax + 2, c->stream));
@@ -776,7 +777,8 @@ lfsr_status lfsr_set_observations(lfsr_ctx* c, const float* lr_views, const floa
     } else {
       CK(c, launch_bicubic(G, S.y, S.x, c->stream));
     }
-    CK(c, launch_setup_wo(G, c->V, S.y, S.omega, S.wo, c->stream));
+    const float* om_ref = S.omega + (G.per_view ? (size_t)G.ref_view * hr : 0);   // omega_0 (A34)
+    CK(c, launch_setup_wo(G, c->V, S.y, om_ref, S.wo, c->stream));
     CK(c, launch_weights(G, S.x, S.wo, S.m, c->stream));
   }
   if (tune && (st = tune_tile_bl(c)) != LFSR_OK) return st;

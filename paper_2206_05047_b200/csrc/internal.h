@@ -63,6 +63,7 @@ struct Geom {
   float cS;                   // theta / 2
   int32_t tile_bl;            // LR rows per tile (host-chosen, 0 = the zeta default; see make_tile_geom)
   int32_t tile_g, tile_nw;    // view groups and warps per CTA (host-chosen, 0 = the cost model's choice)
+  int32_t per_view;           // 1: omega is [n_views][H][ps], view k warped with omega_k (A34)
   float taps[kMaxTaps * 2 + 1];
   float2 tpe[kMaxTaps + 1];   // tap pairs (taps[2v], taps[2v+1]), zero past 2R (packed FP32 operands)
   float2 tpo[kMaxTaps + 1];   // tap pairs (taps[2v+1], taps[2v+2])
@@ -139,7 +140,7 @@ struct State {
   float* wA;     // [n_views][h][lps]
   float* wS[2];  // [s_d][H][ps] ping-pong (read iter&1, write the other)
   float* density;  // [H][ps] splat density sum_k W_k^T 1 (fixed-point bound)
-  float* omega;  // [H][ps]
+  float* omega;  // [H][ps], or [n_views][H][ps] with per-view disparity (A34)
   float* wo;     // [H][ps]
   float* m;      // [H][ps]
   // CG vectors

@@ -127,6 +127,7 @@ struct Tile : YRoute<!INT && TC<Z>::DUMMY, Z / 2> {
   int* ACC;
   const float* OM;
   int PW, PWZ, PY0, PX0, YE0, XE0, H, W;
+  int PS;             // HR row pitch of the global disparity maps
   float tscale;
   int lo;             // offset of the residual accumulator from ACC (ints)
   unsigned koff;      // Z = 2: folded magic offsets of cells_bits()
@@ -221,7 +222,18 @@ struct Tile : YRoute<!INT && TC<Z>::DUMMY, Z / 2> {
     return f2s(Yrow);
   }
 
-  __device__ __forceinline__ void load_om(int er, int lane, float (&om)[Z]) const {
+  // Disparity of the lane's zeta E positions on E row er: the shared map staged in
+  // shared memory (omk == nullptr), or view k's own map omega_k read from global memory
+  // (per-view mode, A34; zero outside the image like the staged map).
+  __device__ __forceinline__ void load_om(int er, int lane, float (&om)[Z], const float* omk) const {
+    if (omk) {
+      const int Yg = YE0 + er, X0g = XE0 + Z * lane;
+      const bool rin = (unsigned)Yg < (unsigned)H;
+      const float* src = omk + (size_t)(rin ? Yg : 0) * PS;
+#pragma unroll
+      for (int s = 0; s < Z; ++s) om[s] = (rin && (unsigned)(X0g + s) < (unsigned)W) ? __ldg(src + X0g + s) : 0.f;
+      return;
+    }
     const float* src = OM + er * TC<Z>::ECOL + Z * lane;
     if constexpr (Z == 2) {
       float2 v = *reinterpret_cast<const float2*>(src);
@@ -236,11 +248,12 @@ struct Tile : YRoute<!INT && TC<Z>::DUMMY, Z / 2> {
   }
 
   // W_k then the horizontal blur taps at this lane's LR column, for E row er.
-  __device__ __forceinline__ float fwd_row(int er, int lane, float drho, float dtau, const Geom& G) const {
+  __device__ __forceinline__ float fwd_row(int er, int lane, float drho, float dtau, const float* omk,
+                                          const Geom& G) const {
     constexpr int NTAP = TC<Z>::NTAP;
     if (!kDummy && !row_in(er)) return 0.f;    // blur zero padding (A11), warp uniform
     float om[Z], wp[Z];
-    load_om(er, lane, om);
+    load_om(er, lane, om, omk);
     const float Yf = yrow(er);
     const float X0 = (float)(XE0 - PX0 + Z * lane);
 #pragma unroll
@@ -283,7 +296,7 @@ struct Tile : YRoute<!INT && TC<Z>::DUMMY, Z / 2> {
   // whose source columns coincide (smooth disparity) are merged first: zeta + 1 pairs
   // instead of 2 zeta (per lane and boundary; the all-or-nothing warp test it replaces
   // cost 4 % at C4/C5).
-  __device__ __forceinline__ void adj_row(int er, int lane, float t1b, float drho, float dtau,
+  __device__ __forceinline__ void adj_row(int er, int lane, float t1b, float drho, float dtau, const float* omk,
                                           const Geom& G) const {
     constexpr int NJ = 2 * TC<Z>::R / Z + 1;
     constexpr int R2 = 2 * TC<Z>::R;
@@ -296,7 +309,7 @@ struct Tile : YRoute<!INT && TC<Z>::DUMMY, Z / 2> {
       tv[j] = lane >= j ? v : 0.f;
     }
     float om[Z];
-    load_om(er, lane, om);
+    load_om(er, lane, om, omk);
     const float Yf = yrow(er);
     const float X0 = (float)(XE0 - PX0 + Z * lane);
     int i00[Z], i01[Z];
@@ -449,7 +462,7 @@ __device__ __forceinline__ float nltv_pixel(const NltvCtx& c, const Geom& G, int
 // Phase 2 of k_tile: every warp streams whole views through the tile (see header).
 // NV views are processed interleaved row by row (independent dependency chains
 // for the scheduler); the last odd view of a warp takes the NV = 1 path.
-template <int Z, int MODE, bool INT, int NV>
+template <int Z, int MODE, bool INT, int NV, bool PV>
 __device__ __forceinline__ void view_pass(const Tile<Z, INT>& t, const Geom& G, const Views& V, const TileIO& io,
                                           const int (&ks)[NV], int lane, int i0, int j0, int BL, double& red_a,
                                           double& red_b, double& red_c) {
@@ -462,12 +475,14 @@ __device__ __forceinline__ void view_pass(const Tile<Z, INT>& t, const Geom& G, 
   const int j = j0 + lane;
   const bool col_ok = lane < LX && j < G.w;
   float drho[NV], dtau[NV], fr[NV][NTAP], br[NV][NTAP], y_nx[NV], wa_nx[NV];
+  const float* omk[NV];   // per-view disparity map omega_k (A34), nullptr: the shared map in shared memory
   size_t lrow0[NV];
   float fa = 0.f, fb = 0.f, fc = 0.f;   // this pass's partial sums (<= BL * NV terms per lane), fp32
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
     drho[v] = V.off[ks[v]].x;
     dtau[v] = V.off[ks[v]].y;
+    omk[v] = PV ? io.omega + (size_t)ks[v] * G.H * G.ps : nullptr;   // compile-time nullptr: shared map
 #pragma unroll
     for (int u = 0; u < NTAP; ++u) { fr[v][u] = 0.f; br[v][u] = 0.f; }
     lrow0[v] = ((size_t)ks[v] * G.h) * G.lps + j;
@@ -483,7 +498,7 @@ __device__ __forceinline__ void view_pass(const Tile<Z, INT>& t, const Geom& G, 
 #pragma unroll
     for (int u = 0; u < KEEP; ++u)
 #pragma unroll
-      for (int v = 0; v < NV; ++v) fr[v][u] = t.fwd_row(u, lane, drho[v], dtau[v], G);
+      for (int v = 0; v < NV; ++v) fr[v][u] = t.fwd_row(u, lane, drho[v], dtau[v], omk[v], G);
   }
   for (int li = 0; li < BL; ++li) {
     const int i = i0 + li;
@@ -500,7 +515,7 @@ __device__ __forceinline__ void view_pass(const Tile<Z, INT>& t, const Geom& G, 
       rho[v] = 0.f;
       if (kFwd) {
 #pragma unroll
-        for (int u = 0; u < Z; ++u) fr[v][KEEP + u] = t.fwd_row(Z * li + KEEP + u, lane, drho[v], dtau[v], G);
+        for (int u = 0; u < Z; ++u) fr[v][KEEP + u] = t.fwd_row(Z * li + KEEP + u, lane, drho[v], dtau[v], omk[v], G);
         float2 a2 = f2s(0.f);                                            // A_k x at LR pixel (i, j)
 #pragma unroll
         for (int u = 0; u + 1 < NTAP; u += 2) a2 = __ffma2_rn(tap2(G, u), f2(fr[v][u], fr[v][u + 1]), a2);
@@ -547,7 +562,7 @@ __device__ __forceinline__ void view_pass(const Tile<Z, INT>& t, const Geom& G, 
         }
         if constexpr (NTAP & 1) br[v][NTAP - 1] = fmaf(G.taps[NTAP - 1], rho[v], br[v][NTAP - 1]);
 #pragma unroll
-        for (int u = 0; u < Z; ++u) t.adj_row(Z * li + u, lane, br[v][u], drho[v], dtau[v], G);
+        for (int u = 0; u < Z; ++u) t.adj_row(Z * li + u, lane, br[v][u], drho[v], dtau[v], omk[v], G);
 #pragma unroll
         for (int u = 0; u < NTAP; ++u) br[v][u] = (u < KEEP) ? br[v][u + Z] : 0.f;
       }
@@ -557,7 +572,7 @@ __device__ __forceinline__ void view_pass(const Tile<Z, INT>& t, const Geom& G, 
 #pragma unroll
     for (int v = 0; v < NV; ++v)
 #pragma unroll
-      for (int u = 0; u < KEEP; ++u) t.adj_row(Z * BL + u, lane, br[v][u], drho[v], dtau[v], G);
+      for (int u = 0; u < KEEP; ++u) t.adj_row(Z * BL + u, lane, br[v][u], drho[v], dtau[v], omk[v], G);
   }
   if (MODE == MODE_NORMAL) red_a += (double)G.cA * (double)fa;
   if (MODE == MODE_GRAD || MODE == MODE_J) {
@@ -571,7 +586,7 @@ __device__ __forceinline__ void view_pass(const Tile<Z, INT>& t, const Geom& G, 
   }
 }
 
-template <int Z, int MODE, bool INT>
+template <int Z, int MODE, bool INT, bool PV>
 __device__ __forceinline__ void views(const Tile<Z, INT>& t, const Geom& G, const Views& V, const TileGeom& T,
                                       const TileIO& io, int grp, int lane, int warp, int NW, int i0, int j0, int BL,
                                       double& red_a, double& red_b, double& red_c) {
@@ -579,13 +594,15 @@ __device__ __forceinline__ void views(const Tile<Z, INT>& t, const Geom& G, cons
   const int kend = min(G.n_views, kbeg + T.vpg);
   for (int k = kbeg + warp; k < kend; k += NW) {
     const int ks[1] = {k};
-    view_pass<Z, MODE, INT, 1>(t, G, V, io, ks, lane, i0, j0, BL, red_a, red_b, red_c);
+    view_pass<Z, MODE, INT, 1, PV>(t, G, V, io, ks, lane, i0, j0, BL, red_a, red_b, red_c);
   }
 }
 
 // FIXBL: the tile height is the compile-time default TC<Z>::BL (the launcher picks this
 // instantiation whenever T.BL equals it: constant loop bounds, ~1.5 % faster at C3).
-template <int Z, int MODE, bool FIXBL>
+// PV: per-view disparity maps omega_k read from global memory (A34); a compile-time
+// switch because even a warp-uniform runtime test cost the shared-map path ~12 %.
+template <int Z, int MODE, bool FIXBL, bool PV>
 __global__ void __launch_bounds__(LaunchCfg<Z>::MAXW * 32, LaunchCfg<Z>::MINB)
 k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
   using C = TC<Z>;
@@ -703,6 +720,7 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
       ACC[LO + i] = 0;
     }
   }
+  if (!PV)
   for (int e = tid; e < EY * ECOL; e += NT) {   // 0 outside the image (the dummy rows rely on it)
     const int er = e / ECOL, c = e - er * ECOL;
     const int Y = YE0 + er, X = XE0 + c;
@@ -801,9 +819,9 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
         }
       }
       tile.P = P; tile.ACC = ACC; tile.OM = OM; tile.PW = PW; tile.PWZ = PWZ; tile.PY0 = PY0; tile.PX0 = PX0;
-      tile.YE0 = YE0; tile.XE0 = XE0; tile.H = H; tile.W = W; tile.tscale = s_scale[0]; tile.lo = LO;
+      tile.YE0 = YE0; tile.XE0 = XE0; tile.H = H; tile.W = W; tile.PS = ps; tile.tscale = s_scale[0]; tile.lo = LO;
       tile.koff = koff; tile.rows_in = rows_in;
-      views<Z, MODE, decltype(tile)::kInt>(tile, G, V, T, io, grp, lane, warp, NW, i0, j0, BL, red_a, red_b, red_c);
+      views<Z, MODE, decltype(tile)::kInt, PV>(tile, G, V, T, io, grp, lane, warp, NW, i0, j0, BL, red_a, red_b, red_c);
     };
     if (cols_in && rows_in) run(Tile<Z, true>{});   // (columns-only interior: measured slower)
     else run(Tile<Z, false>{});
@@ -897,14 +915,15 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
 // Per-zeta host entry points (instantiated once per zeta in tile_z<zeta>.cu).
 template <int Z>
 struct TileZ {
-  template <int MODE, bool F>
+  template <int MODE, bool F, bool PV>
   static cudaError_t launch1(const Geom& G, const Views& V, const TileGeom& T, const TileIO& io, cudaStream_t st) {
-    k_tile<Z, MODE, F><<<T.ntYl * T.ntX * T.groups, T.nwarps * 32, T.smem, st>>>(G, V, T, io);
+    k_tile<Z, MODE, F, PV><<<T.ntYl * T.ntX * T.groups, T.nwarps * 32, T.smem, st>>>(G, V, T, io);
     return cudaGetLastError();
   }
   template <int MODE>
   static cudaError_t launchm(const Geom& G, const Views& V, const TileGeom& T, const TileIO& io, cudaStream_t st) {
-    return T.BL == TC<Z>::BL ? launch1<MODE, true>(G, V, T, io, st) : launch1<MODE, false>(G, V, T, io, st);
+    if (G.per_view) return launch1<MODE, false, true>(G, V, T, io, st);   // per-view maps: no fixed-height instance
+    return T.BL == TC<Z>::BL ? launch1<MODE, true, false>(G, V, T, io, st) : launch1<MODE, false, false>(G, V, T, io, st);
   }
   static cudaError_t launch(int mode, const Geom& G, const Views& V, const TileGeom& T, const TileIO& io,
                            cudaStream_t st) {
@@ -913,31 +932,39 @@ struct TileZ {
       case MODE_NORMAL: return launchm<MODE_NORMAL>(G, V, T, io, st);
       case MODE_A: return launchm<MODE_A>(G, V, T, io, st);
       case MODE_AT: return launchm<MODE_AT>(G, V, T, io, st);
-      case MODE_GRAD: return launch1<MODE_GRAD, false>(G, V, T, io, st);   // gd: no fixed-height instance
-      case MODE_J: return launch1<MODE_J, false>(G, V, T, io, st);
+      // gd: no fixed-height instance
+      case MODE_GRAD: return G.per_view ? launch1<MODE_GRAD, false, true>(G, V, T, io, st)
+                                        : launch1<MODE_GRAD, false, false>(G, V, T, io, st);
+      case MODE_J: return G.per_view ? launch1<MODE_J, false, true>(G, V, T, io, st)
+                                     : launch1<MODE_J, false, false>(G, V, T, io, st);
     }
     return cudaErrorInvalidValue;
   }
-  template <int MODE, bool F>
+  template <int MODE, bool F, bool PV>
   static cudaError_t prep1(size_t smem) {
-    return cudaFuncSetAttribute(k_tile<Z, MODE, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    return cudaFuncSetAttribute(k_tile<Z, MODE, F, PV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  }
+  template <int MODE>
+  static cudaError_t prep3(size_t smem) {
+    cudaError_t e;
+    if ((e = prep1<MODE, true, false>(smem)) != cudaSuccess) return e;
+    if ((e = prep1<MODE, false, false>(smem)) != cudaSuccess) return e;
+    return prep1<MODE, false, true>(smem);
   }
   static cudaError_t prepare(size_t smem) {
     cudaError_t e;
-    if ((e = prep1<MODE_WZ, true>(smem)) != cudaSuccess) return e;
-    if ((e = prep1<MODE_WZ, false>(smem)) != cudaSuccess) return e;
-    if ((e = prep1<MODE_NORMAL, true>(smem)) != cudaSuccess) return e;
-    if ((e = prep1<MODE_NORMAL, false>(smem)) != cudaSuccess) return e;
-    if ((e = prep1<MODE_A, true>(smem)) != cudaSuccess) return e;
-    if ((e = prep1<MODE_A, false>(smem)) != cudaSuccess) return e;
-    if ((e = prep1<MODE_AT, true>(smem)) != cudaSuccess) return e;
-    if ((e = prep1<MODE_GRAD, false>(smem)) != cudaSuccess) return e;
-    if ((e = prep1<MODE_J, false>(smem)) != cudaSuccess) return e;
-    return prep1<MODE_AT, false>(smem);
+    if ((e = prep3<MODE_WZ>(smem)) != cudaSuccess) return e;
+    if ((e = prep3<MODE_NORMAL>(smem)) != cudaSuccess) return e;
+    if ((e = prep3<MODE_A>(smem)) != cudaSuccess) return e;
+    if ((e = prep3<MODE_AT>(smem)) != cudaSuccess) return e;
+    if ((e = prep1<MODE_GRAD, false, false>(smem)) != cudaSuccess) return e;
+    if ((e = prep1<MODE_GRAD, false, true>(smem)) != cudaSuccess) return e;
+    if ((e = prep1<MODE_J, false, false>(smem)) != cudaSuccess) return e;
+    return prep1<MODE_J, false, true>(smem);
   }
   static int occupancy(int threads, size_t smem) {
     int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_tile<Z, MODE_NORMAL, false>, threads, smem) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_tile<Z, MODE_NORMAL, false, false>, threads, smem) !=
         cudaSuccess) {
       cudaGetLastError();
       return 1;

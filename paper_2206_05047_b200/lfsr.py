@@ -261,7 +261,9 @@ class Solver:
         if len(mems) != 1:
             raise ValueError("all inputs of one call must be either host or device memory")
         mem = mems.pop()
-        s = self.lib.lfsr_set_observations(self._h, ptrs[0][0], ptrs[1][0], ptrs[2][0], 0, ptrs[3][0], mem)
+        # [H][W]: one shared map (LFSR_DISP_SHARED); [n_views][H][W]: omega_k per view (LFSR_DISP_PER_VIEW, A34)
+        disp_mode = 1 if len(tuple(disparity.shape)) == 3 else 0
+        s = self.lib.lfsr_set_observations(self._h, ptrs[0][0], ptrs[1][0], ptrs[2][0], disp_mode, ptrs[3][0], mem)
         self._check(s)
 
     def admm_run(self, n_iters: int, want_stats: bool = True):
