@@ -197,8 +197,10 @@ typedef enum {
   LFSR_OP_ST = 3,
   LFSR_OP_NORMAL = 4,
   LFSR_OP_WEIGHTS = 5,
-  LFSR_OP_GRAD = 6     /* in HR x -> out HR subgradient of J at x with the current m:
+  LFSR_OP_GRAD = 6,    /* in HR x -> out HR subgradient of J at x with the current m:
                           sum_k A_k^T (l1 sgn(e_k) + 2 l2 e_k) + S_w^T sgn(S_w x) (A30) */
+  LFSR_OP_BICUBIC = 7  /* in LR [h][w] -> out HR: the bicubic up-sampling of x0 (A15),
+                          used for the Cb / Cr planes of colour input */
 } lfsr_op;
 LFSR_API lfsr_status lfsr_op_apply(lfsr_ctx* ctx, lfsr_op op, const float* in, float* out, lfsr_mem mem);
 
@@ -244,6 +246,17 @@ LFSR_API lfsr_status lfsr_gd_run(lfsr_ctx* ctx, const lfsr_gd_params* gd, int32_
 
 /* Kernel launches of one gd iteration graph (valid after lfsr_gd_run; 0 before). */
 LFSR_API int32_t lfsr_gd_launches_per_iter(const lfsr_ctx* ctx);
+
+/* Colour input ("solve the cost function for Y color channel while
+ * applying bi-cubic interpolation for Cb and Cr channel"; reading A35): full-range
+ * ITU-R BT.601 on [0, 1] -- Y = 0.299 R + 0.587 G + 0.114 B, Cb = 0.5 + (B - Y)/1.772,
+ * Cr = 0.5 + (R - Y)/1.402 -- and its inverse.  rgb is planar [3][n_pixels]; all
+ * pointers are DEVICE memory of the current device; stream: cudaStream_t or NULL.
+ * Stream-ordered, no ctx.  Errors: INVALID_ARG (NULL or non-device pointers), CUDA. */
+LFSR_API lfsr_status lfsr_rgb_to_ycbcr(const float* rgb, float* y, float* cb, float* cr, size_t n_pixels,
+                                       void* stream);
+LFSR_API lfsr_status lfsr_ycbcr_to_rgb(const float* y, const float* cb, const float* cr, float* rgb,
+                                       size_t n_pixels, void* stream);
 
 /* Number of kernel launches one ADMM iteration issues (for the bench's
  * gpu_launches count).  Valid after set_observations; 0 otherwise. */

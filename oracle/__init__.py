@@ -95,6 +95,8 @@ def lib():
             "or_admm": (I, [P, D, D, D, D, I, D, D, D, D, ctypes.POINTER(_Stats)]),
             "or_cost": (ctypes.c_double, [P, D, D, D, D, D, D]),
             "or_gradient": (ctypes.c_double, [P, D, D, D, D, D, D, D]),
+            "or_rgb_to_ycbcr": (None, [ctypes.c_size_t, D, D, D, D]),
+            "or_ycbcr_to_rgb": (None, [ctypes.c_size_t, D, D, D, D]),
             "or_gd": (I, [P, D, D, D, D, I, ctypes.c_double, I, I, ctypes.c_double, D, D,
                           ctypes.POINTER(_GdStats)]),
         }
@@ -370,6 +372,34 @@ def gd(P: Params, y, view_offsets, omega, n_iters: int, step: float, line_search
         raise ValueError("oracle: invalid parameters")
     stats = [{k: getattr(st[i], k) for k in GD_STAT_KEYS} for i in range(n_iters)]
     return GdResult(xs, stats, rc)
+
+
+def rgb_to_ycbcr(rgb):
+    """Planar [3][...] RGB -> (Y, Cb, Cr), full-range BT.601 (reading A35)."""
+    rgb = _d(rgb)
+    shp = rgb.shape[1:]
+    n = int(np.prod(shp))
+    y, cb, cr = np.zeros(shp), np.zeros(shp), np.zeros(shp)
+    lib().or_rgb_to_ycbcr(n, _ptr(rgb), _ptr(y), _ptr(cb), _ptr(cr))
+    return y, cb, cr
+
+
+def ycbcr_to_rgb(y, cb, cr):
+    y, cb, cr = _d(y), _d(cb), _d(cr)
+    out = np.zeros((3,) + y.shape)
+    lib().or_ycbcr_to_rgb(int(y.size), _ptr(y), _ptr(cb), _ptr(cr), _ptr(out))
+    return out
+
+
+def color_sr(P: Params, lr_rgb, view_offsets, omega, n_iters: int):
+    """The paper's colour strategy: ADMM on the Y channel of the views, bicubic
+    up-sampling of the reference view's Cb and Cr, back to RGB.
+    lr_rgb: [n_views][3][h][w].  Returns planar [3][H][W]."""
+    lr_rgb = _d(lr_rgb)
+    ys = np.stack([rgb_to_ycbcr(v)[0] for v in lr_rgb])
+    _, cb, cr = rgb_to_ycbcr(lr_rgb[P.ref_view])
+    xY = admm(P, ys, view_offsets, omega, n_iters).x_iters[-1]
+    return ycbcr_to_rgb(xY, bicubic(cb, P.scale), bicubic(cr, P.scale))
 
 
 def psnr(x, gt, crop: int = 8) -> float:

@@ -736,3 +736,29 @@ int or_gd(const or_params* P, const double* y, const double* view_offsets, const
   free(x); free(xt); free(g); free(wo); free(m);
   return status;
 }
+
+/* ---------------------------------------------------------------------------
+ * Colour input ("solve the cost function for Y color channel while
+ * applying bi-cubic interpolation for Cb and Cr channel"), reading A35: full-range
+ * ITU-R BT.601 YCbCr on [0, 1]:
+ *   Y = 0.299 R + 0.587 G + 0.114 B,  Cb = 0.5 + (B - Y)/1.772,  Cr = 0.5 + (R - Y)/1.402
+ * and its inverse.  Planar [3][n] RGB.  (Pinned: P23, tests/test_oracle_color.py.)
+ * ------------------------------------------------------------------------- */
+void or_rgb_to_ycbcr(size_t n, const double* rgb, double* y, double* cb, double* cr) {
+  for (size_t i = 0; i < n; ++i) {
+    double r = rgb[i], g = rgb[n + i], b = rgb[2 * n + i];
+    y[i] = 0.299 * r + 0.587 * g + 0.114 * b;
+    cb[i] = 0.5 + (b - y[i]) / 1.772;
+    cr[i] = 0.5 + (r - y[i]) / 1.402;
+  }
+}
+
+void or_ycbcr_to_rgb(size_t n, const double* y, const double* cb, const double* cr, double* rgb) {
+  for (size_t i = 0; i < n; ++i) {
+    double r = y[i] + 1.402 * (cr[i] - 0.5);
+    double b = y[i] + 1.772 * (cb[i] - 0.5);
+    rgb[i] = r;
+    rgb[n + i] = (y[i] - 0.299 * r - 0.114 * b) / 0.587;
+    rgb[2 * n + i] = b;
+  }
+}

@@ -1,5 +1,6 @@
 // aux_kernels.cu — setup, CG update and test-operator kernels of liblfsr.
 #include "internal.h"
+#include <algorithm>
 #include <cfloat>
 
 namespace lfsr {
@@ -429,6 +430,37 @@ cudaError_t launch_gd_update(const Geom& G, float* x, const float* g, Control* c
   if (blocks > num_sms * 4) blocks = num_sms * 4;
   if (blocks < 1) blocks = 1;
   k_gd_update<<<blocks, 256, 0, st>>>(G, x, g, ctl, cfg);
+  return cudaGetLastError();
+}
+// Colour handling of the paper's experiments ("solve the cost function
+// for Y color channel while applying bi-cubic interpolation for Cb and Cr"): full-range
+// ITU-R BT.601 YCbCr on [0, 1] (reading A35).  Planar fp32, n pixels per plane.
+__global__ void k_rgb_to_ycbcr(const float* __restrict__ rgb, float* __restrict__ y, float* __restrict__ cb,
+                               float* __restrict__ cr, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const float r = rgb[i], g = rgb[n + i], b = rgb[2 * n + i];
+    const float yy = 0.299f * r + 0.587f * g + 0.114f * b;
+    y[i] = yy;
+    cb[i] = 0.5f + (b - yy) * (1.f / 1.772f);
+    cr[i] = 0.5f + (r - yy) * (1.f / 1.402f);
+  }
+}
+__global__ void k_ycbcr_to_rgb(const float* __restrict__ y, const float* __restrict__ cb,
+                               const float* __restrict__ cr, float* __restrict__ rgb, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const float yy = y[i], u = cb[i] - 0.5f, v = cr[i] - 0.5f;
+    const float r = yy + 1.402f * v, b = yy + 1.772f * u;
+    rgb[i] = r;
+    rgb[n + i] = (yy - 0.299f * r - 0.114f * b) * (1.f / 0.587f);
+    rgb[2 * n + i] = b;
+  }
+}
+cudaError_t launch_color(int to_ycbcr, const float* a, float* y, float* cb, float* cr, size_t n, int num_sms,
+                         cudaStream_t st) {
+  int blocks = (int)std::min<size_t>((n + 255) / 256, (size_t)num_sms * 8);
+  if (blocks < 1) blocks = 1;
+  if (to_ycbcr) k_rgb_to_ycbcr<<<blocks, 256, 0, st>>>(a, y, cb, cr, n);
+  else k_ycbcr_to_rgb<<<blocks, 256, 0, st>>>(y, cb, cr, const_cast<float*>(a), n);
   return cudaGetLastError();
 }
 cudaError_t launch_close(const Geom& G, Control* ctl, cudaStream_t st) {

@@ -39,6 +39,8 @@ cudaError_t launch_apply_ST(const Geom& G, const float* h, const float* m, float
 cudaError_t launch_fold_rows(float* dst, float* src, size_t n, int zero_src, cudaStream_t st);
 cudaError_t launch_allreduce_local(Control* const* ctls, int nparts, int slot0, int count, cudaStream_t st);
 cudaError_t launch_gd_gnorm(const Geom& G, const float* g, Control* ctl, int num_sms, cudaStream_t st);
+cudaError_t launch_color(int to_ycbcr, const float* a, float* y, float* cb, float* cr, size_t n, int num_sms,
+                         cudaStream_t st);
 cudaError_t launch_gd_update(const Geom& G, float* x, const float* g, Control* ctl, const GdCfg& cfg, int num_sms,
                              cudaStream_t st);
 }  // namespace lfsr
@@ -271,6 +273,34 @@ static lfsr_status make_plan(const Geom& G, int n_ranks, int max_shift_rows, std
 extern "C" {
 
 int32_t lfsr_abi_version(void) { return LFSR_ABI_VERSION; }
+
+// Colour conversion (reading A35), device arrays, stream-ordered.
+static lfsr_status color_call(int to_ycbcr, const float* rgb, float* y, float* cb, float* cr, size_t n_pixels,
+                              void* stream) {
+  if (!rgb || !y || !cb || !cr) return LFSR_ERR_INVALID_ARG;
+  if (n_pixels == 0) return LFSR_OK;
+  for (const void* p : {(const void*)rgb, (const void*)y, (const void*)cb, (const void*)cr}) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess || a.type != cudaMemoryTypeDevice) {
+      cudaGetLastError();
+      return LFSR_ERR_INVALID_ARG;
+    }
+  }
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (launch_color(to_ycbcr, rgb, y, cb, cr, n_pixels, sms, (cudaStream_t)stream) != cudaSuccess) {
+    cudaGetLastError();
+    return LFSR_ERR_CUDA;
+  }
+  return LFSR_OK;
+}
+lfsr_status lfsr_rgb_to_ycbcr(const float* rgb, float* y, float* cb, float* cr, size_t n_pixels, void* stream) {
+  return color_call(1, rgb, y, cb, cr, n_pixels, stream);
+}
+lfsr_status lfsr_ycbcr_to_rgb(const float* y, const float* cb, const float* cr, float* rgb, size_t n_pixels,
+                              void* stream) {
+  return color_call(0, rgb, const_cast<float*>(y), const_cast<float*>(cb), const_cast<float*>(cr), n_pixels, stream);
+}
 
 lfsr_status lfsr_strip_plan(const lfsr_params* params, int32_t max_shift_rows, lfsr_strip* out) {
   if (const char* why = validate(params)) {
@@ -1482,6 +1512,13 @@ lfsr_status lfsr_op_apply(lfsr_ctx* c, lfsr_op op, const float* in, float* out, 
       io.out_hr = c->tmp_hr2;
       io.reweight = 0;   // the current weight map m
       CK(c, launch_tile(MODE_GRAD, G, c->V, T, io, s));
+      CK(c, get2d(c, out, G.W, c->tmp_hr2, G.ps, (size_t)G.H, mem));
+      break;
+    }
+    case LFSR_OP_BICUBIC: {   // through the ref-view slot of the LR scratch (k_bicubic reads that view)
+      float* slot = S.tmp_lr + (size_t)G.ref_view * G.h * G.lps;
+      CK(c, put2d(c, slot, G.lps, in, G.w, (size_t)G.h, mem));
+      CK(c, launch_bicubic(G, S.tmp_lr, c->tmp_hr2, s));
       CK(c, get2d(c, out, G.W, c->tmp_hr2, G.ps, (size_t)G.H, mem));
       break;
     }

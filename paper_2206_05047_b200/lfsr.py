@@ -25,14 +25,15 @@ LFSR_OK, LFSR_ERR_INVALID_ARG, LFSR_ERR_STATE, LFSR_ERR_OOM, LFSR_ERR_CUDA, LFSR
     LFSR_ERR_DIVERGED, LFSR_ERR_UNSUPPORTED = range(8)
 STATUS_NAMES = ["OK", "INVALID_ARG", "STATE", "OOM", "CUDA", "NCCL", "DIVERGED", "UNSUPPORTED"]
 MEM_HOST, MEM_DEVICE = 0, 1
-OP_A, OP_AT, OP_S, OP_ST, OP_NORMAL, OP_WEIGHTS, OP_GRAD = range(7)
-OPS = {"A": OP_A, "AT": OP_AT, "S": OP_S, "ST": OP_ST, "NORMAL": OP_NORMAL, "WEIGHTS": OP_WEIGHTS, "GRAD": OP_GRAD}
+OP_A, OP_AT, OP_S, OP_ST, OP_NORMAL, OP_WEIGHTS, OP_GRAD, OP_BICUBIC = range(8)
+OPS = {"A": OP_A, "AT": OP_AT, "S": OP_S, "ST": OP_ST, "NORMAL": OP_NORMAL, "WEIGHTS": OP_WEIGHTS, "GRAD": OP_GRAD,
+       "BICUBIC": OP_BICUBIC}
 
 # every symbol include/lfsr.h declares (checked by tests/test_abi.py)
 EXPORTS = ("lfsr_create", "lfsr_set_observations", "lfsr_admm_run", "lfsr_admm_enqueue", "lfsr_admm_stats",
            "lfsr_get_hr", "lfsr_get_state", "lfsr_op_apply", "lfsr_launches_per_iter", "lfsr_tile_config", "lfsr_profile",
            "lfsr_profile_read", "lfsr_strip_plan", "lfsr_destroy", "lfsr_last_error", "lfsr_abi_version",
-           "lfsr_gd_run", "lfsr_gd_launches_per_iter")
+           "lfsr_gd_run", "lfsr_gd_launches_per_iter", "lfsr_rgb_to_ycbcr", "lfsr_ycbcr_to_rgb")
 
 
 class LFSRError(RuntimeError):
@@ -135,6 +136,10 @@ def load_library(path: str = LIB_PATH):
     lib.lfsr_gd_run.restype = st
     lib.lfsr_gd_launches_per_iter.argtypes = [vp]
     lib.lfsr_gd_launches_per_iter.restype = ctypes.c_int32
+    lib.lfsr_rgb_to_ycbcr.argtypes = [vp, vp, vp, vp, ctypes.c_size_t, vp]
+    lib.lfsr_rgb_to_ycbcr.restype = st
+    lib.lfsr_ycbcr_to_rgb.argtypes = [vp, vp, vp, vp, ctypes.c_size_t, vp]
+    lib.lfsr_ycbcr_to_rgb.restype = st
     lib.lfsr_abi_version.argtypes = []
     lib.lfsr_abi_version.restype = ctypes.c_int32
     _lib = lib
@@ -346,7 +351,7 @@ class Solver:
         op = OPS[name]
         out_shape = {OP_A: (p.n_views, p.lr_height, p.lr_width), OP_AT: (p.H, p.W),
                      OP_S: (p.s_d, p.H, p.W), OP_ST: (p.H, p.W), OP_NORMAL: (p.H, p.W),
-                     OP_WEIGHTS: (p.H, p.W), OP_GRAD: (p.H, p.W)}[op]
+                     OP_WEIGHTS: (p.H, p.W), OP_GRAD: (p.H, p.W), OP_BICUBIC: (p.H, p.W)}[op]
         ptr, mem, keep = self._ptr_in(inp)
         if mem == MEM_DEVICE:
             import torch
@@ -403,3 +408,58 @@ def psnr(x, gt, crop: int = 8) -> float:
         x, gt = x[crop:-crop, crop:-crop], gt[crop:-crop, crop:-crop]
     mse = float(np.mean((x - gt) ** 2))
     return math.inf if mse == 0 else 10.0 * math.log10(1.0 / mse)
+
+
+def _color_check(s, what):
+    if s != LFSR_OK:
+        raise LFSRError(s, what)
+
+
+def rgb_to_ycbcr(rgb, stream: int | None = None):
+    """Planar [3][...] fp32 CUDA tensor -> (Y, Cb, Cr) CUDA tensors (lfsr_rgb_to_ycbcr, BT.601, A35)."""
+    import torch
+    assert rgb.is_cuda and rgb.dtype == torch.float32 and rgb.is_contiguous() and rgb.shape[0] == 3
+    y, cb, cr = (torch.empty(rgb.shape[1:], dtype=torch.float32, device=rgb.device) for _ in range(3))
+    st = stream if stream is not None else torch.cuda.current_stream(rgb.device).cuda_stream
+    _color_check(load_library().lfsr_rgb_to_ycbcr(rgb.data_ptr(), y.data_ptr(), cb.data_ptr(), cr.data_ptr(),
+                                                   y.numel(), st), "lfsr_rgb_to_ycbcr")
+    return y, cb, cr
+
+
+def ycbcr_to_rgb(y, cb, cr, stream: int | None = None):
+    import torch
+    for t in (y, cb, cr):
+        assert t.is_cuda and t.dtype == torch.float32 and t.is_contiguous() and t.shape == y.shape
+    rgb = torch.empty((3,) + tuple(y.shape), dtype=torch.float32, device=y.device)
+    st = stream if stream is not None else torch.cuda.current_stream(y.device).cuda_stream
+    _color_check(load_library().lfsr_ycbcr_to_rgb(y.data_ptr(), cb.data_ptr(), cr.data_ptr(), rgb.data_ptr(),
+                                                   y.numel(), st), "lfsr_ycbcr_to_rgb")
+    return rgb
+
+
+def color_super_resolve(params: Params, lr_rgb, view_offsets, disparity, n_iters: int, x0=None):
+    """The paper's colour strategy: ADMM on the Y channel of every view, the
+    bicubic up-sampling (LFSR_OP_BICUBIC) of the reference view's Cb and Cr, back to
+    RGB -- every step in liblfsr kernels.  lr_rgb: [n_views][3][h][w] fp32 CUDA tensor;
+    view_offsets / disparity as for Solver.set_observations (CUDA tensors).  Returns
+    ([3][H][W] CUDA tensor, ADMM stats)."""
+    import torch
+    stream = torch.cuda.current_stream(lr_rgb.device).cuda_stream
+    nv = lr_rgb.shape[0]
+    assert lr_rgb.is_cuda and lr_rgb.dtype == torch.float32 and lr_rgb.is_contiguous() and lr_rgb.shape[1] == 3
+    hw = tuple(lr_rgb.shape[2:])
+    ys = torch.empty((nv,) + hw, dtype=torch.float32, device=lr_rgb.device)
+    cbs = torch.empty((2, nv) + hw, dtype=torch.float32, device=lr_rgb.device)   # Cb, Cr of every view
+    n = ys[0].numel()
+    lib = load_library()
+    for k in range(nv):   # Y straight into the view stack (no copies)
+        _color_check(lib.lfsr_rgb_to_ycbcr(lr_rgb[k].data_ptr(), ys[k].data_ptr(), cbs[0, k].data_ptr(),
+                                           cbs[1, k].data_ptr(), n, stream), "lfsr_rgb_to_ycbcr")
+    chroma = (cbs[0, params.ref_view], cbs[1, params.ref_view])
+    with Solver(params, stream=stream) as s:
+        s.set_observations(ys, view_offsets, disparity, x0)
+        stats = s.admm_run(n_iters)
+        xY = torch.empty((params.H, params.W), dtype=torch.float32, device=lr_rgb.device)
+        s.get_hr(xY)
+        cb_hr, cr_hr = s.op("BICUBIC", chroma[0]), s.op("BICUBIC", chroma[1])
+    return ycbcr_to_rgb(xY, cb_hr, cr_hr, stream), stats
