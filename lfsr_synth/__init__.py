@@ -448,3 +448,17 @@ def per_view_disparity(omega: np.ndarray, n_views: int, amp: float = 0.2, seed: 
         ph = g.uniform(0.0, 2.0 * np.pi)
         out[k] = (omega + amp * np.sin(2.0 * np.pi * (fy * Y + fx * X) + ph)).astype(np.float32)
     return out
+
+
+def motion_psf(length: int, angle_deg: float = 45.0) -> np.ndarray:
+    """Normalised linear motion-blur kernel (the 45-degree motion blur of P:L962), fp32
+    [(2r+1)][(2r+1)] with r = (length-1)//2: a centred segment whose projection on the
+    dominant axis spans `length` pixels, rasterised by dense sampling.  Input generator only."""
+    r = (length - 1) // 2
+    a = np.deg2rad(angle_deg)
+    c, s = np.cos(a), -np.sin(a)          # row axis points down
+    half = (length - 1) / 2.0 / max(abs(c), abs(s))
+    k = np.zeros((2 * r + 1, 2 * r + 1))
+    for t in np.linspace(-half, half, 64 * length):
+        k[int(round(r + t * s)), int(round(r + t * c))] += 1.0
+    return (k / k.sum()).astype(np.float32)

@@ -46,7 +46,8 @@ class _Params(ctypes.Structure):
                 ("sigma_o2", ctypes.c_double), ("theta", ctypes.c_double),
                 ("cg_max_iters", ctypes.c_int32), ("cg_tol", ctypes.c_double),
                 ("reweight_every_iter", ctypes.c_int32),
-                ("offset_weights", ctypes.POINTER(ctypes.c_double)), ("disp_per_view", ctypes.c_int32)]
+                ("offset_weights", ctypes.POINTER(ctypes.c_double)), ("disp_per_view", ctypes.c_int32),
+                ("psf", ctypes.POINTER(ctypes.c_double)), ("psf_radius", ctypes.c_int32)]
 
 
 class _Stats(ctypes.Structure):
@@ -95,6 +96,8 @@ def lib():
             "or_admm": (I, [P, D, D, D, D, I, D, D, D, D, ctypes.POINTER(_Stats)]),
             "or_cost": (ctypes.c_double, [P, D, D, D, D, D, D]),
             "or_gradient": (ctypes.c_double, [P, D, D, D, D, D, D, D]),
+            "or_apply_Bk": (None, [I, I, I, D, D, D]),
+            "or_apply_BkT": (None, [I, I, I, D, D, D]),
             "or_rgb_to_ycbcr": (None, [ctypes.c_size_t, D, D, D, D]),
             "or_ycbcr_to_rgb": (None, [ctypes.c_size_t, D, D, D, D]),
             "or_gd": (I, [P, D, D, D, D, I, ctypes.c_double, I, I, ctypes.c_double, D, D,
@@ -142,6 +145,7 @@ class Params:
     reweight_every_iter: int = 1
     offset_weights: Optional[Sequence[float]] = None   # s_d weights overriding exp(-|d|^2/sigma_s)
     disp_per_view: int = 0      # 1: omega is [n_views][H][W] (view k warped with omega_k, A34)
+    psf: Optional[np.ndarray] = None   # user convolution kernel [(2r+1)][(2r+1)] replacing the Gaussian (A36)
 
     @property
     def H(self):
@@ -161,10 +165,15 @@ class Params:
             self._ow = np.ascontiguousarray(self.offset_weights, dtype=np.float64)   # kept alive with self
             assert self._ow.shape == (self.s_d,), "offset_weights must have s_d entries"
             ow = _ptr(self._ow)
+        kp, kr = None, 0
+        if self.psf is not None:
+            self._psf = np.ascontiguousarray(self.psf, dtype=np.float64)
+            assert self._psf.ndim == 2 and self._psf.shape[0] == self._psf.shape[1] and self._psf.shape[0] % 2 == 1
+            kp, kr = _ptr(self._psf), (self._psf.shape[0] - 1) // 2
         return _Params(self.n_views, self.lr_h, self.lr_w, self.scale, self.ref_view, self.radius,
                        self.lambda1, self.lambda2, self.lambda_reg, self.sigma_s, self.sigma_e,
                        self.sigma_o1, self.sigma_o2, self.theta, self.cg_max_iters, self.cg_tol,
-                       self.reweight_every_iter, ow, int(self.disp_per_view))
+                       self.reweight_every_iter, ow, int(self.disp_per_view), kp, kr)
 
 
 def blur_taps(scale: int) -> np.ndarray:
@@ -203,6 +212,16 @@ def apply_B(x, scale):
     R = (len(taps) - 1) // 2
     out = np.zeros_like(x)
     lib().or_apply_B(H, W, R, _ptr(taps), _ptr(x), _ptr(out))
+    return out
+
+
+def apply_Bk(x, k, transpose: bool = False):
+    """B with a user convolution kernel k (reading A36), or its transpose."""
+    x, k = _d(x), _d(k)
+    H, W = x.shape
+    out = np.zeros_like(x)
+    f = lib().or_apply_BkT if transpose else lib().or_apply_Bk
+    f(H, W, (k.shape[0] - 1) // 2, _ptr(k), _ptr(x), _ptr(out))
     return out
 
 

@@ -34,6 +34,8 @@
  *   or_admm           pinned: l2-only == lstsq (P10), == textbook scaled ADMM with exact
  *                     x-step (P11), convergence to an independent minimiser (P12)
  *   or_gradient       pinned: central finite differences of J (P18), J == or_cost
+ *   or_apply_Bk/BkT   pinned: the Gaussian outer product == or_apply_B, impulse response
+ *                     (convolution orientation), adjoint (P24)
  *   per-view omega    pinned: equal maps == shared mode, view k == shared mode with omega_k,
  *                     adjoint identity (P22)
  *   or_gd             pinned: smooth case with step 1/L decreases J monotonically and reaches the
@@ -63,6 +65,10 @@ typedef struct {
                                                    view (A12); 1: omega [n_views][H][W], view k
                                                    warped with its own omega_k (P:L580-582,
                                                    NEXT-2, reading A34) */
+  const double* psf;                            /* NULL: the Gaussian B (A11); else a user
+                                                   convolution kernel [(2 psf_radius+1)^2]
+                                                   row-major (NEXT-4, reading A36) */
+  int32_t psf_radius;
 } or_params;
 
 /* The disparity map view k is warped with ("for each perspective theta_k, we
@@ -130,6 +136,40 @@ void or_apply_B(int H, int W, int R, const double* taps, const double* x, double
     }
 }
 
+/* B with a user convolution kernel ("the motion blur can be modelled by a
+ * convolutional kernel as a realization of the linear operator B"; reading A36):
+ *   (B x)(Y,X) = sum_{u,v = -Rp..Rp} k[u+Rp][v+Rp] x(Y-u, X-v), zero outside Omega. */
+void or_apply_Bk(int H, int W, int Rp, const double* k, const double* x, double* out) {
+  int n = 2 * Rp + 1;
+#pragma omp parallel for schedule(static)
+  for (int Y = 0; Y < H; ++Y)
+    for (int X = 0; X < W; ++X) {
+      double s = 0.0;
+      for (int u = -Rp; u <= Rp; ++u)
+        for (int v = -Rp; v <= Rp; ++v) {
+          int yy = Y - u, xx = X - v;
+          if (yy >= 0 && yy < H && xx >= 0 && xx < W) s += k[(u + Rp) * n + (v + Rp)] * x[(size_t)yy * W + xx];
+        }
+      out[(size_t)Y * W + X] = s;
+    }
+}
+
+/* Its transpose: (B^T t)(Y,X) = sum_{u,v} k[u+Rp][v+Rp] t(Y+u, X+v) (zero padding). */
+void or_apply_BkT(int H, int W, int Rp, const double* k, const double* t, double* out) {
+  int n = 2 * Rp + 1;
+#pragma omp parallel for schedule(static)
+  for (int Y = 0; Y < H; ++Y)
+    for (int X = 0; X < W; ++X) {
+      double s = 0.0;
+      for (int u = -Rp; u <= Rp; ++u)
+        for (int v = -Rp; v <= Rp; ++v) {
+          int yy = Y + u, xx = X + v;
+          if (yy >= 0 && yy < H && xx >= 0 && xx < W) s += k[(u + Rp) * n + (v + Rp)] * t[(size_t)yy * W + xx];
+        }
+      out[(size_t)Y * W + X] = s;
+    }
+}
+
 /* Bilinear sample point of the warp W_k at HR pixel (Y,X), reading A12/A13:
  * z + dtheta_k * omega(z) with theta = [rho, tau], rho pairs with
  * the column axis X and tau with the row axis Y; the continuous
@@ -192,7 +232,8 @@ void or_apply_A(const or_params* P, const double* view_offsets, const double* om
   double* t2 = (double*)malloc(sizeof(double) * p);
   for (int k = 0; k < P->n_views; ++k) {
     or_apply_W(H, W, x, omega_of(P, omega, k), view_offsets[2 * k], view_offsets[2 * k + 1], t1);
-    or_apply_B(H, W, R, taps, t1, t2);
+    if (P->psf) or_apply_Bk(H, W, P->psf_radius, P->psf, t1, t2);
+    else or_apply_B(H, W, R, taps, t1, t2);
     or_apply_D(H, W, z, t2, out + k * q);
   }
   free(t1);
@@ -212,7 +253,8 @@ void or_apply_AT(const or_params* P, const double* view_offsets, const double* o
   memset(out, 0, sizeof(double) * p);
   for (int k = 0; k < P->n_views; ++k) {
     or_apply_DT(H, W, z, r + k * q, t1);
-    or_apply_B(H, W, R, taps, t1, t2);
+    if (P->psf) or_apply_BkT(H, W, P->psf_radius, P->psf, t1, t2);
+    else or_apply_B(H, W, R, taps, t1, t2);   /* the Gaussian B is self-adjoint (A11) */
     or_apply_WT(H, W, t2, omega_of(P, omega, k), view_offsets[2 * k], view_offsets[2 * k + 1], t3);
     for (size_t i = 0; i < p; ++i) out[i] += t3[i];
   }
@@ -450,6 +492,7 @@ static int validate(const or_params* P) {
   if (!(P->theta > 0) || P->lambda1 < 0 || P->lambda2 < 0 || P->lambda_reg < 0) return OR_ERR_ARG;
   if (P->lambda1 + P->lambda2 <= 0 || P->cg_max_iters < 1 || P->cg_tol < 0) return OR_ERR_ARG;
   if (!(P->sigma_s > 0) || !(P->sigma_e > 0) || !(P->sigma_o1 > 0) || !(P->sigma_o2 > 0)) return OR_ERR_ARG;
+  if (P->psf && (P->psf_radius < 0 || P->psf_radius > 8)) return OR_ERR_ARG;
   if (P->offset_weights) {
     int sd = (2 * P->radius + 1) * (2 * P->radius + 1) - 1;
     for (int d = 0; d < sd; ++d)
