@@ -104,6 +104,12 @@ typedef struct {
                            dx over the window, centre skipped), copied at lfsr_create --
                            e.g. BTV's alpha^(|dx|+|dy|) for the MISR use (P:L404-412,
                            P:L1110-1116).  Host memory.              */
+  const float* psf;     /* NULL: the Gaussian blur of P:L579 (A11).  Else a user blur kernel
+                           k [(2 psf_radius+1)][(2 psf_radius+1)] row-major, finite, host
+                           memory, copied at lfsr_create: (B x)(Y,X) = sum_{u,v} k[u][v]
+                           x(Y-u, X-v), zero padding (P:L962 motion blur, SURVEY 8f NEXT-4,
+                           reading A36).  Not with LFSR_DISP_PER_VIEW (UNSUPPORTED).  */
+  int32_t psf_radius;   /* 0..R(zeta): 2 at zeta = 2, 3 at zeta = 3, 4                 */
 } lfsr_params;
 
 /* Per-ADMM-iteration record.  J terms refer to x^{n-1} and the

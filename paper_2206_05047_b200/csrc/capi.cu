@@ -163,6 +163,13 @@ static const char* validate(const lfsr_params* p) {
       if (!(p->offset_weights[d] >= 0.f) || !std::isfinite(p->offset_weights[d]))
         return "offset_weights must be finite and >= 0";
   }
+  if (p->psf) {
+    const int Rz = p->scale == 2 ? 2 : 3;   // the fused kernel's blur window
+    if (p->psf_radius < 0 || p->psf_radius > Rz) return "psf_radius must be in [0, 2] (scale 2) or [0, 3] (scale 3, 4)";
+    const int n = (2 * p->psf_radius + 1) * (2 * p->psf_radius + 1);
+    for (int i = 0; i < n; ++i)
+      if (!std::isfinite(p->psf[i])) return "psf must be finite";
+  }
   if (p->device < 0) return "device must be >= 0";
   if (p->n_ranks < 1 || p->n_ranks > 1024) return "n_ranks must be in [1, 1024]";
   if (p->n_ranks == 1 && p->rank != 0) return "rank must be 0 when n_ranks == 1";
@@ -218,6 +225,28 @@ static void fill_geom(const lfsr_params& p, Geom& G) {
     gmax = std::fmax(gmax, sp);
   }
   G.gpoly2 = (float)(gmax * gmax * 1.0001);
+  G.ksum = 1.f;
+  if (p.psf) {   // user blur kernel (A36): flip into the E-offset order of the tile kernel
+    G.psf2d = 1;
+    const int rp = p.psf_radius, np_ = 2 * rp + 1;
+    double ks = 0.0, gp = 0.0;
+    for (int u = -rp; u <= rp; ++u)
+      for (int v = -rp; v <= rp; ++v) {
+        const float k = p.psf[(u + rp) * np_ + (v + rp)];
+        G.psf2[R - u][R - v] = k;
+        ks += std::fabs((double)k);
+      }
+    // |B^T D^T rho| <= max over phases of the polyphase |k| sums times max|rho|
+    for (int py = 0; py < p.scale; ++py)
+      for (int px = 0; px < p.scale; ++px) {
+        double sp = 0.0;
+        for (int a = py; a <= 2 * R; a += p.scale)
+          for (int b = px; b <= 2 * R; b += p.scale) sp += std::fabs((double)G.psf2[a][b]);
+        gp = std::fmax(gp, sp);
+      }
+    G.ksum = (float)(ks * 1.0001);
+    G.gpoly2 = (float)(gp * 1.0001);
+  }
   // NLTV offsets U and spatial weights w_d = exp(-|d|^2/sigma_s) (A8, A9)
   int n = 0;
   for (int dy = -p.nltv_radius; dy <= p.nltv_radius; ++dy)
@@ -372,6 +401,8 @@ lfsr_status lfsr_create(const lfsr_params* params, lfsr_ctx** out) {
   }
   fill_geom(c->prm, c->G);
   c->prm.stream = c->stream;
+  c->prm.offset_weights = nullptr;   // consumed into G (the caller keeps ownership)
+  c->prm.psf = nullptr;
   if (params->n_ranks > 1) {
     c->xmode = params->rank < 0 ? X_LOCAL : X_NCCL;
     if (c->xmode == X_NCCL) {
@@ -696,6 +727,8 @@ lfsr_status lfsr_set_observations(lfsr_ctx* c, const float* lr_views, const floa
   if (!c) return LFSR_ERR_INVALID_ARG;
   if (c->poisoned) FAIL(c, LFSR_ERR_STATE, "ctx is poisoned by an earlier CUDA/NCCL error");
   if (disp_mode != LFSR_DISP_SHARED && disp_mode != LFSR_DISP_PER_VIEW) FAIL(c, LFSR_ERR_INVALID_ARG, "unknown disp_mode");
+  if (disp_mode == LFSR_DISP_PER_VIEW && c->G.psf2d)
+    FAIL(c, LFSR_ERR_UNSUPPORTED, "per-view disparity maps with a user blur kernel are not in this build");
   lfsr_status st;
   if ((st = check_ptr(c, lr_views, mem, "lr_views")) != LFSR_OK) return st;
   if ((st = check_ptr(c, view_offsets, mem, "view_offsets")) != LFSR_OK) return st;

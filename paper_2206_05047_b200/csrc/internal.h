@@ -64,6 +64,9 @@ struct Geom {
   int32_t tile_bl;            // LR rows per tile (host-chosen, 0 = the zeta default; see make_tile_geom)
   int32_t tile_g, tile_nw;    // view groups and warps per CTA (host-chosen, 0 = the cost model's choice)
   int32_t per_view;           // 1: omega is [n_views][H][ps], view k warped with omega_k (A34)
+  int32_t psf2d;              // 1: user blur kernel (A36) in psf2 instead of the separable taps
+  float ksum;                 // sum |k| of the blur kernel (1 for the normalised Gaussian): |B w| <= ksum max|w|
+  float psf2[2 * 3 + 1][2 * 3 + 1];   // psf2[a][b] = k[R-a][R-b]: E-offset (correlation) order, zero padded to 2R+1
   float taps[kMaxTaps * 2 + 1];
   float2 tpe[kMaxTaps + 1];   // tap pairs (taps[2v], taps[2v+1]), zero past 2R (packed FP32 operands)
   float2 tpo[kMaxTaps + 1];   // tap pairs (taps[2v+1], taps[2v+2])

@@ -247,11 +247,12 @@ struct Tile : YRoute<!INT && TC<Z>::DUMMY, Z / 2> {
     }
   }
 
-  // W_k then the horizontal blur taps at this lane's LR column, for E row er.
-  __device__ __forceinline__ float fwd_row(int er, int lane, float drho, float dtau, const float* omk,
-                                          const Geom& G) const {
+  // W_k at the lane's zeta E positions of row er, then the row's values at E columns
+  // zeta*lane + v, v < NTAP (the horizontal blur window of the lane's LR column):
+  // own positions, the rest from the next lanes by shuffles.
+  __device__ __forceinline__ void fwd_vals(int er, int lane, float drho, float dtau, const float* omk,
+                                           float (&val)[TC<Z>::NTAP]) const {
     constexpr int NTAP = TC<Z>::NTAP;
-    if (!kDummy && !row_in(er)) return 0.f;    // blur zero padding (A11), warp uniform
     float om[Z], wp[Z];
     load_om(er, lane, om, omk);
     const float Yf = yrow(er);
@@ -278,10 +279,18 @@ struct Tile : YRoute<!INT && TC<Z>::DUMMY, Z / 2> {
       const float top = fmaf(b, p01 - p00, p00), bot = fmaf(b, p11 - p10, p10);
       wp[s] = col_in(s) ? fmaf(a, bot - top, top) : 0.f;
     }
-    float val[NTAP];
 #pragma unroll
     for (int v = 0; v < NTAP; ++v)
       val[v] = (v < Z) ? wp[v % Z] : __shfl_down_sync(0xffffffffu, wp[v % Z], v / Z);
+  }
+
+  // W_k then the horizontal blur taps at this lane's LR column, for E row er.
+  __device__ __forceinline__ float fwd_row(int er, int lane, float drho, float dtau, const float* omk,
+                                          const Geom& G) const {
+    constexpr int NTAP = TC<Z>::NTAP;
+    if (!kDummy && !row_in(er)) return 0.f;    // blur zero padding (A11), warp uniform
+    float val[NTAP];
+    fwd_vals(er, lane, drho, dtau, omk, val);
     float2 h2 = f2s(0.f);
 #pragma unroll
     for (int v = 0; v + 1 < NTAP; v += 2) h2 = __ffma2_rn(tap2(G, v), f2(val[v], val[v + 1]), h2);
@@ -308,12 +317,7 @@ struct Tile : YRoute<!INT && TC<Z>::DUMMY, Z / 2> {
       const float v = __shfl_up_sync(0xffffffffu, t1b, j);
       tv[j] = lane >= j ? v : 0.f;
     }
-    float om[Z];
-    load_om(er, lane, om, omk);
-    const float Yf = yrow(er);
-    const float X0 = (float)(XE0 - PX0 + Z * lane);
-    int i00[Z], i01[Z];
-    float2 w0[Z], w1[Z];   // (row, row + 1) weights times t on the left / right source column
+    float tt[Z];   // the adjoint blur value of each of the lane's zeta positions
 #pragma unroll
     for (int k = 0; k < NP; ++k) {
       const int s = 2 * k;
@@ -323,6 +327,35 @@ struct Tile : YRoute<!INT && TC<Z>::DUMMY, Z / 2> {
         if (Z * j + s + 1 <= R2) t = __ffma2_rn(tap2(G, Z * j + s), f2s(tv[j]), t);
         else if (Z * j + s <= R2) t.x = fmaf(G.taps[Z * j + s], tv[j], t.x);
       }
+      tt[s] = t.x;
+      tt[s + 1] = t.y;
+    }
+    if constexpr (Z & 1) {
+      constexpr int s = Z - 1;
+      float t = 0.f;
+#pragma unroll
+      for (int j = 0; j < NJ; ++j)
+        if (Z * j + s <= R2) t = fmaf(G.taps[Z * j + s], tv[j], t);
+      tt[s] = t;
+    }
+    scatter(er, lane, tt, drho, dtau, omk);
+  }
+
+  // The exact bilinear scatter (W_k^T) of the adjoint blur values tt of the lane's zeta
+  // positions of E row er into the fixed-point accumulator (the row must be inside the
+  // image or a routed dummy row).
+  __device__ __forceinline__ void scatter(int er, int lane, const float (&tt)[Z], float drho, float dtau,
+                                          const float* omk) const {
+    float om[Z];
+    load_om(er, lane, om, omk);
+    const float Yf = yrow(er);
+    const float X0 = (float)(XE0 - PX0 + Z * lane);
+    int i00[Z], i01[Z];
+    float2 w0[Z], w1[Z];   // (row, row + 1) weights times t on the left / right source column
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+      const int s = 2 * k;
+      const float2 t = f2(tt[s], tt[s + 1]);
       int c0[2], c1[2];
       float2 a, b;
       sample2(ypair(Yf, k), X0 + (float)s, f2(om[s], om[s + 1]), drho, dtau, c0, c1, a, b);
@@ -339,10 +372,7 @@ struct Tile : YRoute<!INT && TC<Z>::DUMMY, Z / 2> {
     }
     if constexpr (Z & 1) {
       constexpr int s = Z - 1;
-      float t = 0.f;
-#pragma unroll
-      for (int j = 0; j < NJ; ++j)
-        if (Z * j + s <= R2) t = fmaf(G.taps[Z * j + s], tv[j], t);
+      const float t = tt[s];
       float a, b;
       sample(yone(Yf), X0 + (float)s, om[s], drho, dtau, i00[s], i01[s], a, b);
       const float ts = col_in(s) ? t * tscale : 0.f;
@@ -462,6 +492,53 @@ __device__ __forceinline__ float nltv_pixel(const NltvCtx& c, const Geom& G, int
 // Phase 2 of k_tile: every warp streams whole views through the tile (see header).
 // NV views are processed interleaved row by row (independent dependency chains
 // for the scheduler); the last odd view of a warp takes the NV = 1 path.
+// Per-LR-pixel step after the forward operator value a = A_k x (i, j), returning the
+// value rho whose adjoint the pass accumulates (own LR pixels only).
+template <int MODE>
+__device__ __forceinline__ float lr_epilogue(float a, float y_cur, float wa_cur, size_t lg, const Geom& G,
+                                             const TileIO& io, float& fa, float& fb, float& fc) {
+  const float lam1 = G.lambda1, lam2 = G.lambda2, ith = G.inv_theta;
+  float rho = 0.f;
+  if (MODE == MODE_A) {
+    io.out_lr[lg] = a;
+  } else if (MODE == MODE_NORMAL) {
+    rho = G.cA * a;
+    fa = fmaf(a, a, fa);                                // <p, c_A A^T A p> = c_A |A p|^2
+  } else if (MODE == MODE_WZ) {
+    const float e_ = a - y_cur;                         // e = A_k x - y_k (Alg.1 line 4)
+    const float wa = wa_cur;
+    const float u = lam1 * e_ + wa;                     // u = F x - b' + w (line 5)
+    const float wn = fminf(fmaxf(u, -ith), ith);        // w+ = u - prox(u) = clamp (A5/A6)
+    const float f = 2.f * wn - wa;                      // f = 2w^n - w^{n-1} (line 8)
+    rho = lam2 * e_ + G.cS * lam1 * f;                  // A^T a + (th/2) F^T f, data rows
+    io.wA[lg] = wn;
+    fa += fabsf(e_);
+    fb = fmaf(e_, e_, fb);
+    fc = fmaf(wn - wa, wn - wa, fc);
+  } else if (MODE == MODE_GRAD || MODE == MODE_J) {
+    const float e_ = a - y_cur;                         // e = A_k x - y_k
+    if (MODE == MODE_GRAD) rho = fmaf(2.f * lam2, e_, lam1 * sgnf(e_));   // l1 sgn(e) + 2 l2 e (A30)
+    fa += fabsf(e_);
+    fb = fmaf(e_, e_, fb);
+  }
+  return rho;
+}
+
+template <int MODE>
+__device__ __forceinline__ void pass_reductions(const Geom& G, float fa, float fb, float fc, double& red_a,
+                                                double& red_b, double& red_c) {
+  if (MODE == MODE_NORMAL) red_a += (double)G.cA * (double)fa;
+  if (MODE == MODE_GRAD || MODE == MODE_J) {
+    red_a += (double)fa;
+    red_b += (double)fb;
+  }
+  if (MODE == MODE_WZ) {
+    red_a += (double)fa;
+    red_b += (double)fb;
+    red_c += (double)fc;
+  }
+}
+
 template <int Z, int MODE, bool INT, int NV, bool PV>
 __device__ __forceinline__ void view_pass(const Tile<Z, INT>& t, const Geom& G, const Views& V, const TileIO& io,
                                           const int (&ks)[NV], int lane, int i0, int j0, int BL, double& red_a,
@@ -471,7 +548,6 @@ __device__ __forceinline__ void view_pass(const Tile<Z, INT>& t, const Geom& G, 
   constexpr bool kFwd = (MODE != MODE_AT);
   constexpr bool kAdj = (MODE != MODE_A && MODE != MODE_J);
   constexpr bool kY = (MODE == MODE_WZ || MODE == MODE_GRAD || MODE == MODE_J);   // reads y_k
-  const float lam1 = G.lambda1, lam2 = G.lambda2, ith = G.inv_theta;
   const int j = j0 + lane;
   const bool col_ok = lane < LX && j < G.w;
   float drho[NV], dtau[NV], fr[NV][NTAP], br[NV][NTAP], y_nx[NV], wa_nx[NV];
@@ -521,30 +597,7 @@ __device__ __forceinline__ void view_pass(const Tile<Z, INT>& t, const Geom& G, 
         for (int u = 0; u + 1 < NTAP; u += 2) a2 = __ffma2_rn(tap2(G, u), f2(fr[v][u], fr[v][u + 1]), a2);
         float a = a2.x + a2.y;
         if constexpr (NTAP & 1) a = fmaf(G.taps[NTAP - 1], fr[v][NTAP - 1], a);
-        if (ok) {
-          if (MODE == MODE_A) {
-            io.out_lr[lg] = a;
-          } else if (MODE == MODE_NORMAL) {
-            rho[v] = G.cA * a;
-            fa = fmaf(a, a, fa);                                // <p, c_A A^T A p> = c_A |A p|^2
-          } else if (MODE == MODE_WZ) {
-            const float e_ = a - y_cur;                         // e = A_k x - y_k (Alg.1 line 4)
-            const float wa = wa_cur;
-            const float u = lam1 * e_ + wa;                     // u = F x - b' + w (line 5)
-            const float wn = fminf(fmaxf(u, -ith), ith);        // w+ = u - prox(u) = clamp (A5/A6)
-            const float f = 2.f * wn - wa;                      // f = 2w^n - w^{n-1} (line 8)
-            rho[v] = lam2 * e_ + G.cS * lam1 * f;               // A^T a + (th/2) F^T f, data rows
-            io.wA[lg] = wn;
-            fa += fabsf(e_);
-            fb = fmaf(e_, e_, fb);
-            fc = fmaf(wn - wa, wn - wa, fc);
-          } else if (MODE == MODE_GRAD || MODE == MODE_J) {
-            const float e_ = a - y_cur;                         // e = A_k x - y_k
-            if (MODE == MODE_GRAD) rho[v] = fmaf(2.f * lam2, e_, lam1 * sgnf(e_));   // l1 sgn(e) + 2 l2 e (A30)
-            fa += fabsf(e_);
-            fb = fmaf(e_, e_, fb);
-          }
-        }
+        if (ok) rho[v] = lr_epilogue<MODE>(a, y_cur, wa_cur, lg, G, io, fa, fb, fc);
 #pragma unroll
         for (int u = 0; u < KEEP; ++u) fr[v][u] = fr[v][u + Z];
       } else {
@@ -574,19 +627,124 @@ __device__ __forceinline__ void view_pass(const Tile<Z, INT>& t, const Geom& G, 
 #pragma unroll
       for (int u = 0; u < KEEP; ++u) t.adj_row(Z * BL + u, lane, br[v][u], drho[v], dtau[v], omk[v], G);
   }
-  if (MODE == MODE_NORMAL) red_a += (double)G.cA * (double)fa;
-  if (MODE == MODE_GRAD || MODE == MODE_J) {
-    red_a += (double)fa;
-    red_b += (double)fb;
-  }
-  if (MODE == MODE_WZ) {
-    red_a += (double)fa;
-    red_b += (double)fb;
-    red_c += (double)fc;
-  }
+  pass_reductions<MODE>(G, fa, fb, fc, red_a, red_b, red_c);
 }
 
-template <int Z, int MODE, bool INT, bool PV>
+// The same pass with a user (non-separable) blur kernel (A36), kernel
+// psf2[a][b] in E-offset order.  Forward: every E row's window values (fwd_vals) feed the
+// Q pending LR rows it lies under with that kernel row (sliding accumulators instead of
+// the separable code's ring of horizontally filtered rows).  Adjoint: the last Q LR rows'
+// rho, already shuffled across the NJ LR columns an E column receives from, are kept; each
+// finished E row sums its kernel taps over them and goes to the same scatter.
+template <int Z, int MODE, bool INT>
+__device__ __forceinline__ void view_pass2d(const Tile<Z, INT>& t, const Geom& G, const Views& V, const TileIO& io,
+                                            int k, int lane, int i0, int j0, int BL, double& red_a, double& red_b,
+                                            double& red_c) {
+  using C = TC<Z>;
+  constexpr int LX = C::LX, NTAP = C::NTAP, KEEP = C::KEEP, R2 = 2 * C::R;
+  constexpr int Q = R2 / Z + 1;      // LR rows one E row lies under (and LR columns one E column)
+  constexpr bool kFwd = (MODE != MODE_AT);
+  constexpr bool kAdj = (MODE != MODE_A && MODE != MODE_J);
+  constexpr bool kY = (MODE == MODE_WZ || MODE == MODE_GRAD || MODE == MODE_J);
+  const int j = j0 + lane;
+  const bool col_ok = lane < LX && j < G.w;
+  const float drho = V.off[k].x, dtau = V.off[k].y;
+  const size_t lrow0 = ((size_t)k * G.h) * G.lps + j;
+  float acc[Q], tvh[Q][Q];
+#pragma unroll
+  for (int d = 0; d < Q; ++d) {
+    acc[d] = 0.f;
+#pragma unroll
+    for (int jj = 0; jj < Q; ++jj) tvh[d][jj] = 0.f;
+  }
+  float fa = 0.f, fb = 0.f, fc = 0.f;
+  float y_nx = 0.f, wa_nx = 0.f;
+  if (kY && col_ok && i0 < G.h) {
+    y_nx = io.y[lrow0 + (size_t)i0 * G.lps];
+    if (MODE == MODE_WZ) wa_nx = io.wA[lrow0 + (size_t)i0 * G.lps];
+  }
+  // E row er sits at offset p below the top of the current LR row's window
+  auto feed = [&](int er, int p) {
+    if (!t.kDummy && !t.row_in(er)) return;          // zero padding (A36)
+    float val[NTAP];
+    t.fwd_vals(er, lane, drho, dtau, nullptr, val);
+#pragma unroll
+    for (int d = 0; d < Q; ++d) {
+      const int a = p - Z * d;
+      if (a < 0 || a > R2) continue;
+      float h = acc[d];
+#pragma unroll
+      for (int b = 0; b < NTAP; ++b) h = fmaf(G.psf2[a][b], val[b], h);
+      acc[d] = h;
+    }
+  };
+  // finished E row er at offset uu below the top of the newest LR row in the history
+  auto emit = [&](int er, int uu) {
+    if (!t.kDummy && !t.row_in(er)) return;
+    float tt[Z];
+#pragma unroll
+    for (int s = 0; s < Z; ++s) {
+      float h = 0.f;
+#pragma unroll
+      for (int d = 0; d < Q; ++d) {
+        const int a = Z * d + uu;
+        if (a > R2) continue;
+#pragma unroll
+        for (int jj = 0; jj < Q; ++jj)
+          if (Z * jj + s <= R2) h = fmaf(G.psf2[a][Z * jj + s], tvh[d][jj], h);
+      }
+      tt[s] = h;
+    }
+    t.scatter(er, lane, tt, drho, dtau, nullptr);
+  };
+  if (kFwd) {
+#pragma unroll
+    for (int u = 0; u < KEEP; ++u) feed(u, u);
+  }
+  for (int li = 0; li < BL; ++li) {
+    const int i = i0 + li;
+    const bool ok = col_ok && i < G.h;
+    const size_t lg = lrow0 + (size_t)i * G.lps;
+    const float y_cur = y_nx, wa_cur = wa_nx;
+    if (kY && col_ok && li + 1 < BL && i + 1 < G.h) {
+      y_nx = io.y[lg + G.lps];
+      if (MODE == MODE_WZ) wa_nx = io.wA[lg + G.lps];
+    }
+    float rho = 0.f;
+    if (kFwd) {
+#pragma unroll
+      for (int u = 0; u < Z; ++u) feed(Z * li + KEEP + u, KEEP + u);
+      const float a = acc[0];                                   // A_k x at LR pixel (i, j)
+#pragma unroll
+      for (int d = 0; d + 1 < Q; ++d) acc[d] = acc[d + 1];
+      acc[Q - 1] = 0.f;
+      if (ok) rho = lr_epilogue<MODE>(a, y_cur, wa_cur, lg, G, io, fa, fb, fc);
+    } else {
+      rho = ok ? io.in_lr[lg] : 0.f;
+    }
+    if (kAdj) {
+#pragma unroll
+      for (int d = Q - 1; d > 0; --d)
+#pragma unroll
+        for (int jj = 0; jj < Q; ++jj) tvh[d][jj] = tvh[d - 1][jj];
+      tvh[0][0] = rho;
+#pragma unroll
+      for (int jj = 1; jj < Q; ++jj) {
+        const float v = __shfl_up_sync(0xffffffffu, rho, jj);
+        tvh[0][jj] = lane >= jj ? v : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < Z; ++u) emit(Z * li + u, u);
+    }
+  }
+  if (kAdj) {
+#pragma unroll
+    for (int u = 0; u < KEEP; ++u) emit(Z * BL + u, Z + u);
+  }
+  pass_reductions<MODE>(G, fa, fb, fc, red_a, red_b, red_c);
+}
+
+template <int Z, int MODE, bool INT, bool PV, bool P2>
 __device__ __forceinline__ void views(const Tile<Z, INT>& t, const Geom& G, const Views& V, const TileGeom& T,
                                       const TileIO& io, int grp, int lane, int warp, int NW, int i0, int j0, int BL,
                                       double& red_a, double& red_b, double& red_c) {
@@ -594,7 +752,8 @@ __device__ __forceinline__ void views(const Tile<Z, INT>& t, const Geom& G, cons
   const int kend = min(G.n_views, kbeg + T.vpg);
   for (int k = kbeg + warp; k < kend; k += NW) {
     const int ks[1] = {k};
-    view_pass<Z, MODE, INT, 1, PV>(t, G, V, io, ks, lane, i0, j0, BL, red_a, red_b, red_c);
+    if constexpr (P2) view_pass2d<Z, MODE, INT>(t, G, V, io, k, lane, i0, j0, BL, red_a, red_b, red_c);
+    else view_pass<Z, MODE, INT, 1, PV>(t, G, V, io, ks, lane, i0, j0, BL, red_a, red_b, red_c);
   }
 }
 
@@ -602,7 +761,8 @@ __device__ __forceinline__ void views(const Tile<Z, INT>& t, const Geom& G, cons
 // instantiation whenever T.BL equals it: constant loop bounds, ~1.5 % faster at C3).
 // PV: per-view disparity maps omega_k read from global memory (A34); a compile-time
 // switch because even a warp-uniform runtime test cost the shared-map path ~12 %.
-template <int Z, int MODE, bool FIXBL, bool PV>
+// P2: user (non-separable) blur kernel (A36, view_pass2d).
+template <int Z, int MODE, bool FIXBL, bool PV, bool P2>
 __global__ void __launch_bounds__(LaunchCfg<Z>::MAXW * 32, LaunchCfg<Z>::MINB)
 k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
   using C = TC<Z>;
@@ -748,10 +908,10 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
   __syncthreads();
   if (tid == 0) {
     float tb = 0.f;
-    if (MODE == MODE_NORMAL) tb = G.cA * s_max;
-    if (MODE == MODE_WZ) tb = G.lambda2 * (s_max + G.ymax) + G.cS * G.lambda1 * 3.f * G.inv_theta;
+    if (MODE == MODE_NORMAL) tb = G.cA * (P2 ? G.ksum * s_max : s_max);
+    if (MODE == MODE_WZ) tb = G.lambda2 * ((P2 ? G.ksum * s_max : s_max) + G.ymax) + G.cS * G.lambda1 * 3.f * G.inv_theta;
     if (MODE == MODE_AT) tb = io.tmax_in;
-    if (MODE == MODE_GRAD) tb = G.lambda1 + 2.f * G.lambda2 * (s_max + G.ymax);   // |l1 sgn(e) + 2 l2 e|
+    if (MODE == MODE_GRAD) tb = G.lambda1 + 2.f * G.lambda2 * ((P2 ? G.ksum * s_max : s_max) + G.ymax);   // |l1 sgn(e) + 2 l2 e|
     tb *= G.gpoly2;   // the polyphase adjoint blur shrinks max|rho|
     float sc = 0.f, isc = 0.f;
     if (tb > 0.f && isfinite(tb)) {
@@ -821,7 +981,7 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
       tile.P = P; tile.ACC = ACC; tile.OM = OM; tile.PW = PW; tile.PWZ = PWZ; tile.PY0 = PY0; tile.PX0 = PX0;
       tile.YE0 = YE0; tile.XE0 = XE0; tile.H = H; tile.W = W; tile.PS = ps; tile.tscale = s_scale[0]; tile.lo = LO;
       tile.koff = koff; tile.rows_in = rows_in;
-      views<Z, MODE, decltype(tile)::kInt, PV>(tile, G, V, T, io, grp, lane, warp, NW, i0, j0, BL, red_a, red_b, red_c);
+      views<Z, MODE, decltype(tile)::kInt, PV, P2>(tile, G, V, T, io, grp, lane, warp, NW, i0, j0, BL, red_a, red_b, red_c);
     };
     if (cols_in && rows_in) run(Tile<Z, true>{});   // (columns-only interior: measured slower)
     else run(Tile<Z, false>{});
@@ -913,17 +1073,22 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
 }
 
 // Per-zeta host entry points (instantiated once per zeta in tile_z<zeta>.cu).
+// Instances: (fixed-height | runtime height) x shared map for every mode; runtime height
+// only for per-view maps (PV) and for a user blur kernel (P2).
 template <int Z>
 struct TileZ {
-  template <int MODE, bool F, bool PV>
+  template <int MODE, bool F, bool PV, bool P2>
   static cudaError_t launch1(const Geom& G, const Views& V, const TileGeom& T, const TileIO& io, cudaStream_t st) {
-    k_tile<Z, MODE, F, PV><<<T.ntYl * T.ntX * T.groups, T.nwarps * 32, T.smem, st>>>(G, V, T, io);
+    k_tile<Z, MODE, F, PV, P2><<<T.ntYl * T.ntX * T.groups, T.nwarps * 32, T.smem, st>>>(G, V, T, io);
     return cudaGetLastError();
   }
   template <int MODE>
   static cudaError_t launchm(const Geom& G, const Views& V, const TileGeom& T, const TileIO& io, cudaStream_t st) {
-    if (G.per_view) return launch1<MODE, false, true>(G, V, T, io, st);   // per-view maps: no fixed-height instance
-    return T.BL == TC<Z>::BL ? launch1<MODE, true, false>(G, V, T, io, st) : launch1<MODE, false, false>(G, V, T, io, st);
+    if (G.psf2d) return launch1<MODE, false, false, true>(G, V, T, io, st);
+    if (G.per_view) return launch1<MODE, false, true, false>(G, V, T, io, st);
+    if (MODE == MODE_GRAD || MODE == MODE_J) return launch1<MODE, false, false, false>(G, V, T, io, st);
+    return T.BL == TC<Z>::BL ? launch1<MODE, true, false, false>(G, V, T, io, st)
+                             : launch1<MODE, false, false, false>(G, V, T, io, st);
   }
   static cudaError_t launch(int mode, const Geom& G, const Views& V, const TileGeom& T, const TileIO& io,
                            cudaStream_t st) {
@@ -932,40 +1097,37 @@ struct TileZ {
       case MODE_NORMAL: return launchm<MODE_NORMAL>(G, V, T, io, st);
       case MODE_A: return launchm<MODE_A>(G, V, T, io, st);
       case MODE_AT: return launchm<MODE_AT>(G, V, T, io, st);
-      // gd: no fixed-height instance
-      case MODE_GRAD: return G.per_view ? launch1<MODE_GRAD, false, true>(G, V, T, io, st)
-                                        : launch1<MODE_GRAD, false, false>(G, V, T, io, st);
-      case MODE_J: return G.per_view ? launch1<MODE_J, false, true>(G, V, T, io, st)
-                                     : launch1<MODE_J, false, false>(G, V, T, io, st);
+      case MODE_GRAD: return launchm<MODE_GRAD>(G, V, T, io, st);
+      case MODE_J: return launchm<MODE_J>(G, V, T, io, st);
     }
     return cudaErrorInvalidValue;
   }
-  template <int MODE, bool F, bool PV>
+  template <int MODE, bool F, bool PV, bool P2>
   static cudaError_t prep1(size_t smem) {
-    return cudaFuncSetAttribute(k_tile<Z, MODE, F, PV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    return cudaFuncSetAttribute(k_tile<Z, MODE, F, PV, P2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   }
   template <int MODE>
-  static cudaError_t prep3(size_t smem) {
+  static cudaError_t prepm(size_t smem) {
     cudaError_t e;
-    if ((e = prep1<MODE, true, false>(smem)) != cudaSuccess) return e;
-    if ((e = prep1<MODE, false, false>(smem)) != cudaSuccess) return e;
-    return prep1<MODE, false, true>(smem);
+    if (MODE != MODE_GRAD && MODE != MODE_J)
+      if ((e = prep1<MODE, true, false, false>(smem)) != cudaSuccess) return e;
+    if ((e = prep1<MODE, false, false, false>(smem)) != cudaSuccess) return e;
+    if ((e = prep1<MODE, false, true, false>(smem)) != cudaSuccess) return e;
+    return prep1<MODE, false, false, true>(smem);
   }
   static cudaError_t prepare(size_t smem) {
     cudaError_t e;
-    if ((e = prep3<MODE_WZ>(smem)) != cudaSuccess) return e;
-    if ((e = prep3<MODE_NORMAL>(smem)) != cudaSuccess) return e;
-    if ((e = prep3<MODE_A>(smem)) != cudaSuccess) return e;
-    if ((e = prep3<MODE_AT>(smem)) != cudaSuccess) return e;
-    if ((e = prep1<MODE_GRAD, false, false>(smem)) != cudaSuccess) return e;
-    if ((e = prep1<MODE_GRAD, false, true>(smem)) != cudaSuccess) return e;
-    if ((e = prep1<MODE_J, false, false>(smem)) != cudaSuccess) return e;
-    return prep1<MODE_J, false, true>(smem);
+    if ((e = prepm<MODE_WZ>(smem)) != cudaSuccess) return e;
+    if ((e = prepm<MODE_NORMAL>(smem)) != cudaSuccess) return e;
+    if ((e = prepm<MODE_A>(smem)) != cudaSuccess) return e;
+    if ((e = prepm<MODE_AT>(smem)) != cudaSuccess) return e;
+    if ((e = prepm<MODE_GRAD>(smem)) != cudaSuccess) return e;
+    return prepm<MODE_J>(smem);
   }
   static int occupancy(int threads, size_t smem) {
     int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_tile<Z, MODE_NORMAL, false, false>, threads, smem) !=
-        cudaSuccess) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_tile<Z, MODE_NORMAL, false, false, false>, threads,
+                                                      smem) != cudaSuccess) {
       cudaGetLastError();
       return 1;
     }

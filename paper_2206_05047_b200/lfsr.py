@@ -51,7 +51,8 @@ class _CParams(ctypes.Structure):
                 ("sigma_o2", ctypes.c_float), ("theta", ctypes.c_float), ("cg_max_iters", ctypes.c_int32),
                 ("cg_tol", ctypes.c_float), ("reweight_every_iter", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("rank", ctypes.c_int32), ("n_ranks", ctypes.c_int32), ("nccl_unique_id", ctypes.c_void_p),
-                ("stream", ctypes.c_void_p), ("offset_weights", ctypes.POINTER(ctypes.c_float))]
+                ("stream", ctypes.c_void_p), ("offset_weights", ctypes.POINTER(ctypes.c_float)),
+                ("psf", ctypes.POINTER(ctypes.c_float)), ("psf_radius", ctypes.c_int32)]
 
 
 class _CStats(ctypes.Structure):
@@ -171,6 +172,7 @@ class Params:
     rank: int = 0             # this process's strip (NCCL mode) or -1: all strips in this ctx
     nccl_unique_id: bytes | None = None
     offset_weights: object = None   # s_d floats (e.g. BTV alpha^(|dx|+|dy|)) replacing exp(-|d|^2/sigma_s)
+    psf: object = None              # user blur kernel [(2r+1)][(2r+1)] replacing the Gaussian (A36)
 
     @property
     def H(self):
@@ -187,7 +189,7 @@ class Params:
     def to_c(self, stream=None) -> _CParams:
         c = _CParams()
         for f in fields(self):
-            if f.name not in ("nccl_unique_id", "offset_weights"):
+            if f.name not in ("nccl_unique_id", "offset_weights", "psf"):
                 setattr(c, f.name, getattr(self, f.name))
         self._ow = None
         if self.offset_weights is not None:
@@ -196,6 +198,14 @@ class Params:
                 raise LFSRError(1, "offset_weights must have s_d = %d entries" % self.s_d)
             self._ow = (ctypes.c_float * len(ow))(*ow)   # copied by lfsr_create
             c.offset_weights = ctypes.cast(self._ow, ctypes.POINTER(ctypes.c_float))
+        self._psf = None
+        if self.psf is not None:
+            k = np.ascontiguousarray(self.psf, dtype=np.float32)
+            if k.ndim != 2 or k.shape[0] != k.shape[1] or k.shape[0] % 2 != 1:
+                raise LFSRError(1, "psf must be a square kernel of odd size")
+            self._psf = k   # copied by lfsr_create
+            c.psf = k.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
+            c.psf_radius = (k.shape[0] - 1) // 2
         self._uid = None
         if self.nccl_unique_id is not None:
             self._uid = ctypes.create_string_buffer(bytes(self.nccl_unique_id), 128)

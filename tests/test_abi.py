@@ -2,6 +2,9 @@
 symbol include/lfsr.h declares, validates parameters before touching a device, and
 fails loudly (LFSR_ERR_CUDA) when no device is usable — never a silent fallback."""
 import ctypes
+import dataclasses
+
+import numpy as np
 import os
 import re
 import subprocess
@@ -57,6 +60,13 @@ def test_validation_before_device(lib):
         assert s == lfsr.LFSR_ERR_INVALID_ARG, b
         assert len(lib.lfsr_last_error(None)) > 0
     assert lib.lfsr_create(ctypes.byref(good.to_c()), None) == lfsr.LFSR_ERR_INVALID_ARG
+    # user blur kernel (A36): radius beyond the zeta window, non-finite taps
+    k = np.ones((3, 3), np.float32)
+    k[1, 1] = np.nan
+    for psf in (np.ones((7, 7), np.float32), k):
+        p = dataclasses.replace(good, psf=psf)
+        h = ctypes.c_void_p()
+        assert lib.lfsr_create(ctypes.byref(p.to_c()), ctypes.byref(h)) == lfsr.LFSR_ERR_INVALID_ARG
     # NULL-safe destroy; calls on NULL ctx are argument errors
     lib.lfsr_destroy(None)
     assert lib.lfsr_admm_run(None, 1, None) == lfsr.LFSR_ERR_INVALID_ARG
