@@ -454,7 +454,17 @@ def color_super_resolve(params: Params, lr_rgb, view_offsets, disparity, n_iters
     view_offsets / disparity as for Solver.set_observations (CUDA tensors).  Returns
     ([3][H][W] CUDA tensor, ADMM stats)."""
     import torch
-    stream = torch.cuda.current_stream(lr_rgb.device).cuda_stream
+    caller = torch.cuda.current_stream(lr_rgb.device)
+    ts = torch.cuda.Stream(device=lr_rgb.device)   # one real stream for every call below (the legacy
+    ts.wait_stream(caller)                          # default stream's NULL handle would give the ctx its own)
+    with torch.cuda.stream(ts):
+        out = _color_sr_on(params, lr_rgb, view_offsets, disparity, n_iters, x0, ts.cuda_stream)
+    caller.wait_stream(ts)
+    return out
+
+
+def _color_sr_on(params, lr_rgb, view_offsets, disparity, n_iters, x0, stream):
+    import torch
     nv = lr_rgb.shape[0]
     assert lr_rgb.is_cuda and lr_rgb.dtype == torch.float32 and lr_rgb.is_contiguous() and lr_rgb.shape[1] == 3
     hw = tuple(lr_rgb.shape[2:])

@@ -27,6 +27,9 @@ import lfsr_synth as S  # noqa: E402
 import paper_2206_05047_b200 as L  # noqa: E402
 
 
+_TS = None
+
+
 def make(lf, reweight, K=5, tol=0.0):
     d = S.SolverDefaults()
     p = L.Params(n_views=lf.n_views, lr_height=lf.y.shape[1], lr_width=lf.y.shape[2], scale=lf.scale,
@@ -34,7 +37,11 @@ def make(lf, reweight, K=5, tol=0.0):
                  lambda_reg=d.lambda_reg, sigma_s=d.sigma_s, sigma_e=d.sigma_e, sigma_o1=d.sigma_o1,
                  sigma_o2=d.sigma_o2, theta=d.theta, cg_max_iters=K, cg_tol=tol,
                  reweight_every_iter=1 if reweight else 0)
-    s = L.Solver(p, stream=torch.cuda.current_stream().cuda_stream)
+    global _TS
+    if _TS is None:   # a real stream: the legacy default stream's handle is NULL (=> ctx-owned stream)
+        _TS = torch.cuda.Stream()
+        torch.cuda.set_stream(_TS)
+    s = L.Solver(p, stream=_TS.cuda_stream)
     s.set_observations(*[torch.from_numpy(a).cuda() for a in (lf.y, lf.view_offsets, lf.omega)])
     return s
 

@@ -30,7 +30,9 @@ with L.Solver(p) as s:           # the degradation model with the motion kernel
     s.set_observations(lf.y, lf.view_offsets, lf.omega)
     y = s.op("A", lf.x_gt.astype(np.float32))
 y = S.add_mixed_noise(y, cfg.sigma, cfg.nu, 2000 + 2).astype(np.float32)
-stream = torch.cuda.current_stream().cuda_stream
+ts = torch.cuda.Stream()          # a real stream (the legacy default stream's handle is NULL)
+torch.cuda.set_stream(ts)
+stream = ts.cuda_stream
 res = {"config": a.config, "psf": "motion length %d angle %.0f" % (a.length, a.angle)}
 with L.Solver(p, stream=stream) as s:
     s.set_observations(*[torch.from_numpy(v).cuda() for v in (y, lf.view_offsets, lf.omega)])
