@@ -36,6 +36,11 @@ __global__ void __launch_bounds__(NT) kbench(float* gout, float* gacc, int seed)
       atomicAdd(&gacc[(blockIdx.x * 4096 + a) & ((1 << 18) - 1)], v);
     } else if (MODE == 6) {   // 1 scalar LDS
       acc += s[a];
+    } else if (MODE == 8) {   // one int64 ATOMS.ADD.64 per cell (hi/lo in one word)
+      atomicAdd(reinterpret_cast<unsigned long long*>(s) + (a & 4095), (unsigned long long)(long long)(int)st);
+    } else if (MODE == 9) {   // two int32 ATOMS.ADD per cell (the hi / lo accumulators, LO words apart)
+      atomicAdd((int*)&s[a & 4095], (int)st);
+      atomicAdd((int*)&s[4096 + (a & 4095)], (int)(st >> 7));
     } else if (MODE == 7) {   // 4 shuffles
       acc += __shfl_sync(0xffffffffu, v, (lane + off) & 31) + __shfl_down_sync(0xffffffffu, acc, 1)
            + __shfl_up_sync(0xffffffffu, v, 1) + __shfl_xor_sync(0xffffffffu, acc, 2);
@@ -53,9 +58,10 @@ int main() {
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   int clk; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
   const char* names[] = {"smem f32 atomicAdd (CAS)", "smem i32 ATOMS.ADD", "warp-private RMW",
-                         "4x LDS.32 gather", "1x LDS.128 gather", "global REDG.F32", "1x LDS.32", "4x SHFL"};
+                         "4x LDS.32 gather", "1x LDS.128 gather", "global REDG.F32", "1x LDS.32", "4x SHFL",
+                         "smem i64 ATOMS.ADD.64", "2x smem i32 ATOMS (hi+lo)"};
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-  for (int mode = 0; mode < 8; ++mode) {
+  for (int mode = 0; mode < 10; ++mode) {
     for (int occ : {4, 8}) {
       int grid = sms * occ;
       for (int rep = 0; rep < 3; ++rep) {
@@ -69,6 +75,8 @@ int main() {
           case 5: kbench<5><<<grid, NT>>>(gout, gacc, rep); break;
           case 6: kbench<6><<<grid, NT>>>(gout, gacc, rep); break;
           case 7: kbench<7><<<grid, NT>>>(gout, gacc, rep); break;
+          case 8: kbench<8><<<grid, NT>>>(gout, gacc, rep); break;
+          case 9: kbench<9><<<grid, NT>>>(gout, gacc, rep); break;
         }
         cudaEventRecord(e1); cudaEventSynchronize(e1);
         float ms; cudaEventElapsedTime(&ms, e0, e1);
