@@ -47,7 +47,8 @@ class _Params(ctypes.Structure):
                 ("cg_max_iters", ctypes.c_int32), ("cg_tol", ctypes.c_double),
                 ("reweight_every_iter", ctypes.c_int32),
                 ("offset_weights", ctypes.POINTER(ctypes.c_double)), ("disp_per_view", ctypes.c_int32),
-                ("psf", ctypes.POINTER(ctypes.c_double)), ("psf_radius", ctypes.c_int32)]
+                ("psf", ctypes.POINTER(ctypes.c_double)), ("psf_radius", ctypes.c_int32),
+                ("paper_adjoint", ctypes.c_int32)]
 
 
 class _Stats(ctypes.Structure):
@@ -97,6 +98,7 @@ def lib():
             "or_cost": (ctypes.c_double, [P, D, D, D, D, D, D]),
             "or_gradient": (ctypes.c_double, [P, D, D, D, D, D, D, D]),
             "or_apply_Bk": (None, [I, I, I, D, D, D]),
+            "or_apply_WTb": (None, [I, I, D, D, ctypes.c_double, ctypes.c_double, D]),
             "or_apply_BkT": (None, [I, I, I, D, D, D]),
             "or_rgb_to_ycbcr": (None, [ctypes.c_size_t, D, D, D, D]),
             "or_ycbcr_to_rgb": (None, [ctypes.c_size_t, D, D, D, D]),
@@ -146,6 +148,7 @@ class Params:
     offset_weights: Optional[Sequence[float]] = None   # s_d weights overriding exp(-|d|^2/sigma_s)
     disp_per_view: int = 0      # 1: omega is [n_views][H][W] (view k warped with omega_k, A34)
     psf: Optional[np.ndarray] = None   # user convolution kernel [(2r+1)][(2r+1)] replacing the Gaussian (A36)
+    paper_adjoint: int = 0      # 1: A^T uses the paper's backward warp W_k^* with omega_0 (A37)
 
     @property
     def H(self):
@@ -173,7 +176,7 @@ class Params:
         return _Params(self.n_views, self.lr_h, self.lr_w, self.scale, self.ref_view, self.radius,
                        self.lambda1, self.lambda2, self.lambda_reg, self.sigma_s, self.sigma_e,
                        self.sigma_o1, self.sigma_o2, self.theta, self.cg_max_iters, self.cg_tol,
-                       self.reweight_every_iter, ow, int(self.disp_per_view), kp, kr)
+                       self.reweight_every_iter, ow, int(self.disp_per_view), kp, kr, int(self.paper_adjoint))
 
 
 def blur_taps(scale: int) -> np.ndarray:
@@ -229,6 +232,14 @@ def apply_W(x, omega, drho, dtau):
     x, omega = _d(x), _d(omega)
     out = np.zeros_like(x)
     lib().or_apply_W(x.shape[0], x.shape[1], _ptr(x), _ptr(omega), float(drho), float(dtau), _ptr(out))
+    return out
+
+
+def apply_WTb(u, omega0, drho, dtau):
+    """The paper's backward warp W_k^* (reading A37): u(z - dtheta_k omega_0(z))."""
+    u, omega0 = _d(u), _d(omega0)
+    out = np.zeros_like(u)
+    lib().or_apply_WTb(u.shape[0], u.shape[1], _ptr(u), _ptr(omega0), float(drho), float(dtau), _ptr(out))
     return out
 
 

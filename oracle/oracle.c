@@ -34,6 +34,8 @@
  *   or_admm           pinned: l2-only == lstsq (P10), == textbook scaled ADMM with exact
  *                     x-step (P11), convergence to an independent minimiser (P12)
  *   or_gradient       pinned: central finite differences of J (P18), J == or_cost
+ *   or_apply_WTb      pinned: integer translation == W_k^T in the interior, constants kept,
+ *                     inverse of W_k for a constant disparity (P25)
  *   or_apply_Bk/BkT   pinned: the Gaussian outer product == or_apply_B, impulse response
  *                     (convolution orientation), adjoint (P24)
  *   per-view omega    pinned: equal maps == shared mode, view k == shared mode with omega_k,
@@ -69,6 +71,9 @@ typedef struct {
                                                    convolution kernel [(2 psf_radius+1)^2]
                                                    row-major (NEXT-4, reading A36) */
   int32_t psf_radius;
+  int32_t paper_adjoint;                        /* 0: A_k^T uses the exact transpose W_k^T (A12);
+                                                   1: the paper's backward warp W_k^* with omega_0
+                                                   in its place (NEXT-2, reading A37) */
 } or_params;
 
 /* The disparity map view k is warped with ("for each perspective theta_k, we
@@ -220,6 +225,23 @@ void or_apply_WT(int H, int W, const double* t, const double* omega, double drho
     }
 }
 
+/* The paper's adjoint warp W_k^* ("the backward warping function W_k^* will warp
+ * the input SAI from perspective theta_k to theta_0 using omega_0"), reading A37:
+ * (W_k^* u)(z) = u(z - dtheta_k omega_0(z)), bilinear, replicate-clamped coordinate (the
+ * mirror of W_k's gather, A12).  Not the transpose of W_k. */
+void or_apply_WTb(int H, int W, const double* u, const double* omega0, double drho, double dtau,
+                  double* out) {
+#pragma omp parallel for schedule(static)
+  for (int Y = 0; Y < H; ++Y)
+    for (int X = 0; X < W; ++X) {
+      int y0, x0, y1, x1;
+      double a, b;
+      warp_point(H, W, Y, X, omega0[(size_t)Y * W + X], -drho, -dtau, &y0, &x0, &y1, &x1, &a, &b);
+      out[(size_t)Y * W + X] = (1 - a) * (1 - b) * u[(size_t)y0 * W + x0] + (1 - a) * b * u[(size_t)y0 * W + x1] +
+                               a * (1 - b) * u[(size_t)y1 * W + x0] + a * b * u[(size_t)y1 * W + x1];
+    }
+}
+
 /* A_k = D B W_k for every view (Eq. sr_model_vec).  out: [n_views][h][w].
  * view_offsets[k] = (drho_k, dtau_k) = theta_k - theta_0 in angular steps. */
 void or_apply_A(const or_params* P, const double* view_offsets, const double* omega,
@@ -240,7 +262,9 @@ void or_apply_A(const or_params* P, const double* view_offsets, const double* om
   free(t2);
 }
 
-/* A^T = sum_k W_k^T B^T D^T (Fig. sr_gpu_admm_as): in [n_views][h][w] -> HR. */
+/* A^T = sum_k W_k^T B^T D^T (Fig. sr_gpu_admm_as): in [n_views][h][w] -> HR.
+ * Paper mode (A37): sum_k W_k^* B^T D^T, so "A^T" and the normal operator built on it are
+ * no longer transposes (M is not symmetric); the algorithms are run unchanged. */
 void or_apply_AT(const or_params* P, const double* view_offsets, const double* omega,
                  const double* r, double* out) {
   int z = P->scale, H = P->lr_h * z, W = P->lr_w * z;
@@ -255,7 +279,10 @@ void or_apply_AT(const or_params* P, const double* view_offsets, const double* o
     or_apply_DT(H, W, z, r + k * q, t1);
     if (P->psf) or_apply_BkT(H, W, P->psf_radius, P->psf, t1, t2);
     else or_apply_B(H, W, R, taps, t1, t2);   /* the Gaussian B is self-adjoint (A11) */
-    or_apply_WT(H, W, t2, omega_of(P, omega, k), view_offsets[2 * k], view_offsets[2 * k + 1], t3);
+    if (P->paper_adjoint)   /* W_k^* with omega_0 (A37) */
+      or_apply_WTb(H, W, t2, omega_of(P, omega, P->ref_view), view_offsets[2 * k], view_offsets[2 * k + 1], t3);
+    else
+      or_apply_WT(H, W, t2, omega_of(P, omega, k), view_offsets[2 * k], view_offsets[2 * k + 1], t3);
     for (size_t i = 0; i < p; ++i) out[i] += t3[i];
   }
   free(t1);
