@@ -110,6 +110,12 @@ typedef struct {
                            x(Y-u, X-v), zero padding (P:L962 motion blur, SURVEY 8f NEXT-4,
                            reading A36).  Not with LFSR_DISP_PER_VIEW (UNSUPPORTED).  */
   int32_t psf_radius;   /* 0..R(zeta): 2 at zeta = 2, 3 at zeta = 3, 4                 */
+  int32_t paper_adjoint; /* 0 (default): A^T uses the exact transpose W_k^T of the warp (A12).
+                           1: the paper's own adjoint warp W_k^* -- a backward warp with
+                           omega_0, (W_k^* u)(z) = u(z - dtheta_k omega_0(z)) (P:L583,
+                           reading A37) -- in A^T, v and the CG operator, which is then not
+                           symmetric (Alg. 1/2 run unchanged).  Single strip, Gaussian blur
+                           and shared disparity only (else UNSUPPORTED).  SURVEY 8f NEXT-2. */
 } lfsr_params;
 
 /* Per-ADMM-iteration record.  J terms refer to x^{n-1} and the

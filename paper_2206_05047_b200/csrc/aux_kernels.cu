@@ -349,6 +349,88 @@ __global__ void __launch_bounds__(256) k_gd_update(const Geom G, float* __restri
 }
 
 // ---------------------------------------------------------------------------
+// Paper-mode adjoint (reading A37): out(z) += sign * sum_k (W_k^* B^T D^T rho_k)(z),
+// (W_k^* u)(z) = u(z - dtheta_k omega_0(z)) bilinear (replicate-clamped).  Gather form: one
+// thread per HR pixel, no atomics.  u at the four bilinear points is
+// sum_{i,j} g(Y - zeta i) g(X - zeta j) rho(i, j) (B^T D^T, zero padding), and the bilinear
+// weights factor per axis, so the sample is sum_i Wy(i) sum_j Wx(j) rho(i, j) over the <= 4 x 4
+// LR pixels whose blur reaches the 2 x 2 points.  Optionally adds <p, data part> to
+// ctl->cur[slot] (the CG <p, Mp>; M is not symmetric in this mode).  Runs after the tile
+// kernel that wrote rho and the NLTV part of `out`.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void paper_axis(float s, int n, int scale, int R, const float* taps, int& i_lo,
+                                           float (&w)[4]) {
+  const float fs = floorf(s);
+  const int p0 = (int)fs, p1 = min(p0 + 1, n - 1);
+  const float a = s - fs;
+  i_lo = (p0 - R + scale - 1 + scale * 8) / scale - 8;   // ceil((p0 - R) / scale), p0 - R >= -8 scale
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const int i = i_lo + t;
+    const int d0 = p0 - scale * i + R, d1 = p1 - scale * i + R;
+    const float g0 = (d0 >= 0 && d0 <= 2 * R) ? taps[d0] : 0.f;
+    const float g1 = (d1 >= 0 && d1 <= 2 * R) ? taps[d1] : 0.f;
+    w[t] = (1.f - a) * g0 + a * g1;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_paper_gather(const Geom G, const Views V, const float* __restrict__ rho,
+                                                      const float* __restrict__ omega0, const float* __restrict__ p,
+                                                      float* __restrict__ out, float sign, Control* ctl, int slot,
+                                                      int cg_k, int row0, int nrows) {
+  __shared__ double red[8];
+  if (cg_k >= 2 && ctl->cur[S_STOP] != 0.0) return;   // CG stopped (the tile kernel returned too)
+  const int X = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int Y = row0 + blockIdx.y * 8 + (threadIdx.x >> 5);
+  double part = 0.0;
+  if (X < G.W && Y < row0 + nrows && Y < G.H) {
+    const size_t gi = (size_t)Y * G.ps + X;
+    const float om = omega0[gi];
+    const int h = G.h, w = G.w, Z = G.scale, R = G.R;
+    const size_t lstride = (size_t)h * G.lps;
+    float acc = 0.f;
+    for (int k = 0; k < G.n_views; ++k) {
+      const float2 o = V.off[k];
+      const float sy = fminf(fmaxf((float)Y - o.y * om, 0.f), (float)(G.H - 1));
+      const float sx = fminf(fmaxf((float)X - o.x * om, 0.f), (float)(G.W - 1));
+      int iy, ix;
+      float wy[4], wx[4];
+      paper_axis(sy, G.H, Z, R, G.taps, iy, wy);
+      paper_axis(sx, G.W, Z, R, G.taps, ix, wx);
+      const float* rk = rho + k * lstride;
+      float v = 0.f;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int i = iy + t;
+        if (i < 0 || i >= h || wy[t] == 0.f) continue;
+        const float* row = rk + (size_t)i * G.lps;
+        float r = 0.f;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = ix + u;
+          if (j >= 0 && j < w) r = fmaf(wx[u], __ldg(row + j), r);
+        }
+        v = fmaf(wy[t], r, v);
+      }
+      acc += v;
+    }
+    out[gi] += sign * acc;
+    if (p) part = (double)p[gi] * (double)(sign * acc);
+  }
+  if (slot >= 0) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s = 0.0;
+      for (int i = 0; i < 8; ++i) s += red[i];
+      if (s != 0.0) atomicAdd(&ctl->cur[slot], s);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Test operators S / S^T (weighted directional gradient / divergence,
 // P:L585-601, reading A10) on dense [s_d][H][ps] stacks.
 // ---------------------------------------------------------------------------
@@ -461,6 +543,13 @@ cudaError_t launch_color(int to_ycbcr, const float* a, float* y, float* cb, floa
   if (blocks < 1) blocks = 1;
   if (to_ycbcr) k_rgb_to_ycbcr<<<blocks, 256, 0, st>>>(a, y, cb, cr, n);
   else k_ycbcr_to_rgb<<<blocks, 256, 0, st>>>(y, cb, cr, const_cast<float*>(a), n);
+  return cudaGetLastError();
+}
+cudaError_t launch_paper_gather(const Geom& G, const Views& V, const float* rho, const float* omega0, const float* p,
+                                float* out, float sign, Control* ctl, int slot, int cg_k, int row0, int nrows,
+                                cudaStream_t st) {
+  dim3 grid((G.W + 31) / 32, (nrows + 7) / 8);
+  k_paper_gather<<<grid, 256, 0, st>>>(G, V, rho, omega0, p, out, sign, ctl, slot, cg_k, row0, nrows);
   return cudaGetLastError();
 }
 cudaError_t launch_close(const Geom& G, Control* ctl, cudaStream_t st) {

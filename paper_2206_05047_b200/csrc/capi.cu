@@ -39,6 +39,9 @@ cudaError_t launch_apply_ST(const Geom& G, const float* h, const float* m, float
 cudaError_t launch_fold_rows(float* dst, float* src, size_t n, int zero_src, cudaStream_t st);
 cudaError_t launch_allreduce_local(Control* const* ctls, int nparts, int slot0, int count, cudaStream_t st);
 cudaError_t launch_gd_gnorm(const Geom& G, const float* g, Control* ctl, int num_sms, cudaStream_t st);
+cudaError_t launch_paper_gather(const Geom& G, const Views& V, const float* rho, const float* omega0, const float* p,
+                                float* out, float sign, Control* ctl, int slot, int cg_k, int row0, int nrows,
+                                cudaStream_t st);
 cudaError_t launch_color(int to_ycbcr, const float* a, float* y, float* cb, float* cr, size_t n, int num_sms,
                          cudaStream_t st);
 cudaError_t launch_gd_update(const Geom& G, float* x, const float* g, Control* ctl, const GdCfg& cfg, int num_sms,
@@ -170,6 +173,7 @@ static const char* validate(const lfsr_params* p) {
     for (int i = 0; i < n; ++i)
       if (!std::isfinite(p->psf[i])) return "psf must be finite";
   }
+  if (p->paper_adjoint != 0 && p->paper_adjoint != 1) return "paper_adjoint must be 0 or 1";
   if (p->device < 0) return "device must be >= 0";
   if (p->n_ranks < 1 || p->n_ranks > 1024) return "n_ranks must be in [1, 1024]";
   if (p->n_ranks == 1 && p->rank != 0) return "rank must be 0 when n_ranks == 1";
@@ -226,6 +230,7 @@ static void fill_geom(const lfsr_params& p, Geom& G) {
   }
   G.gpoly2 = (float)(gmax * gmax * 1.0001);
   G.ksum = 1.f;
+  G.paper = p.paper_adjoint;
   if (p.psf) {   // user blur kernel (A36): flip into the E-offset order of the tile kernel
     G.psf2d = 1;
     const int rp = p.psf_radius, np_ = 2 * rp + 1;
@@ -357,6 +362,10 @@ lfsr_status lfsr_create(const lfsr_params* params, lfsr_ctx** out) {
   if (const char* why = validate(params)) {
     g_create_err = why;
     return LFSR_ERR_INVALID_ARG;
+  }
+  if (params->paper_adjoint && (params->n_ranks > 1 || params->psf)) {
+    g_create_err = "the paper-mode adjoint (paper_adjoint) runs on a single strip with the Gaussian blur";
+    return LFSR_ERR_UNSUPPORTED;
   }
   int ndev = 0;
   cudaError_t e = cudaGetDeviceCount(&ndev);
@@ -558,6 +567,7 @@ static lfsr_status alloc_part(lfsr_ctx* c, Part& P) {
   ALLOC(S.q, hr * 4);
   ALLOC(S.tmp_hr, hr * 4);
   ALLOC(S.tmp_lr, lr * 4);
+  if (G.paper) ALLOC(S.rho, lr * 4);
   ALLOC(S.ctl, sizeof(Control));
   ALLOC(P.ring, (size_t)kRingCap * T_COUNT * sizeof(double));
 #undef ALLOC
@@ -727,8 +737,8 @@ lfsr_status lfsr_set_observations(lfsr_ctx* c, const float* lr_views, const floa
   if (!c) return LFSR_ERR_INVALID_ARG;
   if (c->poisoned) FAIL(c, LFSR_ERR_STATE, "ctx is poisoned by an earlier CUDA/NCCL error");
   if (disp_mode != LFSR_DISP_SHARED && disp_mode != LFSR_DISP_PER_VIEW) FAIL(c, LFSR_ERR_INVALID_ARG, "unknown disp_mode");
-  if (disp_mode == LFSR_DISP_PER_VIEW && c->G.psf2d)
-    FAIL(c, LFSR_ERR_UNSUPPORTED, "per-view disparity maps with a user blur kernel are not in this build");
+  if (disp_mode == LFSR_DISP_PER_VIEW && (c->G.psf2d || c->G.paper))
+    FAIL(c, LFSR_ERR_UNSUPPORTED, "per-view disparity maps with a user blur kernel or the paper-mode adjoint are not in this build");
   lfsr_status st;
   if ((st = check_ptr(c, lr_views, mem, "lr_views")) != LFSR_OK) return st;
   if ((st = check_ptr(c, view_offsets, mem, "view_offsets")) != LFSR_OK) return st;
@@ -860,6 +870,7 @@ lfsr_status lfsr_set_observations(lfsr_ctx* c, const float* lr_views, const floa
 
 static TileIO base_io(const Part& P) {
   TileIO io{};
+  io.rho_out = P.S.rho;   // paper mode only (A37)
   io.omega = P.S.omega;
   io.ctl = P.S.ctl;
   io.m = P.S.m;
@@ -1039,6 +1050,10 @@ static lfsr_status enqueue_iteration(lfsr_ctx* c, cudaStream_t st, int parity) {
     io.reweight = c->prm.reweight_every_iter;
     CK(c, launch_tile(MODE_WZ, G, c->V, P.T, io, st));
     ++launches;
+    if (G.paper) {   // v's data part through the paper's backward warp (A37): r = -v
+      CK(c, launch_paper_gather(G, c->V, P.S.rho, P.S.omega, nullptr, P.S.r, -1.f, P.S.ctl, -1, 0, 0, G.H, st));
+      ++launches;
+    }
   }
   CK(c, mark());
   if (multi) {
@@ -1059,6 +1074,11 @@ static lfsr_status enqueue_iteration(lfsr_ctx* c, cudaStream_t st, int parity) {
       n.do_nltv = 1;
       CK(c, launch_tile(MODE_NORMAL, G, c->V, P.T, n, st));
       ++launches;
+      if (G.paper) {   // q's data part and its share of <p, q> (A37)
+        CK(c, launch_paper_gather(G, c->V, P.S.rho, P.S.omega, P.S.p[k & 1], P.S.q, 1.f, P.S.ctl, S_PQ + k, k, 0,
+                                  G.H, st));
+        ++launches;
+      }
     }
     CK(c, mark());
     if (multi) {
@@ -1233,6 +1253,10 @@ static lfsr_status enqueue_gd(lfsr_ctx* c, cudaStream_t st, const GdCfg& cfg) {
   io.reweight = c->prm.reweight_every_iter;
   CK(c, launch_tile(MODE_GRAD, G, c->V, P.T, io, st));
   ++launches;
+  if (G.paper) {
+    CK(c, launch_paper_gather(G, c->V, P.S.rho, P.S.omega, nullptr, c->gd_g, 1.f, P.S.ctl, -1, 0, 0, G.H, st));
+    ++launches;
+  }
   if (cfg.ls) {
     CK(c, launch_gd_gnorm(G, c->gd_g, P.S.ctl, c->num_sms, st));
     ++launches;
@@ -1497,7 +1521,10 @@ lfsr_status lfsr_op_apply(lfsr_ctx* c, lfsr_op op, const float* in, float* out, 
       memcpy(&io.tmax_in, &ub, 4);
       io.in_lr = S.tmp_lr;
       io.out_hr = c->tmp_hr2;
-      CK(c, launch_tile(MODE_AT, G, c->V, T, io, s));
+      if (G.paper)   // sum_k W_k^* B^T D^T (A37)
+        CK(c, launch_paper_gather(G, c->V, S.tmp_lr, S.omega, nullptr, c->tmp_hr2, 1.f, S.ctl, -1, 0, 0, G.H, s));
+      else
+        CK(c, launch_tile(MODE_AT, G, c->V, T, io, s));
       CK(c, get2d(c, out, G.W, c->tmp_hr2, G.ps, (size_t)G.H, mem));
       break;
     }
@@ -1509,6 +1536,8 @@ lfsr_status lfsr_op_apply(lfsr_ctx* c, lfsr_op op, const float* in, float* out, 
       io.out_hr = c->tmp_hr2;
       io.do_nltv = 1;
       CK(c, launch_tile(MODE_NORMAL, G, c->V, T, io, s));
+      if (G.paper)
+        CK(c, launch_paper_gather(G, c->V, S.rho, S.omega, nullptr, c->tmp_hr2, 1.f, S.ctl, -1, 0, 0, G.H, s));
       CK(c, get2d(c, out, G.W, c->tmp_hr2, G.ps, (size_t)G.H, mem));
       break;
     }
@@ -1545,6 +1574,8 @@ lfsr_status lfsr_op_apply(lfsr_ctx* c, lfsr_op op, const float* in, float* out, 
       io.out_hr = c->tmp_hr2;
       io.reweight = 0;   // the current weight map m
       CK(c, launch_tile(MODE_GRAD, G, c->V, T, io, s));
+      if (G.paper)
+        CK(c, launch_paper_gather(G, c->V, S.rho, S.omega, nullptr, c->tmp_hr2, 1.f, c->op_ctl, -1, 0, 0, G.H, s));
       CK(c, get2d(c, out, G.W, c->tmp_hr2, G.ps, (size_t)G.H, mem));
       break;
     }

@@ -65,6 +65,7 @@ struct Geom {
   int32_t tile_g, tile_nw;    // view groups and warps per CTA (host-chosen, 0 = the cost model's choice)
   int32_t per_view;           // 1: omega is [n_views][H][ps], view k warped with omega_k (A34)
   int32_t psf2d;              // 1: user blur kernel (A36) in psf2 instead of the separable taps
+  int32_t paper;              // 1: the paper's backward-warp adjoint W_k^* with omega_0 (A37)
   float ksum;                 // sum |k| of the blur kernel (1 for the normalised Gaussian): |B w| <= ksum max|w|
   float psf2[2 * 3 + 1][2 * 3 + 1];   // psf2[a][b] = k[R-a][R-b]: E-offset (correlation) order, zero padded to 2R+1
   float taps[kMaxTaps * 2 + 1];
@@ -120,6 +121,7 @@ struct TileIO {
   int32_t reweight;      // WZ: recompute m from x
   int32_t do_nltv;       // NORMAL: include the (th/2) S^T S term
   int32_t ls_t;          // J: line-search trial index t (input tile = x - eta0 2^-t g, in_hr2 = g)
+  float* rho_out;        // paper mode (A37): rho of every LR pixel [n_views][h][lps] for k_paper_gather
   float eta0;            // J: initial step of the line search
   float armijo_c;        // J: Armijo constant c (reading A32)
 };
@@ -153,6 +155,7 @@ struct State {
   // scratch for ops
   float* tmp_hr;   // [H][ps]
   float* tmp_lr;   // [n_views][h][lps]
+  float* rho;      // [n_views][h][lps] paper mode (A37) only
   Control* ctl;
 };
 

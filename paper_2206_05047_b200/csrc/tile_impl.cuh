@@ -539,7 +539,9 @@ __device__ __forceinline__ void pass_reductions(const Geom& G, float fa, float f
   }
 }
 
-template <int Z, int MODE, bool INT, int NV, bool PV>
+// PM (paper-mode adjoint, A37): the pass stops after the epilogue and writes rho to
+// io.rho_out; k_paper_gather applies the backward warp afterwards.
+template <int Z, int MODE, bool INT, int NV, bool PV, bool PM>
 __device__ __forceinline__ void view_pass(const Tile<Z, INT>& t, const Geom& G, const Views& V, const TileIO& io,
                                           const int (&ks)[NV], int lane, int i0, int j0, int BL, double& red_a,
                                           double& red_b, double& red_c) {
@@ -550,6 +552,7 @@ __device__ __forceinline__ void view_pass(const Tile<Z, INT>& t, const Geom& G, 
   constexpr bool kY = (MODE == MODE_WZ || MODE == MODE_GRAD || MODE == MODE_J);   // reads y_k
   const int j = j0 + lane;
   const bool col_ok = lane < LX && j < G.w;
+  constexpr bool kAdjW = kAdj && !PM;   // the exact adjoint scatter of this pass
   float drho[NV], dtau[NV], fr[NV][NTAP], br[NV][NTAP], y_nx[NV], wa_nx[NV];
   const float* omk[NV];   // per-view disparity map omega_k (A34), nullptr: the shared map in shared memory
   size_t lrow0[NV];
@@ -598,13 +601,14 @@ __device__ __forceinline__ void view_pass(const Tile<Z, INT>& t, const Geom& G, 
         float a = a2.x + a2.y;
         if constexpr (NTAP & 1) a = fmaf(G.taps[NTAP - 1], fr[v][NTAP - 1], a);
         if (ok) rho[v] = lr_epilogue<MODE>(a, y_cur, wa_cur, lg, G, io, fa, fb, fc);
+        if (PM && ok) io.rho_out[lg] = rho[v];
 #pragma unroll
         for (int u = 0; u < KEEP; ++u) fr[v][u] = fr[v][u + Z];
       } else {
         rho[v] = ok ? io.in_lr[lg] : 0.f;
       }
     }
-    if (kAdj) {
+    if (kAdjW) {
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
 #pragma unroll
@@ -621,7 +625,7 @@ __device__ __forceinline__ void view_pass(const Tile<Z, INT>& t, const Geom& G, 
       }
     }
   }
-  if (kAdj) {
+  if (kAdjW) {
 #pragma unroll
     for (int v = 0; v < NV; ++v)
 #pragma unroll
@@ -744,7 +748,7 @@ __device__ __forceinline__ void view_pass2d(const Tile<Z, INT>& t, const Geom& G
   pass_reductions<MODE>(G, fa, fb, fc, red_a, red_b, red_c);
 }
 
-template <int Z, int MODE, bool INT, bool PV, bool P2>
+template <int Z, int MODE, bool INT, bool PV, bool P2, bool PM>
 __device__ __forceinline__ void views(const Tile<Z, INT>& t, const Geom& G, const Views& V, const TileGeom& T,
                                       const TileIO& io, int grp, int lane, int warp, int NW, int i0, int j0, int BL,
                                       double& red_a, double& red_b, double& red_c) {
@@ -753,7 +757,7 @@ __device__ __forceinline__ void views(const Tile<Z, INT>& t, const Geom& G, cons
   for (int k = kbeg + warp; k < kend; k += NW) {
     const int ks[1] = {k};
     if constexpr (P2) view_pass2d<Z, MODE, INT>(t, G, V, io, k, lane, i0, j0, BL, red_a, red_b, red_c);
-    else view_pass<Z, MODE, INT, 1, PV>(t, G, V, io, ks, lane, i0, j0, BL, red_a, red_b, red_c);
+    else view_pass<Z, MODE, INT, 1, PV, PM>(t, G, V, io, ks, lane, i0, j0, BL, red_a, red_b, red_c);
   }
 }
 
@@ -762,7 +766,8 @@ __device__ __forceinline__ void views(const Tile<Z, INT>& t, const Geom& G, cons
 // PV: per-view disparity maps omega_k read from global memory (A34); a compile-time
 // switch because even a warp-uniform runtime test cost the shared-map path ~12 %.
 // P2: user (non-separable) blur kernel (A36, view_pass2d).
-template <int Z, int MODE, bool FIXBL, bool PV, bool P2>
+// PM: paper-mode adjoint (A37): no scatter, rho to io.rho_out (k_paper_gather follows).
+template <int Z, int MODE, bool FIXBL, bool PV, bool P2, bool PM>
 __global__ void __launch_bounds__(LaunchCfg<Z>::MAXW * 32, LaunchCfg<Z>::MINB)
 k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
   using C = TC<Z>;
@@ -981,7 +986,7 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
       tile.P = P; tile.ACC = ACC; tile.OM = OM; tile.PW = PW; tile.PWZ = PWZ; tile.PY0 = PY0; tile.PX0 = PX0;
       tile.YE0 = YE0; tile.XE0 = XE0; tile.H = H; tile.W = W; tile.PS = ps; tile.tscale = s_scale[0]; tile.lo = LO;
       tile.koff = koff; tile.rows_in = rows_in;
-      views<Z, MODE, decltype(tile)::kInt, PV, P2>(tile, G, V, T, io, grp, lane, warp, NW, i0, j0, BL, red_a, red_b, red_c);
+      views<Z, MODE, decltype(tile)::kInt, PV, P2, PM>(tile, G, V, T, io, grp, lane, warp, NW, i0, j0, BL, red_a, red_b, red_c);
     };
     if (cols_in && rows_in) run(Tile<Z, true>{});   // (columns-only interior: measured slower)
     else run(Tile<Z, false>{});
@@ -1066,7 +1071,7 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
     const int slot[3] = {S_L1, S_L2, S_REG};
     block_reduce_add<3>(v, RED, ctl->cur, slot);
   } else if (MODE == MODE_NORMAL && io.cg_k >= 1) {
-    double v[2] = {red_a + red_b, pi0_part};
+    double v[2] = {(PM ? 0.0 : red_a) + red_b, pi0_part};   // PM: the data part comes from the gather
     const int slot[2] = {S_PQ + io.cg_k, S_PI + 0};
     block_reduce_add<2>(v, RED, ctl->cur, slot);
   }
@@ -1077,13 +1082,16 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
 // only for per-view maps (PV) and for a user blur kernel (P2).
 template <int Z>
 struct TileZ {
-  template <int MODE, bool F, bool PV, bool P2>
+  template <int MODE, bool F, bool PV, bool P2, bool PM = false>
   static cudaError_t launch1(const Geom& G, const Views& V, const TileGeom& T, const TileIO& io, cudaStream_t st) {
-    k_tile<Z, MODE, F, PV, P2><<<T.ntYl * T.ntX * T.groups, T.nwarps * 32, T.smem, st>>>(G, V, T, io);
+    k_tile<Z, MODE, F, PV, P2, PM><<<T.ntYl * T.ntX * T.groups, T.nwarps * 32, T.smem, st>>>(G, V, T, io);
     return cudaGetLastError();
   }
   template <int MODE>
   static cudaError_t launchm(const Geom& G, const Views& V, const TileGeom& T, const TileIO& io, cudaStream_t st) {
+    constexpr bool kHasAdj = (MODE == MODE_WZ || MODE == MODE_NORMAL || MODE == MODE_GRAD);
+    if constexpr (kHasAdj)
+      if (G.paper) return launch1<MODE, false, false, false, true>(G, V, T, io, st);
     if (G.psf2d) return launch1<MODE, false, false, true>(G, V, T, io, st);
     if (G.per_view) return launch1<MODE, false, true, false>(G, V, T, io, st);
     if (MODE == MODE_GRAD || MODE == MODE_J) return launch1<MODE, false, false, false>(G, V, T, io, st);
@@ -1102,9 +1110,10 @@ struct TileZ {
     }
     return cudaErrorInvalidValue;
   }
-  template <int MODE, bool F, bool PV, bool P2>
+  template <int MODE, bool F, bool PV, bool P2, bool PM = false>
   static cudaError_t prep1(size_t smem) {
-    return cudaFuncSetAttribute(k_tile<Z, MODE, F, PV, P2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    return cudaFuncSetAttribute(k_tile<Z, MODE, F, PV, P2, PM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem);
   }
   template <int MODE>
   static cudaError_t prepm(size_t smem) {
@@ -1113,6 +1122,8 @@ struct TileZ {
       if ((e = prep1<MODE, true, false, false>(smem)) != cudaSuccess) return e;
     if ((e = prep1<MODE, false, false, false>(smem)) != cudaSuccess) return e;
     if ((e = prep1<MODE, false, true, false>(smem)) != cudaSuccess) return e;
+    if constexpr (MODE == MODE_WZ || MODE == MODE_NORMAL || MODE == MODE_GRAD)
+      if ((e = prep1<MODE, false, false, false, true>(smem)) != cudaSuccess) return e;
     return prep1<MODE, false, false, true>(smem);
   }
   static cudaError_t prepare(size_t smem) {
@@ -1126,7 +1137,7 @@ struct TileZ {
   }
   static int occupancy(int threads, size_t smem) {
     int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_tile<Z, MODE_NORMAL, false, false, false>, threads,
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_tile<Z, MODE_NORMAL, false, false, false, false>, threads,
                                                       smem) != cudaSuccess) {
       cudaGetLastError();
       return 1;

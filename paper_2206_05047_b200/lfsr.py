@@ -52,7 +52,8 @@ class _CParams(ctypes.Structure):
                 ("cg_tol", ctypes.c_float), ("reweight_every_iter", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("rank", ctypes.c_int32), ("n_ranks", ctypes.c_int32), ("nccl_unique_id", ctypes.c_void_p),
                 ("stream", ctypes.c_void_p), ("offset_weights", ctypes.POINTER(ctypes.c_float)),
-                ("psf", ctypes.POINTER(ctypes.c_float)), ("psf_radius", ctypes.c_int32)]
+                ("psf", ctypes.POINTER(ctypes.c_float)), ("psf_radius", ctypes.c_int32),
+                ("paper_adjoint", ctypes.c_int32)]
 
 
 class _CStats(ctypes.Structure):
@@ -173,6 +174,7 @@ class Params:
     nccl_unique_id: bytes | None = None
     offset_weights: object = None   # s_d floats (e.g. BTV alpha^(|dx|+|dy|)) replacing exp(-|d|^2/sigma_s)
     psf: object = None              # user blur kernel [(2r+1)][(2r+1)] replacing the Gaussian (A36)
+    paper_adjoint: int = 0          # 1: the paper's backward-warp adjoint W_k^* with omega_0 (A37)
 
     @property
     def H(self):

@@ -67,6 +67,13 @@ def test_validation_before_device(lib):
         p = dataclasses.replace(good, psf=psf)
         h = ctypes.c_void_p()
         assert lib.lfsr_create(ctypes.byref(p.to_c()), ctypes.byref(h)) == lfsr.LFSR_ERR_INVALID_ARG
+    # the paper-mode adjoint (A37) is single-strip, Gaussian-blur only
+    for over in (dict(paper_adjoint=1, n_ranks=2, rank=-1), dict(paper_adjoint=1, psf=np.ones((3, 3), np.float32) / 9)):
+        p = dataclasses.replace(good, **over)
+        h = ctypes.c_void_p()
+        assert lib.lfsr_create(ctypes.byref(p.to_c()), ctypes.byref(h)) == lfsr.LFSR_ERR_UNSUPPORTED
+    p = dataclasses.replace(good, paper_adjoint=2)
+    assert lib.lfsr_create(ctypes.byref(p.to_c()), ctypes.byref(ctypes.c_void_p())) == lfsr.LFSR_ERR_INVALID_ARG
     # NULL-safe destroy; calls on NULL ctx are argument errors
     lib.lfsr_destroy(None)
     assert lib.lfsr_admm_run(None, 1, None) == lfsr.LFSR_ERR_INVALID_ARG

@@ -9,11 +9,14 @@ cfgname = sys.argv[1] if len(sys.argv) > 1 else "C3"
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 10
 per_view = len(sys.argv) > 3 and sys.argv[3] == "pv"   # per-view disparity maps (A34)
 user_psf = len(sys.argv) > 3 and sys.argv[3] == "psf"  # 45-degree motion kernel as B (A36)
+paper = len(sys.argv) > 3 and sys.argv[3] == "paper"    # the paper's backward-warp adjoint (A37)
 t0 = time.time()
 lf = S.make_lightfield(cfgname)
 print("gen %.1fs" % (time.time() - t0), flush=True)
 cfg = S.CONFIGS[cfgname]
 p = L.params_for(cfg, S.defaults_for(cfg))
+if paper:
+    p.paper_adjoint = 1
 if user_psf:
     p.psf = S.motion_psf(5 if cfg.scale == 2 else 7, 45.0)
 stream = torch.cuda.Stream()
@@ -34,7 +37,7 @@ for i in range(iters):
     s.profile_read()
 ms, n = s.profile_read()
 st = s.admm_stats(3, iters)
-print(json.dumps({"cfg": cfgname, "per_view": per_view, "psf": user_psf, "ms_per_iter": plain, "it_per_s": 1000 / plain, "it_per_s_profiled": 1000 * iters / tot,
+print(json.dumps({"cfg": cfgname, "per_view": per_view, "psf": user_psf, "paper_adjoint": paper, "ms_per_iter": plain, "it_per_s": 1000 / plain, "it_per_s_profiled": 1000 * iters / tot,
                   "kernel_ms_per_launch": [m / max(c, 1) for m, c in zip(ms, n)], "launches": n,
                   "J_first": st[0]["J"], "J_last": st[-1]["J"], "psnr": L.psnr(s.get_hr(), lf.x_gt),
                   "psnr_x0": None}))
