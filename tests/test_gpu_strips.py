@@ -11,14 +11,14 @@ from test_gpu_parity import check_iterates, oparams, rel_l2
 pytestmark = pytest.mark.gpu
 
 
-def solve(L, lf, n, **over):
+def solve(L, lf, n, omega=None, **over):
     d = S.SolverDefaults()
     p = L.Params(n_views=lf.n_views, lr_height=lf.y.shape[1], lr_width=lf.y.shape[2], scale=lf.scale,
                  ref_view=lf.ref_view, nltv_radius=d.radius, lambda1=d.lambda1, lambda2=d.lambda2,
                  lambda_reg=d.lambda_reg, sigma_s=d.sigma_s, sigma_e=d.sigma_e, sigma_o1=d.sigma_o1,
                  sigma_o2=d.sigma_o2, theta=d.theta, cg_max_iters=d.cg_max_iters, cg_tol=d.cg_tol, **over)
     s = L.Solver(p)
-    s.set_observations(lf.y, lf.view_offsets, lf.omega)
+    s.set_observations(lf.y, lf.view_offsets, lf.omega if omega is None else omega)
     xs = [s.get_hr()]
     stats = []
     for _ in range(n):
@@ -50,3 +50,17 @@ def test_virtual_ranks_match_oracle(lfsr_mod):
     p, xs, stats, st = solve(lfsr_mod, lf, 8, n_ranks=2, rank=-1)
     ora = O.admm(oparams(p), lf.y, lf.view_offsets, lf.omega, 8)
     check_iterates(p, ora, xs, stats, st, lf.x_gt)
+
+
+def test_virtual_ranks_per_view_maps_and_user_psf(lfsr_mod):
+    """The strip decomposition with the NEXT-2 per-view maps and the NEXT-4 user blur kernel:
+    every rank holds every omega_k; the kernel radius stays within the halo's R."""
+    lf = S.make_lightfield("C2")
+    oms = S.per_view_disparity(lf.omega, lf.n_views, amp=0.2, seed=4)
+    for kw in (dict(omega=oms), dict(psf=S.motion_psf(5, 45.0))):
+        _, xs1, st1, _ = solve(lfsr_mod, lf, 2, **kw)
+        _, xsn, stn, _ = solve(lfsr_mod, lf, 2, n_ranks=3, rank=-1, **kw)
+        for i in range(3):
+            assert rel_l2(xsn[i], xs1[i]) <= 1e-5, (kw.keys(), i, rel_l2(xsn[i], xs1[i]))
+        for a, b in zip(st1, stn):
+            assert a["cg_iters"] == b["cg_iters"] and abs(a["J"] - b["J"]) <= 1e-6 * abs(a["J"])
