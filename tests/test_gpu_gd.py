@@ -41,10 +41,15 @@ def c1_params(lfsr_mod, lf, **over):
 
 
 def run_gd_pair(lfsr_mod, lf, n, step, line_search, **over):
+    """Both sides start from the same fp32 x0 (the oracle's bicubic up-sampling, rounded): the
+    subgradient's sgn(0) = 0 decisions on exactly flat regions then agree (with each side's own
+    bicubic, flat regions are 0 in one precision and +-1 ulp in the other)."""
     p = c1_params(lfsr_mod, lf, **over)
-    ora = O.gd(oparams(p), lf.y, lf.view_offsets, lf.omega, n, step, line_search=line_search, max_halvings=30)
+    x0 = O.bicubic(lf.y[p.ref_view], p.scale).astype(np.float32)
+    ora = O.gd(oparams(p), lf.y, lf.view_offsets, lf.omega, n, step, line_search=line_search, max_halvings=30,
+               x0=x0)
     s = lfsr_mod.Solver(p)
-    s.set_observations(lf.y, lf.view_offsets, lf.omega)
+    s.set_observations(lf.y, lf.view_offsets, lf.omega, x0)
     xs, stats = [s.get_hr()], []
     for _ in range(n):
         stats += s.gd_run(1, step, line_search=line_search, max_trials=30)
@@ -138,3 +143,24 @@ def test_gd_api_rules(lfsr_mod):
     x2 = s2.get_hr()
     s2.close()
     assert rel_l2(x1, x2) <= 1e-6
+
+
+def test_gd_ls_parity_full_size_C3(lfsr_mod):
+    """gd-ls at BASELINE's C3 size (9x9 views, 256^2 -> 512^2) in the launch configuration of
+    lfsr_gd_run, 2 iterations against the oracle.  sgn(e) is a discrete decision taken in each
+    side's precision (reading A30): of the 5.3 M residuals a handful lie within fp32 rounding of
+    zero, and each such flip moves x by O(eta) on the HR footprint of one LR pixel (a few dozen
+    pixels).  So the bar here is: line-search decisions identical, cost terms within 1e-4, and
+    every pixel within 1e-5 of the oracle except at most 0.1 % (the flip footprints)."""
+    lf = S.make_lightfield("C3")
+    ora, xs, stats, _ = run_gd_pair(lfsr_mod, lf, 2, 2.0 ** -5, True)
+    for n, (g, o) in enumerate(zip(stats, ora.stats)):
+        assert g["ls_evals"] == o["ls_evals"] and g["ls_failed"] == o["ls_failed"], (n, g, o)
+        for k in ("J", "data_l1", "data_l2", "reg_l1", "grad_sq"):
+            assert abs(g[k] - o[k]) <= ITER_TOL * abs(o[k]), (n, k, g[k], o[k])
+    for n in range(len(xs)):
+        d = np.abs(xs[n].astype(np.float64) - ora.x_iters[n])
+        frac = float(np.mean(d > 1e-5))
+        print("gd-ls C3 x^%d: rel L2 %.2e, pixels off by > 1e-5: %.4f %%" % (n, rel_l2(xs[n], ora.x_iters[n]),
+                                                                          100 * frac))
+        assert frac <= 1e-3, (n, frac)

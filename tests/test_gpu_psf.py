@@ -92,3 +92,27 @@ def test_motion_blur_admm_parity_C1(lfsr_mod):
     assert abs(O.psnr(xs[-1], lf.x_gt) - O.psnr(ora.x_iters[-1], lf.x_gt)) <= PSNR_TOL
     print("motion-blur C1 per-iterate rel L2:", ["%.2e" % e for e in errs],
           "PSNR %.2f -> %.2f" % (O.psnr(xs[0], lf.x_gt), O.psnr(xs[-1], lf.x_gt)))
+
+
+def test_motion_blur_admm_parity_full_size_C3(lfsr_mod):
+    """User blur kernel at C3 size (9x9 views, 256^2 -> 512^2): 2 ADMM iterations vs the oracle."""
+    lf = S.make_lightfield("C3")
+    k = S.motion_psf(5, 45.0)
+    d = S.SolverDefaults()
+    p = lfsr_mod.Params(n_views=lf.n_views, lr_height=256, lr_width=256, scale=2, ref_view=lf.ref_view,
+                        nltv_radius=d.radius, lambda1=d.lambda1, lambda2=d.lambda2, lambda_reg=d.lambda_reg,
+                        sigma_s=d.sigma_s, sigma_e=d.sigma_e, sigma_o1=d.sigma_o1, sigma_o2=d.sigma_o2,
+                        theta=d.theta, cg_max_iters=d.cg_max_iters, cg_tol=d.cg_tol, psf=k)
+    P = oparams(p)
+    P.psf = k.astype(np.float64)
+    n = 2
+    ora = O.admm(P, lf.y, lf.view_offsets, lf.omega, n)
+    s = lfsr_mod.Solver(p)
+    s.set_observations(lf.y, lf.view_offsets, lf.omega)
+    xs = [s.get_hr()]
+    for _ in range(n):
+        s.admm_run(1)
+        xs.append(s.get_hr())
+    s.close()
+    errs = [rel_l2(xs[i], ora.x_iters[i]) for i in range(n + 1)]
+    assert max(errs) <= ITER_TOL, errs
