@@ -250,11 +250,17 @@ struct Tile : YRoute<!INT && TC<Z>::DUMMY, Z / 2> {
   // W_k at the lane's zeta E positions of row er, then the row's values at E columns
   // zeta*lane + v, v < NTAP (the horizontal blur window of the lane's LR column):
   // own positions, the rest from the next lanes by shuffles.
+  // omr: the row's disparities already in registers (per-view ring of view_pass), or nullptr.
   __device__ __forceinline__ void fwd_vals(int er, int lane, float drho, float dtau, const float* omk,
-                                           float (&val)[TC<Z>::NTAP]) const {
+                                           float (&val)[TC<Z>::NTAP], const float* omr = nullptr) const {
     constexpr int NTAP = TC<Z>::NTAP;
     float om[Z], wp[Z];
-    load_om(er, lane, om, omk);
+    if (omr) {
+#pragma unroll
+      for (int s = 0; s < Z; ++s) om[s] = omr[s];
+    } else {
+      load_om(er, lane, om, omk);
+    }
     const float Yf = yrow(er);
     const float X0 = (float)(XE0 - PX0 + Z * lane);
 #pragma unroll
@@ -286,11 +292,11 @@ struct Tile : YRoute<!INT && TC<Z>::DUMMY, Z / 2> {
 
   // W_k then the horizontal blur taps at this lane's LR column, for E row er.
   __device__ __forceinline__ float fwd_row(int er, int lane, float drho, float dtau, const float* omk,
-                                          const Geom& G) const {
+                                          const Geom& G, const float* omr = nullptr) const {
     constexpr int NTAP = TC<Z>::NTAP;
     if (!kDummy && !row_in(er)) return 0.f;    // blur zero padding (A11), warp uniform
     float val[NTAP];
-    fwd_vals(er, lane, drho, dtau, omk, val);
+    fwd_vals(er, lane, drho, dtau, omk, val, omr);
     float2 h2 = f2s(0.f);
 #pragma unroll
     for (int v = 0; v + 1 < NTAP; v += 2) h2 = __ffma2_rn(tap2(G, v), f2(val[v], val[v + 1]), h2);
@@ -306,7 +312,7 @@ struct Tile : YRoute<!INT && TC<Z>::DUMMY, Z / 2> {
   // instead of 2 zeta (per lane and boundary; the all-or-nothing warp test it replaces
   // cost 4 % at C4/C5).
   __device__ __forceinline__ void adj_row(int er, int lane, float t1b, float drho, float dtau, const float* omk,
-                                          const Geom& G) const {
+                                          const Geom& G, const float* omr = nullptr) const {
     constexpr int NJ = 2 * TC<Z>::R / Z + 1;
     constexpr int R2 = 2 * TC<Z>::R;
     if (!kDummy && !row_in(er)) return;        // E positions outside the image carry no adjoint (A11)
@@ -338,16 +344,21 @@ struct Tile : YRoute<!INT && TC<Z>::DUMMY, Z / 2> {
         if (Z * j + s <= R2) t = fmaf(G.taps[Z * j + s], tv[j], t);
       tt[s] = t;
     }
-    scatter(er, lane, tt, drho, dtau, omk);
+    scatter(er, lane, tt, drho, dtau, omk, omr);
   }
 
   // The exact bilinear scatter (W_k^T) of the adjoint blur values tt of the lane's zeta
   // positions of E row er into the fixed-point accumulator (the row must be inside the
   // image or a routed dummy row).
   __device__ __forceinline__ void scatter(int er, int lane, const float (&tt)[Z], float drho, float dtau,
-                                          const float* omk) const {
+                                          const float* omk, const float* omr = nullptr) const {
     float om[Z];
-    load_om(er, lane, om, omk);
+    if (omr) {
+#pragma unroll
+      for (int s = 0; s < Z; ++s) om[s] = omr[s];
+    } else {
+      load_om(er, lane, om, omk);
+    }
     const float Yf = yrow(er);
     const float X0 = (float)(XE0 - PX0 + Z * lane);
     int i00[Z], i01[Z];
@@ -555,6 +566,10 @@ __device__ __forceinline__ void view_pass(const Tile<Z, INT>& t, const Geom& G, 
   constexpr bool kAdjW = kAdj && !PM;   // the exact adjoint scatter of this pass
   float drho[NV], dtau[NV], fr[NV][NTAP], br[NV][NTAP], y_nx[NV], wa_nx[NV];
   const float* omk[NV];   // per-view disparity map omega_k (A34), nullptr: the shared map in shared memory
+  // PV: each E row's omega_k values are read from global memory once, when the forward pass
+  // reaches the row, and kept (ring position u = E row zeta*li + u, like fr) until its adjoint
+  constexpr int NOR = PV ? NTAP : 1;
+  float omr[NV][NOR][Z];
   size_t lrow0[NV];
   float fa = 0.f, fb = 0.f, fc = 0.f;   // this pass's partial sums (<= BL * NV terms per lane), fp32
 #pragma unroll
@@ -577,7 +592,14 @@ __device__ __forceinline__ void view_pass(const Tile<Z, INT>& t, const Geom& G, 
 #pragma unroll
     for (int u = 0; u < KEEP; ++u)
 #pragma unroll
-      for (int v = 0; v < NV; ++v) fr[v][u] = t.fwd_row(u, lane, drho[v], dtau[v], omk[v], G);
+      for (int v = 0; v < NV; ++v) {
+        if constexpr (PV) {
+          t.load_om(u, lane, omr[v][u], omk[v]);
+          fr[v][u] = t.fwd_row(u, lane, drho[v], dtau[v], omk[v], G, omr[v][u]);
+        } else {
+          fr[v][u] = t.fwd_row(u, lane, drho[v], dtau[v], omk[v], G);
+        }
+      }
   }
   for (int li = 0; li < BL; ++li) {
     const int i = i0 + li;
@@ -594,7 +616,14 @@ __device__ __forceinline__ void view_pass(const Tile<Z, INT>& t, const Geom& G, 
       rho[v] = 0.f;
       if (kFwd) {
 #pragma unroll
-        for (int u = 0; u < Z; ++u) fr[v][KEEP + u] = t.fwd_row(Z * li + KEEP + u, lane, drho[v], dtau[v], omk[v], G);
+        for (int u = 0; u < Z; ++u) {
+          if constexpr (PV) {
+            t.load_om(Z * li + KEEP + u, lane, omr[v][KEEP + u], omk[v]);
+            fr[v][KEEP + u] = t.fwd_row(Z * li + KEEP + u, lane, drho[v], dtau[v], omk[v], G, omr[v][KEEP + u]);
+          } else {
+            fr[v][KEEP + u] = t.fwd_row(Z * li + KEEP + u, lane, drho[v], dtau[v], omk[v], G);
+          }
+        }
         float2 a2 = f2s(0.f);                                            // A_k x at LR pixel (i, j)
 #pragma unroll
         for (int u = 0; u + 1 < NTAP; u += 2) a2 = __ffma2_rn(tap2(G, u), f2(fr[v][u], fr[v][u + 1]), a2);
@@ -619,7 +648,14 @@ __device__ __forceinline__ void view_pass(const Tile<Z, INT>& t, const Geom& G, 
         }
         if constexpr (NTAP & 1) br[v][NTAP - 1] = fmaf(G.taps[NTAP - 1], rho[v], br[v][NTAP - 1]);
 #pragma unroll
-        for (int u = 0; u < Z; ++u) t.adj_row(Z * li + u, lane, br[v][u], drho[v], dtau[v], omk[v], G);
+        for (int u = 0; u < Z; ++u)
+          t.adj_row(Z * li + u, lane, br[v][u], drho[v], dtau[v], omk[v], G, (PV && kFwd) ? omr[v][u] : nullptr);
+        if constexpr (PV && kFwd) {
+#pragma unroll
+          for (int u = 0; u < KEEP; ++u)
+#pragma unroll
+            for (int s = 0; s < Z; ++s) omr[v][u][s] = omr[v][u + Z][s];
+        }
 #pragma unroll
         for (int u = 0; u < NTAP; ++u) br[v][u] = (u < KEEP) ? br[v][u + Z] : 0.f;
       }
@@ -629,7 +665,8 @@ __device__ __forceinline__ void view_pass(const Tile<Z, INT>& t, const Geom& G, 
 #pragma unroll
     for (int v = 0; v < NV; ++v)
 #pragma unroll
-      for (int u = 0; u < KEEP; ++u) t.adj_row(Z * BL + u, lane, br[v][u], drho[v], dtau[v], omk[v], G);
+      for (int u = 0; u < KEEP; ++u)
+        t.adj_row(Z * BL + u, lane, br[v][u], drho[v], dtau[v], omk[v], G, (PV && kFwd) ? omr[v][u] : nullptr);
   }
   pass_reductions<MODE>(G, fa, fb, fc, red_a, red_b, red_c);
 }
