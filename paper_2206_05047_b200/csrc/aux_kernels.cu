@@ -358,62 +358,109 @@ __global__ void __launch_bounds__(256) k_gd_update(const Geom G, float* __restri
 // ctl->cur[slot] (the CG <p, Mp>; M is not symmetric in this mode).  Runs after the tile
 // kernel that wrote rho and the NLTV part of `out`.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void paper_axis(float s, int n, int scale, int R, const float* taps, int& i_lo,
-                                           float (&w)[4]) {
+// One axis of the gather: the LR indices i_lo .. i_lo + 3 whose blur reaches the two bilinear
+// points p0 = floor(s), p0 + 1, and their weights w[t] = (1 - a) g(p0 - zeta i) + a g(p0 + 1 - zeta i)
+// (g = the blur taps, zero outside [-R, R]).  With phi = (R - p0) mod zeta, i_lo = (p0 - R + phi) /
+// zeta and the tap offsets are 2R - phi - zeta t (+1), so the tap pairs come from a per-phase table
+// tp[phi][t] (shared memory, built once per block).  At the clamped last sample a = 0.
+__device__ __forceinline__ void paper_axis(float s, int scale, int R, const float2* tp, int& i_lo, float (&w)[4]) {
   const float fs = floorf(s);
-  const int p0 = (int)fs, p1 = min(p0 + 1, n - 1);
+  const int p0 = (int)fs;
   const float a = s - fs;
-  i_lo = (p0 - R + scale - 1 + scale * 8) / scale - 8;   // ceil((p0 - R) / scale), p0 - R >= -8 scale
+  const int phi = ((R - p0) % scale + scale) % scale;
+  i_lo = (p0 - R + phi) / scale;
 #pragma unroll
   for (int t = 0; t < 4; ++t) {
-    const int i = i_lo + t;
-    const int d0 = p0 - scale * i + R, d1 = p1 - scale * i + R;
-    const float g0 = (d0 >= 0 && d0 <= 2 * R) ? taps[d0] : 0.f;
-    const float g1 = (d1 >= 0 && d1 <= 2 * R) ? taps[d1] : 0.f;
-    w[t] = (1.f - a) * g0 + a * g1;
+    const float2 g = tp[phi * 4 + t];
+    w[t] = fmaf(a, g.y - g.x, g.x);
   }
+}
+
+// LR window of one 32 x 8 HR pixel block: every bilinear point z - dtheta_k omega_0(z) of the
+// block lies within the block +- (SY, SX) (+1 for the second point), so the rho the block
+// reads lies in LR rows [i_lo, i_lo + RH) and columns [j_lo, j_lo + RW) for every view.
+struct GatherWin {
+  int i_lo, j_lo, RH, RW;
+};
+__host__ __device__ inline int floor_div_pos(int a, int b) { return (a + 64 * b) / b - 64; }   // a >= -64 b
+__host__ __device__ inline GatherWin gather_window(const Geom& G, int by0, int bx0) {
+  GatherWin w;
+  const int ylo = max(by0 - G.SY, 0), yhi = min(by0 + 7 + G.SY, G.H - 1) + 1;
+  const int xlo = max(bx0 - G.SX, 0), xhi = min(bx0 + 31 + G.SX, G.W - 1) + 1;
+  w.i_lo = floor_div_pos(ylo - G.R + G.scale - 1, G.scale);
+  w.j_lo = floor_div_pos(xlo - G.R + G.scale - 1, G.scale);
+  w.RH = floor_div_pos(yhi + G.R, G.scale) - w.i_lo + 1;
+  w.RW = floor_div_pos(xhi + G.R, G.scale) - w.j_lo + 1;
+  return w;
+}
+// shared-memory words per staged view (+3 rows / columns of slack: the 4 x 4 read window
+// of a pixel may run past the block window where its weights are zero)
+static inline int gather_stride(const Geom& G) {
+  const int RH = (8 + 2 * G.SY + 1 + 2 * G.R) / G.scale + 2, RW = (32 + 2 * G.SX + 1 + 2 * G.R) / G.scale + 2;
+  return (RH + 3) * (RW + 3);
 }
 
 __global__ void __launch_bounds__(256) k_paper_gather(const Geom G, const Views V, const float* __restrict__ rho,
                                                       const float* __restrict__ omega0, const float* __restrict__ p,
                                                       float* __restrict__ out, float sign, Control* ctl, int slot,
-                                                      int cg_k, int row0, int nrows) {
+                                                      int cg_k, int row0, int nrows, int vchunk, int stride) {
+  extern __shared__ float s_rho[];   // vchunk views x stride words
   __shared__ double red[8];
+  __shared__ float2 s_tp[4 * 4];     // tap pairs per phase (paper_axis)
   if (cg_k >= 2 && ctl->cur[S_STOP] != 0.0) return;   // CG stopped (the tile kernel returned too)
-  const int X = blockIdx.x * 32 + (threadIdx.x & 31);
-  const int Y = row0 + blockIdx.y * 8 + (threadIdx.x >> 5);
-  double part = 0.0;
-  if (X < G.W && Y < row0 + nrows && Y < G.H) {
-    const size_t gi = (size_t)Y * G.ps + X;
-    const float om = omega0[gi];
-    const int h = G.h, w = G.w, Z = G.scale, R = G.R;
-    const size_t lstride = (size_t)h * G.lps;
-    float acc = 0.f;
-    for (int k = 0; k < G.n_views; ++k) {
-      const float2 o = V.off[k];
-      const float sy = fminf(fmaxf((float)Y - o.y * om, 0.f), (float)(G.H - 1));
-      const float sx = fminf(fmaxf((float)X - o.x * om, 0.f), (float)(G.W - 1));
-      int iy, ix;
-      float wy[4], wx[4];
-      paper_axis(sy, G.H, Z, R, G.taps, iy, wy);
-      paper_axis(sx, G.W, Z, R, G.taps, ix, wx);
-      const float* rk = rho + k * lstride;
-      float v = 0.f;
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const int i = iy + t;
-        if (i < 0 || i >= h || wy[t] == 0.f) continue;
-        const float* row = rk + (size_t)i * G.lps;
-        float r = 0.f;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int j = ix + u;
-          if (j >= 0 && j < w) r = fmaf(wx[u], __ldg(row + j), r);
-        }
-        v = fmaf(wy[t], r, v);
-      }
-      acc += v;
+  if (threadIdx.x < 4 * G.scale) {
+    const int phi = threadIdx.x / 4, t = threadIdx.x % 4;
+    const int d = 2 * G.R - phi - G.scale * t;
+    s_tp[threadIdx.x] = make_float2((d >= 0 && d <= 2 * G.R) ? G.taps[d] : 0.f,
+                                    (d + 1 >= 0 && d + 1 <= 2 * G.R) ? G.taps[d + 1] : 0.f);
+  }
+  const int bx0 = blockIdx.x * 32, by0 = row0 + blockIdx.y * 8;
+  const int X = bx0 + (threadIdx.x & 31);
+  const int Y = by0 + (threadIdx.x >> 5);
+  const bool valid = X < G.W && Y < row0 + nrows && Y < G.H;
+  const GatherWin gw = gather_window(G, by0, bx0);
+  const int PWs = gw.RW + 3, PHs = gw.RH + 3;
+  const int h = G.h, w = G.w, Z = G.scale, R = G.R;
+  const size_t lstride = (size_t)h * G.lps;
+  const size_t gi = (size_t)min(Y, G.H - 1) * G.ps + min(X, G.W - 1);
+  const float om = omega0[gi];
+  float acc = 0.f;
+  for (int k0 = 0; k0 < G.n_views; k0 += vchunk) {
+    const int nk = min(vchunk, G.n_views - k0);
+    __syncthreads();   // the previous chunk's reads are done
+    for (int e = threadIdx.x; e < nk * PHs * PWs; e += blockDim.x) {
+      const int kk = e / (PHs * PWs), r = e - kk * (PHs * PWs);
+      const int i = gw.i_lo + r / PWs, j = gw.j_lo + r % PWs;
+      s_rho[kk * stride + r] =
+          (i >= 0 && i < h && j >= 0 && j < w) ? __ldg(rho + (k0 + kk) * lstride + (size_t)i * G.lps + j) : 0.f;
     }
+    __syncthreads();
+    if (valid) {
+      for (int kk = 0; kk < nk; ++kk) {
+        const float2 o = V.off[k0 + kk];
+        const float sy = fminf(fmaxf((float)Y - o.y * om, 0.f), (float)(G.H - 1));
+        const float sx = fminf(fmaxf((float)X - o.x * om, 0.f), (float)(G.W - 1));
+        int iy, ix;
+        float wy[4], wx[4];
+        paper_axis(sy, Z, R, s_tp, iy, wy);
+        paper_axis(sx, Z, R, s_tp, ix, wx);
+        const float* base = s_rho + kk * stride + (iy - gw.i_lo) * PWs + (ix - gw.j_lo);
+        float v = 0.f;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const float* row = base + t * PWs;
+          float r = wx[0] * row[0];
+          r = fmaf(wx[1], row[1], r);
+          r = fmaf(wx[2], row[2], r);
+          r = fmaf(wx[3], row[3], r);
+          v = fmaf(wy[t], r, v);
+        }
+        acc += v;
+      }
+    }
+  }
+  double part = 0.0;
+  if (valid) {
     out[gi] += sign * acc;
     if (p) part = (double)p[gi] * (double)(sign * acc);
   }
@@ -549,7 +596,11 @@ cudaError_t launch_paper_gather(const Geom& G, const Views& V, const float* rho,
                                 float* out, float sign, Control* ctl, int slot, int cg_k, int row0, int nrows,
                                 cudaStream_t st) {
   dim3 grid((G.W + 31) / 32, (nrows + 7) / 8);
-  k_paper_gather<<<grid, 256, 0, st>>>(G, V, rho, omega0, p, out, sign, ctl, slot, cg_k, row0, nrows);
+  const int stride = gather_stride(G);
+  int vchunk = std::max(1, std::min(16, (int)(40 * 1024 / (4 * (size_t)stride))));   // <= 40 KB staged
+  vchunk = std::min(vchunk, G.n_views);
+  k_paper_gather<<<grid, 256, (size_t)vchunk * stride * 4, st>>>(G, V, rho, omega0, p, out, sign, ctl, slot, cg_k,
+                                                                 row0, nrows, vchunk, stride);
   return cudaGetLastError();
 }
 cudaError_t launch_close(const Geom& G, Control* ctl, cudaStream_t st) {
