@@ -317,7 +317,9 @@ def main():
         e2e = {"value": args.e2e_steps * n_it * (1 if strips else world) / (tot / 1000.0), "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(xout.numel()) * 4 + 8 * 11 * n_it,
                "step": "full solve: set_observations (H2D + setup) + %d ADMM iterations + get_hr (D2H)" % n_it,
-               "ms_per_solve": tot / args.e2e_steps, "psnr_db": L.psnr(xout.numpy(), lf.x_gt)}
+               "ms_per_solve": tot / args.e2e_steps,
+               "solve_hr_mpix_per_s": (1 if strips else world) * hr_mpix / (tot / args.e2e_steps / 1000.0),
+               "psnr_db": L.psnr(xout.numpy(), lf.x_gt)}
 
     # ---- roofline of the dominant kernel (the CG normal-operator tile kernel)
     alg = algorithmic(cfg, d)
@@ -378,6 +380,13 @@ def main():
                 "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
                 "scaling": "strong" if strips else "weak", "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic", "hr_mpix_it_per_s": value * hr_mpix,
+                "cu_per_s": value * 2 * (d.cg_max_iters + 1),   # computation units (A33)
+                "paper_context": {
+                    "gpu_vs_oracle": (value / cpu["value"]) if cpu and cpu.get("value") else None,
+                    "paper_gpu_vs_cpu": "43-77x: unnamed OpenCL GPUs vs an i7-5820K, one ADMM iteration, 9x9 "
+                                        "views (P:L1194-1203); context only (other hardware, precision, workload)",
+                    "paper_vs_fl_misr": "2.46x (x2) / 1.57x (x3): 1x GTX 1080Ti vs 4x GTX 1080Ti FL-MISR, DIV8K "
+                                        "MISR (P:L1110-1120); context only"},
                 "config": {"workload": cfg.name, "desc": cfg.note, "views": cfg.n_views, "scale": cfg.scale,
                            "hr": [cfg.H, cfg.W], "cg_steps": d.cg_max_iters, "nltv_window": "5x5",
                            "l2_flush": "512 MiB write between timed steps (outside the events)" if flush is not None else "none",
