@@ -116,10 +116,14 @@ __global__ void k_weights(const Geom G, const float* __restrict__ x, const float
 }
 
 // max |v| over an [H][ps] array (non-negative floats order like their bit patterns).
+// (n is a multiple of 4: pitched rows of 32 floats; float4 loads)
 __global__ void k_absmax(const float* __restrict__ v, size_t n, unsigned* out) {
   float mx = 0.f;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
-    mx = fmaxf(mx, fabsf(v[i]));
+  const float4* v4 = reinterpret_cast<const float4*>(v);
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n / 4; i += (size_t)gridDim.x * blockDim.x) {
+    const float4 a = __ldg(v4 + i);
+    mx = fmaxf(fmaxf(mx, fmaxf(fabsf(a.x), fabsf(a.y))), fmaxf(fabsf(a.z), fabsf(a.w)));
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(mx));
@@ -535,7 +539,9 @@ cudaError_t launch_weights(const Geom& G, const float* x, const float* wo, float
   return cudaGetLastError();
 }
 cudaError_t launch_absmax(const float* v, size_t n, unsigned* out, cudaStream_t st) {
-  k_absmax<<<256, 256, 0, st>>>(v, n, out);
+  const size_t n4 = n / 4;
+  const int blocks = (int)std::max<size_t>(1, std::min<size_t>((n4 + 255) / 256, 148 * 8));
+  k_absmax<<<blocks, 256, 0, st>>>(v, n, out);
   return cudaGetLastError();
 }
 cudaError_t launch_cg_update(const Geom& G, float* x, float* r, const float* p, float* q, Control* ctl, int k,

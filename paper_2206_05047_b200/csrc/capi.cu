@@ -81,6 +81,7 @@ struct lfsr_ctx {
   int num_sms = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t cap_stream = nullptr;
+  cudaEvent_t ev_in[2] = {nullptr, nullptr};   // set_observations: y copy on cap_stream overlapping the omega setup
   bool own_stream = false;
   bool poisoned = false;
   bool ready = false;
@@ -470,6 +471,8 @@ void lfsr_destroy(lfsr_ctx* c) {
   if (!c->poisoned) cudaStreamSynchronize(c->stream);
   free_state(c);
   for (cudaEvent_t e : c->prof_ev) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->ev_in)
+    if (e) cudaEventDestroy(e);
   if (c->comm) {
     if (c->poisoned) nccl_comm_abort(c->comm);
     else nccl_comm_destroy(c->comm);
@@ -526,8 +529,10 @@ static cudaMemcpyKind kind_in(lfsr_mem mem) { return mem == LFSR_MEM_HOST ? cuda
 static cudaMemcpyKind kind_out(lfsr_mem mem) { return mem == LFSR_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice; }
 
 // Copy a dense [rows][cols] array into a pitched [rows][pitch] device array.
-static cudaError_t put2d(lfsr_ctx* c, float* dst, int pitch, const float* src, int cols, size_t rows, lfsr_mem mem) {
-  return cudaMemcpy2DAsync(dst, (size_t)pitch * 4, src, (size_t)cols * 4, (size_t)cols * 4, rows, kind_in(mem), c->stream);
+static cudaError_t put2d(lfsr_ctx* c, float* dst, int pitch, const float* src, int cols, size_t rows, lfsr_mem mem,
+                         cudaStream_t st = nullptr) {
+  return cudaMemcpy2DAsync(dst, (size_t)pitch * 4, src, (size_t)cols * 4, (size_t)cols * 4, rows, kind_in(mem),
+                           st ? st : c->stream);
 }
 static cudaError_t get2d(lfsr_ctx* c, float* dst, int cols, const float* src, int pitch, size_t rows, lfsr_mem mem) {
   return cudaMemcpy2DAsync(dst, (size_t)cols * 4, src, (size_t)pitch * 4, (size_t)cols * 4, rows, kind_out(mem), c->stream);
@@ -806,9 +811,16 @@ lfsr_status lfsr_set_observations(lfsr_ctx* c, const float* lr_views, const floa
     h.ring = P.ring;
     h.cap = kRingCap;
     CK(c, cudaMemcpyAsync(P.S.ctl, &h, sizeof(Control), cudaMemcpyHostToDevice, c->stream));
-    CK(c, put2d(c, P.S.y, G.lps, lr_views, G.w, (size_t)G.n_views * G.h, mem));
     CK(c, put2d(c, P.S.omega, G.ps, disparity, G.W, (size_t)G.H * n_om, mem));
   }
+  // the observations (the large copy) go on the capture stream, so the omega-only setup
+  // below (max|omega|, the splat density) overlaps the transfer
+  for (cudaEvent_t& e : c->ev_in)
+    if (!e) CK(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  CK(c, cudaEventRecord(c->ev_in[0], c->stream));
+  CK(c, cudaStreamWaitEvent(c->cap_stream, c->ev_in[0], 0));
+  for (Part& P : c->parts) CK(c, put2d(c, P.S.y, G.lps, lr_views, G.w, (size_t)G.n_views * G.h, mem, c->cap_stream));
+  CK(c, cudaEventRecord(c->ev_in[1], c->cap_stream));
   State& S0 = c->parts[0].S;
 
   // three maxima with one round trip: max|omega| (halo sizes S = ceil(max_k |dtheta_k|
@@ -819,6 +831,7 @@ lfsr_status lfsr_set_observations(lfsr_ctx* c, const float* lr_views, const floa
   CK(c, launch_absmax(S0.omega, hr * n_om, umax, c->stream));
   CK(c, launch_density(G, c->V, S0.omega, S0.density, c->stream));
   CK(c, launch_absmax(S0.density, hr, umax + 1, c->stream));
+  CK(c, cudaStreamWaitEvent(c->stream, c->ev_in[1], 0));   // y is in place
   CK(c, launch_absmax(S0.y, lr, umax + 2, c->stream));
   unsigned ubits[3] = {0, 0, 0};
   CK(c, cudaMemcpyAsync(ubits, umax, sizeof ubits, cudaMemcpyDeviceToHost, c->stream));
