@@ -256,6 +256,21 @@ typedef struct {
  * UNSUPPORTED (strip decompositions, n_ranks > 1), DIVERGED, OOM, CUDA. */
 LFSR_API lfsr_status lfsr_gd_run(lfsr_ctx* ctx, const lfsr_gd_params* gd, int32_t n_iters, lfsr_gd_stats* stats);
 
+/* Solve n_fields independent light fields of this ctx's geometry, each exactly as
+ * lfsr_set_observations (shared disparity, bicubic x0) + lfsr_admm_run(n_iters) +
+ * lfsr_get_hr would, pipelined: field i+1's inputs are copied to the device and its
+ * setup maxima computed on a second stream while field i's iterations run, and x_i is
+ * copied back asynchronously (the serving path of many light fields, e.g. one per
+ * reference view θ0).  All arrays are HOST memory, one pointer per field:
+ * lr_views[i] [n_views][h][w], view_offsets[i] [n_views][2], disparity[i] [H][W],
+ * x_out[i] [H][W]; page-locked buffers are needed for the copies to overlap (pageable
+ * ones work, serialised).  Blocks until every field is done.  Afterwards the ctx holds
+ * the last field's state.  Errors: INVALID_ARG, UNSUPPORTED (strip decompositions),
+ * DIVERGED (any field), OOM, CUDA. */
+LFSR_API lfsr_status lfsr_solve_batch(lfsr_ctx* ctx, int32_t n_fields, const float* const* lr_views,
+                                      const float* const* view_offsets, const float* const* disparity,
+                                      int32_t n_iters, float* const* x_out);
+
 /* Kernel launches of one gd iteration graph (valid after lfsr_gd_run; 0 before). */
 LFSR_API int32_t lfsr_gd_launches_per_iter(const lfsr_ctx* ctx);
 

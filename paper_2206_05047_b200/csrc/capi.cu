@@ -82,6 +82,19 @@ struct lfsr_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t cap_stream = nullptr;
   cudaEvent_t ev_in[2] = {nullptr, nullptr};   // set_observations: y copy on cap_stream overlapping the omega setup
+  // lfsr_solve_batch: the next field's inputs are staged (copied, maxima) on cap_stream while
+  // the current field solves; graph execs replaced during a batch are retired, not destroyed
+  float* stage_y = nullptr;
+  float* stage_om = nullptr;
+  float* stage_dens = nullptr;
+  unsigned* stage_umax = nullptr;
+  unsigned* h_ubits = nullptr;     // pinned [3]
+  Control* h_ctl = nullptr;        // pinned control-block image
+  double* h_rec = nullptr;         // pinned [batch][T_COUNT] last-iteration records
+  int h_rec_cap = 0;
+  cudaEvent_t ev_b[2] = {nullptr, nullptr};   // [0] staged, [1] previous field solved
+  bool retire = false;
+  std::vector<cudaGraphExec_t> retired;
   bool own_stream = false;
   bool poisoned = false;
   bool ready = false;
@@ -441,7 +454,8 @@ lfsr_status lfsr_create(const lfsr_params* params, lfsr_ctx** out) {
 static void free_graph(lfsr_ctx* c) {
   for (auto& g : c->graph)
     if (g) {
-      cudaGraphExecDestroy(g);
+      if (c->retire) c->retired.push_back(g);   // launches may still be pending (lfsr_solve_batch)
+      else cudaGraphExecDestroy(g);
       g = nullptr;
     }
   if (c->gd_graph) {
@@ -458,6 +472,8 @@ static void free_state(lfsr_ctx* c) {
   c->tmp_hr2 = nullptr;
   c->tmp_s = nullptr;
   c->gd_g = nullptr;
+  c->stage_y = c->stage_om = c->stage_dens = nullptr;
+  c->stage_umax = nullptr;
   c->op_ctl = nullptr;
   c->umax = nullptr;
   c->d_ctls = nullptr;
@@ -473,6 +489,12 @@ void lfsr_destroy(lfsr_ctx* c) {
   for (cudaEvent_t e : c->prof_ev) cudaEventDestroy(e);
   for (cudaEvent_t e : c->ev_in)
     if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->ev_b)
+    if (e) cudaEventDestroy(e);
+  for (cudaGraphExec_t g : c->retired) cudaGraphExecDestroy(g);
+  if (c->h_ubits) cudaFreeHost(c->h_ubits);
+  if (c->h_ctl) cudaFreeHost(c->h_ctl);
+  if (c->h_rec) cudaFreeHost(c->h_rec);
   if (c->comm) {
     if (c->poisoned) nccl_comm_abort(c->comm);
     else nccl_comm_destroy(c->comm);
@@ -1368,6 +1390,156 @@ lfsr_status lfsr_gd_run(lfsr_ctx* c, const lfsr_gd_params* gp, int32_t n_iters, 
 }
 
 int32_t lfsr_gd_launches_per_iter(const lfsr_ctx* c) { return (c && c->gd_graph) ? c->gd_launches : 0; }
+
+// ---------------------------------------------------------------------------
+// Batch of independent light fields through one ctx (the serving path): field i + 1's
+// inputs are copied to the device and its setup maxima computed on the capture stream
+// while field i's ADMM iterations run on the ctx stream; x_i comes back asynchronously.
+// Per field the device work is the same as set_observations + admm_run + get_hr.
+// ---------------------------------------------------------------------------
+static lfsr_status batch_stage(lfsr_ctx* c, const float* y, const float* off, const float* disp, Views& V2) {
+  const Geom& G = c->G;
+  const size_t hr = (size_t)G.H * G.ps, lr = (size_t)G.n_views * G.h * G.lps;
+  cudaStream_t cs = c->cap_stream;
+  CK(c, cudaStreamWaitEvent(cs, c->ev_b[1], 0));   // the buffers of field i - 1 are free
+  CK(c, put2d(c, c->stage_om, G.ps, disp, G.W, (size_t)G.H, LFSR_MEM_HOST, cs));
+  CK(c, put2d(c, c->stage_y, G.lps, y, G.w, (size_t)G.n_views * G.h, LFSR_MEM_HOST, cs));
+  CK(c, cudaMemsetAsync(c->stage_dens, 0, hr * 4, cs));
+  CK(c, cudaMemsetAsync(c->stage_umax, 0, 3 * sizeof(unsigned), cs));
+  for (int k = 0; k < G.n_views; ++k) V2.off[k] = make_float2(off[2 * k], off[2 * k + 1]);
+  CK(c, launch_absmax(c->stage_om, hr, c->stage_umax, cs));
+  CK(c, launch_density(G, V2, c->stage_om, c->stage_dens, cs));
+  CK(c, launch_absmax(c->stage_dens, hr, c->stage_umax + 1, cs));
+  CK(c, launch_absmax(c->stage_y, lr, c->stage_umax + 2, cs));
+  CK(c, cudaMemcpyAsync(c->h_ubits, c->stage_umax, 3 * sizeof(unsigned), cudaMemcpyDeviceToHost, cs));
+  CK(c, cudaEventRecord(c->ev_b[0], cs));
+  return LFSR_OK;
+}
+
+static lfsr_status batch_finish(lfsr_ctx* c, const float* off, const Views& V2) {
+  Geom& G = c->G;
+  const size_t hr = (size_t)G.H * G.ps, lr = (size_t)G.n_views * G.h * G.lps, ws = (size_t)G.s_d * hr;
+  CK(c, cudaEventSynchronize(c->ev_b[0]));   // the maxima (the ctx stream keeps solving meanwhile)
+  float om_max, mx_rho = 0.f, mx_tau = 0.f;
+  memcpy(&om_max, &c->h_ubits[0], 4);
+  if (!std::isfinite(om_max)) FAIL(c, LFSR_ERR_INVALID_ARG, "disparity must be finite");
+  for (int k = 0; k < G.n_views; ++k) {
+    if (!std::isfinite(off[2 * k]) || !std::isfinite(off[2 * k + 1]))
+      FAIL(c, LFSR_ERR_INVALID_ARG, "view_offsets must be finite");
+    mx_rho = std::fmax(mx_rho, std::fabs(off[2 * k]));
+    mx_tau = std::fmax(mx_tau, std::fabs(off[2 * k + 1]));
+  }
+  State& S = c->parts[0].S;
+  std::swap(S.y, c->stage_y);          // the staged inputs become the state; the old ones are staged into next
+  std::swap(S.omega, c->stage_om);
+  std::swap(S.density, c->stage_dens);
+  c->V = V2;
+  G.SX = std::min((int)std::ceil(mx_rho * om_max), G.W);
+  G.SY = std::min((int)std::ceil(mx_tau * om_max), G.H);
+  memcpy(&G.dmax, &c->h_ubits[1], 4);
+  memcpy(&G.ymax, &c->h_ubits[2], 4);
+  if (!std::isfinite(G.ymax)) G.ymax = 0.f;
+  bool tune = false;
+  initial_tiles(c, &tune);
+  lfsr_status st;
+  if ((st = setup_tiles(c)) != LFSR_OK) return st;
+  // reset (Alg.1 lines 1-2) and a1 on the ctx stream, after field i's iterations and x_i's copy
+  CK(c, cudaMemsetAsync(S.wA, 0, lr * 4, c->stream));
+  CK(c, cudaMemsetAsync(S.wS[0], 0, ws * 4, c->stream));
+  CK(c, cudaMemsetAsync(S.wS[1], 0, ws * 4, c->stream));
+  CK(c, cudaMemsetAsync(S.r, 0, hr * 4, c->stream));
+  CK(c, cudaMemsetAsync(S.q, 0, hr * 4, c->stream));
+  CK(c, cudaMemsetAsync(S.p[0], 0, hr * 4, c->stream));
+  CK(c, cudaMemsetAsync(S.p[1], 0, hr * 4, c->stream));
+  CK(c, cudaMemcpyAsync(S.ctl, c->h_ctl, sizeof(Control), cudaMemcpyHostToDevice, c->stream));
+  c->h_iter = 0;
+  c->solver = 0;
+  CK(c, launch_bicubic(G, S.y, S.x, c->stream));
+  CK(c, launch_setup_wo(G, c->V, S.y, S.omega, S.wo, c->stream));
+  CK(c, launch_weights(G, S.x, S.wo, S.m, c->stream));
+  if (tune && (st = tune_tile_bl(c)) != LFSR_OK) return st;
+  return build_graphs(c);
+}
+
+lfsr_status lfsr_solve_batch(lfsr_ctx* c, int32_t n_fields, const float* const* lr_views,
+                             const float* const* view_offsets, const float* const* disparity, int32_t n_iters,
+                             float* const* x_out) {
+  if (!c) return LFSR_ERR_INVALID_ARG;
+  if (c->poisoned) FAIL(c, LFSR_ERR_STATE, "ctx is poisoned by an earlier CUDA/NCCL error");
+  if (n_fields < 1 || n_iters < 1 || !lr_views || !view_offsets || !disparity || !x_out)
+    FAIL(c, LFSR_ERR_INVALID_ARG, "n_fields, n_iters >= 1 and non-NULL pointer arrays required");
+  if (c->xmode != X_NONE) FAIL(c, LFSR_ERR_UNSUPPORTED, "lfsr_solve_batch runs on a single strip");
+  if (n_iters > kRingCap) FAIL(c, LFSR_ERR_INVALID_ARG, "n_iters must be <= 4096");
+  lfsr_status st;
+  for (int i = 0; i < n_fields; ++i) {
+    if ((st = check_ptr(c, lr_views[i], LFSR_MEM_HOST, "lr_views[i]")) != LFSR_OK) return st;
+    if ((st = check_ptr(c, view_offsets[i], LFSR_MEM_HOST, "view_offsets[i]")) != LFSR_OK) return st;
+    if ((st = check_ptr(c, disparity[i], LFSR_MEM_HOST, "disparity[i]")) != LFSR_OK) return st;
+    if ((st = check_ptr(c, x_out[i], LFSR_MEM_HOST, "x_out[i]")) != LFSR_OK) return st;
+  }
+  // field 0: the ordinary path (allocation, tiling, graphs)
+  if ((st = lfsr_set_observations(c, lr_views[0], view_offsets[0], disparity[0], LFSR_DISP_SHARED, nullptr,
+                                  LFSR_MEM_HOST)) != LFSR_OK)
+    return st;
+  const Geom& G = c->G;
+  const size_t hr = (size_t)G.H * G.ps, lr = (size_t)G.n_views * G.h * G.lps;
+  if (!c->stage_y) {
+    void* p = nullptr;
+    cudaError_t e;
+    if ((e = dalloc(c, &p, lr * 4)) != cudaSuccess) return cuda_fail(c, e, "alloc");
+    c->stage_y = (float*)p;
+    if ((e = dalloc(c, &p, hr * 4)) != cudaSuccess) return cuda_fail(c, e, "alloc");
+    c->stage_om = (float*)p;
+    if ((e = dalloc(c, &p, hr * 4)) != cudaSuccess) return cuda_fail(c, e, "alloc");
+    c->stage_dens = (float*)p;
+    if ((e = dalloc(c, &p, 4 * sizeof(unsigned))) != cudaSuccess) return cuda_fail(c, e, "alloc");
+    c->stage_umax = (unsigned*)p;
+  }
+  if (!c->h_ubits) CK(c, cudaMallocHost(&c->h_ubits, 4 * sizeof(unsigned)));
+  if (!c->h_ctl) {
+    CK(c, cudaMallocHost(&c->h_ctl, sizeof(Control)));
+    Control h{};
+    h.ring = c->parts[0].ring;
+    h.cap = kRingCap;
+    *c->h_ctl = h;
+  }
+  if (c->h_rec_cap < n_fields) {
+    if (c->h_rec) cudaFreeHost(c->h_rec);
+    c->h_rec = nullptr;
+    c->h_rec_cap = 0;
+    CK(c, cudaMallocHost(&c->h_rec, (size_t)n_fields * T_COUNT * sizeof(double)));
+    c->h_rec_cap = n_fields;
+  }
+  for (cudaEvent_t& e : c->ev_b)
+    if (!e) CK(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  CK(c, cudaEventRecord(c->ev_b[1], c->stream));   // nothing of this batch is using the staging buffers
+  c->retire = true;
+  Views V2;
+  st = LFSR_OK;
+  for (int i = 0; i < n_fields && st == LFSR_OK; ++i) {
+    if ((st = lfsr_admm_enqueue(c, n_iters)) != LFSR_OK) break;
+    const double* rec = c->parts[0].ring + (size_t)((c->h_iter - 1) % kRingCap) * T_COUNT;
+    cudaError_t e = get2d(c, x_out[i], G.W, c->parts[0].S.x, G.ps, (size_t)G.H, LFSR_MEM_HOST);
+    if (e != cudaSuccess) { st = cuda_fail(c, e, "x_out copy"); break; }
+    e = cudaMemcpyAsync(c->h_rec + (size_t)i * T_COUNT, rec, T_COUNT * sizeof(double), cudaMemcpyDeviceToHost,
+                        c->stream);
+    if (e != cudaSuccess) { st = cuda_fail(c, e, "record copy"); break; }
+    if (i + 1 < n_fields) {
+      if ((st = batch_stage(c, lr_views[i + 1], view_offsets[i + 1], disparity[i + 1], V2)) != LFSR_OK) break;
+      if ((e = cudaEventRecord(c->ev_b[1], c->stream)) != cudaSuccess) { st = cuda_fail(c, e, "event"); break; }
+      st = batch_finish(c, view_offsets[i + 1], V2);
+    }
+  }
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  c->retire = false;
+  for (cudaGraphExec_t g : c->retired) cudaGraphExecDestroy(g);
+  c->retired.clear();
+  if (st != LFSR_OK) return st;
+  if (e != cudaSuccess) return cuda_fail(c, e, "cudaStreamSynchronize");
+  for (int i = 0; i < n_fields; ++i)
+    if (c->h_rec[(size_t)i * T_COUNT + T_NF] != 0.0) FAIL(c, LFSR_ERR_DIVERGED, "non-finite x or cost in a batch field");
+  return LFSR_OK;
+}
 
 lfsr_status lfsr_profile(lfsr_ctx* c, int32_t enable) {
   lfsr_status st = check_run(c);

@@ -33,7 +33,7 @@ OPS = {"A": OP_A, "AT": OP_AT, "S": OP_S, "ST": OP_ST, "NORMAL": OP_NORMAL, "WEI
 EXPORTS = ("lfsr_create", "lfsr_set_observations", "lfsr_admm_run", "lfsr_admm_enqueue", "lfsr_admm_stats",
            "lfsr_get_hr", "lfsr_get_state", "lfsr_op_apply", "lfsr_launches_per_iter", "lfsr_tile_config", "lfsr_profile",
            "lfsr_profile_read", "lfsr_strip_plan", "lfsr_destroy", "lfsr_last_error", "lfsr_abi_version",
-           "lfsr_gd_run", "lfsr_gd_launches_per_iter", "lfsr_rgb_to_ycbcr", "lfsr_ycbcr_to_rgb")
+           "lfsr_gd_run", "lfsr_gd_launches_per_iter", "lfsr_rgb_to_ycbcr", "lfsr_ycbcr_to_rgb", "lfsr_solve_batch")
 
 
 class LFSRError(RuntimeError):
@@ -138,6 +138,8 @@ def load_library(path: str = LIB_PATH):
     lib.lfsr_gd_run.restype = st
     lib.lfsr_gd_launches_per_iter.argtypes = [vp]
     lib.lfsr_gd_launches_per_iter.restype = ctypes.c_int32
+    lib.lfsr_solve_batch.argtypes = [vp, ctypes.c_int32, P(vp), P(vp), P(vp), ctypes.c_int32, P(vp)]
+    lib.lfsr_solve_batch.restype = st
     lib.lfsr_rgb_to_ycbcr.argtypes = [vp, vp, vp, vp, ctypes.c_size_t, vp]
     lib.lfsr_rgb_to_ycbcr.restype = st
     lib.lfsr_ycbcr_to_rgb.argtypes = [vp, vp, vp, vp, ctypes.c_size_t, vp]
@@ -322,6 +324,28 @@ class Solver:
             raise err
         self._check(s)
         return stats
+
+    def solve_batch(self, fields, n_iters: int, outs=None):
+        """lfsr_solve_batch: fields = [(lr_views, view_offsets, disparity), ...] host arrays (page-locked
+        torch tensors for overlapped copies, or numpy); returns the HR estimates (into `outs` if given)."""
+        n = len(fields)
+        keep = []
+        arrs = [[], [], []]
+        for f in fields:
+            for j, a in enumerate(f):
+                ptr, mem, k = self._ptr_in(a)
+                if mem != MEM_HOST:
+                    raise ValueError("lfsr_solve_batch takes host arrays")
+                keep.append(k)
+                arrs[j].append(ptr)
+        p = self.params
+        if outs is None:
+            outs = [np.empty((p.H, p.W), np.float32) for _ in range(n)]
+        optr = [o.data_ptr() if _is_torch(o) else o.ctypes.data for o in outs]
+        A = lambda v: (ctypes.c_void_p * n)(*v)
+        self._check(self.lib.lfsr_solve_batch(self._h, n, A(arrs[0]), A(arrs[1]), A(arrs[2]), int(n_iters),
+                                              A(optr)))
+        return outs
 
     def gd_launches_per_iter(self) -> int:
         return int(self.lib.lfsr_gd_launches_per_iter(self._h))
