@@ -23,10 +23,15 @@
 // Arithmetic is packed FP32 (FFMA2/FADD2/FMUL2) over a lane's column pairs; the
 // tiling (BL, view groups, warps) is chosen per problem by tile_kernels.cu /
 // capi.cu.
+// Compile-time variants: PV reads each view's own disparity map omega_k
+// (A34), P2 replaces the separable Gaussian by a user blur kernel (view_pass2d, A36), PM
+// stops after the epilogue and leaves the adjoint to the paper's backward warp
+// (k_paper_gather, A37).
 //
 // Fixed-point scale: every CTA bounds |t| (the blurred adjoint value of one
 // source) by tb (c_A max|p| for NORMAL; l2 (max|x| + max|y|) + (th/2) l1 3/th for
-// WZ) and the accumulated weight per cell by the splat density max_z sum_k
+// WZ; l1 + 2 l2 (max|x| + max|y|) for GRAD; max|x| carries sum|k| with a user kernel)
+// and the accumulated weight per cell by the splat density max_z sum_k
 // (W_k^T 1)(z) (computed once at setup), and picks 2^s with |w t 2^s| < 2^21 and
 // |acc| < 2^30: the per-contribution rounding is <= 2^-22 tb.
 #pragma once
