@@ -48,3 +48,22 @@ def test_batch_rejects_device_arrays(lfsr_mod):
     with lfsr_mod.Solver(p) as s:
         with pytest.raises(ValueError):
             s.solve_batch([(torch.from_numpy(lf.y).cuda(), lf.view_offsets, lf.omega)], 2)
+
+
+@pytest.mark.parametrize("over", [dict(psf="motion"), dict(paper_adjoint=1)], ids=["psf", "paper"])
+def test_batch_with_modes(lfsr_mod, over):
+    """The serving path with a user blur kernel and with the paper-mode adjoint."""
+    kw = dict(over)
+    if kw.get("psf") == "motion":
+        kw["psf"] = S.motion_psf(5, 45.0)
+    lfs = [S.make_lightfield("C1", seed=700 + i) for i in range(3)]
+    p = params(lfsr_mod, "C1")
+    for k, v in kw.items():
+        setattr(p, k, v)
+    with lfsr_mod.Solver(p) as s:
+        outs = s.solve_batch([(lf.y, lf.view_offsets, lf.omega) for lf in lfs], 3)
+    with lfsr_mod.Solver(p) as s:
+        for lf, o in zip(lfs, outs):
+            s.set_observations(lf.y, lf.view_offsets, lf.omega)
+            s.admm_run(3)
+            assert rel_l2(o, s.get_hr()) <= 1e-6
