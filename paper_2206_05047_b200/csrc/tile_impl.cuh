@@ -437,13 +437,15 @@ __device__ __forceinline__ float nltv_pixel(const NltvCtx& c, const Geom& G, int
   const float mz = c.M[mi];
   float acc = 0.f;
   float fpq = 0.f, freg = 0.f, fres = 0.f;   // this pixel's reduction terms (<= s_d each), fp32
+  // the m tile pitch is a compile-time constant on the unrolled (RAD > 0) path
+  const int MW = RAD > 0 ? TC<Z>::TX + 2 * RAD : c.MW;
   auto one = [&](int d, int dy, int dx) {
     const float wd = G.wd[d];
     const bool fin = !CHECK || ((Y + dy >= 0) && (Y + dy < c.H) && (X + dx >= 0) && (X + dx < c.W));
     const bool bin = !CHECK || ((Y - dy >= 0) && (Y - dy < c.H) && (X - dx >= 0) && (X - dx < c.W));
     const float xf = c.P[pidx<Z>(py + dy, px + dx, c.PW, c.PWZ)];   // in the tile even when outside Omega
     const float xb = c.P[pidx<Z>(py - dy, px - dx, c.PW, c.PWZ)];
-    const float mb = c.M[mi - dy * c.MW - dx];
+    const float mb = c.M[mi - dy * MW - dx];
     if (MODE == MODE_GRAD || MODE == MODE_J) {
       // G_d = W_d (.) Delta_d x and the subgradient S_w^T sgn(G) in gather form (A30)
       const float wz = wd * mz;
