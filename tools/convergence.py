@@ -58,8 +58,13 @@ def timed(fn):
 
 def run_admm(lf, reweight, K, cu_budget, tol=0.0):
     s = make(lf, reweight, K, tol)
-    n = max(1, cu_budget // (2 * (K + 1)) + 1)
-    st, ms = timed(lambda: s.admm_run(n))
+    st, ms, cu = [], 0.0, 0
+    while cu < cu_budget and len(st) < 400:   # with tau > 0 the CG steps per iteration vary
+        r, t = timed(lambda: s.admm_run(1))
+        st += r
+        ms += t
+        cu += 2 * (1 + r[0]["cg_iters"])
+    n = len(st)
     x = s.get_hr()
     s.close()
     cu = np.concatenate([[0], np.cumsum([2 * (1 + r["cg_iters"]) for r in st])])
@@ -121,6 +126,14 @@ def main():
            "cu_rule": "reading A33: gd 2 + trials per iteration, ADMM 2(1 + CG steps)"}
     res["admm-5"] = run_admm(lf, a.reweight, 5, a.cu)
     res["admm-10"] = run_admm(lf, a.reweight, 10, a.cu)
+    # with the CG early stop active (Alg.2 line 5): tau = 1e-3 of the first <r0, r0>
+    s0 = make(lf, a.reweight)
+    pi0 = s0.admm_run(1)[0]["cg_pi0"]
+    s0.close()
+    tau = 1e-3 * pi0
+    res["tau"] = tau
+    res["admm-5-tau"] = run_admm(lf, a.reweight, 5, a.cu, tol=tau)
+    res["admm-10-tau"] = run_admm(lf, a.reweight, 10, a.cu, tol=tau)
     sweep = {}
     for k in range(2, 14):
         try:
@@ -137,9 +150,10 @@ def main():
                                "gd": time_solver(lf, a.reweight, "gd", res["gd"]["step"]),
                                "gd-ls": time_solver(lf, a.reweight, "gd-ls", 1.0)}
     marks = [c for c in (24, 48, 96, 120, 192, 240, 480) if c <= a.cu]
-    res["J_at_cu"] = {name: {c: at_cu(res[name], c) for c in marks} for name in ("admm-5", "admm-10", "gd", "gd-ls")}
+    names = ("admm-5", "admm-10", "admm-5-tau", "admm-10-tau", "gd", "gd-ls")
+    res["J_at_cu"] = {name: {c: at_cu(res[name], c) for c in marks} for name in names}
     print(json.dumps({k: v for k, v in res.items() if k in ("config", "J_at_cu", "gd_sweep_final_J", "warm_ms_per_iter")}, indent=1))
-    for name in ("admm-5", "admm-10", "gd", "gd-ls"):
+    for name in names:
         r = res[name]
         print("%-8s iters %3d  %.3f ms/iter  final J %.6g  PSNR %.2f dB" % (name, r["iters"], r["ms_per_iter"],
                                                                         r["J"][-1], r["psnr_final"]))
