@@ -290,13 +290,14 @@ LFSR_API lfsr_status lfsr_ycbcr_to_rgb(const float* y, const float* cb, const fl
 LFSR_API int32_t lfsr_launches_per_iter(const lfsr_ctx* ctx);
 
 /* Tiling of the fused operator kernel chosen for this context:
- * LR rows per tile, view groups (CTAs per tile) and warps per CTA.  A single
- * strip picks them at its first lfsr_set_observations of a geometry by timing
- * the CG normal-operator kernel for a few candidates (cached per process;
- * environment LFSR_TILE_BL / LFSR_TILE_GNW="groups,warps" force them).  Any
- * out pointer may be NULL.  LFSR_ERR_STATE before set_observations. */
+ * LR rows per tile, view groups (CTAs per tile), warps per CTA, and warps per
+ * CTA of the CG normal-operator launches (may be wider: up to 16 at zeta = 2).
+ * A single strip picks them at its first lfsr_set_observations of a geometry by
+ * timing the CG normal-operator kernel for a few candidates (cached per process;
+ * environment LFSR_TILE_BL / LFSR_TILE_GNW="groups,warps" / LFSR_TILE_NWN force
+ * them).  Any out pointer may be NULL.  LFSR_ERR_STATE before set_observations. */
 LFSR_API lfsr_status lfsr_tile_config(const lfsr_ctx* ctx, int32_t* tile_rows, int32_t* view_groups,
-                                      int32_t* warps_per_cta);
+                                      int32_t* warps_per_cta, int32_t* cg_warps_per_cta);
 
 /* Row-strip plan of the multi-GPU decomposition (DESIGN 10): rank r
  * owns tile rows [tile_row0, tile_row1) = LR rows [lr_row0, lr_row1) = HR rows

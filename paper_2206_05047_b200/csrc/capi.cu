@@ -22,6 +22,7 @@ TileGeom make_tile_geom(const Geom& G, int num_sms, int tr0, int tr1);
 void tile_static(int scale, int& BL, int& LX, int& R, int& KEEP);
 int tile_bl_candidates(int scale, int* out, int cap);
 int tile_max_warps(int scale);
+int tile_max_warps_normal(int scale);
 cudaError_t prepare_tile_kernels(int scale, size_t smem);
 cudaError_t launch_tile(int mode, const Geom& G, const Views& V, const TileGeom& T, const TileIO& io,
                         cudaStream_t st);
@@ -508,13 +509,15 @@ const char* lfsr_last_error(const lfsr_ctx* c) { return c ? c->err.c_str() : g_c
 
 int32_t lfsr_launches_per_iter(const lfsr_ctx* c) { return (c && c->ready) ? c->launches_per_iter : 0; }
 
-lfsr_status lfsr_tile_config(const lfsr_ctx* c, int32_t* tile_rows, int32_t* view_groups, int32_t* warps_per_cta) {
+lfsr_status lfsr_tile_config(const lfsr_ctx* c, int32_t* tile_rows, int32_t* view_groups, int32_t* warps_per_cta,
+                             int32_t* cg_warps_per_cta) {
   if (!c) return LFSR_ERR_INVALID_ARG;
   if (!c->ready || c->parts.empty()) return LFSR_ERR_STATE;
   const TileGeom& T = c->parts[0].T;
   if (tile_rows) *tile_rows = T.BL;
   if (view_groups) *view_groups = T.groups;
   if (warps_per_cta) *warps_per_cta = T.nwarps;
+  if (cg_warps_per_cta) *cg_warps_per_cta = T.nwarps_n;
   return LFSR_OK;
 }
 
@@ -636,8 +639,8 @@ static lfsr_status setup_tiles(lfsr_ctx* c) {
   }
   c->Tfull = make_tile_geom(G, c->num_sms, -1, -1);
   if (c->Tfull.smem > 227 * 1024) FAIL(c, LFSR_ERR_UNSUPPORTED, "disparity range too large for the shared-memory tile");
-  size_t smem_max = c->Tfull.smem;   // the kernels' dynamic smem limit must cover every strip's launch
-  for (const Part& P : c->parts) smem_max = std::max(smem_max, P.T.smem);
+  size_t smem_max = std::max(c->Tfull.smem, c->Tfull.smem_normal);   // must cover every launch
+  for (const Part& P : c->parts) smem_max = std::max(smem_max, std::max(P.T.smem, P.T.smem_normal));
   CK(c, prepare_tile_kernels(G.scale, smem_max));
 
   return LFSR_OK;
@@ -652,7 +655,7 @@ static lfsr_status setup_tiles(lfsr_ctx* c) {
 // match lfsr_strip_plan, which has no observations to tune on).
 static std::mutex g_tune_mu;
 struct TileChoice {
-  int bl, g, nw;
+  int bl, g, nw, nwn;   // nwn: warps of the CG-operator launches
 };
 static std::map<std::string, TileChoice> g_tuned;
 
@@ -667,7 +670,7 @@ static std::string tune_key(const lfsr_ctx* c) {
 static void initial_tiles(lfsr_ctx* c, bool* tune) {
   Geom& G = c->G;
   *tune = false;
-  G.tile_bl = G.tile_g = G.tile_nw = 0;
+  G.tile_bl = G.tile_g = G.tile_nw = G.tile_nwn = 0;
   if (const char* e = getenv("LFSR_TILE_BL")) {
     const int v = atoi(e);
     if (v > 0) G.tile_bl = v;
@@ -676,6 +679,10 @@ static void initial_tiles(lfsr_ctx* c, bool* tune) {
     int g = 0, w = 0;
     if (sscanf(e, "%d,%d", &g, &w) == 2 && g > 0 && w > 0) { G.tile_g = g; G.tile_nw = w; }
   }
+  if (const char* e = getenv("LFSR_TILE_NWN")) {   // warps of the CG-operator launches
+    const int v = atoi(e);
+    if (v > 0) G.tile_nwn = v;
+  }
   if (G.tile_bl || G.tile_g || c->xmode != X_NONE) return;
   std::lock_guard<std::mutex> lk(g_tune_mu);
   auto it = g_tuned.find(tune_key(c));
@@ -683,6 +690,7 @@ static void initial_tiles(lfsr_ctx* c, bool* tune) {
     G.tile_bl = it->second.bl;
     G.tile_g = it->second.g;
     G.tile_nw = it->second.nw;
+    G.tile_nwn = it->second.nwn;
     return;
   }
   *tune = true;
@@ -703,7 +711,7 @@ static lfsr_status tune_tile_bl(lfsr_ctx* c) {
   cudaEvent_t e0, e1;
   CK(c, cudaEventCreate(&e0));
   CK(c, cudaEventCreate(&e1));
-  TileChoice best{0, 0, 0};
+  TileChoice best{0, 0, 0, 0};
   float best_ms = 1e30f;
   for (int i = 0; i < n; ++i) {
     if (cand[i] > G.h && i > 0) continue;
@@ -742,8 +750,38 @@ static lfsr_status tune_tile_bl(lfsr_ctx* c) {
                 ms * 1000.f / 3);
       if (ms < best_ms * 0.98f) {   // a later candidate must win by 2 % (stable choice)
         best_ms = ms;
-        best = TileChoice{cand[i], T.groups, T.nwarps};
+        best = TileChoice{cand[i], T.groups, T.nwarps, T.nwarps};
       }
+    }
+  }
+  // the CG-operator launches may use wider CTAs than the wz-step (zeta = 2: up to 16 warps):
+  // kept if 2 % faster for the chosen tiling
+  const int maxwn = tile_max_warps_normal(G.scale);
+  if (maxwn > best.nw && best.bl > 0) {
+    G.tile_bl = best.bl;
+    G.tile_g = best.g;
+    G.tile_nw = best.nw;
+    G.tile_nwn = maxwn;
+    TileGeom T = make_tile_geom(G, c->num_sms, -1, -1);
+    if (T.smem_normal <= 227 * 1024 && T.nwarps_n == maxwn) {
+      CK(c, prepare_tile_kernels(G.scale, std::max(T.smem, T.smem_normal)));
+      TileIO io = base_io(P);
+      io.ctl = c->tune_ctl;
+      io.in_hr = P.S.x;
+      io.out_hr = P.S.tmp_hr;
+      io.do_nltv = 1;
+      CK(c, cudaMemsetAsync(c->tune_ctl, 0, sizeof(Control), c->stream));
+      CK(c, launch_tile(MODE_NORMAL, G, c->V, T, io, c->stream));     // warm
+      CK(c, cudaEventRecord(e0, c->stream));
+      for (int r = 0; r < 3; ++r) CK(c, launch_tile(MODE_NORMAL, G, c->V, T, io, c->stream));
+      CK(c, cudaEventRecord(e1, c->stream));
+      CK(c, cudaEventSynchronize(e1));
+      float ms = 0.f;
+      CK(c, cudaEventElapsedTime(&ms, e0, e1));
+      if (getenv("LFSR_TUNE_VERBOSE"))
+        fprintf(stderr, "lfsr tile tuning: BL %d groups %d warps %d, CG operator %d warps  %.1f us\n", best.bl,
+                best.g, best.nw, maxwn, ms * 1000.f / 3);
+      if (ms < best_ms * 0.98f) best.nwn = maxwn;
     }
   }
   cudaEventDestroy(e0);
@@ -752,6 +790,7 @@ static lfsr_status tune_tile_bl(lfsr_ctx* c) {
   G.tile_bl = best.bl;
   G.tile_g = best.g;
   G.tile_nw = best.nw;
+  G.tile_nwn = best.nwn;
   {
     std::lock_guard<std::mutex> lk(g_tune_mu);
     g_tuned[tune_key(c)] = best;

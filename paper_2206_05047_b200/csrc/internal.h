@@ -63,6 +63,7 @@ struct Geom {
   float cS;                   // theta / 2
   int32_t tile_bl;            // LR rows per tile (host-chosen, 0 = the zeta default; see make_tile_geom)
   int32_t tile_g, tile_nw;    // view groups and warps per CTA (host-chosen, 0 = the cost model's choice)
+  int32_t tile_nwn;           // warps per CTA of the NORMAL launches (host-chosen, 0 = tile_nw)
   int32_t per_view;           // 1: omega is [n_views][H][ps], view k warped with omega_k (A34)
   int32_t psf2d;              // 1: user blur kernel (A36) in psf2 instead of the separable taps
   int32_t paper;              // 1: the paper's backward-warp adjoint W_k^* with omega_0 (A37)
@@ -96,6 +97,7 @@ struct TileGeom {
   int32_t groups;             // view groups (CTAs per tile)
   int32_t vpg;                // views per group
   int32_t nwarps;             // warps per CTA (views of a group are dealt round-robin)
+  int32_t nwarps_n;           // warps per CTA of the NORMAL (CG operator) launches (may exceed nwarps)
   size_t smem;                // dynamic shared memory bytes (largest mode)
   size_t smem_normal;         // ... of the NORMAL mode
 };

@@ -37,10 +37,21 @@ template <> struct TileCfg<2> { static constexpr int R = 2, LX = 30, BL = 16; };
 template <> struct TileCfg<3> { static constexpr int R = 3, LX = 30, BL = 11; };
 template <> struct TileCfg<4> { static constexpr int R = 3, LX = 31, BL = 6; };
 
+#ifndef LFSR_MAXW2N
+#define LFSR_MAXW2N 16    // zeta = 2 CG-operator launches: up to 16 warps (the kernel fits 128 registers)
+#endif
+
 template <int Z> struct LaunchCfg;
 template <> struct LaunchCfg<2> { static constexpr int MAXW = LFSR_MAXW2, MINB = LFSR_MINB2; };
 template <> struct LaunchCfg<3> { static constexpr int MAXW = LFSR_MAXW3, MINB = LFSR_MINB3; };
 template <> struct LaunchCfg<4> { static constexpr int MAXW = LFSR_MAXW4, MINB = LFSR_MINB4; };
+
+// per mode: the CG-operator kernel at zeta = 2 may run 16-warp CTAs (e.g. 25 views in 2 rounds
+// instead of 3); the other modes keep the 12-warp bound (a 512-thread bound costs them registers)
+template <int Z, int MODE> struct LaunchCfgM {
+  static constexpr int MAXW = (Z == 2 && MODE == MODE_NORMAL) ? LFSR_MAXW2N : LaunchCfg<Z>::MAXW;
+  static constexpr int MINB = LaunchCfg<Z>::MINB;
+};
 
 template <int Z> struct TC {
   static constexpr int R = TileCfg<Z>::R, LX = TileCfg<Z>::LX, BL = TileCfg<Z>::BL;

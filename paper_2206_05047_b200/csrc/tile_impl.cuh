@@ -812,7 +812,7 @@ __device__ __forceinline__ void views(const Tile<Z, INT>& t, const Geom& G, cons
 // P2: user (non-separable) blur kernel (A36, view_pass2d).
 // PM: paper-mode adjoint (A37): no scatter, rho to io.rho_out (k_paper_gather follows).
 template <int Z, int MODE, bool FIXBL, bool PV, bool P2, bool PM>
-__global__ void __launch_bounds__(LaunchCfg<Z>::MAXW * 32, LaunchCfg<Z>::MINB)
+__global__ void __launch_bounds__(LaunchCfgM<Z, MODE>::MAXW * 32, LaunchCfgM<Z, MODE>::MINB)
 k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
   using C = TC<Z>;
   constexpr int R = C::R, LX = C::LX, TX = C::TX, ECOL = C::ECOL;
@@ -1128,7 +1128,9 @@ template <int Z>
 struct TileZ {
   template <int MODE, bool F, bool PV, bool P2, bool PM = false>
   static cudaError_t launch1(const Geom& G, const Views& V, const TileGeom& T, const TileIO& io, cudaStream_t st) {
-    k_tile<Z, MODE, F, PV, P2, PM><<<T.ntYl * T.ntX * T.groups, T.nwarps * 32, T.smem, st>>>(G, V, T, io);
+    const int nw = MODE == MODE_NORMAL ? T.nwarps_n : T.nwarps;
+    const size_t sm = MODE == MODE_NORMAL ? T.smem_normal : T.smem;
+    k_tile<Z, MODE, F, PV, P2, PM><<<T.ntYl * T.ntX * T.groups, nw * 32, sm, st>>>(G, V, T, io);
     return cudaGetLastError();
   }
   template <int MODE>

@@ -73,6 +73,9 @@ int tile_bl_candidates(int scale, int* out, int cap) {
 int tile_max_warps(int scale) {
   return scale == 2 ? LaunchCfg<2>::MAXW : scale == 3 ? LaunchCfg<3>::MAXW : LaunchCfg<4>::MAXW;
 }
+int tile_max_warps_normal(int scale) {
+  return scale == 2 ? LaunchCfgM<2, MODE_NORMAL>::MAXW : tile_max_warps(scale);
+}
 
 // Views per warp and warps per CTA: every warp of a group gets the same number of
 // views (or one less); view groups are added until the grid fills the GPU.
@@ -126,7 +129,9 @@ TileGeom make_tile_geom(const Geom& G, int num_sms, int tr0, int tr1) {
   T.vpg = (G.n_views + best_g - 1) / best_g;
   T.groups = (G.n_views + T.vpg - 1) / T.vpg;
   T.smem = smem_bytes(T, T.nwarps);
-  T.smem_normal = T.smem;
+  const int max_n = G.scale == 2 ? LaunchCfgM<2, MODE_NORMAL>::MAXW : max_warps;
+  T.nwarps_n = (G.tile_nwn > 0 && G.tile_nwn <= max_n) ? G.tile_nwn : T.nwarps;
+  T.smem_normal = smem_bytes(T, T.nwarps_n);
   return T;
 }
 

@@ -126,7 +126,7 @@ def load_library(path: str = LIB_PATH):
     lib.lfsr_launches_per_iter.argtypes = [vp]
     lib.lfsr_launches_per_iter.restype = ctypes.c_int32
     i32p = ctypes.POINTER(ctypes.c_int32)
-    lib.lfsr_tile_config.argtypes = [vp, i32p, i32p, i32p]
+    lib.lfsr_tile_config.argtypes = [vp, i32p, i32p, i32p, i32p]
     lib.lfsr_tile_config.restype = st
     lib.lfsr_destroy.argtypes = [vp]
     lib.lfsr_destroy.restype = None
@@ -405,9 +405,10 @@ class Solver:
     @property
     def tile_config(self) -> dict:
         """lfsr_tile_config: the fused kernel's tiling (tile rows, view groups, warps per CTA)."""
-        b, g, w = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
-        self._check(self.lib.lfsr_tile_config(self._h, ctypes.byref(b), ctypes.byref(g), ctypes.byref(w)))
-        return {"tile_rows": b.value, "view_groups": g.value, "warps_per_cta": w.value}
+        b, g, w, wn = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        self._check(self.lib.lfsr_tile_config(self._h, ctypes.byref(b), ctypes.byref(g), ctypes.byref(w),
+                                              ctypes.byref(wn)))
+        return {"tile_rows": b.value, "view_groups": g.value, "warps_per_cta": w.value, "cg_warps_per_cta": wn.value}
 
 
 def strip_plan(params: Params, max_shift_rows: int):

@@ -14,5 +14,6 @@ lf = S.make_lightfield(cfg)
 s = L.Solver(L.params_for(S.CONFIGS[cfg], S.defaults_for(cfg)))
 s.set_observations(lf.y, lf.view_offsets, lf.omega)
 t = s.tile_config
-print("LFSR_TILE_BL=%d LFSR_TILE_GNW=%d,%d" % (t["tile_rows"], t["view_groups"], t["warps_per_cta"]))
+print("LFSR_TILE_BL=%d LFSR_TILE_GNW=%d,%d LFSR_TILE_NWN=%d" % (t["tile_rows"], t["view_groups"], t["warps_per_cta"],
+                                                          t["cg_warps_per_cta"]))
 s.close()
