@@ -162,6 +162,16 @@ def cores():
     return int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def run_reference(args, cfg, d, rank):
     if rank != 0:
         return
@@ -181,7 +191,8 @@ def run_reference(args, cfg, d, rank):
             "data": "synthetic", "hr_mpix_it_per_s": value * hr_mpix,
             "config": {"workload": cfg.name, "desc": cfg.note, "views": cfg.n_views, "scale": cfg.scale,
                        "hr": [cfg.H, cfg.W], "cg_steps": d.cg_max_iters, "l2_flush": "n/a (CPU)"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores(), "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores(), "kind": "oracle", "sample": sample,
+                             "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -403,7 +414,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             sec = time_oracle(lf, cfg, d, 1)
-            cpu = {"value": 1.0 / sec, "unit": UNIT, "cores": cores(), "kind": "oracle",
+            cpu = {"value": 1.0 / sec, "unit": UNIT, "cores": cores(), "kind": "oracle", "cpu_model": cpu_model(),
                    "sample": "%s: one full ADMM iteration (K=%d) of the fp64 oracle on the host cores" %
                              (cfg.name, d.cg_max_iters)}
         except Exception as e:  # pragma: no cover
