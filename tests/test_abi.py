@@ -77,6 +77,10 @@ def test_validation_before_device(lib):
     # NULL-safe destroy; calls on NULL ctx are argument errors
     lib.lfsr_destroy(None)
     assert lib.lfsr_admm_run(None, 1, None) == lfsr.LFSR_ERR_INVALID_ARG
+    assert lib.lfsr_gd_run(None, None, 1, None) != lfsr.LFSR_OK
+    assert lib.lfsr_solve_batch(None, 1, None, None, None, 1, None) == lfsr.LFSR_ERR_INVALID_ARG
+    assert lib.lfsr_rgb_to_ycbcr(None, None, None, None, 10, None) == lfsr.LFSR_ERR_INVALID_ARG
+    assert lib.lfsr_ycbcr_to_rgb(None, None, None, None, 10, None) == lfsr.LFSR_ERR_INVALID_ARG
 
 
 def test_no_silent_cpu_fallback(lib):
