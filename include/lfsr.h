@@ -312,6 +312,12 @@ typedef struct {
 } lfsr_strip;
 LFSR_API lfsr_status lfsr_strip_plan(const lfsr_params* params, int32_t max_shift_rows, lfsr_strip* out /*[n_ranks]*/);
 
+/* The cudaStream_t the ctx runs on (params->stream, or the ctx-owned stream when that
+ * was NULL), so a caller that passes device memory can order its own streams against
+ * the ctx's (event wait before a call that reads its buffers, and after one that writes
+ * them).  Errors: INVALID_ARG (NULL ctx or out). */
+LFSR_API lfsr_status lfsr_get_stream(const lfsr_ctx* ctx, void** stream);
+
 /* Free everything; NULL-safe. */
 LFSR_API void lfsr_destroy(lfsr_ctx* ctx);
 

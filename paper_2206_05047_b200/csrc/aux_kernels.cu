@@ -118,15 +118,20 @@ __global__ void k_weights(const Geom G, const float* __restrict__ x, const float
 // max |v| over an [H][ps] array (non-negative floats order like their bit patterns).
 // (n is a multiple of 4: pitched rows of 32 floats; float4 loads)
 __global__ void k_absmax(const float* __restrict__ v, size_t n, unsigned* out) {
-  float mx = 0.f;
+  // max over the bit patterns of |v| as unsigned integers: for non-negative floats the order of
+  // the bits is the order of the values, and a NaN (exponent all ones, mantissa != 0) sorts above
+  // +inf, so a single NaN makes the result NaN (fmaxf would drop it and let it through validation)
+  unsigned mx = 0u;
   const float4* v4 = reinterpret_cast<const float4*>(v);
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n / 4; i += (size_t)gridDim.x * blockDim.x) {
     const float4 a = __ldg(v4 + i);
-    mx = fmaxf(fmaxf(mx, fmaxf(fabsf(a.x), fabsf(a.y))), fmaxf(fabsf(a.z), fabsf(a.w)));
+    const unsigned b0 = __float_as_uint(a.x) & 0x7fffffffu, b1 = __float_as_uint(a.y) & 0x7fffffffu;
+    const unsigned b2 = __float_as_uint(a.z) & 0x7fffffffu, b3 = __float_as_uint(a.w) & 0x7fffffffu;
+    mx = max(mx, max(max(b0, b1), max(b2, b3)));
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(mx));
+  for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, mx);
 }
 
 // ---------------------------------------------------------------------------

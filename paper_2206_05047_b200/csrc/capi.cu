@@ -505,6 +505,12 @@ void lfsr_destroy(lfsr_ctx* c) {
   delete c;
 }
 
+lfsr_status lfsr_get_stream(const lfsr_ctx* c, void** stream) {
+  if (!c || !stream) return LFSR_ERR_INVALID_ARG;
+  *stream = (void*)c->stream;
+  return LFSR_OK;
+}
+
 const char* lfsr_last_error(const lfsr_ctx* c) { return c ? c->err.c_str() : g_create_err.c_str(); }
 
 int32_t lfsr_launches_per_iter(const lfsr_ctx* c) { return (c && c->ready) ? c->launches_per_iter : 0; }
@@ -798,6 +804,21 @@ static lfsr_status tune_tile_bl(lfsr_ctx* c) {
   return setup_tiles(c);
 }
 
+// Halo of the input tile around the E region: S = ceil(max_k |dtheta_k| max|omega|)
+// per axis, evaluated in double (a huge finite product must not overflow the int).  The tile
+// kernel samples inside the replicate-padded tile without clamping, so a shift reaching past the
+// image (every sample of such a view clamps to the border) is outside what it supports.
+static lfsr_status set_shift_halo(lfsr_ctx* c, float om_max, float mx_rho, float mx_tau) {
+  Geom& G = c->G;
+  if (!std::isfinite(om_max)) FAIL(c, LFSR_ERR_INVALID_ARG, "disparity must be finite (NaN or inf found)");
+  const double sx = std::ceil((double)mx_rho * (double)om_max), sy = std::ceil((double)mx_tau * (double)om_max);
+  if (sx > (double)G.W || sy > (double)G.H)
+    FAIL(c, LFSR_ERR_UNSUPPORTED, "max |view offset| x max |disparity| exceeds the image size");
+  G.SX = (int)sx;
+  G.SY = (int)sy;
+  return LFSR_OK;
+}
+
 lfsr_status lfsr_set_observations(lfsr_ctx* c, const float* lr_views, const float* view_offsets,
                                   const float* disparity, lfsr_disp_mode disp_mode, const float* x0, lfsr_mem mem) {
   if (!c) return LFSR_ERR_INVALID_ARG;
@@ -899,14 +920,12 @@ lfsr_status lfsr_set_observations(lfsr_ctx* c, const float* lr_views, const floa
   CK(c, cudaStreamSynchronize(c->stream));
   float om_max;
   memcpy(&om_max, &ubits[0], 4);
-  if (!std::isfinite(om_max)) FAIL(c, LFSR_ERR_INVALID_ARG, "disparity must be finite");
   float mx_rho = 0.f, mx_tau = 0.f;
   for (int k = 0; k < nv; ++k) {
     mx_rho = std::fmax(mx_rho, std::fabs(off[2 * k]));
     mx_tau = std::fmax(mx_tau, std::fabs(off[2 * k + 1]));
   }
-  G.SX = std::min((int)std::ceil(mx_rho * om_max), G.W);
-  G.SY = std::min((int)std::ceil(mx_tau * om_max), G.H);
+  if ((st = set_shift_halo(c, om_max, mx_rho, mx_tau)) != LFSR_OK) return st;
   memcpy(&G.dmax, &ubits[1], 4);
   memcpy(&G.ymax, &ubits[2], 4);
   if (!std::isfinite(G.ymax)) G.ymax = 0.f;  // non-finite observations surface as DIVERGED
@@ -1301,10 +1320,10 @@ lfsr_status lfsr_admm_run(lfsr_ctx* c, int32_t n_iters, lfsr_iter_stats* stats) 
   if (st != LFSR_OK) return st;
   if (n_iters < 0) FAIL(c, LFSR_ERR_INVALID_ARG, "n_iters must be >= 0");
   if (n_iters == 0) return LFSR_OK;
-  const int first = c->h_iter + 1;
-  if ((st = lfsr_admm_enqueue(c, n_iters)) != LFSR_OK) return st;
   const int n_read = std::min(n_iters, kRingCap);
   if (stats && n_read < n_iters) FAIL(c, LFSR_ERR_INVALID_ARG, "stats requested for more than 4096 iterations");
+  const int first = c->h_iter + 1;
+  if ((st = lfsr_admm_enqueue(c, n_iters)) != LFSR_OK) return st;
   return lfsr_admm_stats(c, first + (n_iters - n_read), n_read, stats);
 }
 
@@ -1461,26 +1480,25 @@ static lfsr_status batch_finish(lfsr_ctx* c, const float* off, const Views& V2) 
   CK(c, cudaEventSynchronize(c->ev_b[0]));   // the maxima (the ctx stream keeps solving meanwhile)
   float om_max, mx_rho = 0.f, mx_tau = 0.f;
   memcpy(&om_max, &c->h_ubits[0], 4);
-  if (!std::isfinite(om_max)) FAIL(c, LFSR_ERR_INVALID_ARG, "disparity must be finite");
   for (int k = 0; k < G.n_views; ++k) {
     if (!std::isfinite(off[2 * k]) || !std::isfinite(off[2 * k + 1]))
       FAIL(c, LFSR_ERR_INVALID_ARG, "view_offsets must be finite");
     mx_rho = std::fmax(mx_rho, std::fabs(off[2 * k]));
     mx_tau = std::fmax(mx_tau, std::fabs(off[2 * k + 1]));
   }
+  c->ready = false;   // nothing below may leave a half-switched ctx usable (set again by lfsr_solve_batch)
+  lfsr_status st;
+  if ((st = set_shift_halo(c, om_max, mx_rho, mx_tau)) != LFSR_OK) return st;
   State& S = c->parts[0].S;
   std::swap(S.y, c->stage_y);          // the staged inputs become the state; the old ones are staged into next
   std::swap(S.omega, c->stage_om);
   std::swap(S.density, c->stage_dens);
   c->V = V2;
-  G.SX = std::min((int)std::ceil(mx_rho * om_max), G.W);
-  G.SY = std::min((int)std::ceil(mx_tau * om_max), G.H);
   memcpy(&G.dmax, &c->h_ubits[1], 4);
   memcpy(&G.ymax, &c->h_ubits[2], 4);
   if (!std::isfinite(G.ymax)) G.ymax = 0.f;
   bool tune = false;
   initial_tiles(c, &tune);
-  lfsr_status st;
   if ((st = setup_tiles(c)) != LFSR_OK) return st;
   // reset (Alg.1 lines 1-2) and a1 on the ctx stream, after field i's iterations and x_i's copy
   CK(c, cudaMemsetAsync(S.wA, 0, lr * 4, c->stream));
@@ -1497,7 +1515,9 @@ static lfsr_status batch_finish(lfsr_ctx* c, const float* off, const Views& V2) 
   CK(c, launch_setup_wo(G, c->V, S.y, S.omega, S.wo, c->stream));
   CK(c, launch_weights(G, S.x, S.wo, S.m, c->stream));
   if (tune && (st = tune_tile_bl(c)) != LFSR_OK) return st;
-  return build_graphs(c);
+  if ((st = build_graphs(c)) != LFSR_OK) return st;
+  c->ready = true;
+  return LFSR_OK;
 }
 
 lfsr_status lfsr_solve_batch(lfsr_ctx* c, int32_t n_fields, const float* const* lr_views,

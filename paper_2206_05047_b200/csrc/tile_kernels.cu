@@ -4,6 +4,9 @@
 #include "tile_cfg.h"
 #include <algorithm>
 #include <cmath>
+#include <map>
+#include <mutex>
+#include <utility>
 
 namespace lfsr {
 
@@ -43,13 +46,27 @@ static int occupancy_for(int scale, int threads, size_t smem) {
   }
 }
 
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-process, per-device property of each
+// kernel instance, so it is only ever raised: a ctx created later with a smaller tile must not
+// lower the limit below the footprint of a ctx that is still alive (its next launch would fail).
+static std::mutex g_prep_mu;
+static std::map<std::pair<int, int>, size_t> g_prep;   // (device, zeta) -> attribute set so far
+
 cudaError_t prepare_tile_kernels(int scale, size_t smem) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(g_prep_mu);
+  size_t& cur = g_prep[std::make_pair(dev, scale)];
+  if (smem <= cur) return cudaSuccess;
   switch (scale) {
-    case 2: return tile_prepare_z2(smem);
-    case 3: return tile_prepare_z3(smem);
-    case 4: return tile_prepare_z4(smem);
+    case 2: e = tile_prepare_z2(smem); break;
+    case 3: e = tile_prepare_z3(smem); break;
+    case 4: e = tile_prepare_z4(smem); break;
+    default: return cudaErrorInvalidValue;
   }
-  return cudaErrorInvalidValue;
+  if (e == cudaSuccess) cur = smem;
+  return e;
 }
 
 // Static tile constants for the strip planner (capi.cu); BL is the default.

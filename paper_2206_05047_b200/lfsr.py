@@ -33,7 +33,8 @@ OPS = {"A": OP_A, "AT": OP_AT, "S": OP_S, "ST": OP_ST, "NORMAL": OP_NORMAL, "WEI
 EXPORTS = ("lfsr_create", "lfsr_set_observations", "lfsr_admm_run", "lfsr_admm_enqueue", "lfsr_admm_stats",
            "lfsr_get_hr", "lfsr_get_state", "lfsr_op_apply", "lfsr_launches_per_iter", "lfsr_tile_config", "lfsr_profile",
            "lfsr_profile_read", "lfsr_strip_plan", "lfsr_destroy", "lfsr_last_error", "lfsr_abi_version",
-           "lfsr_gd_run", "lfsr_gd_launches_per_iter", "lfsr_rgb_to_ycbcr", "lfsr_ycbcr_to_rgb", "lfsr_solve_batch")
+           "lfsr_gd_run", "lfsr_gd_launches_per_iter", "lfsr_rgb_to_ycbcr", "lfsr_ycbcr_to_rgb", "lfsr_solve_batch",
+           "lfsr_get_stream")
 
 
 class LFSRError(RuntimeError):
@@ -144,6 +145,8 @@ def load_library(path: str = LIB_PATH):
     lib.lfsr_rgb_to_ycbcr.restype = st
     lib.lfsr_ycbcr_to_rgb.argtypes = [vp, vp, vp, vp, ctypes.c_size_t, vp]
     lib.lfsr_ycbcr_to_rgb.restype = st
+    lib.lfsr_get_stream.argtypes = [vp, P(vp)]
+    lib.lfsr_get_stream.restype = st
     lib.lfsr_abi_version.argtypes = []
     lib.lfsr_abi_version.restype = ctypes.c_int32
     _lib = lib
@@ -235,6 +238,8 @@ class Solver:
             raise LFSRError(s, self.lib.lfsr_last_error(None).decode())
         self._h = h
         self._keep = []
+        self._user_stream = stream is not None
+        self._ext = None   # torch view of the ctx-owned stream (device-tensor calls, see _dev_call)
 
     # -- helpers ------------------------------------------------------------
     def _check(self, s):
@@ -255,6 +260,30 @@ class Solver:
             return t.data_ptr(), (MEM_DEVICE if t.is_cuda else MEM_HOST), t
         arr = np.ascontiguousarray(a, dtype=np.float32)
         return arr.ctypes.data, MEM_HOST, arr
+
+    def _dev_call(self, fn, tensors):
+        """Run fn() (a C call reading / writing the device tensors `tensors`) ordered against torch's
+        current stream.  With a caller-supplied stream the caller orders its own work (that stream
+        is the ctx stream).  With the ctx-owned stream: the ctx stream waits for torch's current
+        stream before the call, torch's current stream waits for the ctx stream after it, and every
+        tensor (including marshalling temporaries) is recorded on the ctx stream so the caching
+        allocator cannot hand its memory out while the ctx may still use it."""
+        if self._user_stream or not tensors:
+            return fn()
+        import torch
+        dev = tensors[0].device
+        if self._ext is None:
+            sp = ctypes.c_void_p()
+            self._check(self.lib.lfsr_get_stream(self._h, ctypes.byref(sp)))
+            self._ext = torch.cuda.ExternalStream(sp.value, device=dev)
+        cur = torch.cuda.current_stream(dev)
+        self._ext.wait_stream(cur)
+        try:
+            return fn()
+        finally:
+            for t in tensors:
+                t.record_stream(self._ext)
+            cur.wait_stream(self._ext)
 
     def close(self):
         if getattr(self, "_h", None):
@@ -282,8 +311,10 @@ class Solver:
         mem = mems.pop()
         # [H][W]: one shared map (LFSR_DISP_SHARED); [n_views][H][W]: omega_k per view (LFSR_DISP_PER_VIEW, A34)
         disp_mode = 1 if len(tuple(disparity.shape)) == 3 else 0
-        s = self.lib.lfsr_set_observations(self._h, ptrs[0][0], ptrs[1][0], ptrs[2][0], disp_mode, ptrs[3][0], mem)
-        self._check(s)
+        call = lambda: self.lib.lfsr_set_observations(self._h, ptrs[0][0], ptrs[1][0], ptrs[2][0], disp_mode,
+                                                      ptrs[3][0], mem)
+        dev = [p[2] for p in ptrs if p[2] is not None] if mem == MEM_DEVICE else []
+        self._check(self._dev_call(call, dev))
 
     def admm_run(self, n_iters: int, want_stats: bool = True):
         st = (_CStats * max(int(n_iters), 1))() if want_stats else None
@@ -369,7 +400,7 @@ class Solver:
             return out
         mem = MEM_DEVICE if (_is_torch(out) and out.is_cuda) else MEM_HOST
         ptr = out.data_ptr() if _is_torch(out) else out.ctypes.data
-        self._check(self.lib.lfsr_get_hr(self._h, ptr, mem))
+        self._check(self._dev_call(lambda: self.lib.lfsr_get_hr(self._h, ptr, mem), [out] if mem == MEM_DEVICE else []))
         return out
 
     def get_state(self):
@@ -392,7 +423,8 @@ class Solver:
         if mem == MEM_DEVICE:
             import torch
             out = torch.empty(out_shape, dtype=torch.float32, device=keep.device)
-            self._check(self.lib.lfsr_op_apply(self._h, op, ptr, out.data_ptr(), MEM_DEVICE))
+            self._check(self._dev_call(lambda: self.lib.lfsr_op_apply(self._h, op, ptr, out.data_ptr(), MEM_DEVICE),
+                                       [keep, out]))
             return out
         out = np.empty(out_shape, np.float32)
         self._check(self.lib.lfsr_op_apply(self._h, op, ptr, out.ctypes.data, MEM_HOST))

@@ -177,13 +177,51 @@ def test_admm_parity_forced_tile_height(lfsr_mod, monkeypatch, cfg, bl, gnw):
     check_iterates(p, ora, xs, stats, st, lf.x_gt)
 
 
-@pytest.mark.parametrize("cfg,n", [("C2", 4), ("C3", 2), ("C4", 2)])
+def log_parity(name, p, ora, xs, stats, errs, gt):
+    """One line per parity run (pytest -rP / -s shows it; profiles/ keeps the round's log)."""
+    d_psnr = O.psnr(xs[-1], gt) - O.psnr(ora.x_iters[-1], gt)
+    jrel = max(abs(g["J"] - o["J"]) / abs(o["J"]) for g, o in zip(stats, ora.stats))
+    rrel = max(abs(g["primal_res"] - o["primal_res"]) / max(o["primal_res"], 1e-12) for g, o in zip(stats, ora.stats))
+    print("PARITY %s N=%d zeta=%d: max rel L2 x^n %.2e (per n: %s); max rel J %.2e; max rel primal_res %.2e; "
+          "PSNR gpu %.4f oracle %.4f delta %+.5f dB" % (name, len(xs) - 1, p.scale, max(errs),
+                                                      " ".join("%.1e" % e for e in errs), jrel, rrel,
+                                                      O.psnr(xs[-1], gt), O.psnr(ora.x_iters[-1], gt), d_psnr))
+
+
+@pytest.mark.parametrize("cfg,n", [("C2", 10), ("C3", 10), ("C4", 10)])
 def test_admm_parity_full_size(lfsr_mod, cfg, n):
-    """BASELINE configs at full size, in the launch configuration bench.py times."""
+    """BASELINE configs at full size, in the launch configuration bench.py times and at the bench's
+    N = 10 (x^n per iterate <= 1e-4, J / primal residual, w_A / w_S, final PSNR within 0.01 dB)."""
     lf = S.make_lightfield(cfg)
     p, ora, xs, stats, st = run_pair(lfsr_mod, lf, n)
     errs = check_iterates(p, ora, xs, stats, st, lf.x_gt)
-    print(cfg, "per-iterate rel L2:", ["%.2e" % e for e in errs])
+    log_parity(cfg, p, ora, xs, stats, errs, lf.x_gt)
+
+
+# C5-shaped (9x9 views, zeta = 4, R = 3) at a size the oracle runs in seconds per iteration
+C5R = {kind: S.Config("C5r", 9, 128, 128, 4, 0.02 if kind == "natural" else 0.05, 5.0 if kind == "natural" else 20.0,
+                      1.0 if kind == "natural" else 1.5, kind, 5, "C5-shaped reduced: 9x9 views 128^2 -> 512^2")
+       for kind in ("natural", "hci")}
+
+
+@pytest.mark.parametrize("kind", ["natural", "hci"])
+def test_admm_parity_zeta4_C5_shaped(lfsr_mod, kind):
+    """The zeta = 4 wz-step (MODE_WZ of the zeta = 4 kernel instances: weights, data shrink/dual,
+    NLTV shrink/dual, r = -v) and CG against the oracle iterate by iterate: 9x9 views, 128^2 -> 512^2,
+    N = 5, both scene kinds (natural: C5's; hci: depth edges, severe noise)."""
+    lf = S.make_lightfield(C5R[kind], seed=1505 if kind == "natural" else 1506)
+    p, ora, xs, stats, st = run_pair(lfsr_mod, lf, 5)
+    errs = check_iterates(p, ora, xs, stats, st, lf.x_gt)
+    log_parity("C5r-" + kind, p, ora, xs, stats, errs, lf.x_gt)
+
+
+def test_admm_parity_full_size_C5(lfsr_mod):
+    """C5 (9x9 views, 512^2 -> 2048^2, zeta = 4) at full size, whole ADMM iterations (N = 2) against
+    the oracle (about half a minute per iteration on the host cores)."""
+    lf = S.make_lightfield("C5")
+    p, ora, xs, stats, st = run_pair(lfsr_mod, lf, 2)
+    errs = check_iterates(p, ora, xs, stats, st, lf.x_gt)
+    log_parity("C5", p, ora, xs, stats, errs, lf.x_gt)
 
 
 def test_continuation_and_determinism(lfsr_mod):
@@ -222,6 +260,48 @@ def test_device_pointer_path(lfsr_mod):
     assert rel_l2(out.cpu().numpy(), b.get_hr()) < 1e-6
 
 
+def test_device_tensors_without_stream(lfsr_mod):
+    """A Solver on its own stream (no stream given) used with CUDA tensors produced by torch work on
+    torch's current stream: the binding orders the ctx stream after it and torch after the ctx
+    (lfsr_get_stream), so the results equal the host path."""
+    import torch
+    lf = S.make_lightfield("C1")
+    p = lfsr_mod.Params(n_views=9, lr_height=32, lr_width=32, scale=2, ref_view=4)
+    a = lfsr_mod.Solver(p)
+    y = torch.from_numpy(lf.y).cuda() * 1.0          # produced by a kernel on torch's stream
+    a.set_observations(y, torch.from_numpy(lf.view_offsets).cuda(), torch.from_numpy(lf.omega).cuda())
+    xin = torch.linspace(-1, 1, p.H * p.W, device="cuda").reshape(p.H, p.W) * 2.0
+    out = a.op("NORMAL", xin.double())               # a marshalling temporary (.float()) on the device
+    got = (out * 1.0).cpu().numpy()                  # consumed by torch right away
+    b = lfsr_mod.Solver(p)
+    b.set_observations(lf.y, lf.view_offsets, lf.omega)
+    assert rel_l2(got, b.op("NORMAL", xin.cpu().numpy())) < 1e-6
+    a.admm_run(2)
+    b.admm_run(2)
+    xd = torch.zeros((p.H, p.W), device="cuda")
+    a.get_hr(xd)
+    assert rel_l2((xd + 0.0).cpu().numpy(), b.get_hr()) < 1e-6
+
+
+def test_two_contexts_of_different_geometry(lfsr_mod):
+    """The kernels' dynamic shared-memory limit is a per-process attribute: a ctx set up later with a
+    smaller tile must not lower it below the footprint of a live ctx with a larger one."""
+    big = S.make_lightfield("C2")
+    pb = lfsr_mod.params_for(S.CONFIGS["C2"], S.SolverDefaults())
+    a = lfsr_mod.Solver(pb)
+    a.set_observations(big.y, big.view_offsets, big.omega)
+    small = S.make_lightfield("C1")
+    ps = lfsr_mod.params_for(S.CONFIGS["C1"], S.SolverDefaults())
+    b = lfsr_mod.Solver(ps)
+    b.set_observations(small.y, small.view_offsets, small.omega * 0.1)   # a thinner halo: smaller tile
+    assert len(b.admm_run(1)) == 1
+    assert len(a.admm_run(1)) == 1
+    x = np.random.default_rng(3).uniform(-1, 1, (pb.H, pb.W)).astype(np.float32)
+    assert np.isfinite(a.op("NORMAL", x)).all()
+    a.close()
+    b.close()
+
+
 def test_error_paths(lfsr_mod):
     p = lfsr_mod.Params(n_views=9, lr_height=32, lr_width=32, scale=2, ref_view=4)
     s = lfsr_mod.Solver(p)
@@ -234,11 +314,19 @@ def test_error_paths(lfsr_mod):
     with pytest.raises(lfsr_mod.LFSRError) as ei:
         s.set_observations(lf.y, bad, lf.omega)
     assert ei.value.status == 1
-    # divergence guard: NaN disparity is rejected up front
+    # non-finite disparity (inf, and NaN -- invalid pixels of real disparity maps) is rejected up front
+    for bad_v in (np.inf, np.nan, -np.nan):
+        om = lf.omega.copy()
+        om[3, 3] = bad_v
+        with pytest.raises(lfsr_mod.LFSRError) as ei:
+            s.set_observations(lf.y, lf.view_offsets, om)
+        assert ei.value.status == 1, bad_v
+    # a shift reaching past the image is refused (UNSUPPORTED), not sampled out of the tile
     om = lf.omega.copy()
-    om[3, 3] = np.inf
-    with pytest.raises(lfsr_mod.LFSRError):
+    om[5, 5] = 1e30
+    with pytest.raises(lfsr_mod.LFSRError) as ei:
         s.set_observations(lf.y, lf.view_offsets, om)
+    assert ei.value.status == 7
     s.set_observations(lf.y, lf.view_offsets, lf.omega)
     assert len(s.admm_run(2)) == 2
     assert s.launches_per_iter == 1 + 2 * p.cg_max_iters

@@ -273,6 +273,7 @@ def textbook_admm(Ad, Sd, y, l1, l2, th, x0, N):
     w = np.zeros(F.shape[0])
     G = A.T @ A + 0.5 * th * F.T @ F  # G^T G of Eq. sr_l1l2l1_lsf (without the sqrt factors)
     xs = [x.copy()]
+    ws = [w.copy()]
     for _ in range(N):
         u = F @ x - bp + w
         zz = np.maximum(np.abs(u) - 1 / th, 0) * np.sign(u)   # prox
@@ -280,6 +281,8 @@ def textbook_admm(Ad, Sd, y, l1, l2, th, x0, N):
         rhs = A.T @ b + 0.5 * th * F.T @ (zz + bp - w)          # normal equations of
         x = np.linalg.solve(G, rhs)
         xs.append(x.copy())
+        ws.append(w.copy())
+    textbook_admm.ws = ws   # the scaled dual sequence w^0..w^N (block order [data rows; NLTV rows])
     return xs
 
 
@@ -296,6 +299,33 @@ def test_P11_alg1_equals_textbook_scaled_admm(oracle_lib):
     res = O.admm(P, y, vo, om, N)
     for n in range(N + 1):
         assert np.allclose(res.x_iters[n].ravel(), xs[n], atol=1e-8), n
+
+
+def test_P11_primal_residual_and_duals_equal_textbook(oracle_lib):
+    """A27's primal residual |w^n - w^{n-1}|_2 pinned by value: the textbook scaled ADMM above tracks
+    w = [w_A; w_S] on the compact F = [l1/sqrt(l2) A; S] (whose data rows are l1 (Abar x - y), so its
+    scaled dual is the oracle's w_A itself, and its NLTV rows are S_w x, the oracle's w_S), so the
+    oracle's reported primal_res of iteration n must equal |ws[n] - ws[n-1]| of that independent
+    sequence, and its final w_A / w_S states must equal ws[N]."""
+    P, y, vo, om, x = tiny(seed=37, nv=3, h=4, w=4, z=2, lambda1=0.9, lambda2=1.5, theta=2.0, lambda_reg=0.6,
+                           sigma_e=0.05, cg_max_iters=EXACT_K, reweight_every_iter=0)
+    y = y.astype(np.float64)
+    x0 = O.bicubic(y[P.ref_view], P.scale)
+    wo, _, _ = O.setup_wo(P, y, vo, om)
+    m = O.weights_m(x0, wo, P.lambda_reg, P.sigma_e)
+    Ad, Sd = dense_ops(P, vo, om, m)
+    N = 6
+    textbook_admm(Ad, Sd, y.ravel(), P.lambda1, P.lambda2, P.theta, x0.ravel(), N)
+    ws = textbook_admm.ws
+    res = O.admm(P, y, vo, om, N)
+    for n in range(1, N + 1):
+        want = float(np.linalg.norm(ws[n] - ws[n - 1]))
+        assert want > 1e-6, n                       # the pin is not vacuous
+        assert rel(res.stats[n - 1]["primal_res"], want) < 1e-9, (n, res.stats[n - 1]["primal_res"], want)
+    nA = Ad.shape[0]
+    assert np.allclose(res.wA.ravel(), ws[N][:nA], atol=1e-9)
+    # dense_ops builds S_w column by column from O.apply_S, whose rows are ordered [s_d][H][W]
+    assert np.allclose(res.wS.ravel(), ws[N][nA:], atol=1e-9)
 
 
 def test_P11_f_identity_and_residual(oracle_lib):
