@@ -265,9 +265,12 @@ class Solver:
         """Run fn() (a C call reading / writing the device tensors `tensors`) ordered against torch's
         current stream.  With a caller-supplied stream the caller orders its own work (that stream
         is the ctx stream).  With the ctx-owned stream: the ctx stream waits for torch's current
-        stream before the call, torch's current stream waits for the ctx stream after it, and every
-        tensor (including marshalling temporaries) is recorded on the ctx stream so the caching
-        allocator cannot hand its memory out while the ctx may still use it."""
+        stream before the call and torch's current stream waits for the ctx stream after it.  The
+        library keeps no caller pointer past the work that call enqueues, so that wait also covers
+        the tensors' memory (marshalling temporaries included): torch's caching allocator reuses a
+        freed block only in the order of the stream it was allocated on, which is now behind the
+        ctx's work.  (No record_stream: the ctx stream dies with the ctx, and the allocator would
+        later record an event on it.)"""
         if self._user_stream or not tensors:
             return fn()
         import torch
@@ -281,8 +284,6 @@ class Solver:
         try:
             return fn()
         finally:
-            for t in tensors:
-                t.record_stream(self._ext)
             cur.wait_stream(self._ext)
 
     def close(self):
