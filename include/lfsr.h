@@ -109,7 +109,11 @@ typedef struct {
                            memory, copied at lfsr_create: (B x)(Y,X) = sum_{u,v} k[u][v]
                            x(Y-u, X-v), zero padding (P:L962 motion blur, SURVEY 8f NEXT-4,
                            reading A36).  Not with LFSR_DISP_PER_VIEW (UNSUPPORTED).  */
-  int32_t psf_radius;   /* 0..R(zeta): 2 at zeta = 2, 3 at zeta = 3, 4                 */
+  int32_t psf_radius;   /* 0..7 (up to 15x15).  Kernels within the Gaussian's window
+                           (radius <= 2 at zeta = 2, <= 3 at zeta = 3, 4) run in the
+                           default tile instances, larger ones in the radius-7 instances
+                           (narrower tiles); those are single-strip only (n_ranks > 1:
+                           UNSUPPORTED).  INVALID_ARG outside 0..7.                    */
   int32_t paper_adjoint; /* 0 (default): A^T uses the exact transpose W_k^T of the warp (A12).
                            1: the paper's own adjoint warp W_k^* -- a backward warp with
                            omega_0, (W_k^* u)(z) = u(z - dtheta_k omega_0(z)) (P:L583,

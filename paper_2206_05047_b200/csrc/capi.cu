@@ -182,8 +182,9 @@ static const char* validate(const lfsr_params* p) {
         return "offset_weights must be finite and >= 0";
   }
   if (p->psf) {
-    const int Rz = p->scale == 2 ? 2 : 3;   // the fused kernel's blur window
-    if (p->psf_radius < 0 || p->psf_radius > Rz) return "psf_radius must be in [0, 2] (scale 2) or [0, 3] (scale 3, 4)";
+    // kernels up to the Gaussian's window (R = 2 at scale 2, 3 at 3, 4) run in the default tile
+    // instances, larger ones (up to 15x15) in the kPsfBigR instances
+    if (p->psf_radius < 0 || p->psf_radius > kPsfBigR) return "psf_radius must be in [0, 7]";
     const int n = (2 * p->psf_radius + 1) * (2 * p->psf_radius + 1);
     for (int i = 0; i < n; ++i)
       if (!std::isfinite(p->psf[i])) return "psf must be finite";
@@ -249,19 +250,21 @@ static void fill_geom(const lfsr_params& p, Geom& G) {
   if (p.psf) {   // user blur kernel (A36): flip into the E-offset order of the tile kernel
     G.psf2d = 1;
     const int rp = p.psf_radius, np_ = 2 * rp + 1;
+    const int rb = rp > R ? kPsfBigR : R;   // layout radius: the default or the large-kernel instances
+    G.psf_rb = rb;
     double ks = 0.0, gp = 0.0;
     for (int u = -rp; u <= rp; ++u)
       for (int v = -rp; v <= rp; ++v) {
         const float k = p.psf[(u + rp) * np_ + (v + rp)];
-        G.psf2[R - u][R - v] = k;
+        G.psf2[rb - u][rb - v] = k;
         ks += std::fabs((double)k);
       }
     // |B^T D^T rho| <= max over phases of the polyphase |k| sums times max|rho|
     for (int py = 0; py < p.scale; ++py)
       for (int px = 0; px < p.scale; ++px) {
         double sp = 0.0;
-        for (int a = py; a <= 2 * R; a += p.scale)
-          for (int b = px; b <= 2 * R; b += p.scale) sp += std::fabs((double)G.psf2[a][b]);
+        for (int a = py; a <= 2 * rb; a += p.scale)
+          for (int b = px; b <= 2 * rb; b += p.scale) sp += std::fabs((double)G.psf2[a][b]);
         gp = std::fmax(gp, sp);
       }
     G.ksum = (float)(ks * 1.0001);
@@ -380,6 +383,10 @@ lfsr_status lfsr_create(const lfsr_params* params, lfsr_ctx** out) {
   }
   if (params->paper_adjoint && (params->n_ranks > 1 || params->psf)) {
     g_create_err = "the paper-mode adjoint (paper_adjoint) runs on a single strip with the Gaussian blur";
+    return LFSR_ERR_UNSUPPORTED;
+  }
+  if (params->psf && params->n_ranks > 1 && params->psf_radius > (params->scale == 2 ? 2 : 3)) {
+    g_create_err = "a user blur kernel larger than the Gaussian window runs on a single strip";
     return LFSR_ERR_UNSUPPORTED;
   }
   int ndev = 0;
@@ -668,8 +675,8 @@ static std::map<std::string, TileChoice> g_tuned;
 static std::string tune_key(const lfsr_ctx* c) {
   const Geom& G = c->G;
   char k[256];
-  snprintf(k, sizeof k, "%d/%d/%d/%d/%d/%d/%d/%d/%d", c->prm.device, G.scale, G.h, G.w, G.n_views, G.SX, G.SY,
-           G.radius, c->num_sms);
+  snprintf(k, sizeof k, "%d/%d/%d/%d/%d/%d/%d/%d/%d/%d", c->prm.device, G.scale, G.h, G.w, G.n_views, G.SX, G.SY,
+           G.radius, c->num_sms, G.psf2d ? G.psf_rb : 0);
   return k;
 }
 
@@ -713,7 +720,8 @@ static lfsr_status tune_tile_bl(lfsr_ctx* c) {
   }
   int cand[8];
   const int n = tile_bl_candidates(G.scale, cand, 8);
-  const int maxw = tile_max_warps(G.scale);
+  const bool big = G.psf2d && G.psf_rb == kPsfBigR;   // large user kernel: 8-warp instances
+  const int maxw = big ? 8 : tile_max_warps(G.scale);
   cudaEvent_t e0, e1;
   CK(c, cudaEventCreate(&e0));
   CK(c, cudaEventCreate(&e1));
@@ -762,7 +770,7 @@ static lfsr_status tune_tile_bl(lfsr_ctx* c) {
   }
   // the CG-operator launches may use wider CTAs than the wz-step (zeta = 2: up to 16 warps):
   // kept if 2 % faster for the chosen tiling
-  const int maxwn = tile_max_warps_normal(G.scale);
+  const int maxwn = big ? 8 : tile_max_warps_normal(G.scale);
   if (maxwn > best.nw && best.bl > 0) {
     G.tile_bl = best.bl;
     G.tile_g = best.g;

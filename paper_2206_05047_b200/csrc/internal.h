@@ -12,6 +12,7 @@ constexpr int kMaxOffsets = 80;  // s_d for r <= 4
 constexpr int kMaxK = 64;        // CG steps per ADMM iteration
 constexpr int kThreads = 256;    // threads per tile CTA
 constexpr int kMaxLs = 32;       // gd-ls: Armijo trials per iteration (reading A32)
+constexpr int kPsfBigR = 7;      // blur radius of the large user-kernel tile instances (A36: up to 15x15)
 
 // Scalar slots of the current ADMM iteration (doubles in Control::cur).
 enum Slot : int {
@@ -68,7 +69,8 @@ struct Geom {
   int32_t psf2d;              // 1: user blur kernel (A36) in psf2 instead of the separable taps
   int32_t paper;              // 1: the paper's backward-warp adjoint W_k^* with omega_0 (A37)
   float ksum;                 // sum |k| of the blur kernel (1 for the normalised Gaussian): |B w| <= ksum max|w|
-  float psf2[2 * 3 + 1][2 * 3 + 1];   // psf2[a][b] = k[R-a][R-b]: E-offset (correlation) order, zero padded to 2R+1
+  int32_t psf_rb;             // blur radius of the psf2 layout: R (kernel radius <= R) or 7 (larger kernels)
+  float psf2[2 * 7 + 1][2 * 7 + 1];   // psf2[a][b] = k[rb-a][rb-b]: E-offset (correlation) order, zero padded to 2 rb + 1
   float taps[kMaxTaps * 2 + 1];
   float2 tpe[kMaxTaps + 1];   // tap pairs (taps[2v], taps[2v+1]), zero past 2R (packed FP32 operands)
   float2 tpo[kMaxTaps + 1];   // tap pairs (taps[2v+1], taps[2v+2])

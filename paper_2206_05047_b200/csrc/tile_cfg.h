@@ -53,8 +53,21 @@ template <int Z, int MODE> struct LaunchCfgM {
   static constexpr int MINB = LaunchCfg<Z>::MINB;
 };
 
-template <int Z> struct TC {
-  static constexpr int R = TileCfg<Z>::R, LX = TileCfg<Z>::LX, BL = TileCfg<Z>::BL;
+// the large user-kernel instances (RB = kPsfBigR: Q x Q LR-row/column histories per lane) run
+// 8-warp CTAs with up to 255 registers instead of spilling under the 12-warp bound
+template <int Z, int MODE, int RB> struct LaunchCfgR {
+  static constexpr bool kBig = RB != TileCfg<Z>::R;
+  static constexpr int MAXW = kBig ? 8 : LaunchCfgM<Z, MODE>::MAXW;
+  static constexpr int MINB = kBig ? 1 : LaunchCfgM<Z, MODE>::MINB;
+};
+
+// Tile constants for blur radius RB: the Gaussian's R(zeta) (TC<Z>), or kPsfBigR for the
+// large user-kernel instances (A36: up to 15x15).  One warp spans the E columns of LX LR
+// columns: EXv = zeta (LX - 1) + 2 RB + 1 <= 32 zeta.
+template <int Z, int RB> struct TCR {
+  static constexpr int R = RB;
+  static constexpr int LX = (RB == TileCfg<Z>::R) ? TileCfg<Z>::LX : (32 * Z - (2 * RB + 1)) / Z + 1;
+  static constexpr int BL = TileCfg<Z>::BL;
   static constexpr int NTAP = 2 * R + 1;
   static constexpr int KEEP = NTAP - Z;           // forward-ring rows carried between LR rows
   static constexpr int TX = Z * LX;              // tile rows TY = Z BL, E rows EY = Z BL + KEEP (runtime)
@@ -66,5 +79,6 @@ template <int Z> struct TC {
   static constexpr bool DUMMY = LFSR_DUMMY_MASK & (1 << Z);
   static_assert(EXv <= ECOL, "strip too wide for one warp");
 };
+template <int Z> using TC = TCR<Z, TileCfg<Z>::R>;
 
 }  // namespace lfsr

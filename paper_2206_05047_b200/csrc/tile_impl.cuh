@@ -124,8 +124,8 @@ struct YRoute {
 template <int NP>
 struct YRoute<false, NP> {};
 
-template <int Z, bool INT>
-struct Tile : YRoute<!INT && TC<Z>::DUMMY, Z / 2> {
+template <int Z, bool INT, int RB>
+struct Tile : YRoute<!INT && TCR<Z, RB>::DUMMY, Z / 2> {
   static constexpr int NP = Z / 2;     // column pairs per lane
   static constexpr bool kInt = INT;
   const float* P;
@@ -207,11 +207,11 @@ struct Tile : YRoute<!INT && TC<Z>::DUMMY, Z / 2> {
 
   // E positions outside the image carry zero (blur zero padding, A11): rows by a
   // warp-uniform test (row_in), columns by the per-lane mask (col_in).
-  __device__ __forceinline__ bool col_in(int s) const { return INT || TC<Z>::DUMMY || ((colmask >> s) & 1u); }
+  __device__ __forceinline__ bool col_in(int s) const { return INT || TCR<Z, RB>::DUMMY || ((colmask >> s) & 1u); }
   __device__ __forceinline__ float2 colsel(float2 v, int s) const {
-    return (INT || TC<Z>::DUMMY) ? v : f2(col_in(s) ? v.x : 0.f, col_in(s + 1) ? v.y : 0.f);
+    return (INT || TCR<Z, RB>::DUMMY) ? v : f2(col_in(s) ? v.x : 0.f, col_in(s + 1) ? v.y : 0.f);
   }
-  static constexpr bool kDummy = !INT && TC<Z>::DUMMY;
+  static constexpr bool kDummy = !INT && TCR<Z, RB>::DUMMY;
   // E row of the samples: the row itself, or the dummy zero rows when it is outside the image
   __device__ __forceinline__ float yrow(int er) const {
     const float Yf = (float)(YE0 - PY0 + er);
@@ -239,7 +239,7 @@ struct Tile : YRoute<!INT && TC<Z>::DUMMY, Z / 2> {
       for (int s = 0; s < Z; ++s) om[s] = (rin && (unsigned)(X0g + s) < (unsigned)W) ? __ldg(src + X0g + s) : 0.f;
       return;
     }
-    const float* src = OM + er * TC<Z>::ECOL + Z * lane;
+    const float* src = OM + er * TCR<Z, RB>::ECOL + Z * lane;
     if constexpr (Z == 2) {
       float2 v = *reinterpret_cast<const float2*>(src);
       om[0] = v.x; om[1] = v.y;
@@ -257,8 +257,8 @@ struct Tile : YRoute<!INT && TC<Z>::DUMMY, Z / 2> {
   // own positions, the rest from the next lanes by shuffles.
   // omr: the row's disparities already in registers (per-view ring of view_pass), or nullptr.
   __device__ __forceinline__ void fwd_vals(int er, int lane, float drho, float dtau, const float* omk,
-                                           float (&val)[TC<Z>::NTAP], const float* omr = nullptr) const {
-    constexpr int NTAP = TC<Z>::NTAP;
+                                           float (&val)[TCR<Z, RB>::NTAP], const float* omr = nullptr) const {
+    constexpr int NTAP = TCR<Z, RB>::NTAP;
     float om[Z], wp[Z];
     if (omr) {
 #pragma unroll
@@ -298,7 +298,7 @@ struct Tile : YRoute<!INT && TC<Z>::DUMMY, Z / 2> {
   // W_k then the horizontal blur taps at this lane's LR column, for E row er.
   __device__ __forceinline__ float fwd_row(int er, int lane, float drho, float dtau, const float* omk,
                                           const Geom& G, const float* omr = nullptr) const {
-    constexpr int NTAP = TC<Z>::NTAP;
+    constexpr int NTAP = TCR<Z, RB>::NTAP;
     if (!kDummy && !row_in(er)) return 0.f;    // blur zero padding (A11), warp uniform
     float val[NTAP];
     fwd_vals(er, lane, drho, dtau, omk, val, omr);
@@ -318,8 +318,8 @@ struct Tile : YRoute<!INT && TC<Z>::DUMMY, Z / 2> {
   // cost 4 % at C4/C5).
   __device__ __forceinline__ void adj_row(int er, int lane, float t1b, float drho, float dtau, const float* omk,
                                           const Geom& G, const float* omr = nullptr) const {
-    constexpr int NJ = 2 * TC<Z>::R / Z + 1;
-    constexpr int R2 = 2 * TC<Z>::R;
+    constexpr int NJ = 2 * TCR<Z, RB>::R / Z + 1;
+    constexpr int R2 = 2 * TCR<Z, RB>::R;
     if (!kDummy && !row_in(er)) return;        // E positions outside the image carry no adjoint (A11)
     float tv[NJ];
     tv[0] = t1b;
@@ -430,7 +430,7 @@ struct NltvCtx {
   float ith;
 };
 
-template <int Z, int MODE, bool CHECK, int RAD>
+template <int Z, int MODE, bool CHECK, int RAD, int RB>
 __device__ __forceinline__ float nltv_pixel(const NltvCtx& c, const Geom& G, int Y, int X, int py, int px, int mi,
                                             size_t gi, double& pq, double& reg, double& res) {
   const float xz = c.P[pidx<Z>(py, px, c.PW, c.PWZ)];
@@ -438,7 +438,7 @@ __device__ __forceinline__ float nltv_pixel(const NltvCtx& c, const Geom& G, int
   float acc = 0.f;
   float fpq = 0.f, freg = 0.f, fres = 0.f;   // this pixel's reduction terms (<= s_d each), fp32
   // the m tile pitch is a compile-time constant on the unrolled (RAD > 0) path
-  const int MW = RAD > 0 ? TC<Z>::TX + 2 * RAD : c.MW;
+  const int MW = RAD > 0 ? TCR<Z, RB>::TX + 2 * RAD : c.MW;
   auto one = [&](int d, int dy, int dx) {
     const float wd = G.wd[d];
     const bool fin = !CHECK || ((Y + dy >= 0) && (Y + dy < c.H) && (X + dx >= 0) && (X + dx < c.W));
@@ -559,11 +559,11 @@ __device__ __forceinline__ void pass_reductions(const Geom& G, float fa, float f
 
 // PM (paper-mode adjoint, A37): the pass stops after the epilogue and writes rho to
 // io.rho_out; k_paper_gather applies the backward warp afterwards.
-template <int Z, int MODE, bool INT, int NV, bool PV, bool PM>
-__device__ __forceinline__ void view_pass(const Tile<Z, INT>& t, const Geom& G, const Views& V, const TileIO& io,
+template <int Z, int MODE, bool INT, int NV, bool PV, bool PM, int RB>
+__device__ __forceinline__ void view_pass(const Tile<Z, INT, RB>& t, const Geom& G, const Views& V, const TileIO& io,
                                           const int (&ks)[NV], int lane, int i0, int j0, int BL, double& red_a,
                                           double& red_b, double& red_c) {
-  using C = TC<Z>;
+  using C = TCR<Z, RB>;
   constexpr int LX = C::LX, NTAP = C::NTAP, KEEP = C::KEEP;
   constexpr bool kFwd = (MODE != MODE_AT);
   constexpr bool kAdj = (MODE != MODE_A && MODE != MODE_J);
@@ -681,14 +681,16 @@ __device__ __forceinline__ void view_pass(const Tile<Z, INT>& t, const Geom& G, 
 // The same pass with a user (non-separable) blur kernel (A36), kernel
 // psf2[a][b] in E-offset order.  Forward: every E row's window values (fwd_vals) feed the
 // Q pending LR rows it lies under with that kernel row (sliding accumulators instead of
-// the separable code's ring of horizontally filtered rows).  Adjoint: the last Q LR rows'
-// rho, already shuffled across the NJ LR columns an E column receives from, are kept; each
-// finished E row sums its kernel taps over them and goes to the same scatter.
-template <int Z, int MODE, bool INT>
-__device__ __forceinline__ void view_pass2d(const Tile<Z, INT>& t, const Geom& G, const Views& V, const TileIO& io,
+// the separable code's ring of horizontally filtered rows).  Adjoint: each lane keeps the
+// rho of its own LR column for the last Q LR rows; a finished E row forms, per kernel
+// column b, the vertical partial sum over those rows, and the partials of the LR columns to
+// the left (the Q columns an E column receives from) arrive by warp shuffles -- Q registers
+// of history instead of Q x Q (kernels up to 15 x 15 without spills).
+template <int Z, int MODE, bool INT, int RB>
+__device__ __forceinline__ void view_pass2d(const Tile<Z, INT, RB>& t, const Geom& G, const Views& V, const TileIO& io,
                                             int k, int lane, int i0, int j0, int BL, double& red_a, double& red_b,
                                             double& red_c) {
-  using C = TC<Z>;
+  using C = TCR<Z, RB>;
   constexpr int LX = C::LX, NTAP = C::NTAP, KEEP = C::KEEP, R2 = 2 * C::R;
   constexpr int Q = R2 / Z + 1;      // LR rows one E row lies under (and LR columns one E column)
   constexpr bool kFwd = (MODE != MODE_AT);
@@ -698,12 +700,11 @@ __device__ __forceinline__ void view_pass2d(const Tile<Z, INT>& t, const Geom& G
   const bool col_ok = lane < LX && j < G.w;
   const float drho = V.off[k].x, dtau = V.off[k].y;
   const size_t lrow0 = ((size_t)k * G.h) * G.lps + j;
-  float acc[Q], tvh[Q][Q];
+  float acc[Q], rh[Q];
 #pragma unroll
   for (int d = 0; d < Q; ++d) {
     acc[d] = 0.f;
-#pragma unroll
-    for (int jj = 0; jj < Q; ++jj) tvh[d][jj] = 0.f;
+    rh[d] = 0.f;
   }
   float fa = 0.f, fb = 0.f, fc = 0.f;
   float y_nx = 0.f, wa_nx = 0.f;
@@ -731,17 +732,26 @@ __device__ __forceinline__ void view_pass2d(const Tile<Z, INT>& t, const Geom& G
     if (!t.kDummy && !t.row_in(er)) return;
     float tt[Z];
 #pragma unroll
-    for (int s = 0; s < Z; ++s) {
-      float h = 0.f;
+    for (int s = 0; s < Z; ++s) tt[s] = 0.f;
 #pragma unroll
-      for (int d = 0; d < Q; ++d) {
-        const int a = Z * d + uu;
-        if (a > R2) continue;
+    for (int jj = 0; jj < Q; ++jj) {
 #pragma unroll
-        for (int jj = 0; jj < Q; ++jj)
-          if (Z * jj + s <= R2) h = fmaf(G.psf2[a][Z * jj + s], tvh[d][jj], h);
+      for (int s = 0; s < Z; ++s) {
+        const int b = Z * jj + s;
+        if (b > R2) continue;
+        float h = 0.f;   // column (lane - jj)'s vertical partial for kernel column b
+#pragma unroll
+        for (int d = 0; d < Q; ++d) {
+          const int a = Z * d + uu;
+          if (a <= R2) h = fmaf(G.psf2[a][b], rh[d], h);
+        }
+        if (jj == 0) {
+          tt[s] += h;
+        } else {
+          const float v = __shfl_up_sync(0xffffffffu, h, jj);
+          tt[s] += lane >= jj ? v : 0.f;
+        }
       }
-      tt[s] = h;
     }
     t.scatter(er, lane, tt, drho, dtau, nullptr);
   };
@@ -772,15 +782,8 @@ __device__ __forceinline__ void view_pass2d(const Tile<Z, INT>& t, const Geom& G
     }
     if (kAdj) {
 #pragma unroll
-      for (int d = Q - 1; d > 0; --d)
-#pragma unroll
-        for (int jj = 0; jj < Q; ++jj) tvh[d][jj] = tvh[d - 1][jj];
-      tvh[0][0] = rho;
-#pragma unroll
-      for (int jj = 1; jj < Q; ++jj) {
-        const float v = __shfl_up_sync(0xffffffffu, rho, jj);
-        tvh[0][jj] = lane >= jj ? v : 0.f;
-      }
+      for (int d = Q - 1; d > 0; --d) rh[d] = rh[d - 1];
+      rh[0] = rho;
 #pragma unroll
       for (int u = 0; u < Z; ++u) emit(Z * li + u, u);
     }
@@ -792,29 +795,30 @@ __device__ __forceinline__ void view_pass2d(const Tile<Z, INT>& t, const Geom& G
   pass_reductions<MODE>(G, fa, fb, fc, red_a, red_b, red_c);
 }
 
-template <int Z, int MODE, bool INT, bool PV, bool P2, bool PM>
-__device__ __forceinline__ void views(const Tile<Z, INT>& t, const Geom& G, const Views& V, const TileGeom& T,
+template <int Z, int MODE, bool INT, bool PV, bool P2, bool PM, int RB>
+__device__ __forceinline__ void views(const Tile<Z, INT, RB>& t, const Geom& G, const Views& V, const TileGeom& T,
                                       const TileIO& io, int grp, int lane, int warp, int NW, int i0, int j0, int BL,
                                       double& red_a, double& red_b, double& red_c) {
   const int kbeg = grp * T.vpg;
   const int kend = min(G.n_views, kbeg + T.vpg);
   for (int k = kbeg + warp; k < kend; k += NW) {
     const int ks[1] = {k};
-    if constexpr (P2) view_pass2d<Z, MODE, INT>(t, G, V, io, k, lane, i0, j0, BL, red_a, red_b, red_c);
-    else view_pass<Z, MODE, INT, 1, PV, PM>(t, G, V, io, ks, lane, i0, j0, BL, red_a, red_b, red_c);
+    if constexpr (P2) view_pass2d<Z, MODE, INT, RB>(t, G, V, io, k, lane, i0, j0, BL, red_a, red_b, red_c);
+    else view_pass<Z, MODE, INT, 1, PV, PM, RB>(t, G, V, io, ks, lane, i0, j0, BL, red_a, red_b, red_c);
   }
 }
 
-// FIXBL: the tile height is the compile-time default TC<Z>::BL (the launcher picks this
+// FIXBL: the tile height is the compile-time default TCR<Z, RB>::BL (the launcher picks this
 // instantiation whenever T.BL equals it: constant loop bounds, ~1.5 % faster at C3).
 // PV: per-view disparity maps omega_k read from global memory (A34); a compile-time
 // switch because even a warp-uniform runtime test cost the shared-map path ~12 %.
 // P2: user (non-separable) blur kernel (A36, view_pass2d).
 // PM: paper-mode adjoint (A37): no scatter, rho to io.rho_out (k_paper_gather follows).
-template <int Z, int MODE, bool FIXBL, bool PV, bool P2, bool PM>
-__global__ void __launch_bounds__(LaunchCfgM<Z, MODE>::MAXW * 32, LaunchCfgM<Z, MODE>::MINB)
+// RB: blur radius of the instance (the Gaussian's R(zeta), or kPsfBigR for large user kernels).
+template <int Z, int MODE, bool FIXBL, bool PV, bool P2, bool PM, int RB = TileCfg<Z>::R>
+__global__ void __launch_bounds__(LaunchCfgR<Z, MODE, RB>::MAXW * 32, LaunchCfgR<Z, MODE, RB>::MINB)
 k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
-  using C = TC<Z>;
+  using C = TCR<Z, RB>;
   constexpr int R = C::R, LX = C::LX, TX = C::TX, ECOL = C::ECOL;
   const int BL = FIXBL ? C::BL : T.BL, TY = Z * BL, EY = Z * BL + C::KEEP;
   constexpr bool kFwd = (MODE != MODE_AT);
@@ -1030,10 +1034,10 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
       tile.P = P; tile.ACC = ACC; tile.OM = OM; tile.PW = PW; tile.PWZ = PWZ; tile.PY0 = PY0; tile.PX0 = PX0;
       tile.YE0 = YE0; tile.XE0 = XE0; tile.H = H; tile.W = W; tile.PS = ps; tile.tscale = s_scale[0]; tile.lo = LO;
       tile.koff = koff; tile.rows_in = rows_in;
-      views<Z, MODE, decltype(tile)::kInt, PV, P2, PM>(tile, G, V, T, io, grp, lane, warp, NW, i0, j0, BL, red_a, red_b, red_c);
+      views<Z, MODE, decltype(tile)::kInt, PV, P2, PM, RB>(tile, G, V, T, io, grp, lane, warp, NW, i0, j0, BL, red_a, red_b, red_c);
     };
-    if (cols_in && rows_in) run(Tile<Z, true>{});   // (columns-only interior: measured slower)
-    else run(Tile<Z, false>{});
+    if (cols_in && rows_in) run(Tile<Z, true, RB>{});   // (columns-only interior: measured slower)
+    else run(Tile<Z, false, RB>{});
   }
   if (MODE == MODE_A) return;
 
@@ -1068,10 +1072,10 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
           double pq = 0.0;
           const bool inner = Y >= rr && Y < H - rr && X >= rr && X < W - rr;
           if (rr == 2) {
-            acc = inner ? nltv_pixel<Z, MODE, false, 2>(c, G, Y, X, py, px, mi, gi, pq, red_reg, red_c)
-                        : nltv_pixel<Z, MODE, true, 2>(c, G, Y, X, py, px, mi, gi, pq, red_reg, red_c);
+            acc = inner ? nltv_pixel<Z, MODE, false, 2, RB>(c, G, Y, X, py, px, mi, gi, pq, red_reg, red_c)
+                        : nltv_pixel<Z, MODE, true, 2, RB>(c, G, Y, X, py, px, mi, gi, pq, red_reg, red_c);
           } else {
-            acc = nltv_pixel<Z, MODE, true, 0>(c, G, Y, X, py, px, mi, gi, pq, red_reg, red_c);
+            acc = nltv_pixel<Z, MODE, true, 0, RB>(c, G, Y, X, py, px, mi, gi, pq, red_reg, red_c);
           }
           if (MODE == MODE_WZ || MODE == MODE_NORMAL) acc *= G.cS;
           red_b += (double)G.cS * pq;
@@ -1126,11 +1130,11 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
 // only for per-view maps (PV) and for a user blur kernel (P2).
 template <int Z>
 struct TileZ {
-  template <int MODE, bool F, bool PV, bool P2, bool PM = false>
+  template <int MODE, bool F, bool PV, bool P2, bool PM = false, int RB = TileCfg<Z>::R>
   static cudaError_t launch1(const Geom& G, const Views& V, const TileGeom& T, const TileIO& io, cudaStream_t st) {
     const int nw = MODE == MODE_NORMAL ? T.nwarps_n : T.nwarps;
     const size_t sm = MODE == MODE_NORMAL ? T.smem_normal : T.smem;
-    k_tile<Z, MODE, F, PV, P2, PM><<<T.ntYl * T.ntX * T.groups, nw * 32, sm, st>>>(G, V, T, io);
+    k_tile<Z, MODE, F, PV, P2, PM, RB><<<T.ntYl * T.ntX * T.groups, nw * 32, sm, st>>>(G, V, T, io);
     return cudaGetLastError();
   }
   template <int MODE>
@@ -1138,7 +1142,9 @@ struct TileZ {
     constexpr bool kHasAdj = (MODE == MODE_WZ || MODE == MODE_NORMAL || MODE == MODE_GRAD);
     if constexpr (kHasAdj)
       if (G.paper) return launch1<MODE, false, false, false, true>(G, V, T, io, st);
-    if (G.psf2d) return launch1<MODE, false, false, true>(G, V, T, io, st);
+    if (G.psf2d)
+      return G.psf_rb == kPsfBigR ? launch1<MODE, false, false, true, false, kPsfBigR>(G, V, T, io, st)
+                                  : launch1<MODE, false, false, true>(G, V, T, io, st);
     if (G.per_view) return launch1<MODE, false, true, false>(G, V, T, io, st);
     if (MODE == MODE_GRAD || MODE == MODE_J) return launch1<MODE, false, false, false>(G, V, T, io, st);
     return T.BL == TC<Z>::BL ? launch1<MODE, true, false, false>(G, V, T, io, st)
@@ -1156,9 +1162,9 @@ struct TileZ {
     }
     return cudaErrorInvalidValue;
   }
-  template <int MODE, bool F, bool PV, bool P2, bool PM = false>
+  template <int MODE, bool F, bool PV, bool P2, bool PM = false, int RB = TileCfg<Z>::R>
   static cudaError_t prep1(size_t smem) {
-    return cudaFuncSetAttribute(k_tile<Z, MODE, F, PV, P2, PM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    return cudaFuncSetAttribute(k_tile<Z, MODE, F, PV, P2, PM, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem);
   }
   template <int MODE>
@@ -1170,6 +1176,7 @@ struct TileZ {
     if ((e = prep1<MODE, false, true, false>(smem)) != cudaSuccess) return e;
     if constexpr (MODE == MODE_WZ || MODE == MODE_NORMAL || MODE == MODE_GRAD)
       if ((e = prep1<MODE, false, false, false, true>(smem)) != cudaSuccess) return e;
+    if ((e = prep1<MODE, false, false, true, false, kPsfBigR>(smem)) != cudaSuccess) return e;
     return prep1<MODE, false, false, true>(smem);
   }
   static cudaError_t prepare(size_t smem) {

@@ -13,9 +13,9 @@ namespace lfsr {
 // --------------------------------------------------------------------------------
 // Host-side geometry and launchers
 // --------------------------------------------------------------------------------
-template <int Z>
+template <int Z, int RB = TileCfg<Z>::R>
 static void fill_static(TileGeom& T) {
-  using C = TC<Z>;
+  using C = TCR<Z, RB>;
   if (T.BL <= 0) T.BL = C::BL;
   T.LX = C::LX; T.TY = Z * T.BL; T.TX = C::TX;
   T.EY = Z * T.BL + C::KEEP; T.ECOL = C::ECOL; T.EXv = C::EXv;
@@ -99,10 +99,11 @@ int tile_max_warps_normal(int scale) {
 TileGeom make_tile_geom(const Geom& G, int num_sms, int tr0, int tr1) {
   TileGeom T{};
   T.BL = G.tile_bl;
+  const bool big = G.psf2d && G.psf_rb == kPsfBigR;   // large user blur kernel (A36): its own E region
   switch (G.scale) {
-    case 2: fill_static<2>(T); break;
-    case 3: fill_static<3>(T); break;
-    default: fill_static<4>(T); break;
+    case 2: big ? fill_static<2, kPsfBigR>(T) : fill_static<2>(T); break;
+    case 3: big ? fill_static<3, kPsfBigR>(T) : fill_static<3>(T); break;
+    default: big ? fill_static<4, kPsfBigR>(T) : fill_static<4>(T); break;
   }
   T.SYe = G.SY > G.radius ? G.SY : G.radius;
   T.SXe = G.SX > G.radius ? G.SX : G.radius;
@@ -117,7 +118,8 @@ TileGeom make_tile_geom(const Geom& G, int num_sms, int tr0, int tr1) {
   T.tY0 = tr0 < 0 ? 0 : tr0;
   T.ntYl = (tr1 < 0 ? T.ntY : tr1) - T.tY0;
   const int tiles = T.ntYl * T.ntX;
-  const int max_warps = G.scale == 2 ? LaunchCfg<2>::MAXW : G.scale == 3 ? LaunchCfg<3>::MAXW : LaunchCfg<4>::MAXW;
+  const int max_warps = big ? LaunchCfgR<2, MODE_WZ, kPsfBigR>::MAXW
+                        : G.scale == 2 ? LaunchCfg<2>::MAXW : G.scale == 3 ? LaunchCfg<3>::MAXW : LaunchCfg<4>::MAXW;
   T.smem = smem_bytes(T, max_warps);
   if (prepare_tile_kernels(G.scale, T.smem) != cudaSuccess) cudaGetLastError();
   int best_g = 1, best_w = 1;
@@ -146,7 +148,7 @@ TileGeom make_tile_geom(const Geom& G, int num_sms, int tr0, int tr1) {
   T.vpg = (G.n_views + best_g - 1) / best_g;
   T.groups = (G.n_views + T.vpg - 1) / T.vpg;
   T.smem = smem_bytes(T, T.nwarps);
-  const int max_n = G.scale == 2 ? LaunchCfgM<2, MODE_NORMAL>::MAXW : max_warps;
+  const int max_n = (G.scale == 2 && !big) ? LaunchCfgM<2, MODE_NORMAL>::MAXW : max_warps;
   T.nwarps_n = (G.tile_nwn > 0 && G.tile_nwn <= max_n) ? G.tile_nwn : T.nwarps;
   T.smem_normal = smem_bytes(T, T.nwarps_n);
   return T;

@@ -60,15 +60,17 @@ def test_validation_before_device(lib):
         assert s == lfsr.LFSR_ERR_INVALID_ARG, b
         assert len(lib.lfsr_last_error(None)) > 0
     assert lib.lfsr_create(ctypes.byref(good.to_c()), None) == lfsr.LFSR_ERR_INVALID_ARG
-    # user blur kernel (A36): radius beyond the zeta window, non-finite taps
+    # user blur kernel (A36): radius beyond 7 (15x15), non-finite taps
     k = np.ones((3, 3), np.float32)
     k[1, 1] = np.nan
-    for psf in (np.ones((7, 7), np.float32), k):
+    for psf in (np.ones((17, 17), np.float32), k):
         p = dataclasses.replace(good, psf=psf)
         h = ctypes.c_void_p()
         assert lib.lfsr_create(ctypes.byref(p.to_c()), ctypes.byref(h)) == lfsr.LFSR_ERR_INVALID_ARG
     # the paper-mode adjoint (A37) is single-strip, Gaussian-blur only
-    for over in (dict(paper_adjoint=1, n_ranks=2, rank=-1), dict(paper_adjoint=1, psf=np.ones((3, 3), np.float32) / 9)):
+    # (and a kernel larger than the Gaussian window is single-strip)
+    for over in (dict(paper_adjoint=1, n_ranks=2, rank=-1), dict(paper_adjoint=1, psf=np.ones((3, 3), np.float32) / 9),
+                 dict(psf=np.ones((9, 9), np.float32) / 81, n_ranks=2, rank=-1)):
         p = dataclasses.replace(good, **over)
         h = ctypes.c_void_p()
         assert lib.lfsr_create(ctypes.byref(p.to_c()), ctypes.byref(h)) == lfsr.LFSR_ERR_UNSUPPORTED

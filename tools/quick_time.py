@@ -8,7 +8,7 @@ import paper_2206_05047_b200 as L
 cfgname = sys.argv[1] if len(sys.argv) > 1 else "C3"
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 10
 per_view = len(sys.argv) > 3 and sys.argv[3] == "pv"   # per-view disparity maps (A34)
-user_psf = len(sys.argv) > 3 and sys.argv[3] == "psf"  # 45-degree motion kernel as B (A36)
+user_psf = len(sys.argv) > 3 and sys.argv[3].startswith("psf")  # 45-degree motion kernel as B (A36); psf<len>
 paper = len(sys.argv) > 3 and sys.argv[3] == "paper"    # the paper's backward-warp adjoint (A37)
 t0 = time.time()
 lf = S.make_lightfield(cfgname)
@@ -18,7 +18,8 @@ p = L.params_for(cfg, S.defaults_for(cfg))
 if paper:
     p.paper_adjoint = 1
 if user_psf:
-    p.psf = S.motion_psf(5 if cfg.scale == 2 else 7, 45.0)
+    n = int(sys.argv[3][3:]) if len(sys.argv[3]) > 3 else (5 if cfg.scale == 2 else 7)
+    p.psf = S.motion_psf(n, 45.0)
 stream = torch.cuda.Stream()
 torch.cuda.set_stream(stream)
 s = L.Solver(p, stream=stream.cuda_stream)
