@@ -303,6 +303,19 @@ LFSR_API int32_t lfsr_launches_per_iter(const lfsr_ctx* ctx);
 LFSR_API lfsr_status lfsr_tile_config(const lfsr_ctx* ctx, int32_t* tile_rows, int32_t* view_groups,
                                       int32_t* warps_per_cta, int32_t* cg_warps_per_cta);
 
+/* The MISR / global-shift fast path of the CG normal operator.
+ * When the disparity map is one constant (every view a global translation, as the MISR frames
+ * of P:L1110-1116), lfsr_set_observations assembles the data part of M (A7) as a
+ * zeta^2-phase stencil on the host in fp64, and each CG step runs it on the interior rectangle
+ * Z_s where it is exact, with the exact tile kernel on the border tiles for the band outside
+ * Z_s.  Requires the shared disparity layout, the Gaussian blur, the exact adjoint, a single
+ * strip, nltv_radius 2; LFSR_MISR_FAST=0 in the environment at lfsr_set_observations turns it
+ * off; lfsr_solve_batch never uses it.  Results match the generic path to fp32 rounding.
+ * active: 1 if the current observations use it.  rect (NULL or int32[8]): Z_s as [y0, y1) x
+ * [x0, x1), then the HR pixels no border tile owns, same layout.  Errors: INVALID_ARG (ctx or
+ * active NULL), STATE (before lfsr_set_observations). */
+LFSR_API lfsr_status lfsr_fast_path(const lfsr_ctx* ctx, int32_t* active, int32_t* rect);
+
 /* Row-strip plan of the multi-GPU decomposition (DESIGN 10): rank r
  * owns tile rows [tile_row0, tile_row1) = LR rows [lr_row0, lr_row1) = HR rows
  * [hr_row0, hr_row1); before every operator pass it needs halo_top HR rows above

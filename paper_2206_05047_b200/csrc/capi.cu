@@ -45,6 +45,9 @@ cudaError_t launch_paper_gather(const Geom& G, const Views& V, const float* rho,
                                 cudaStream_t st);
 cudaError_t launch_color(int to_ycbcr, const float* a, float* y, float* cb, float* cr, size_t n, int num_sms,
                          cudaStream_t st);
+cudaError_t launch_omega_const(const Geom& G, const float* omega, unsigned* flag, cudaStream_t st);
+cudaError_t launch_misr_normal(const Geom& G, const MisrStencil& S, const MisrArgs& a, cudaStream_t st);
+cudaError_t prepare_misr_kernels();
 cudaError_t launch_gd_update(const Geom& G, float* x, const float* g, Control* ctl, const GdCfg& cfg, int num_sms,
                              cudaStream_t st);
 }  // namespace lfsr
@@ -118,6 +121,18 @@ struct lfsr_ctx {
   std::vector<cudaEvent_t> prof_ev;
   double prof_ms[3] = {0, 0, 0}; // accumulated wz / normal / update milliseconds
   int64_t prof_n[3] = {0, 0, 0};
+  // MISR fast path (misr.cu): constant disparity -> the CG operator's data part
+  // as a precomputed zeta^2-phase stencil on Z_s, the exact tile kernel on the border tiles
+  bool misr = false;
+  bool in_batch = false;           // lfsr_solve_batch swaps fields under one graph: no fast path there
+  MisrStencil* misr_S = nullptr;   // host copy (passed by value to k_misr_normal)
+  MisrArgs misr_a{};               // regions (pointers filled per launch)
+  TileGeom Tborder{};              // c->Tfull restricted to the border tiles
+  int* d_tlist = nullptr;
+  int tlist_cap = 0;
+  float* d_misr_tab = nullptr;     // separable form: T_y [H][2WR+1], T_x [W][2WR+1]
+  size_t misr_tab_bytes = 0;
+  bool misr_border = true;         // the dense form runs the border tiles through k_tile
   std::string err;
 };
 
@@ -485,6 +500,11 @@ static void free_state(lfsr_ctx* c) {
   c->op_ctl = nullptr;
   c->umax = nullptr;
   c->d_ctls = nullptr;
+  c->d_tlist = nullptr;
+  c->tlist_cap = 0;
+  c->d_misr_tab = nullptr;
+  c->misr_tab_bytes = 0;
+  c->misr = false;
   for (auto& k : c->alloc_key) k = 0;
   c->ready = false;
 }
@@ -503,6 +523,7 @@ void lfsr_destroy(lfsr_ctx* c) {
   if (c->h_ubits) cudaFreeHost(c->h_ubits);
   if (c->h_ctl) cudaFreeHost(c->h_ctl);
   if (c->h_rec) cudaFreeHost(c->h_rec);
+  delete c->misr_S;
   if (c->comm) {
     if (c->poisoned) nccl_comm_abort(c->comm);
     else nccl_comm_destroy(c->comm);
@@ -521,6 +542,18 @@ lfsr_status lfsr_get_stream(const lfsr_ctx* c, void** stream) {
 const char* lfsr_last_error(const lfsr_ctx* c) { return c ? c->err.c_str() : g_create_err.c_str(); }
 
 int32_t lfsr_launches_per_iter(const lfsr_ctx* c) { return (c && c->ready) ? c->launches_per_iter : 0; }
+
+lfsr_status lfsr_fast_path(const lfsr_ctx* c, int32_t* active, int32_t* rect) {
+  if (!c || !active) return LFSR_ERR_INVALID_ARG;
+  if (!c->ready) return LFSR_ERR_STATE;
+  *active = c->misr ? 1 : 0;
+  if (rect) {
+    const MisrArgs& a = c->misr_a;
+    const int32_t v[8] = {a.zs_y0, a.zs_y1, a.zs_x0, a.zs_x1, a.o_y0, a.o_y1, a.o_x0, a.o_x1};
+    for (int i = 0; i < 8; ++i) rect[i] = c->misr ? v[i] : 0;
+  }
+  return LFSR_OK;
+}
 
 lfsr_status lfsr_tile_config(const lfsr_ctx* c, int32_t* tile_rows, int32_t* view_groups, int32_t* warps_per_cta,
                              int32_t* cg_warps_per_cta) {
@@ -827,6 +860,356 @@ static lfsr_status set_shift_halo(lfsr_ctx* c, float om_max, float mx_rho, float
   return LFSR_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// MISR fast path (misr.cu).  With a constant disparity c every view is a
+// global shift s_k = dtheta_k c; the operator A_k = D B W_k is then, per axis, the composition
+// of 1-D maps, A_k = A_k^y (x) A_k^x away from the border, and the data normal operator is the
+// zeta^2-phase stencil S[phase][dy][dx] = c_A sum_k T_k^y[phase_y][dy] T_k^x[phase_x][dx] with
+// T_k[phi][D] = sum_l A_k[l, z0] A_k[l, z0 + D] (z0 = phi mod zeta, interior).  Assembled here in
+// fp64 with the oracle's arithmetic (samples at Y + dtau c, X + drho c in double, A13), rounded
+// to fp32 once.  Z_s: the outputs whose contributing LR pixels all have unclamped, unpadded rows
+// (per axis, brute force); the border tiles: every tile holding an LR pixel that reaches an output
+// outside Z_s, or owning such an output.
+// ---------------------------------------------------------------------------
+struct Axis1 {
+  int lo = 0, hi = 0;          // Z_s on this axis: [lo, hi)
+  std::vector<char> lb;        // LR index belongs to a border tile band
+};
+
+static void misr_axis(int N, int n, int Z, int R, int rad, const std::vector<int>& nk, const std::vector<double>& fk,
+                      Axis1& out) {
+  const int K = (int)nk.size();
+  auto interior = [&](int l) {
+    if (l < 0 || l >= n) return false;
+    for (int u = -R; u <= R; ++u) {
+      const int a = Z * l + u;
+      if (a < 0 || a > N - 1) return false;
+      for (int k = 0; k < K; ++k)
+        if (a + nk[k] < 0 || a + nk[k] + (fk[k] > 0.0 ? 1 : 0) > N - 1) return false;
+    }
+    return true;
+  };
+  std::vector<char> lin(n);
+  for (int l = 0; l < n; ++l) lin[l] = interior(l);
+  std::vector<char> valid(N, 0);
+  for (int z = 0; z < N; ++z) {
+    bool ok = z >= rad && z < N - rad;
+    for (int k = 0; k < K && ok; ++k)
+      for (int e = 0; e <= 1 && ok; ++e)
+        for (int u = -R; u <= R && ok; ++u) {
+          const int t = z - u - nk[k] - e;   // = Z l
+          if (((t % Z) + Z) % Z) continue;
+          const int l = (t - ((t % Z) + Z) % Z) / Z;
+          if (l < 0 || l >= n || !lin[l]) ok = false;
+        }
+    valid[z] = ok;
+  }
+  // largest run of valid outputs
+  int best_lo = 0, best_len = 0;
+  for (int z = 0; z < N;) {
+    if (!valid[z]) { ++z; continue; }
+    int e = z;
+    while (e < N && valid[e]) ++e;
+    if (e - z > best_len) { best_len = e - z; best_lo = z; }
+    z = e;
+  }
+  out.lo = best_lo;
+  out.hi = best_lo + best_len;
+  out.lb.assign(n, 0);
+  for (int l = 0; l < n; ++l)
+    for (int k = 0; k < K; ++k)
+      for (int e = 0; e <= 1; ++e)
+        for (int u = -R; u <= R; ++u) {
+          const int z = std::min(std::max(Z * l + u + nk[k] + e, 0), N - 1);
+          if (z < out.lo || z >= out.hi) out.lb[l] = 1;
+        }
+  for (int z = 0; z < N; ++z)
+    if (z < out.lo || z >= out.hi) out.lb[std::min(z / Z, n - 1)] = 1;
+}
+
+// T[phi][D + 2WR'] for one view along one axis (interior): sum over the LR rows l of A[l, z0] A[l, z0 + D].
+static void misr_T(int Z, int R, const std::vector<double>& g, int nk, double fk, std::vector<double>& T) {
+  const int WR = 2 * R + 1, NW = 2 * WR + 1;
+  T.assign((size_t)Z * NW, 0.0);
+  const int L0 = 100000;   // a virtual interior LR index (far from any shift)
+  for (int phi = 0; phi < Z; ++phi) {
+    const int z0 = Z * L0 + phi;
+    const int lc = (z0 - nk) / Z;   // the LR rows that reach z0 lie within R + 1 of z0 - nk
+    for (int l = lc - R - 2; l <= lc + R + 2; ++l) {
+      // row of A along this axis: positions Z l + u + nk + e with weight g[u] w(e)
+      double row[64];
+      int base = Z * l - R + nk;   // position of index 0
+      for (int i = 0; i < 64; ++i) row[i] = 0.0;
+      for (int u = -R; u <= R; ++u) {
+        row[u + R] += g[u + R] * (1.0 - fk);
+        row[u + R + 1] += g[u + R] * fk;
+      }
+      const int i0 = z0 - base;
+      if (i0 < 0 || i0 > 2 * R + 1 || row[i0] == 0.0) continue;
+      for (int i = 0; i <= 2 * R + 1; ++i) {
+        const int D = base + i - z0;
+        if (D < -WR || D > WR || row[i] == 0.0) continue;
+        T[(size_t)phi * NW + D + WR] += row[i0] * row[i];
+      }
+    }
+  }
+}
+
+// The exact banded 1-D matrix T = A^T A of one view along one axis, border included: A[l, .] =
+// sum_u g[u] x (bilinear weights of the sample at clamp(Z l + u + shift, 0, N - 1)), positions
+// Z l + u outside [0, N) dropped (blur zero padding, A11), y1 = min(y0 + 1, N - 1) (A12/A13, the
+// oracle's arithmetic in fp64).  Row z holds T[z][z + D], |D| <= 2R + 1.
+static void misr_T_exact(int N, int n, int Z, int R, const std::vector<double>& g, double shift,
+                         std::vector<double>& T) {
+  const int WR = 2 * R + 1, NW = 2 * WR + 1;
+  T.assign((size_t)N * NW, 0.0);
+  std::vector<std::pair<int, double>> row;
+  for (int l = 0; l < n; ++l) {
+    row.clear();
+    for (int u = -R; u <= R; ++u) {
+      const int a = Z * l + u;
+      if (a < 0 || a > N - 1) continue;
+      const double s = std::fmin(std::fmax((double)a + shift, 0.0), (double)(N - 1));
+      const int y0 = (int)std::floor(s), y1 = std::min(y0 + 1, N - 1);
+      const double f = s - y0;
+      row.emplace_back(y0, g[u + R] * (1.0 - f));
+      row.emplace_back(y1, g[u + R] * f);
+    }
+    for (const auto& i : row)
+      for (const auto& j : row) {
+        const int D = j.first - i.first;
+        if (D < -WR || D > WR) continue;   // cannot happen (|D| <= 2R + 1), kept as a guard
+        T[(size_t)i.first * NW + D + WR] += i.second * j.second;
+      }
+  }
+}
+
+static lfsr_status misr_setup(lfsr_ctx* c, float omega_c) {
+  Geom& G = c->G;
+  c->misr = false;
+  const char* env = getenv("LFSR_MISR_FAST");
+  if (env && env[0] == '0') return LFSR_OK;
+  if (c->in_batch || c->xmode != X_NONE || G.per_view || G.psf2d || G.paper || G.radius != 2 || G.s_d != 24)
+    return LFSR_OK;
+  const int Z = G.scale, R = G.R, WR = 2 * R + 1, NW = 2 * WR + 1;
+  if ((size_t)Z * Z * NW * NW > (size_t)kMisrMaxCoef) return LFSR_OK;
+  const int K = G.n_views;
+  std::vector<int> ny(K), nx(K);
+  std::vector<double> fy(K), fx(K);
+  for (int k = 0; k < K; ++k) {
+    const double sy = (double)c->V.off[k].y * (double)omega_c, sx = (double)c->V.off[k].x * (double)omega_c;
+    ny[k] = (int)std::floor(sy);
+    fy[k] = sy - ny[k];
+    nx[k] = (int)std::floor(sx);
+    fx[k] = sx - nx[k];
+  }
+  Axis1 ay, ax;
+  misr_axis(G.H, G.h, Z, R, G.radius, ny, fy, ay);
+  misr_axis(G.W, G.w, Z, R, G.radius, nx, fx, ax);
+  const bool interior_ok = ay.hi - ay.lo >= 2 * Z && ax.hi - ax.lo >= 2 * Z;   // dense form: an interior worth it
+  // Gaussian taps in fp64 (A11), as fill_geom
+  const double sig = 0.25 * std::sqrt((double)Z * Z - 1.0);
+  std::vector<double> g(2 * R + 1);
+  double sum = 0.0;
+  for (int u = -R; u <= R; ++u) sum += (g[u + R] = std::exp(-(double)u * u / (2.0 * sig * sig)));
+  for (double& v : g) v /= sum;
+  if (!c->misr_S) c->misr_S = new MisrStencil;
+  MisrStencil& S = *c->misr_S;
+  memset(&S, 0, sizeof S);
+  std::vector<double> acc((size_t)Z * Z * NW * NW, 0.0), Ty, Tx;
+  const double cA = (double)G.lambda2 + 0.5 * (double)G.theta * (double)G.lambda1 * (double)G.lambda1;
+  for (int k = 0; k < K; ++k) {
+    misr_T(Z, R, g, ny[k], fy[k], Ty);
+    misr_T(Z, R, g, nx[k], fx[k], Tx);
+    for (int py = 0; py < Z; ++py)
+      for (int px = 0; px < Z; ++px)
+        for (int dy = 0; dy < NW; ++dy)
+          for (int dx = 0; dx < NW; ++dx)
+            acc[(((size_t)py * Z + px) * NW + dy) * NW + dx] += Ty[(size_t)py * NW + dy] * Tx[(size_t)px * NW + dx];
+  }
+  for (size_t i = 0; i < acc.size(); ++i) S.s[i] = (float)(cA * acc[i]);
+  const bool sep = true;   // candidate; the separable form is decided on the exact 1-D matrices below
+  double W2 = 0.0;
+  for (int d = 0; d < 24; ++d) {
+    S.w2[d] = G.wd[d] * G.wd[d];
+    S.w2f[d] = G.wd[23 - d] * G.wd[23 - d];   // -d in the A9 order (the window is symmetric)
+    W2 += (double)S.w2[d];
+  }
+  S.W2 = (float)W2;
+  // separable NLTV weights: w_d^2 = u[dy] u[dx] (d != 0) with symmetric weights (Gaussian w_d, BTV)
+  {
+    auto w2 = [&](int dy, int dx) {
+      const int lin = (dy + 2) * 5 + (dx + 2);
+      return (double)G.wd[lin > 12 ? lin - 1 : lin] * (double)G.wd[lin > 12 ? lin - 1 : lin];
+    };
+    double u[5] = {0, 0, 0, 0, 0};
+    const double w11 = w2(1, 1);
+    bool ok = sep && w11 > 0.0;
+    if (ok) {
+      u[2] = std::sqrt(w2(0, 1) * w2(1, 0) / w11);
+      ok = u[2] > 0.0;
+    }
+    if (ok) {
+      for (int t = -2; t <= 2; ++t)
+        if (t) u[t + 2] = w2(t, 0) / u[2];
+      double emax = 0.0, vmax = 0.0;
+      for (int dy = -2; dy <= 2; ++dy)
+        for (int dx = -2; dx <= 2; ++dx) {
+          if (!dy && !dx) continue;
+          emax = std::fmax(emax, std::fabs(u[dy + 2] * u[dx + 2] - w2(dy, dx)));
+          emax = std::fmax(emax, std::fabs(w2(-dy, -dx) - w2(dy, dx)));   // symmetric (w_{-d} = w_d)
+          vmax = std::fmax(vmax, w2(dy, dx));
+        }
+      ok = emax <= 1e-6 * vmax;
+    }
+    S.sep = ok ? 1 : 0;
+    for (int t = 0; t < 5; ++t) S.u[t] = (float)u[t];
+  }
+  if (S.sep) {
+    // exact 1-D matrices, border included: M_data = c_A sum_a T_y,a (x) X_a with one class left,
+    // so the stencil covers the whole image and no border kernel runs
+    std::vector<std::pair<double, std::vector<double>>> ycls;   // (y shift, sum of the class's T_x)
+    std::vector<double> Ex, Ey;
+    for (int k = 0; k < K; ++k) {
+      const double sy = (double)c->V.off[k].y * (double)omega_c, sx = (double)c->V.off[k].x * (double)omega_c;
+      misr_T_exact(G.W, G.w, Z, R, g, sx, Ex);
+      bool found = false;
+      for (auto& cl : ycls)
+        if (cl.first == sy) {
+          for (size_t i = 0; i < Ex.size(); ++i) cl.second[i] += Ex[i];
+          found = true;
+          break;
+        }
+      if (!found) ycls.emplace_back(sy, Ex);
+    }
+    // classes with the same horizontal sum share one T_y sum
+    std::vector<double> Tyt((size_t)G.H * NW, 0.0);
+    const std::vector<double>& X0 = ycls[0].second;
+    double vmax = 0.0;
+    for (double v : X0) vmax = std::fmax(vmax, std::fabs(v));
+    bool one = true;
+    for (const auto& cl : ycls) {
+      double dmax = 0.0;
+      for (size_t i = 0; i < X0.size(); ++i) dmax = std::fmax(dmax, std::fabs(cl.second[i] - X0[i]));
+      if (dmax > 1e-13 * vmax) one = false;
+      misr_T_exact(G.H, G.h, Z, R, g, cl.first, Ey);
+      for (size_t i = 0; i < Ey.size(); ++i) Tyt[i] += Ey[i];
+    }
+    if (one) {
+      std::vector<float> ty(Tyt.size()), tx(X0.size());
+      for (size_t i = 0; i < Tyt.size(); ++i) ty[i] = (float)(cA * Tyt[i]);
+      for (size_t i = 0; i < X0.size(); ++i) tx[i] = (float)X0[i];
+      const size_t need = (ty.size() + tx.size()) * sizeof(float);
+      if (c->misr_tab_bytes < need || !c->d_misr_tab) {
+        void* p = nullptr;
+        cudaError_t e = dalloc(c, &p, need);
+        if (e != cudaSuccess) return cuda_fail(c, e, "alloc");
+        c->d_misr_tab = (float*)p;
+        c->misr_tab_bytes = need;
+      }
+      CK(c, cudaMemcpyAsync(c->d_misr_tab, ty.data(), ty.size() * 4, cudaMemcpyHostToDevice, c->stream));
+      CK(c, cudaMemcpyAsync(c->d_misr_tab + ty.size(), tx.data(), tx.size() * 4, cudaMemcpyHostToDevice, c->stream));
+      CK(c, cudaStreamSynchronize(c->stream));   // host vectors are locals
+      c->Tborder = c->Tfull;
+      c->Tborder.ntl = 0;
+      MisrArgs& a = c->misr_a;
+      a = MisrArgs{};
+      a.zs_y0 = 0; a.zs_y1 = G.H; a.zs_x0 = 0; a.zs_x1 = G.W;
+      a.o_y0 = 0; a.o_y1 = G.H; a.o_x0 = 0; a.o_x1 = G.W;
+      a.tyt = c->d_misr_tab;
+      a.txt = c->d_misr_tab + ty.size();
+      c->misr_border = false;
+      CK(c, prepare_misr_kernels());
+      c->misr = true;
+      return LFSR_OK;
+    }
+    S.sep = 0;   // not one class: the phase stencil on Z_s and the border kernel
+  }
+  if (!interior_ok) return LFSR_OK;
+  // border tiles of the whole-image tiling
+  const TileGeom& T = c->Tfull;
+  std::vector<char> brow(T.ntY, 0), bcol(T.ntX, 0);
+  for (int l = 0; l < G.h; ++l)
+    if (ay.lb[l]) brow[l / T.BL] = 1;
+  for (int l = 0; l < G.w; ++l)
+    if (ax.lb[l]) bcol[l / T.LX] = 1;
+  auto middle = [](const std::vector<char>& b, int& a0, int& a1) {   // non-border range must be contiguous
+    a0 = 0;
+    while (a0 < (int)b.size() && b[a0]) ++a0;
+    a1 = a0;
+    while (a1 < (int)b.size() && !b[a1]) ++a1;
+    for (int i = a1; i < (int)b.size(); ++i)
+      if (!b[i]) return false;
+    return true;
+  };
+  int ty0, ty1, tx0, tx1;
+  if (!middle(brow, ty0, ty1) || !middle(bcol, tx0, tx1)) return LFSR_OK;
+  std::vector<int> list;
+  for (int ty = 0; ty < T.ntY; ++ty)
+    for (int tx = 0; tx < T.ntX; ++tx)
+      if (brow[ty] || bcol[tx]) list.push_back(ty * T.ntX + tx);
+  if (c->tlist_cap < (int)list.size() || !c->d_tlist) {
+    void* p = nullptr;
+    cudaError_t e = dalloc(c, &p, std::max<size_t>(1, (size_t)T.ntY * T.ntX) * sizeof(int));
+    if (e != cudaSuccess) return cuda_fail(c, e, "alloc");
+    c->d_tlist = (int*)p;
+    c->tlist_cap = T.ntY * T.ntX;
+  }
+  if (!list.empty())
+    CK(c, cudaMemcpyAsync(c->d_tlist, list.data(), list.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  CK(c, cudaStreamSynchronize(c->stream));   // the host list is a local
+  c->Tborder = T;
+  c->Tborder.tlist = c->d_tlist;
+  c->Tborder.ntl = (int)list.size();
+  MisrArgs& a = c->misr_a;
+  a = MisrArgs{};
+  a.zs_y0 = ay.lo; a.zs_y1 = ay.hi; a.zs_x0 = ax.lo; a.zs_x1 = ax.hi;
+  a.o_y0 = std::min(Z * T.BL * ty0, G.H); a.o_y1 = std::min(Z * T.BL * ty1, G.H);
+  a.o_x0 = std::min(Z * T.LX * tx0, G.W); a.o_x1 = std::min(Z * T.LX * tx1, G.W);
+  c->misr_border = true;
+  CK(c, prepare_misr_kernels());
+  c->misr = true;
+  return LFSR_OK;
+}
+
+// q = M p on the MISR fast path: the exact tile kernel on the border tiles (flush masked to the
+// band outside Z_s, no <p, Mp> share), then the stencil kernel (Z_s, p_k / pi_0 on the pixels no
+// border tile owns, <p, q> over the image).  k >= 1: CG step k of part P; k = 0: plain operator
+// from `in` into `out`.
+static lfsr_status misr_normal(lfsr_ctx* c, Part& P, int k, const float* in, float* out, Control* ctl,
+                               cudaStream_t st) {
+  const Geom& G = c->G;
+  TileIO n = base_io(P);
+  n.ctl = ctl;
+  n.out_hr = out;
+  n.do_nltv = 1;
+  n.zs_on = 1;
+  n.zs_y0 = c->misr_a.zs_y0; n.zs_y1 = c->misr_a.zs_y1; n.zs_x0 = c->misr_a.zs_x0; n.zs_x1 = c->misr_a.zs_x1;
+  n.no_pq = 1;
+  MisrArgs a = c->misr_a;
+  a.m = P.S.m;
+  a.q = out;
+  a.ctl = ctl;
+  a.cg_k = k;
+  a.do_nltv = 1;
+  if (k >= 1) {
+    n.in_hr = P.S.r;
+    n.in_hr2 = P.S.p[(k - 1) & 1];
+    n.p_out = P.S.p[k & 1];
+    n.cg_k = k;
+    a.r = P.S.r;
+    a.p_prev = P.S.p[(k - 1) & 1];
+    a.p_out = P.S.p[k & 1];
+  } else {
+    n.in_hr = in;
+    a.p_in = in;
+  }
+  if (c->misr_border && c->Tborder.ntl > 0) CK(c, launch_tile(MODE_NORMAL, G, c->V, c->Tborder, n, st));
+  CK(c, launch_misr_normal(G, *c->misr_S, a, st));
+  return LFSR_OK;
+}
+
 lfsr_status lfsr_set_observations(lfsr_ctx* c, const float* lr_views, const float* view_offsets,
                                   const float* disparity, lfsr_disp_mode disp_mode, const float* x0, lfsr_mem mem) {
   if (!c) return LFSR_ERR_INVALID_ARG;
@@ -870,7 +1253,7 @@ lfsr_status lfsr_set_observations(lfsr_ctx* c, const float* lr_views, const floa
     cudaError_t e;
     if ((e = dalloc(c, &p, hr * 4)) != cudaSuccess) return cuda_fail(c, e, "alloc");
     c->tmp_hr2 = (float*)p;
-    if ((e = dalloc(c, &p, 3 * sizeof(unsigned))) != cudaSuccess) return cuda_fail(c, e, "alloc");
+    if ((e = dalloc(c, &p, 4 * sizeof(unsigned))) != cudaSuccess) return cuda_fail(c, e, "alloc");
     c->umax = (unsigned*)p;
     if (nparts > 1) {
       if ((e = dalloc(c, &p, sizeof(Control*) * nparts)) != cudaSuccess) return cuda_fail(c, e, "alloc");
@@ -917,14 +1300,19 @@ lfsr_status lfsr_set_observations(lfsr_ctx* c, const float* lr_views, const floa
   // max|omega|) per axis, in fp32 like the kernels), and the fixed-point bounds max|y| and
   // the splat density max_z sum_k (W_k^T 1)(z)
   for (int k = 0; k < nv; ++k) c->V.off[k] = make_float2(off[2 * k], off[2 * k + 1]);
-  CK(c, cudaMemsetAsync(umax, 0, 3 * sizeof(unsigned), c->stream));
+  CK(c, cudaMemsetAsync(umax, 0, 4 * sizeof(unsigned), c->stream));
   CK(c, launch_absmax(S0.omega, hr * n_om, umax, c->stream));
+  // constant disparity (global shifts: the MISR fast path, misr_setup) -- shared map only
+  if (!G.per_view) CK(c, launch_omega_const(G, S0.omega, umax + 3, c->stream));
+  else CK(c, cudaMemsetAsync(umax + 3, 0xff, sizeof(unsigned), c->stream));
   CK(c, launch_density(G, c->V, S0.omega, S0.density, c->stream));
   CK(c, launch_absmax(S0.density, hr, umax + 1, c->stream));
   CK(c, cudaStreamWaitEvent(c->stream, c->ev_in[1], 0));   // y is in place
   CK(c, launch_absmax(S0.y, lr, umax + 2, c->stream));
-  unsigned ubits[3] = {0, 0, 0};
+  unsigned ubits[4] = {0, 0, 0, 0};
+  float omega00 = 0.f;
   CK(c, cudaMemcpyAsync(ubits, umax, sizeof ubits, cudaMemcpyDeviceToHost, c->stream));
+  CK(c, cudaMemcpyAsync(&omega00, S0.omega, sizeof omega00, cudaMemcpyDeviceToHost, c->stream));
   CK(c, cudaStreamSynchronize(c->stream));
   float om_max;
   memcpy(&om_max, &ubits[0], 4);
@@ -956,6 +1344,8 @@ lfsr_status lfsr_set_observations(lfsr_ctx* c, const float* lr_views, const floa
     CK(c, launch_weights(G, S.x, S.wo, S.m, c->stream));
   }
   if (tune && (st = tune_tile_bl(c)) != LFSR_OK) return st;
+  c->misr = false;
+  if (ubits[3] == 0 && (st = misr_setup(c, omega00)) != LFSR_OK) return st;
   const auto tg0 = std::chrono::steady_clock::now();
   lfsr_status gs = build_graphs(c);
   if (gs != LFSR_OK) return gs;
@@ -1165,7 +1555,13 @@ static lfsr_status enqueue_iteration(lfsr_ctx* c, cudaStream_t st, int parity) {
     XC(xfill(c, st, rs.data(), ht, hb));                                  // r_0 halo
   }
   for (int k = 1; k <= G.K; ++k) {
+    if (c->misr) {   // constant shifts: border tiles + the precomputed stencil (misr.cu)
+      Part& P = c->parts[0];
+      XC(misr_normal(c, P, k, nullptr, P.S.q, P.S.ctl, st));
+      launches += (c->misr_border && c->Tborder.ntl > 0) ? 2 : 1;
+    }
     for (Part& P : c->parts) {
+      if (c->misr) break;
       TileIO n = base_io(P);
       n.in_hr = P.S.r;
       n.in_hr2 = P.S.p[(k - 1) & 1];
@@ -1544,6 +1940,11 @@ lfsr_status lfsr_solve_batch(lfsr_ctx* c, int32_t n_fields, const float* const* 
     if ((st = check_ptr(c, disparity[i], LFSR_MEM_HOST, "disparity[i]")) != LFSR_OK) return st;
     if ((st = check_ptr(c, x_out[i], LFSR_MEM_HOST, "x_out[i]")) != LFSR_OK) return st;
   }
+  struct BatchFlag {   // the MISR fast path is per field (its stencil depends on the disparity)
+    lfsr_ctx* c;
+    ~BatchFlag() { c->in_batch = false; }
+  } batch_flag{c};
+  c->in_batch = true;
   // field 0: the ordinary path (allocation, tiling, graphs)
   if ((st = lfsr_set_observations(c, lr_views[0], view_offsets[0], disparity[0], LFSR_DISP_SHARED, nullptr,
                                   LFSR_MEM_HOST)) != LFSR_OK)
@@ -1787,7 +2188,11 @@ lfsr_status lfsr_op_apply(lfsr_ctx* c, lfsr_op op, const float* in, float* out, 
       io.in_hr = S.tmp_hr;
       io.out_hr = c->tmp_hr2;
       io.do_nltv = 1;
-      CK(c, launch_tile(MODE_NORMAL, G, c->V, T, io, s));
+      if (c->misr) {
+        if ((st = misr_normal(c, P0, 0, S.tmp_hr, c->tmp_hr2, S.ctl, s)) != LFSR_OK) return st;
+      } else {
+        CK(c, launch_tile(MODE_NORMAL, G, c->V, T, io, s));
+      }
       if (G.paper)
         CK(c, launch_paper_gather(G, c->V, S.rho, S.omega, nullptr, c->tmp_hr2, 1.f, S.ctl, -1, 0, 0, G.H, s));
       CK(c, get2d(c, out, G.W, c->tmp_hr2, G.ps, (size_t)G.H, mem));

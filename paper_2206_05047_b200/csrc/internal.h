@@ -100,6 +100,8 @@ struct TileGeom {
   int32_t vpg;                // views per group
   int32_t nwarps;             // warps per CTA (views of a group are dealt round-robin)
   int32_t nwarps_n;           // warps per CTA of the NORMAL (CG operator) launches (may exceed nwarps)
+  const int* tlist;           // MISR fast path: the border tiles only (indices into the ntYl x ntX grid), or null
+  int32_t ntl;                // entries of tlist (0: every tile)
   size_t smem;                // dynamic shared memory bytes (largest mode)
   size_t smem_normal;         // ... of the NORMAL mode
 };
@@ -128,11 +130,44 @@ struct TileIO {
   float* rho_out;        // paper mode (A37): rho of every LR pixel [n_views][h][lps] for k_paper_gather
   float eta0;            // J: initial step of the line search
   float armijo_c;        // J: Armijo constant c (reading A32)
+  int32_t zs_on;         // MISR fast path: flush only outside the stencil rectangle Z_s ...
+  int32_t zs_y0, zs_y1, zs_x0, zs_x1;
+  int32_t no_pq;         // ... and leave <p, Mp> to k_misr_normal
 };
 
 // WZ: ADMM wz-step; NORMAL: CG normal operator; A / AT: test operators;
 // GRAD: cost terms and subgradient of J for gd (A30); J: cost terms of one gd-ls trial.
 enum TileMode : int { MODE_WZ = 0, MODE_NORMAL = 1, MODE_A = 2, MODE_AT = 3, MODE_GRAD = 4, MODE_J = 5 };
+
+// MISR fast path (misr.cu): the zeta^2-phase stencil of the data normal operator for constant
+// shifts, the NLTV weights, and the launch arguments.
+constexpr int kMisrMaxCoef = 16 * 15 * 15;   // zeta^2 phases x (4R+3)^2 taps, zeta <= 4 (R <= 3)
+
+struct MisrStencil {
+  float s[kMisrMaxCoef];   // [phase py*zeta+px][dy + WR][dx + WR], WR = 2R + 1; c_A folded in
+  float w2[24], w2f[24];   // w_d^2 and w_{-d}^2 in the offset order of A9 (5x5 window)
+  float W2;                // sum_d w_d^2
+  // separable form (sep = 1; views on a Cartesian grid of shifts, symmetric separable NLTV
+  // weights w_d^2 = u[dy] u[dx], d != 0): M_data = T_y (x) T_x exactly, border included, with the
+  // banded 1-D matrices in MisrArgs::tyt / txt -- no border kernel
+  int32_t sep;
+  float u[5];
+};
+
+struct MisrArgs {
+  const float* r;       // CG residual (k >= 1) ...
+  const float* p_prev;  // ... and the previous direction (k >= 2)
+  const float* p_in;    // k = 0 (plain operator): the input
+  float* p_out;         // k >= 1: p_k on the owned rectangle
+  const float* m;       // weight map (NLTV)
+  const float* tyt;     // sep: T_y [H][2WR+1] (c_A folded in), T_x [W][2WR+1]; row z holds the taps to z + D
+  const float* txt;
+  float* q;             // output (stored on Z_s; the band is the border kernel's)
+  Control* ctl;
+  int cg_k, do_nltv;
+  int zs_y0, zs_y1, zs_x0, zs_x1;   // stencil-exact rectangle Z_s
+  int o_y0, o_y1, o_x0, o_x1;       // pixels not owned by a border tile (p_out, pi_0)
+};
 
 // gd / gd-ls configuration of one iteration graph (readings A30-A33).
 struct GdCfg {

@@ -828,8 +828,8 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
   extern __shared__ __align__(16) float smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int NT = blockDim.x, NW = NT >> 5;
-  const int ntiles = T.ntYl * T.ntX;                 // tiles of this strip (all tiles with one rank)
-  const int tile = blockIdx.x % ntiles;
+  const int ntiles = T.ntl ? T.ntl : T.ntYl * T.ntX;  // tiles of this strip (all tiles with one rank),
+  const int tile = T.ntl ? T.tlist[blockIdx.x % ntiles] : blockIdx.x % ntiles;   // or the MISR border tiles
   const int grp = blockIdx.x / ntiles;
   const int ti = T.tY0 + tile / T.ntX, tj = tile % T.ntX;
   const int i0 = ti * BL, j0 = tj * LX;          // LR origin of the tile
@@ -1106,6 +1106,8 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
         v += NL[oy * TX + ox];
       // padding cells fold onto their replicate source (transpose of the padding)
       const int cy = min(max(gy, 0), H - 1), cx = min(max(gx, 0), W - 1);
+      // MISR fast path: k_misr_normal owns the outputs inside the stencil rectangle Z_s
+      if (io.zs_on && cy >= io.zs_y0 && cy < io.zs_y1 && cx >= io.zs_x0 && cx < io.zs_x1) continue;
       if (v != 0.f) atomicAdd(&io.out_hr[(size_t)cy * ps + cx], sign * v);
     }
   }
@@ -1119,7 +1121,8 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
     const int slot[3] = {S_L1, S_L2, S_REG};
     block_reduce_add<3>(v, RED, ctl->cur, slot);
   } else if (MODE == MODE_NORMAL && io.cg_k >= 1) {
-    double v[2] = {(PM ? 0.0 : red_a) + red_b, pi0_part};   // PM: the data part comes from the gather
+    // PM: the data part comes from the gather; MISR fast path: k_misr_normal forms <p, q>
+    double v[2] = {io.no_pq ? 0.0 : (PM ? 0.0 : red_a) + red_b, pi0_part};
     const int slot[2] = {S_PQ + io.cg_k, S_PI + 0};
     block_reduce_add<2>(v, RED, ctl->cur, slot);
   }
@@ -1134,7 +1137,7 @@ struct TileZ {
   static cudaError_t launch1(const Geom& G, const Views& V, const TileGeom& T, const TileIO& io, cudaStream_t st) {
     const int nw = MODE == MODE_NORMAL ? T.nwarps_n : T.nwarps;
     const size_t sm = MODE == MODE_NORMAL ? T.smem_normal : T.smem;
-    k_tile<Z, MODE, F, PV, P2, PM, RB><<<T.ntYl * T.ntX * T.groups, nw * 32, sm, st>>>(G, V, T, io);
+    k_tile<Z, MODE, F, PV, P2, PM, RB><<<(T.ntl ? T.ntl : T.ntYl * T.ntX) * T.groups, nw * 32, sm, st>>>(G, V, T, io);
     return cudaGetLastError();
   }
   template <int MODE>

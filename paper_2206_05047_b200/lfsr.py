@@ -34,7 +34,7 @@ EXPORTS = ("lfsr_create", "lfsr_set_observations", "lfsr_admm_run", "lfsr_admm_e
            "lfsr_get_hr", "lfsr_get_state", "lfsr_op_apply", "lfsr_launches_per_iter", "lfsr_tile_config", "lfsr_profile",
            "lfsr_profile_read", "lfsr_strip_plan", "lfsr_destroy", "lfsr_last_error", "lfsr_abi_version",
            "lfsr_gd_run", "lfsr_gd_launches_per_iter", "lfsr_rgb_to_ycbcr", "lfsr_ycbcr_to_rgb", "lfsr_solve_batch",
-           "lfsr_get_stream")
+           "lfsr_get_stream", "lfsr_fast_path")
 
 
 class LFSRError(RuntimeError):
@@ -129,6 +129,8 @@ def load_library(path: str = LIB_PATH):
     i32p = ctypes.POINTER(ctypes.c_int32)
     lib.lfsr_tile_config.argtypes = [vp, i32p, i32p, i32p, i32p]
     lib.lfsr_tile_config.restype = st
+    lib.lfsr_fast_path.argtypes = [vp, i32p, i32p]
+    lib.lfsr_fast_path.restype = st
     lib.lfsr_destroy.argtypes = [vp]
     lib.lfsr_destroy.restype = None
     lib.lfsr_last_error.argtypes = [vp]
@@ -434,6 +436,14 @@ class Solver:
     @property
     def launches_per_iter(self) -> int:
         return int(self.lib.lfsr_launches_per_iter(self._h))
+
+    @property
+    def fast_path(self) -> dict:
+        """lfsr_fast_path: whether the MISR stencil path runs, with its rectangles."""
+        act = ctypes.c_int32()
+        rect = (ctypes.c_int32 * 8)()
+        self._check(self.lib.lfsr_fast_path(self._h, ctypes.byref(act), rect))
+        return {"misr": bool(act.value), "zs": tuple(rect[:4]), "owned": tuple(rect[4:])}
 
     @property
     def tile_config(self) -> dict:
