@@ -421,7 +421,8 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    strips = world > 1 and args.multi == "strips" and not share
+    # (sharing one GPU, strips need an NCCL that allows it: LFSR_NCCL_LIB = the test double)
+    strips = world > 1 and args.multi == "strips" and (not share or bool(os.environ.get("LFSR_NCCL_LIB")))
     # strips: every rank holds the same light field and owns a strip of it;
     # replicas: each rank super-resolves its own light field (independent problem, own seed)
     lf = S.make_lightfield(cfg, seed=None if (rank == 0 or strips) else 10007 * rank + 1000)

@@ -2046,7 +2046,10 @@ lfsr_status lfsr_profile_read(lfsr_ctx* c, double* ms, int64_t* launches) {
 
 // Gather every strip's own rows of the solver state into strip 0's buffers
 // (virtual ranks: device copies; NCCL: broadcast from each rank).
-static lfsr_status gather(lfsr_ctx* c) {
+// Collect the strips' rows of the state on strip 0 / every rank: what = G_X (x, lfsr_get_hr), | G_M
+// (the weight map, lfsr_op_apply), | G_W (the duals w_A, w_S, lfsr_get_state).
+enum GatherWhat : int { G_X = 1, G_M = 2, G_W = 4 };
+static lfsr_status gather(lfsr_ctx* c, int what) {
   if (c->xmode == X_NONE) return LFSR_OK;
   const Geom& G = c->G;
   const size_t rowf = G.ps, lrowf = G.lps, plane = (size_t)G.H * G.ps;
@@ -2057,17 +2060,19 @@ static lfsr_status gather(lfsr_ctx* c) {
       const State& S = c->parts[i].S;
       const lfsr_strip& s = c->parts[i].plan;
       const size_t a = s.hr_row0 * rowf, n = (size_t)(s.hr_row1 - s.hr_row0) * rowf;
-      CK(c, cudaMemcpyAsync(D.x + a, S.x + a, n * 4, cudaMemcpyDeviceToDevice, c->stream));
-      CK(c, cudaMemcpyAsync(D.m + a, S.m + a, n * 4, cudaMemcpyDeviceToDevice, c->stream));
-      CK(c, cudaMemcpy2DAsync(D.wS[cur] + a, plane * 4, S.wS[cur] + a, plane * 4, n * 4, G.s_d,
-                              cudaMemcpyDeviceToDevice, c->stream));
-      const size_t la = s.lr_row0 * lrowf, ln = (size_t)(s.lr_row1 - s.lr_row0) * lrowf;
-      CK(c, cudaMemcpy2DAsync(D.wA + la, (size_t)G.h * lrowf * 4, S.wA + la, (size_t)G.h * lrowf * 4, ln * 4,
-                              G.n_views, cudaMemcpyDeviceToDevice, c->stream));
+      if (what & G_X) CK(c, cudaMemcpyAsync(D.x + a, S.x + a, n * 4, cudaMemcpyDeviceToDevice, c->stream));
+      if (what & G_M) CK(c, cudaMemcpyAsync(D.m + a, S.m + a, n * 4, cudaMemcpyDeviceToDevice, c->stream));
+      if (what & G_W) {
+        CK(c, cudaMemcpy2DAsync(D.wS[cur] + a, plane * 4, S.wS[cur] + a, plane * 4, n * 4, G.s_d,
+                                cudaMemcpyDeviceToDevice, c->stream));
+        const size_t la = s.lr_row0 * lrowf, ln = (size_t)(s.lr_row1 - s.lr_row0) * lrowf;
+        CK(c, cudaMemcpy2DAsync(D.wA + la, (size_t)G.h * lrowf * 4, S.wA + la, (size_t)G.h * lrowf * 4, ln * 4,
+                                G.n_views, cudaMemcpyDeviceToDevice, c->stream));
+      }
     }
     return LFSR_OK;
   }
-  // NCCL: every rank broadcasts its strip
+  // NCCL: every rank broadcasts its strip of what was asked for (lfsr_get_hr: x only)
   std::vector<lfsr_strip> plan;
   std::string why;
   make_plan(G, c->prm.n_ranks, G.SY, plan, why);
@@ -2075,12 +2080,15 @@ static lfsr_status gather(lfsr_ctx* c) {
   NK(c, nccl_group_start());
   for (const lfsr_strip& s : plan) {
     const size_t a = s.hr_row0 * rowf, n = (size_t)(s.hr_row1 - s.hr_row0) * rowf;
-    NK(c, nccl_bcast_f32(D.x + a, n, s.rank, c->comm, c->stream));
-    NK(c, nccl_bcast_f32(D.m + a, n, s.rank, c->comm, c->stream));
-    for (int d = 0; d < G.s_d; ++d) NK(c, nccl_bcast_f32(D.wS[cur] + d * plane + a, n, s.rank, c->comm, c->stream));
-    const size_t la = s.lr_row0 * lrowf, ln = (size_t)(s.lr_row1 - s.lr_row0) * lrowf;
-    for (int k = 0; k < G.n_views; ++k)
-      NK(c, nccl_bcast_f32(D.wA + (size_t)k * G.h * lrowf + la, ln, s.rank, c->comm, c->stream));
+    if (what & G_X) NK(c, nccl_bcast_f32(D.x + a, n, s.rank, c->comm, c->stream));
+    if (what & G_M) NK(c, nccl_bcast_f32(D.m + a, n, s.rank, c->comm, c->stream));
+    if (what & G_W) {
+      for (int d = 0; d < G.s_d; ++d)
+        NK(c, nccl_bcast_f32(D.wS[cur] + d * plane + a, n, s.rank, c->comm, c->stream));
+      const size_t la = s.lr_row0 * lrowf, ln = (size_t)(s.lr_row1 - s.lr_row0) * lrowf;
+      for (int k = 0; k < G.n_views; ++k)
+        NK(c, nccl_bcast_f32(D.wA + (size_t)k * G.h * lrowf + la, ln, s.rank, c->comm, c->stream));
+    }
   }
   NK(c, nccl_group_end());
   return LFSR_OK;
@@ -2093,7 +2101,7 @@ lfsr_status lfsr_get_hr(lfsr_ctx* c, float* x_out, lfsr_mem mem) {
   lfsr_status st;
   if ((st = check_ptr(c, x_out, mem, "x_out")) != LFSR_OK) return st;
   CK(c, cudaSetDevice(c->prm.device));
-  if ((st = gather(c)) != LFSR_OK) return st;
+  if ((st = gather(c, G_X)) != LFSR_OK) return st;
   CK(c, get2d(c, x_out, c->G.W, c->parts[0].S.x, c->G.ps, (size_t)c->G.H, mem));
   if (mem == LFSR_MEM_HOST) CK(c, cudaStreamSynchronize(c->stream));
   return LFSR_OK;
@@ -2106,7 +2114,7 @@ lfsr_status lfsr_get_state(lfsr_ctx* c, float* w_A, float* w_S, float* x, float*
   const Geom& G = c->G;
   lfsr_status st;
   CK(c, cudaSetDevice(c->prm.device));
-  if ((st = gather(c)) != LFSR_OK) return st;
+  if ((st = gather(c, G_X | G_M | G_W)) != LFSR_OK) return st;   // the same collectives on every rank
   const State& S = c->parts[0].S;
   if (w_A) {
     if ((st = check_ptr(c, w_A, mem, "w_A")) != LFSR_OK) return st;
@@ -2136,7 +2144,7 @@ lfsr_status lfsr_op_apply(lfsr_ctx* c, lfsr_op op, const float* in, float* out, 
   if ((st = check_ptr(c, in, mem, "in")) != LFSR_OK) return st;
   if ((st = check_ptr(c, out, mem, "out")) != LFSR_OK) return st;
   CK(c, cudaSetDevice(c->prm.device));
-  if ((st = gather(c)) != LFSR_OK) return st;   // the current weight map m on strip 0
+  if ((st = gather(c, G_M)) != LFSR_OK) return st;   // the current weight map m on strip 0
   const Geom& G = c->G;
   Part& P0 = c->parts[0];
   State& S = P0.S;

@@ -4,6 +4,7 @@
 #include "nccl_shim.h"
 
 #include <dlfcn.h>
+#include <cstdlib>
 #include <mutex>
 
 namespace lfsr {
@@ -28,7 +29,10 @@ Api g_api;
 std::once_flag g_once;
 
 void load() {
-  const char* names[] = {"libnccl.so.2", "libnccl.so"};
+  // LFSR_NCCL_LIB: an explicit library path (tests point it at their NCCL test double,
+  // tests/fake_nccl, to run this path with several processes on one GPU)
+  const char* env = getenv("LFSR_NCCL_LIB");
+  const char* names[] = {env && env[0] ? env : "libnccl.so.2", "libnccl.so.2", "libnccl.so"};
   void* h = nullptr;
   for (const char* n : names)
     if ((h = dlopen(n, RTLD_NOW | RTLD_GLOBAL))) break;
