@@ -45,6 +45,8 @@ cudaError_t launch_paper_gather(const Geom& G, const Views& V, const float* rho,
                                 cudaStream_t st);
 cudaError_t launch_color(int to_ycbcr, const float* a, float* y, float* cb, float* cr, size_t n, int num_sms,
                          cudaStream_t st);
+cudaError_t launch_wz_nltv(const Geom& G, const float* x, const float* m, float* wS0, float* wS1, float* r,
+                           Control* ctl, int row0, int row1, cudaStream_t st);
 cudaError_t launch_omega_const(const Geom& G, const float* omega, unsigned* flag, cudaStream_t st);
 cudaError_t launch_misr_normal(const Geom& G, const MisrStencil& S, const MisrArgs& a, cudaStream_t st);
 cudaError_t prepare_misr_kernels();
@@ -1521,6 +1523,12 @@ static lfsr_status enqueue_iteration(lfsr_ctx* c, cudaStream_t st, int parity) {
     }
   }
   const int r = G.radius;
+  // NLTV rows of the wz-step in their own streaming kernel (nltv.cu) for large images (measured: C5
+  // 2048^2 -11 % wz-step time, M2 2048^2 even, C2 / C3 512^2 +5 % -- there the tile kernel's phase
+  // 3 hides the stream behind its view passes); LFSR_NLTV_SPLIT=0 / 1 forces either
+  const char* ns_env = getenv("LFSR_NLTV_SPLIT");
+  const bool nltv_big = (size_t)G.H * G.W >= ((size_t)1 << 21);
+  const bool nltv_split = G.radius == 2 && (ns_env && ns_env[0] ? ns_env[0] == '1' : nltv_big);
   lfsr_status s_;
 #define XC(expr)                                 \
   do {                                           \
@@ -1539,10 +1547,18 @@ static lfsr_status enqueue_iteration(lfsr_ctx* c, cudaStream_t st, int parity) {
     io.wo = P.S.wo;
     io.out_hr = P.S.r;
     io.reweight = c->prm.reweight_every_iter;
+    io.wz_no_nltv = nltv_split ? 1 : 0;
     CK(c, launch_tile(MODE_WZ, G, c->V, P.T, io, st));
     ++launches;
     if (G.paper) {   // v's data part through the paper's backward warp (A37): r = -v
       CK(c, launch_paper_gather(G, c->V, P.S.rho, P.S.omega, nullptr, P.S.r, -1.f, P.S.ctl, -1, 0, 0, G.H, st));
+      ++launches;
+    }
+  }
+  if (nltv_split) {   // the NLTV rows of the wz-step as a streaming kernel (nltv.cu), own rows
+    if (multi) XC(xfill(c, st, ms.data(), r, r));                         // m of the neighbours' rows
+    for (Part& P : c->parts) {
+      CK(c, launch_wz_nltv(G, P.S.x, P.S.m, P.S.wS[0], P.S.wS[1], P.S.r, P.S.ctl, P.plan.hr_row0, P.plan.hr_row1, st));
       ++launches;
     }
   }

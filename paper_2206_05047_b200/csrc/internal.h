@@ -133,6 +133,7 @@ struct TileIO {
   int32_t zs_on;         // MISR fast path: flush only outside the stencil rectangle Z_s ...
   int32_t zs_y0, zs_y1, zs_x0, zs_x1;
   int32_t no_pq;         // ... and leave <p, Mp> to k_misr_normal
+  int32_t wz_no_nltv;    // WZ: the NLTV rows run in k_wz_nltv (nltv.cu) instead of phase 3
 };
 
 // WZ: ADMM wz-step; NORMAL: CG normal operator; A / AT: test operators;

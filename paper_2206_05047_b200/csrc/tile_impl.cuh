@@ -1046,7 +1046,8 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
   // work (the w_S stream in WZ) fills the wait for the slowest warp.
   double red_reg = 0.0;
   const int ng = T.groups;
-  const bool nltv = (MODE == MODE_WZ || MODE == MODE_GRAD || MODE == MODE_J) || (MODE == MODE_NORMAL && io.do_nltv);
+  const bool nltv = (MODE == MODE_WZ && !io.wz_no_nltv) || MODE == MODE_GRAD || MODE == MODE_J ||
+                    (MODE == MODE_NORMAL && io.do_nltv);
   if (nltv) {
     NltvCtx c;
     c.P = P; c.M = M; c.PW = PW; c.PWZ = PWZ; c.MW = MW; c.H = H; c.W = W; c.ps = ps;

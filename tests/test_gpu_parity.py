@@ -414,3 +414,32 @@ def test_misr_admm_parity(lfsr_mod):
     lf = S.make_lightfield("M1")
     p, ora, xs, stats, st = run_pair(lfsr_mod, lf, 10, defaults=S.MisrDefaults())
     check_iterates(p, ora, xs, stats, st, lf.x_gt)
+
+
+# ----------------------------------------------------------------------------- k_wz_nltv (nltv.cu)
+@pytest.mark.parametrize("cfg,n", [("C1", 10), ("C4", 2)])
+def test_nltv_split_kernel_parity(lfsr_mod, cfg, n, monkeypatch):
+    """The NLTV rows of the wz-step in the streaming kernel (default for large images; forced here on
+    small ones, C4's 513 columns exercise the ragged last float4 chunk) against the oracle."""
+    monkeypatch.setenv("LFSR_NLTV_SPLIT", "1")
+    lf = S.make_lightfield(cfg)
+    p, ora, xs, stats, st = run_pair(lfsr_mod, lf, n)
+    check_iterates(p, ora, xs, stats, st, lf.x_gt)
+    errs = [rel_l2(xs[i], ora.x_iters[i]) for i in range(n + 1)]
+    print("PARITY nltv-split %s N=%d: %s" % (cfg, n, " ".join("%.1e" % e for e in errs)))
+
+
+def test_nltv_split_strips(lfsr_mod, monkeypatch):
+    """The split kernel on each strip's own rows (virtual ranks) equals the single-strip solve."""
+    monkeypatch.setenv("LFSR_NLTV_SPLIT", "1")
+    lf = S.make_lightfield("C2")
+    d = S.SolverDefaults()
+    out = []
+    for over in ({}, dict(n_ranks=3, rank=-1)):
+        p = lfsr_mod.params_for(S.CONFIGS["C2"], d, **over)
+        s = lfsr_mod.Solver(p)
+        s.set_observations(lf.y, lf.view_offsets, lf.omega)
+        s.admm_run(2)
+        out.append(s.get_hr())
+        s.close()
+    assert rel_l2(out[1], out[0]) <= 1e-5
