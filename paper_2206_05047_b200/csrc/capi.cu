@@ -4,6 +4,7 @@
 #include "../../include/lfsr.h"
 #include "internal.h"
 #include "nccl_shim.h"
+#include <nvtx3/nvToolsExt.h>   // header-only; ranges show in nsys / ncu when a tool is attached
 
 #include <algorithm>
 #include <chrono>
@@ -139,6 +140,12 @@ struct lfsr_ctx {
 };
 
 static thread_local std::string g_create_err;
+
+// NVTX range for the host side of an API call or a setup phase (SURVEY §5 tracing)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 #define FAIL(ctx, code, msg)          \
   do {                                \
@@ -390,6 +397,7 @@ lfsr_status lfsr_strip_plan(const lfsr_params* params, int32_t max_shift_rows, l
 }
 
 lfsr_status lfsr_create(const lfsr_params* params, lfsr_ctx** out) {
+  NvtxRange nvtx_("lfsr_create");
   if (!out) {
     g_create_err = "out is NULL";
     return LFSR_ERR_INVALID_ARG;
@@ -1214,6 +1222,7 @@ static lfsr_status misr_normal(lfsr_ctx* c, Part& P, int k, const float* in, flo
 
 lfsr_status lfsr_set_observations(lfsr_ctx* c, const float* lr_views, const float* view_offsets,
                                   const float* disparity, lfsr_disp_mode disp_mode, const float* x0, lfsr_mem mem) {
+  NvtxRange nvtx_("lfsr_set_observations");
   if (!c) return LFSR_ERR_INVALID_ARG;
   if (c->poisoned) FAIL(c, LFSR_ERR_STATE, "ctx is poisoned by an earlier CUDA/NCCL error");
   if (disp_mode != LFSR_DISP_SHARED && disp_mode != LFSR_DISP_PER_VIEW) FAIL(c, LFSR_ERR_INVALID_ARG, "unknown disp_mode");
@@ -1345,9 +1354,15 @@ lfsr_status lfsr_set_observations(lfsr_ctx* c, const float* lr_views, const floa
     CK(c, launch_setup_wo(G, c->V, S.y, om_ref, S.wo, c->stream));
     CK(c, launch_weights(G, S.x, S.wo, S.m, c->stream));
   }
-  if (tune && (st = tune_tile_bl(c)) != LFSR_OK) return st;
+  if (tune) {
+    NvtxRange r_("tile tuning");
+    if ((st = tune_tile_bl(c)) != LFSR_OK) return st;
+  }
   c->misr = false;
-  if (ubits[3] == 0 && (st = misr_setup(c, omega00)) != LFSR_OK) return st;
+  if (ubits[3] == 0) {
+    NvtxRange r_("MISR stencil assembly");
+    if ((st = misr_setup(c, omega00)) != LFSR_OK) return st;
+  }
   const auto tg0 = std::chrono::steady_clock::now();
   lfsr_status gs = build_graphs(c);
   if (gs != LFSR_OK) return gs;
@@ -1638,6 +1653,7 @@ static lfsr_status enqueue_iteration(lfsr_ctx* c, cudaStream_t st, int parity) {
 }
 
 static lfsr_status build_graphs(lfsr_ctx* c) {
+  NvtxRange r_("ADMM iteration graph capture");
   free_graph(c);
   if (c->profile) {
     size_t need = 2 + 2 * (size_t)c->G.K;
@@ -1673,6 +1689,7 @@ static lfsr_status check_run(lfsr_ctx* c) {
 }
 
 lfsr_status lfsr_admm_enqueue(lfsr_ctx* c, int32_t n_iters) {
+  NvtxRange nvtx_("lfsr_admm_enqueue");
   lfsr_status st = check_run(c);
   if (st != LFSR_OK) return st;
   if (n_iters < 0) FAIL(c, LFSR_ERR_INVALID_ARG, "n_iters must be >= 0");
@@ -1736,6 +1753,7 @@ lfsr_status lfsr_admm_stats(lfsr_ctx* c, int32_t first_iter, int32_t n_iters, lf
 }
 
 lfsr_status lfsr_admm_run(lfsr_ctx* c, int32_t n_iters, lfsr_iter_stats* stats) {
+  NvtxRange nvtx_("lfsr_admm_run");
   lfsr_status st = check_run(c);
   if (st != LFSR_OK) return st;
   if (n_iters < 0) FAIL(c, LFSR_ERR_INVALID_ARG, "n_iters must be >= 0");
@@ -1792,6 +1810,7 @@ static lfsr_status enqueue_gd(lfsr_ctx* c, cudaStream_t st, const GdCfg& cfg) {
 }
 
 lfsr_status lfsr_gd_run(lfsr_ctx* c, const lfsr_gd_params* gp, int32_t n_iters, lfsr_gd_stats* stats) {
+  NvtxRange nvtx_("lfsr_gd_run");
   lfsr_status st = check_run(c);
   if (st != LFSR_OK) return st;
   if (!gp) FAIL(c, LFSR_ERR_INVALID_ARG, "gd params must not be NULL");
@@ -1943,6 +1962,7 @@ static lfsr_status batch_finish(lfsr_ctx* c, const float* off, const Views& V2) 
 lfsr_status lfsr_solve_batch(lfsr_ctx* c, int32_t n_fields, const float* const* lr_views,
                              const float* const* view_offsets, const float* const* disparity, int32_t n_iters,
                              float* const* x_out) {
+  NvtxRange nvtx_("lfsr_solve_batch");
   if (!c) return LFSR_ERR_INVALID_ARG;
   if (c->poisoned) FAIL(c, LFSR_ERR_STATE, "ctx is poisoned by an earlier CUDA/NCCL error");
   if (n_fields < 1 || n_iters < 1 || !lr_views || !view_offsets || !disparity || !x_out)
@@ -2111,6 +2131,7 @@ static lfsr_status gather(lfsr_ctx* c, int what) {
 }
 
 lfsr_status lfsr_get_hr(lfsr_ctx* c, float* x_out, lfsr_mem mem) {
+  NvtxRange nvtx_("lfsr_get_hr");
   if (!c) return LFSR_ERR_INVALID_ARG;
   if (c->poisoned) FAIL(c, LFSR_ERR_STATE, "ctx is poisoned by an earlier CUDA/NCCL error");
   if (!c->ready) FAIL(c, LFSR_ERR_STATE, "lfsr_get_hr before lfsr_set_observations");
