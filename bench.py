@@ -540,13 +540,13 @@ def main():
 
     # ---- roofline of the dominant kernel (the CG normal-operator tile kernel)
     _, _, _, clk_hz = peaks()
-    if kn[1] == 0:   # strips (NCCL): per-kernel events are not recorded; use the step time split evenly
-        kms, kn = [t_ms * 0.2, t_ms * 0.75, t_ms * 0.05], [args.steps, args.steps * d.cg_max_iters,
-                                                          args.steps * d.cg_max_iters]
-    roofline = roofline_for(cfg, d, kms, kn, t_max, args.steps, world if strips else 1, clk_hz)
-    roofline["timing"] += " (%.4f ms/step with the events; `value` is the region without them)" % (
-        t_prof_ms / args.steps)
-    k_normal_ms, k_wz_ms, k_upd_ms = (kms[1] / max(kn[1], 1), kms[0] / max(kn[0], 1), kms[2] / max(kn[2], 1))
+    if kn[1] > 0:
+        roofline = roofline_for(cfg, d, kms, kn, t_max, args.steps, world if strips else 1, clk_hz)
+        roofline["timing"] += " (%.4f ms/step with the events; `value` is the region without them)" % (
+            t_prof_ms / args.steps)
+        k_normal_ms, k_wz_ms, k_upd_ms = (kms[1] / kn[1], kms[0] / max(kn[0], 1), kms[2] / max(kn[2], 1))
+    else:   # strips (NCCL): no per-kernel events in the graph; the kernels' roofline is the replica run's
+        roofline, k_normal_ms, k_wz_ms, k_upd_ms = None, None, None, None
     launches = sol.launches_per_iter * args.steps * (1 if strips else world)
     sol.close()
     del dev_in
@@ -574,6 +574,12 @@ def main():
             replicas = {"value": world * 1000.0 / float(tt.item()), "unit": UNIT, "scaling": "weak",
                         "ms_per_step": float(tt.item()),
                         "mode": "dp%d: every rank its own light field, no data-path collective" % world}
+            if roofline is None and rr.get("roofline"):
+                roofline = dict(rr["roofline"])
+                roofline["timing"] = ("per-kernel CUDA events of the replica run on this rank (the strip "
+                                      "graphs carry no per-kernel events); " + roofline["timing"])
+                k = rr["kernel_ms_per_launch"]
+                k_normal_ms, k_wz_ms, k_upd_ms = k["normal"], k["wz"], k["cg_update"]
         except Exception as e:  # pragma: no cover
             replicas = {"error": str(e)[:300]}
 
