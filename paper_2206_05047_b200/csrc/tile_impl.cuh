@@ -42,6 +42,18 @@
 
 namespace lfsr {
 
+#ifdef LFSR_CTA_TIMING   // development: per-CTA phase timestamps of the NORMAL launches (tools/cta_timing.py)
+static __device__ unsigned long long g_cta_t[4096][4];   // per translation unit (zeta)
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define CTA_T(i) do { if (MODE == MODE_NORMAL && threadIdx.x == 0 && blockIdx.x < 4096) g_cta_t[blockIdx.x][i] = gtimer(); } while (0)
+#else
+#define CTA_T(i) do { } while (0)
+#endif
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -840,6 +852,7 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
   const int H = G.H, W = G.W, ps = G.ps;
   Control* ctl = io.ctl;
   if (MODE == MODE_NORMAL && io.cg_k >= 2 && ctl->cur[S_STOP] != 0.0) return;  // CG stopped
+  CTA_T(0);
   // gd-ls trial t runs only while no earlier trial met the Armijo condition (A32); every
   // CTA reads the same fp64 sums, so all take the same decision
   float ls_beta = 0.f;
@@ -1040,6 +1053,7 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
     else run(Tile<Z, false, RB>{});
   }
   if (MODE == MODE_A) return;
+  CTA_T(1);
 
   // ---- phase 3: NLTV term of the own pixels (view group g takes own rows g, g+G, ...);
   // warps that finish their views early pull rows from a shared counter, so the NLTV
@@ -1092,6 +1106,7 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
     return;
   }
   __syncthreads();   // views and NLTV done: ACC and NL complete
+  CTA_T(2);
 
   // ---- phase 4: flush accumulator + NLTV (tile + halo) with RED.ADD ----------
   {
@@ -1127,6 +1142,7 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
     const int slot[2] = {S_PQ + io.cg_k, S_PI + 0};
     block_reduce_add<2>(v, RED, ctl->cur, slot);
   }
+  CTA_T(3);
 }
 
 // Per-zeta host entry points (instantiated once per zeta in tile_z<zeta>.cu).

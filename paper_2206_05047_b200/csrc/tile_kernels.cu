@@ -165,3 +165,4 @@ cudaError_t launch_tile(int mode, const Geom& G, const Views& V, const TileGeom&
 }
 
 }  // namespace lfsr
+
