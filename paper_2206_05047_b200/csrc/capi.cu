@@ -69,6 +69,10 @@ struct Part {
   lfsr_strip plan{};
   State S{};
   TileGeom T{};
+  // strips: the tiles whose input tile lies in the own rows (no halo needed; they run on the side
+  // stream while the halos are exchanged) and the rest (after the exchange)
+  TileGeom Tin{}, Tbd{};
+  int* d_tl = nullptr;
   double* ring = nullptr;
   float* stage[2] = {nullptr, nullptr};  // NCCL fold staging: [0] rows from the previous rank, [1] from the next
   size_t stage_rows = 0;
@@ -126,6 +130,8 @@ struct lfsr_ctx {
   int64_t prof_n[3] = {0, 0, 0};
   // MISR fast path (misr.cu): constant disparity -> the CG operator's data part
   // as a precomputed zeta^2-phase stencil on Z_s, the exact tile kernel on the border tiles
+  cudaStream_t side = nullptr;      // strips: interior tiles overlap the halo exchange
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool misr = false;
   bool in_batch = false;           // lfsr_solve_batch swaps fields under one graph: no fast path there
   MisrStencil* misr_S = nullptr;   // host copy (passed by value to k_misr_normal)
@@ -455,6 +461,18 @@ lfsr_status lfsr_create(const lfsr_params* params, lfsr_ctx** out) {
     delete c;
     return LFSR_ERR_CUDA;
   }
+  if (params->n_ranks > 1 &&
+      ((e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking)) != cudaSuccess ||
+       (e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming)) != cudaSuccess ||
+       (e = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming)) != cudaSuccess)) {
+    g_create_err = cudaGetErrorString(e);
+    if (c->side) cudaStreamDestroy(c->side);
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    cudaStreamDestroy(c->cap_stream);
+    if (c->own_stream) cudaStreamDestroy(c->stream);
+    delete c;
+    return LFSR_ERR_CUDA;
+  }
   fill_geom(c->prm, c->G);
   c->prm.stream = c->stream;
   c->prm.offset_weights = nullptr;   // consumed into G (the caller keeps ownership)
@@ -539,6 +557,9 @@ void lfsr_destroy(lfsr_ctx* c) {
     else nccl_comm_destroy(c->comm);
   }
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
+  if (c->side) cudaStreamDestroy(c->side);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -680,6 +701,37 @@ static lfsr_status setup_tiles(lfsr_ctx* c) {
     P.plan = plan[c->xmode == X_NCCL ? c->prm.rank : i];
     P.T = make_tile_geom(G, c->num_sms, P.plan.tile_row0, P.plan.tile_row1);
     if (P.T.smem > 227 * 1024) FAIL(c, LFSR_ERR_UNSUPPORTED, "disparity range too large for the shared-memory tile");
+    if (c->prm.n_ranks > 1) {   // interior tiles: the input tile (E region + disparity halo) inside the own rows
+      const TileGeom& T = P.T;
+      const int reach_up = T.SYe + 1 + (T.EY - T.TY) + 0, zt = G.scale * T.BL;
+      std::vector<int> in_l, bd_l;
+      for (int t = 0; t < T.ntYl; ++t) {
+        const int y0 = (T.tY0 + t) * zt;                        // own HR rows of the tile row
+        const int R = G.R;
+        const int top = y0 - R - T.SYe - 1, bot = y0 + T.EY - R + T.SYe + 1;   // input rows [top, bot)
+        (void)reach_up;
+        const bool up_ok = P.plan.halo_top == 0 || top >= P.plan.hr_row0;
+        const bool dn_ok = P.plan.halo_bottom == 0 || bot <= P.plan.hr_row1;
+        for (int tx = 0; tx < T.ntX; ++tx) (up_ok && dn_ok ? in_l : bd_l).push_back(t * T.ntX + tx);
+      }
+      if (!P.d_tl) {
+        void* p = nullptr;
+        cudaError_t e;
+        if ((e = dalloc(c, &p, (size_t)(T.ntY + 1) * T.ntX * sizeof(int))) != cudaSuccess) return cuda_fail(c, e, "alloc");
+        P.d_tl = (int*)p;
+      }
+      std::vector<int> all(in_l);
+      all.insert(all.end(), bd_l.begin(), bd_l.end());
+      if (!all.empty())
+        CK(c, cudaMemcpyAsync(P.d_tl, all.data(), all.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+      CK(c, cudaStreamSynchronize(c->stream));   // `all` is a local
+      P.Tin = T;
+      P.Tin.tlist = P.d_tl;
+      P.Tin.ntl = (int)in_l.size();
+      P.Tbd = T;
+      P.Tbd.tlist = P.d_tl + in_l.size();
+      P.Tbd.ntl = (int)bd_l.size();
+    }
     if (c->xmode == X_NCCL) {  // fold staging, sized by the halos
       const size_t rows = (size_t)std::max(P.plan.halo_top, P.plan.halo_bottom) + 64;
       if (P.stage_rows < rows) {
@@ -1398,9 +1450,13 @@ struct Rows {
 };
 
 static lfsr_status xfill(lfsr_ctx* c, cudaStream_t st, float* const* bufs, int top, int bot, int planes = 1,
-                         size_t plane_stride = 0) {
+                         size_t plane_stride = 0, float* const* bufs2 = nullptr) {
   const Geom& G = c->G;
   const size_t rowf = (size_t)G.ps;
+  if (bufs2 && c->xmode == X_LOCAL) {   // two single-plane buffer sets: one after the other
+    lfsr_status s1 = xfill(c, st, bufs, top, bot, planes, plane_stride);
+    return s1 != LFSR_OK ? s1 : xfill(c, st, bufs2, top, bot, planes, plane_stride);
+  }
   if (c->xmode == X_LOCAL) {
     const int n = (int)c->parts.size();
     for (int i = 0; i < n; ++i) {
@@ -1418,10 +1474,9 @@ static lfsr_status xfill(lfsr_ctx* c, cudaStream_t st, float* const* bufs, int t
   if (c->xmode == X_NCCL) {
     const lfsr_strip& s = c->parts[0].plan;
     const int r = s.rank, n = c->prm.n_ranks;
-    float* b = bufs[0];
-    NK(c, nccl_group_start());
-    for (int pl = 0; pl < planes; ++pl) {
-      float* bp = b + pl * plane_stride;
+    NK(c, nccl_group_start());   // one group (one NCCL launch) for both buffer sets
+    for (int pl = 0; pl < planes * (bufs2 ? 2 : 1); ++pl) {
+      float* bp = pl < planes ? bufs[0] + pl * plane_stride : bufs2[0] + (pl - planes) * plane_stride;
       if (r > 0) {  // my first `bot` rows are the previous strip's lower halo; receive my upper halo
         const int sa = s.hr_row0, sb = std::min(s.hr_row0 + bot, s.hr_row1);
         NK(c, nccl_send_f32(bp + sa * rowf, (sb - sa) * rowf, r - 1, c->comm, st));
@@ -1550,21 +1605,49 @@ static lfsr_status enqueue_iteration(lfsr_ctx* c, cudaStream_t st, int parity) {
     if ((s_ = (expr)) != LFSR_OK) return s_;     \
   } while (0)
 
-  if (multi) XC(xfill(c, st, xs.data(), ht, hb));   // x halo for the wz-step
+  // strips: the tiles whose input tile lies in the own rows run on the side stream while the halo is
+  // exchanged (fork / join inside the captured graph); the boundary tiles after the exchange
+  const char* ov_env = getenv("LFSR_STRIP_OVERLAP");
+  const bool overlap = multi && c->side && !(ov_env && ov_env[0] == '0');
+  auto split_launch = [&](auto&& fill, auto&& launch_part) -> lfsr_status {
+    if (!overlap) {
+      lfsr_status q_ = fill();
+      if (q_ != LFSR_OK) return q_;
+      for (Part& P : c->parts) {
+        if ((q_ = launch_part(P, P.T, st)) != LFSR_OK) return q_;
+      }
+      return LFSR_OK;
+    }
+    CK(c, cudaEventRecord(c->ev_fork, st));
+    CK(c, cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+    lfsr_status q_;
+    for (Part& P : c->parts)
+      if (P.Tin.ntl > 0 && (q_ = launch_part(P, P.Tin, c->side)) != LFSR_OK) return q_;
+    CK(c, cudaEventRecord(c->ev_join, c->side));
+    if ((q_ = fill()) != LFSR_OK) return q_;
+    for (Part& P : c->parts)
+      if (P.Tbd.ntl > 0 && (q_ = launch_part(P, P.Tbd, st)) != LFSR_OK) return q_;
+    CK(c, cudaStreamWaitEvent(st, c->ev_join, 0));
+    return LFSR_OK;
+  };
   CK(c, mark());
+  XC(split_launch([&]() { return multi ? xfill(c, st, xs.data(), ht, hb) : LFSR_OK; },   // x halo
+                  [&](Part& P, const TileGeom& T, cudaStream_t s2) -> lfsr_status {
+                    TileIO io = base_io(P);
+                    io.in_hr = P.S.x;
+                    io.y = P.S.y;
+                    io.wA = P.S.wA;
+                    io.wS0 = P.S.wS[0];
+                    io.wS1 = P.S.wS[1];
+                    io.wo = P.S.wo;
+                    io.out_hr = P.S.r;
+                    io.reweight = c->prm.reweight_every_iter;
+                    io.wz_no_nltv = nltv_split ? 1 : 0;
+                    CK(c, launch_tile(MODE_WZ, G, c->V, T, io, s2));
+                    ++launches;
+                    return LFSR_OK;
+                  }));
   for (Part& P : c->parts) {
-    TileIO io = base_io(P);
-    io.in_hr = P.S.x;
-    io.y = P.S.y;
-    io.wA = P.S.wA;
-    io.wS0 = P.S.wS[0];
-    io.wS1 = P.S.wS[1];
-    io.wo = P.S.wo;
-    io.out_hr = P.S.r;
-    io.reweight = c->prm.reweight_every_iter;
-    io.wz_no_nltv = nltv_split ? 1 : 0;
-    CK(c, launch_tile(MODE_WZ, G, c->V, P.T, io, st));
-    ++launches;
     if (G.paper) {   // v's data part through the paper's backward warp (A37): r = -v
       CK(c, launch_paper_gather(G, c->V, P.S.rho, P.S.omega, nullptr, P.S.r, -1.f, P.S.ctl, -1, 0, 0, G.H, st));
       ++launches;
@@ -1583,7 +1666,6 @@ static lfsr_status enqueue_iteration(lfsr_ctx* c, cudaStream_t st, int parity) {
     XC(xfill(c, st, ms.data(), r, r));                                    // m for the NLTV normal term
     XC(xfill(c, st, wsw.data(), r, r, G.s_d, (size_t)G.H * G.ps));        // new w_S for the next wz-step
     XC(xallreduce(c, st, S_L1, 4));                                       // J terms, |dw|^2
-    XC(xfill(c, st, rs.data(), ht, hb));                                  // r_0 halo
   }
   for (int k = 1; k <= G.K; ++k) {
     if (c->misr) {   // constant shifts: border tiles + the precomputed stencil (misr.cu)
@@ -1591,18 +1673,29 @@ static lfsr_status enqueue_iteration(lfsr_ctx* c, cudaStream_t st, int parity) {
       XC(misr_normal(c, P, k, nullptr, P.S.q, P.S.ctl, st));
       launches += (c->misr_border && c->Tborder.ntl > 0) ? 2 : 1;
     }
-    for (Part& P : c->parts) {
-      if (c->misr) break;
-      TileIO n = base_io(P);
-      n.in_hr = P.S.r;
-      n.in_hr2 = P.S.p[(k - 1) & 1];
-      n.p_out = P.S.p[k & 1];
-      n.out_hr = P.S.q;
-      n.cg_k = k;
-      n.do_nltv = 1;
-      CK(c, launch_tile(MODE_NORMAL, G, c->V, P.T, n, st));
-      ++launches;
-      if (G.paper) {   // q's data part and its share of <p, q> (A37)
+    if (!c->misr) {
+      for (int i = 0; i < np; ++i) pk[i] = c->parts[i].S.p[(k - 1) & 1];
+      // the halos of r (and of p_{k-1} from k = 2) for this step's operator, overlapped with the
+      // interior tiles (k = 1: r_0 = -v after the wz-step's fold)
+      XC(split_launch([&]() -> lfsr_status {
+                        if (!multi) return LFSR_OK;
+                        return k == 1 ? xfill(c, st, rs.data(), ht, hb)
+                                      : xfill(c, st, rs.data(), ht, hb, 1, 0, pk.data());
+                      },
+                      [&](Part& P, const TileGeom& T, cudaStream_t s2) -> lfsr_status {
+                        TileIO n = base_io(P);
+                        n.in_hr = P.S.r;
+                        n.in_hr2 = P.S.p[(k - 1) & 1];
+                        n.p_out = P.S.p[k & 1];
+                        n.out_hr = P.S.q;
+                        n.cg_k = k;
+                        n.do_nltv = 1;
+                        CK(c, launch_tile(MODE_NORMAL, G, c->V, T, n, s2));
+                        ++launches;
+                        return LFSR_OK;
+                      }));
+      if (G.paper) {   // q's data part and its share of <p, q> (A37; single strip)
+        Part& P = c->parts[0];
         CK(c, launch_paper_gather(G, c->V, P.S.rho, P.S.omega, P.S.p[k & 1], P.S.q, 1.f, P.S.ctl, S_PQ + k, k, 0,
                                   G.H, st));
         ++launches;
@@ -1634,11 +1727,7 @@ static lfsr_status enqueue_iteration(lfsr_ctx* c, cudaStream_t st, int parity) {
           if (b > s.hr_row1)
             CK(c, cudaMemsetAsync(P.S.r + (size_t)s.hr_row1 * G.ps, 0, (size_t)(b - s.hr_row1) * G.ps * 4, st));
         }
-      } else {
-        for (int i = 0; i < np; ++i) pk[i] = c->parts[i].S.p[k & 1];
-        XC(xfill(c, st, rs.data(), ht, hb));
-        XC(xfill(c, st, pk.data(), ht, hb));
-      }
+      }   // (k < K: the r and p halos are exchanged at the start of step k + 1, next to its interior tiles)
     }
   }
   if (multi) {
