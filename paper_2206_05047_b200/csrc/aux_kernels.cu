@@ -247,6 +247,106 @@ __global__ void __launch_bounds__(256) k_cg_update(const Geom G, float* __restri
 }
 
 // ---------------------------------------------------------------------------
+// CG update of the strip decomposition in the Chronopoulos-Gear form: step j
+// (0-based) has w_j = M r_j, gamma_j = <r_j, r_j> and delta_j = <r_j, w_j> from the operator
+// kernel -- reduced across the strips in ONE all-reduce -- and
+//   beta = gamma_j / gamma_{j-1},  alpha = gamma_j / (delta_j - beta gamma_j / alpha_{j-1})
+//   p = r + beta p,  s = w + beta s,  x += alpha p,  r -= alpha s
+// (j = 0: beta = 0, alpha = gamma_0 / delta_0).  Equivalent to Alg.2 (readings A1-A4) in exact
+// arithmetic: s_j = M p_j, delta_j - beta gamma_j / alpha_{j-1} = <p_j, M p_j>.  Stop rule A1 on
+// gamma_j (= pi_j), breakdown A28 on the denominator.  The last step also forms pi_K = |r_K|^2
+// (own rows; the caller all-reduces it) for the stats record.  w is zeroed for the next step.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_cgcg_update(const Geom G, float* __restrict__ x, float* __restrict__ r,
+                                                     float* __restrict__ p, float* __restrict__ sv,
+                                                     float* __restrict__ w, Control* ctl, int j, int row0,
+                                                     int nrows) {
+  __shared__ double red[8 * 2];
+  __shared__ bool am_last;
+  const double gam = ctl->cur[S_CG + 2 * j], del = ctl->cur[S_CG + 2 * j + 1];
+  const bool stopped = ctl->cur[S_STOP] != 0.0;
+  const bool small = gam < (double)G.cg_tol || gam == 0.0;
+  double beta = 0.0, den = del;
+  if (j > 0) {
+    beta = gam / ctl->cur[S_PI + j - 1];
+    den = del - beta * gam / ctl->cur[S_ALPHA];
+  }
+  const bool active = !stopped && !small && den > 0.0;
+  const float alpha = active ? (float)(gam / den) : 0.f, betaf = (float)beta;
+  const bool last = (j == G.K - 1);
+  double pi_part = 0.0, nf_part = 0.0;
+  const size_t off4 = (size_t)row0 * G.ps / 4, n4 = (size_t)nrows * G.ps / 4;
+  float4* x4 = reinterpret_cast<float4*>(x) + off4;
+  float4* r4 = reinterpret_cast<float4*>(r) + off4;
+  float4* p4 = reinterpret_cast<float4*>(p) + off4;
+  float4* s4 = reinterpret_cast<float4*>(sv) + off4;
+  float4* w4 = reinterpret_cast<float4*>(w) + off4;
+  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
+    const float4 wv = w4[i];
+    if (active) {
+      float4 rv = r4[i], pv = j > 0 ? p4[i] : z4, s = j > 0 ? s4[i] : z4, xv = x4[i];
+      pv.x = rv.x + betaf * pv.x; pv.y = rv.y + betaf * pv.y; pv.z = rv.z + betaf * pv.z; pv.w = rv.w + betaf * pv.w;
+      s.x = wv.x + betaf * s.x; s.y = wv.y + betaf * s.y; s.z = wv.z + betaf * s.z; s.w = wv.w + betaf * s.w;
+      xv.x += alpha * pv.x; xv.y += alpha * pv.y; xv.z += alpha * pv.z; xv.w += alpha * pv.w;
+      rv.x -= alpha * s.x; rv.y -= alpha * s.y; rv.z -= alpha * s.z; rv.w -= alpha * s.w;
+      p4[i] = pv;
+      s4[i] = s;
+      x4[i] = xv;
+      if (last) pi_part += (double)rv.x * rv.x + (double)rv.y * rv.y + (double)rv.z * rv.z + (double)rv.w * rv.w;
+      if (last) nf_part += (float)(!isfinite(xv.x)) + (!isfinite(xv.y)) + (!isfinite(xv.z)) + (!isfinite(xv.w));
+      r4[i] = last ? z4 : rv;   // the next wz-step accumulates r = -v into zeros
+    } else if (last) {
+      const float4 xv = x4[i];
+      nf_part += (float)(!isfinite(xv.x)) + (!isfinite(xv.y)) + (!isfinite(xv.z)) + (!isfinite(xv.w));
+      r4[i] = z4;
+    }
+    w4[i] = z4;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    pi_part += __shfl_xor_sync(0xffffffffu, pi_part, o);
+    nf_part += __shfl_xor_sync(0xffffffffu, nf_part, o);
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) { red[warp * 2] = pi_part; red[warp * 2 + 1] = nf_part; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int q = 0; q < (int)(blockDim.x / 32); ++q) { a += red[q * 2]; b += red[q * 2 + 1]; }
+    if (a != 0.0) atomicAdd(&ctl->cur[S_PI + j + 1], a);   // pi_K (last step only; all-reduced by the caller)
+    if (b != 0.0) atomicAdd(&ctl->cur[S_NF], b);
+    __threadfence();
+    const unsigned prev = atomicAdd(&ctl->done, 1u);
+    am_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!am_last || threadIdx.x != 0) return;
+  __threadfence();
+  volatile double* cur = ctl->cur;
+  if (!stopped) cur[S_PI + j] = gam;   // pi_j for the record (Alg.2 bookkeeping)
+  if (active) {
+    cur[S_CGIT] = cur[S_CGIT] + 1.0;
+    cur[S_ALPHA] = gam / den;
+  } else if (!stopped) {
+    cur[S_STOP] = 1.0;
+    if (!small && !(den > 0.0)) cur[S_BREAK] = 1.0;
+  }
+  __threadfence();
+  ctl->done = 0u;
+}
+
+cudaError_t launch_cgcg_update(const Geom& G, float* x, float* r, float* p, float* s, float* w, Control* ctl, int j,
+                               int row0, int nrows, int num_sms, cudaStream_t st) {
+  const size_t n4 = (size_t)nrows * G.ps / 4;
+  int blocks = (int)((n4 + 255) / 256);
+  if (blocks > num_sms * 4) blocks = num_sms * 4;
+  if (blocks < 1) blocks = 1;
+  k_cgcg_update<<<blocks, 256, 0, st>>>(G, x, r, p, s, w, ctl, j, row0, nrows);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 // gd / gd-ls (the baselines of the paper's solver comparison, P:L910-933;
 // readings A30-A33).  One iteration = k_tile<GRAD> (cost terms of x and the
 // subgradient g, accumulated into a zeroed buffer) [+ k_gd_gnorm and L trial

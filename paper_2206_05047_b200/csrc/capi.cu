@@ -46,6 +46,8 @@ cudaError_t launch_paper_gather(const Geom& G, const Views& V, const float* rho,
                                 cudaStream_t st);
 cudaError_t launch_color(int to_ycbcr, const float* a, float* y, float* cb, float* cr, size_t n, int num_sms,
                          cudaStream_t st);
+cudaError_t launch_cgcg_update(const Geom& G, float* x, float* r, float* p, float* s, float* w, Control* ctl, int j,
+                               int row0, int nrows, int num_sms, cudaStream_t st);
 cudaError_t launch_wz_nltv(const Geom& G, const float* x, const float* m, float* wS0, float* wS1, float* r,
                            Control* ctl, int row0, int row1, cudaStream_t st);
 cudaError_t launch_omega_const(const Geom& G, const float* omega, unsigned* flag, cudaStream_t st);
@@ -1667,7 +1669,45 @@ static lfsr_status enqueue_iteration(lfsr_ctx* c, cudaStream_t st, int parity) {
     XC(xfill(c, st, wsw.data(), r, r, G.s_d, (size_t)G.H * G.ps));        // new w_S for the next wz-step
     XC(xallreduce(c, st, S_L1, 4));                                       // J terms, |dw|^2
   }
-  for (int k = 1; k <= G.K; ++k) {
+  // strips: CG in the Chronopoulos-Gear form -- one operator pass on r and ONE all-reduce of
+  // (gamma, delta) per step, one halo fill (r only); LFSR_STRIP_CG=standard keeps Alg.2's two
+  const char* cg_env = getenv("LFSR_STRIP_CG");
+  const bool cgcg = multi && !G.paper && !(cg_env && cg_env[0] == 's');
+  for (int j = 0; cgcg && j < G.K; ++j) {
+    XC(split_launch([&]() { return xfill(c, st, rs.data(), ht, hb); },   // r_j halo
+                    [&](Part& P, const TileGeom& T, cudaStream_t s2) -> lfsr_status {
+                      TileIO n = base_io(P);
+                      n.in_hr = P.S.r;
+                      n.out_hr = P.S.q;   // w_j = M r_j
+                      n.cg_k = 1;
+                      n.cgcg_slot = S_CG + 2 * j;
+                      n.cgcg_step = j;
+                      n.do_nltv = 1;
+                      CK(c, launch_tile(MODE_NORMAL, G, c->V, T, n, s2));
+                      ++launches;
+                      return LFSR_OK;
+                    }));
+    XC(xfold(c, st, qs.data(), ht, hb));
+    XC(xallreduce(c, st, S_CG + 2 * j, 2));   // (gamma_j, delta_j)
+    for (Part& P : c->parts) {
+      const lfsr_strip& sp = P.plan;
+      CK(c, launch_cgcg_update(G, P.S.x, P.S.r, P.S.p[0], P.S.p[1], P.S.q, P.S.ctl, j, sp.hr_row0,
+                               sp.hr_row1 - sp.hr_row0, c->num_sms, st));
+      ++launches;
+    }
+    if (j == G.K - 1) {
+      XC(xallreduce(c, st, S_PI + G.K, 1));   // pi_K for the record
+      XC(xallreduce(c, st, S_NF, 1));
+      for (Part& P : c->parts) {   // r's halo rows start the next wz-step at zero (see below)
+        const lfsr_strip& sp = P.plan;
+        const int a = std::max(sp.hr_row0 - ht, 0), b = std::min(sp.hr_row1 + hb, G.H);
+        if (sp.hr_row0 > a) CK(c, cudaMemsetAsync(P.S.r + (size_t)a * G.ps, 0, (size_t)(sp.hr_row0 - a) * G.ps * 4, st));
+        if (b > sp.hr_row1)
+          CK(c, cudaMemsetAsync(P.S.r + (size_t)sp.hr_row1 * G.ps, 0, (size_t)(b - sp.hr_row1) * G.ps * 4, st));
+      }
+    }
+  }
+  for (int k = 1; !cgcg && k <= G.K; ++k) {
     if (c->misr) {   // constant shifts: border tiles + the precomputed stencil (misr.cu)
       Part& P = c->parts[0];
       XC(misr_normal(c, P, k, nullptr, P.S.q, P.S.ctl, st));

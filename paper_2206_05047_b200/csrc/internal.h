@@ -28,7 +28,9 @@ enum Slot : int {
   S_PQ = S_PI + kMaxK + 1,  // <p_k, M p_k>, k = 1..K at S_PQ + k
   S_GN = S_PQ + kMaxK + 1,  // gd: |g|^2
   S_TJ = S_GN + 1,          // gd-ls: cost terms (sum|e|, sum e^2, sum|G|) of trial t at S_TJ + 3t
-  S_COUNT = S_TJ + 3 * kMaxLs
+  S_CG = S_TJ + 3 * kMaxLs, // strips, Chronopoulos-Gear CG: (gamma_j, delta_j) of step j at S_CG + 2j
+  S_ALPHA = S_CG + 2 * (kMaxK + 1),   // ... and the previous step's alpha
+  S_COUNT = S_ALPHA + 1
 };
 
 // Stats record layout in the ring (doubles).
@@ -134,6 +136,8 @@ struct TileIO {
   int32_t zs_y0, zs_y1, zs_x0, zs_x1;
   int32_t no_pq;         // ... and leave <p, Mp> to k_misr_normal
   int32_t wz_no_nltv;    // WZ: the NLTV rows run in k_wz_nltv (nltv.cu) instead of phase 3
+  int32_t cgcg_slot;     // NORMAL, strips (Chronopoulos-Gear): > 0: w = M r with gamma = <r, r> -> cur[slot],
+  int32_t cgcg_step;     //   delta = <r, M r> -> cur[slot + 1]; step index j (j >= 1: skip once CG stopped)
 };
 
 // WZ: ADMM wz-step; NORMAL: CG normal operator; A / AT: test operators;

@@ -851,7 +851,7 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
   const int PH = T.PH, PW = T.PW, PWn = ECOL + 2 * T.SXe + 2;
   const int H = G.H, W = G.W, ps = G.ps;
   Control* ctl = io.ctl;
-  if (MODE == MODE_NORMAL && io.cg_k >= 2 && ctl->cur[S_STOP] != 0.0) return;  // CG stopped
+  if (MODE == MODE_NORMAL && (io.cg_k >= 2 || io.cgcg_step >= 1) && ctl->cur[S_STOP] != 0.0) return;  // CG stopped
   CTA_T(0);
   // gd-ls trial t runs only while no earlier trial met the Armijo condition (A32); every
   // CTA reads the same fp64 sums, so all take the same decision
@@ -927,7 +927,7 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
           } else {
             val = val + beta * v2[u];
           }
-          if (own[u] && grp == 0) io.p_out[gi[u]] = val;
+          if (own[u] && grp == 0 && io.p_out) io.p_out[gi[u]] = val;
         }
         if (MODE == MODE_J) val = fmaf(beta, v2[u], val);   // the same rounding as k_gd_update
         pmax = fmaxf(pmax, fabsf(val));
@@ -1139,7 +1139,8 @@ k_tile(const Geom G, const Views V, const TileGeom T, const TileIO io) {
   } else if (MODE == MODE_NORMAL && io.cg_k >= 1) {
     // PM: the data part comes from the gather; MISR fast path: k_misr_normal forms <p, q>
     double v[2] = {io.no_pq ? 0.0 : (PM ? 0.0 : red_a) + red_b, pi0_part};
-    const int slot[2] = {S_PQ + io.cg_k, S_PI + 0};
+    // Chronopoulos-Gear (strips): delta = <r, M r> and gamma = <r, r> side by side (one all-reduce)
+    const int slot[2] = {io.cgcg_slot > 0 ? io.cgcg_slot + 1 : S_PQ + io.cg_k, io.cgcg_slot > 0 ? io.cgcg_slot : S_PI + 0};
     block_reduce_add<2>(v, RED, ctl->cur, slot);
   }
   CTA_T(3);
