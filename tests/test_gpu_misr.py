@@ -32,20 +32,21 @@ def _solver(lfsr_mod, p, y, vo, om, fast=True):
     return s
 
 
-def misr_instance(seed, grid, lr, z, c=1.0, frac=False):
+def misr_instance(seed, grid, lr, z, c=1.0, frac=False, lw=None):
     """grid x grid frames, constant disparity c; offsets = MISR shifts (integer HR px) or generic
-    fractional offsets (the 'fractional' case makes every W_k a bilinear translation)."""
+    fractional offsets (the 'fractional' case makes every W_k a bilinear translation); lr x lw LR."""
     g = np.random.Generator(np.random.Philox(seed))
-    H = lr * z
+    lw = lr if lw is None else lw
+    H, W = lr * z, lw * z
     if frac == "grid":     # a light-field grid of views with one constant disparity: separable form
         vo = S.grid_offsets(grid)
     elif frac:
         vo = g.uniform(-2.5, 2.5, (grid * grid, 2)).astype(np.float32)
     else:
         vo = S.misr_offsets(grid)
-    om = np.full((H, H), c, np.float32)
-    y = g.uniform(0.0, 1.0, (grid * grid, lr, lr)).astype(np.float32)
-    x = g.uniform(0.0, 1.0, (H, H)).astype(np.float32)
+    om = np.full((H, W), c, np.float32)
+    y = g.uniform(0.0, 1.0, (grid * grid, lr, lw)).astype(np.float32)
+    x = g.uniform(0.0, 1.0, (H, W)).astype(np.float32)
     return y, vo, om, x
 
 
@@ -58,15 +59,20 @@ CASES = [dict(seed=1, grid=2, lr=64, z=2, c=1.0, frac=False),       # M2-shaped
          dict(seed=7, grid=3, lr=33, z=4, c=1.0, frac=False),
          dict(seed=8, grid=3, lr=64, z=2, c=0.37, frac="grid"),     # LF grid, constant fractional disparity
          dict(seed=9, grid=5, lr=45, z=3, c=-1.3, frac="grid"),
-         dict(seed=10, grid=9, lr=40, z=4, c=0.9, frac="grid")]
+         dict(seed=10, grid=9, lr=40, z=4, c=0.9, frac="grid"),
+         dict(seed=11, grid=2, lr=37, lw=90, z=2, c=1.0, frac=False),      # non-square, ragged tiles
+         dict(seed=12, grid=3, lr=70, lw=29, z=3, c=0.45, frac="grid"),
+         dict(seed=13, grid=3, lr=61, lw=95, z=2, c=0.3, frac=True)]
 
 
-@pytest.mark.parametrize("case", CASES, ids=lambda c: "g%d_lr%d_z%d_%s" % (c["grid"], c["lr"], c["z"],
-                                                                             c["frac"] if c["frac"] else "int"))
+@pytest.mark.parametrize("case", CASES, ids=lambda c: "g%d_lr%dx%d_z%d_%s" % (
+    c["grid"], c["lr"], c.get("lw", c["lr"]), c["z"], c["frac"] if c["frac"] else "int"))
 def test_misr_fast_normal_parity(lfsr_mod, case):
-    y, vo, om, x = misr_instance(case["seed"], case["grid"], case["lr"], case["z"], case["c"], case["frac"])
+    y, vo, om, x = misr_instance(case["seed"], case["grid"], case["lr"], case["z"], case["c"], case["frac"],
+                                 case.get("lw"))
     d = S.MisrDefaults()
-    p = lfsr_mod.Params(n_views=len(vo), lr_height=case["lr"], lr_width=case["lr"], scale=case["z"], ref_view=0,
+    p = lfsr_mod.Params(n_views=len(vo), lr_height=case["lr"], lr_width=case.get("lw", case["lr"]), scale=case["z"],
+                        ref_view=0,
                         nltv_radius=2, lambda1=d.lambda1, lambda2=0.7, lambda_reg=0.3, sigma_s=d.sigma_s,
                         sigma_e=0.2, sigma_o1=0.5, sigma_o2=0.2, theta=d.theta, cg_max_iters=5)
     sf = _solver(lfsr_mod, p, y, vo, om, fast=True)
