@@ -316,6 +316,22 @@ LFSR_API lfsr_status lfsr_tile_config(const lfsr_ctx* ctx, int32_t* tile_rows, i
  * active NULL), STATE (before lfsr_set_observations). */
 LFSR_API lfsr_status lfsr_fast_path(const lfsr_ctx* ctx, int32_t* active, int32_t* rect);
 
+/* Which implementation applies the CG normal operator M (A7) for the current
+ * observations.  path: 0 = the fused tile kernel (warp / blur / decimate and
+ * their adjoints for every view, each CG step); 1 = the MISR fast path (lfsr_fast_path);
+ * 2 = the assembled data operator: at lfsr_set_observations the rows a_{k,i} of the stacked
+ * A_k = D B W_k whose cells fit a (2R+2)^2 window are summed into a stencil per HR pixel
+ * (c_A sum a a^T, the symmetric half stored, (2R+1)-radius), the other rows -- blur windows
+ * straddling a depth edge -- are applied as rows (t = c_A a.p, then t a); the NLTV part is formed
+ * from the weights m on the fly.  Path 2 needs a single strip, the Gaussian blur, the exact
+ * adjoint and nltv_radius <= 2; LFSR_ASM=0 in the environment at lfsr_set_observations keeps
+ * path 0.  Results match path 0 to fp32 rounding.  irregular_rows: rows applied as rows (-1 when
+ * not read back: lfsr_solve_batch fields after the first), total_rows = n_views h w; setup_ms:
+ * wall time of the assembly (synchronised).  Any out pointer except path may be NULL.  Errors:
+ * INVALID_ARG (ctx or path NULL), STATE (before lfsr_set_observations). */
+LFSR_API lfsr_status lfsr_normal_path(const lfsr_ctx* ctx, int32_t* path, int64_t* irregular_rows,
+                                      int64_t* total_rows, double* setup_ms);
+
 /* Row-strip plan of the multi-GPU decomposition (DESIGN 10): rank r
  * owns tile rows [tile_row0, tile_row1) = LR rows [lr_row0, lr_row1) = HR rows
  * [hr_row0, hr_row1); before every operator pass it needs halo_top HR rows above

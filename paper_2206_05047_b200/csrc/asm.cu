@@ -1,0 +1,733 @@
+// asm.cu — the assembled data normal operator of the CG x-step.
+//
+// The CG normal operator (A7)
+//     M = c_A sum_k A_k^T A_k + (th/2) S_W^T S_W,      A_k = D B W_k
+// has a data part that does not change during a solve: omega, the blur and the views are fixed
+// once set_observations returns, only the NLTV weights m change per ADMM iteration.
+// Written row by row of the stacked A (one row per view k and LR pixel i,
+//     a_{k,i} = sum_{u,v} g[u] g[v] bil_k(zeta i + (u, v))       (positions outside Omega dropped, A11)
+// with bil_k(z) the four bilinear weights of the sample z + dtheta_k omega(z), A12/A13), the data
+// part is the sum of outer products c_A sum_{k,i} a a^T.  A row whose cells fit a (2R + 2)^2
+// window ("regular": everywhere except where the blur window straddles a depth edge, ~96 % of the
+// rows of the HCI-shaped C3 light field) only couples cells at most SR = 2R + 1 apart per axis,
+// so the regular rows sum to a banded operator stored as a stencil per HR pixel, (2 SR + 1)^2
+// coefficients of which the symmetric half (NH = 61 at zeta = 2, 113 at zeta = 3, 4) is kept:
+//     st[h][a] = c_A sum_{regular (k,i)} a_{k,i}[a] a_{k,i}[a + d_h],   d_h = (h / NSW, h % NSW) (see hoff)
+//     (M_reg p)(a) = st[0][a] p(a) + sum_{h>0} st[h][a] p(a + d_h) + st[h][a - d_h] p(a - d_h).
+// The irregular rows are applied exactly as rows: t = c_A a . p (k_asm_irr_t), then t a added
+// into q (k_asm_irr_scatter: per output tile, a two-word integer fixed-point sum in shared memory,
+// order-independent, then one RED.ADD per touched cell).
+//
+// Kernels:
+//   k_asm_classify  setup: the irregular rows -> a compact list (k, i) with their cell boxes;
+//                   k_asm_tcount / k_asm_tscan / k_asm_tfill: per 32 x 32 output tile, the
+//                   irregular rows whose box meets it (CSR)
+//   k_asm_stencil   setup: the stencil planes, one CTA per 16 x 16 output cells, thread = cell
+//                   (owner computes: every coefficient is summed by one thread in a fixed
+//                   order, no atomics); the rows of the CTA's footprint are built in shared
+//                   memory view by view
+//   k_asm_normal    per CG step: q = M_reg p + (th/2) S_W^T S_W p on a 32 x 32 output tile --
+//                   p = r + beta p_{k-1} formed in the tile load and written for the own pixels,
+//                   the stencil (HBM stream of NH planes; the transposed half re-reads the
+//                   neighbours' coefficients, L1/L2 hits), the weighted NLTV part from m (as
+//                   k_misr_normal), <p, q> and pi_0 into the CG slots (Alg.2 lines 3, 6-7)
+//   k_asm_irr_t     per CG step: t of every irregular row from p_k (NP lanes per row, lane = blur
+//                   row), the bound max|t| for the fixed-point scale, <p, M_irr p> = sum t^2 / c_A
+//   k_asm_irr_scatter  per CG step: t a into q, equal shares of the tile lists per CTA
+#include "internal.h"
+#include <climits>
+#include <type_traits>
+
+namespace lfsr {
+
+template <int Z> struct AsmCfg {
+  static constexpr int R = Z == 2 ? 2 : 3;            // Gaussian blur radius (A11)
+  static constexpr int NP = 2 * R + 1;                // positions per axis of a row
+  static constexpr int WRr = 2 * R + 2;               // regular row window (cells per axis)
+  static constexpr int WR2 = WRr * WRr;
+  static constexpr int WR2P = WR2 + 1;                // odd shared-memory stride of a row
+  static constexpr int SR = WRr - 1;                  // stencil radius
+  static constexpr int NSW = 2 * SR + 1;
+  static constexpr int NH = (NSW * NSW + 1) / 2;      // stored half (incl. the centre)
+  // setup kernel: 16 x 16 cells per CTA, rows of the footprint in chunks of CAP
+  static constexpr int TA = 16, NTA = TA * TA;
+  static constexpr int CAP = Z == 2 ? 288 : 160;
+  static constexpr size_t kSmemStencil = (size_t)NH * NTA * 4 + (size_t)CAP * (WR2P + 2) * 4;
+  // CG-step kernel: 128 x 8 output pixels, warp = row, lane = 4 pixels
+  static constexpr int TH = 8, TW = 128;
+  static constexpr int PC = TW + 16;                  // tile columns [X0 - 8, X0 + TW + 8)
+  static constexpr int PR = TH + 2 * SR, MR = TH + 4;
+  static constexpr int NF = NSW * NSW;                // full stencil planes
+  static constexpr size_t kSmemNormal = (size_t)(PR * PC + 2 * MR * PC) * 4;
+};
+
+// half-window offset of coefficient h: h = dy * NSW + dx with dy = 0, dx in [0, SR] or dy in
+// [1, SR], dx in [-SR, SR]
+template <int NSW, int SR>
+__host__ __device__ constexpr int hoff_dy(int h) { return (h + SR) / NSW; }
+template <int NSW, int SR>
+__host__ __device__ constexpr int hoff_dx(int h) { return h - hoff_dy<NSW, SR>(h) * NSW; }
+
+__device__ __forceinline__ int fdiv(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }   // floor, b > 0
+__device__ __forceinline__ int cdiv(int a, int b) { return -fdiv(-a, b); }                            // ceil
+
+// The bilinear sample of view k at HR position (Y, X), replicate-clamped (A12/A13); the same
+// arithmetic in every kernel of this file so that the regular / irregular split is consistent.
+struct Samp {
+  int y0, x0, y1, x1;
+  float fy, fx;
+};
+__device__ __forceinline__ Samp asm_sample(const Geom& G, const float* om, float drho, float dtau, int Y, int X) {
+  const float o = __ldg(om + (size_t)Y * G.ps + X);
+  const float sy = fminf(fmaxf(fmaf(dtau, o, (float)Y), 0.f), (float)(G.H - 1));
+  const float sx = fminf(fmaxf(fmaf(drho, o, (float)X), 0.f), (float)(G.W - 1));
+  const float by = floorf(sy), bx = floorf(sx);
+  Samp s;
+  s.y0 = (int)by;
+  s.x0 = (int)bx;
+  s.fy = sy - by;
+  s.fx = sx - bx;
+  s.y1 = min(s.y0 + 1, G.H - 1);
+  s.x1 = min(s.x0 + 1, G.W - 1);
+  return s;
+}
+
+__device__ __forceinline__ const float* asm_omega(const Geom& G, const float* omega, int k) {
+  return omega + (G.per_view ? (size_t)k * G.H * G.ps : 0);
+}
+
+// Cell bounding box of row (k, iy, ix); returns true when it is regular.
+template <int Z>
+__device__ __forceinline__ bool asm_row_bbox(const Geom& G, const float* om, float drho, float dtau, int iy, int ix,
+                                             int& by, int& bx, int* ey = nullptr, int* ex = nullptr) {
+  using C = AsmCfg<Z>;
+  int y0 = 1 << 30, y1 = -(1 << 30), x0 = 1 << 30, x1 = -(1 << 30);
+#pragma unroll
+  for (int u = -C::R; u <= C::R; ++u) {
+    const int Y = Z * iy + u;
+    if (Y < 0 || Y >= G.H) continue;
+#pragma unroll
+    for (int v = -C::R; v <= C::R; ++v) {
+      const int X = Z * ix + v;
+      if (X < 0 || X >= G.W) continue;
+      const Samp s = asm_sample(G, om, drho, dtau, Y, X);
+      y0 = min(y0, s.y0);
+      y1 = max(y1, s.y1);
+      x0 = min(x0, s.x0);
+      x1 = max(x1, s.x1);
+    }
+  }
+  by = y0;
+  bx = x0;
+  if (ey) *ey = y1;
+  if (ex) *ex = x1;
+  return y1 - y0 < C::WRr && x1 - x0 < C::WRr;
+}
+
+// ---------------------------------------------------------------------------------------------
+// setup 1: irregular rows -> compact list (k, i) + cell boxes
+// ---------------------------------------------------------------------------------------------
+template <int Z>
+__global__ void __launch_bounds__(256) k_asm_classify(const Geom G, const Views V, const float* __restrict__ omega,
+                                                      unsigned* count, int2* __restrict__ list,
+                                                      unsigned* __restrict__ pmask, int pmw) {
+  using C = AsmCfg<Z>;
+  const int lane = threadIdx.x, ix = blockIdx.x * 32 + lane, iy = blockIdx.y * 8 + threadIdx.y, k = blockIdx.z;
+  bool irr = false;
+  int by = 0, bx = 0;
+  if (ix < G.w && iy < G.h) irr = !asm_row_bbox<Z>(G, asm_omega(G, omega, k), V.off[k].x, V.off[k].y, iy, ix, by, bx);
+  const unsigned b = __ballot_sync(0xffffffffu, irr);
+  if (!b) return;
+  unsigned base = 0;
+  if (lane == 0) base = atomicAdd(count, (unsigned)__popc(b));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (!irr) return;
+  list[base + __popc(b & ((1u << lane) - 1u))] = make_int2(k, iy * G.w + ix);
+  // the HR positions of the row's blur window (inside Omega) join the position set P_k
+  for (int u = -C::R; u <= C::R; ++u) {
+    const int Y = Z * iy + u;
+    if (Y < 0 || Y >= G.H) continue;
+    for (int v = -C::R; v <= C::R; ++v) {
+      const int X = Z * ix + v;
+      if (X < 0 || X >= G.W) continue;
+      atomicOr(pmask + ((size_t)k * G.H + Y) * pmw + (X >> 5), 1u << (X & 31));
+    }
+  }
+}
+
+// setup 2: P_k as a compact list of linear indices k H W + Y W + X (warp ballots over the mask)
+__global__ void __launch_bounds__(256) k_asm_plist(const Geom G, const unsigned* __restrict__ pmask, int pmw,
+                                                   unsigned* count, unsigned* __restrict__ plist) {
+  const size_t nwords = (size_t)G.n_views * G.H * pmw;
+  const int lane = threadIdx.x & 31;
+  for (size_t w0 = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) & ~(size_t)31; w0 < nwords;
+       w0 += (size_t)gridDim.x * blockDim.x) {
+    // each lane holds one mask word; the warp walks the 32 words' bits together
+    const size_t wi = w0 + lane;
+    const unsigned word = wi < nwords ? __ldg(pmask + wi) : 0u;
+    const size_t row = wi / pmw;   // k H + Y
+    const int xw = (int)(wi - row * pmw) * 32;
+    const int n = __popc(word);
+    unsigned base = 0;
+    int tot = n;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {   // inclusive scan of the counts
+      const int t = __shfl_up_sync(0xffffffffu, tot, o);
+      if (lane >= o) tot += t;
+    }
+    const int all = __shfl_sync(0xffffffffu, tot, 31);
+    if (lane == 31 && all) base = atomicAdd(count, (unsigned)all);
+    base = __shfl_sync(0xffffffffu, base, 31) + (unsigned)(tot - n);
+    unsigned wb = word;
+    while (wb) {
+      const int bpos = __ffs(wb) - 1;
+      wb &= wb - 1;
+      const size_t k = row / G.H, Y = row - k * G.H;
+      plist[base++] = (unsigned)(k * G.H * G.W + Y * G.W + xw + bpos);
+    }
+  }
+}
+
+template <int Z>
+__global__ void __launch_bounds__(256, 2) k_asm_stencil(const Geom G, const Views V, const float* __restrict__ omega,
+                                                     float om_max, float* __restrict__ st, int psS, size_t plane) {
+  using C = AsmCfg<Z>;
+  constexpr int WRr = C::WRr, WR2P = C::WR2P, NH = C::NH, NSW = C::NSW, NTA = C::NTA, CAP = C::CAP;
+  extern __shared__ __align__(16) float sm_asm[];
+  float* acc = sm_asm;                               // [NH][NTA]
+  float* rw = acc + NH * NTA;                        // [CAP][WR2P] row windows
+  int* rby = reinterpret_cast<int*>(rw + CAP * WR2P);   // [CAP] window base row (INT_MIN: irregular)
+  int* rbx = rby + CAP;
+  __shared__ int s_oy[2], s_ox[2];                   // min / max of (base - zeta i) over the chunk's regular rows
+  const int tid = threadIdx.x;
+  const int A0y = blockIdx.y * C::TA, A0x = blockIdx.x * C::TA;
+  const int Ay = A0y + tid / C::TA, Ax = A0x + tid % C::TA;
+  for (int h = 0; h < NH; ++h) acc[h * NTA + tid] = 0.f;
+
+  for (int k = 0; k < G.n_views; ++k) {
+    const float drho = V.off[k].x, dtau = V.off[k].y;
+    const float* om = asm_omega(G, omega, k);
+    const int sY = (int)ceilf(fabsf(dtau) * om_max), sX = (int)ceilf(fabsf(drho) * om_max);
+    // LR rows whose cells can reach the tile: cells of row i lie in [zeta i - R - s, zeta i + R + s + 1]
+    const int iy0 = max(0, cdiv(A0y - C::R - sY - 1, Z)), iy1 = min(G.h - 1, fdiv(A0y + C::TA - 1 + C::R + sY, Z));
+    const int ix0 = max(0, cdiv(A0x - C::R - sX - 1, Z)), ix1 = min(G.w - 1, fdiv(A0x + C::TA - 1 + C::R + sX, Z));
+    if (iy0 > iy1 || ix0 > ix1) continue;
+    const int nx = ix1 - ix0 + 1;
+    const int cx = min(nx, CAP), cy = max(1, CAP / cx);
+    for (int cy0 = iy0; cy0 <= iy1; cy0 += cy) {
+      for (int cx0 = ix0; cx0 <= ix1; cx0 += cx) {
+        const int ny_c = min(cy, iy1 - cy0 + 1), nx_c = min(cx, ix1 - cx0 + 1);
+        __syncthreads();   // the previous chunk's rows are consumed
+        if (tid == 0) {
+          s_oy[0] = s_ox[0] = 1 << 30;
+          s_oy[1] = s_ox[1] = -(1 << 30);
+        }
+        __syncthreads();
+        for (int r = tid; r < ny_c * nx_c; r += NTA) {
+          const int iy = cy0 + r / nx_c, ix = cx0 + r % nx_c;
+          int by, bx;
+          const bool reg = asm_row_bbox<Z>(G, om, drho, dtau, iy, ix, by, bx);
+          float* w = rw + r * WR2P;
+          if (reg) {
+#pragma unroll
+            for (int e = 0; e < C::WR2; ++e) w[e] = 0.f;
+#pragma unroll
+            for (int u = -C::R; u <= C::R; ++u) {
+              const int Y = Z * iy + u;
+              if (Y < 0 || Y >= G.H) continue;
+#pragma unroll
+              for (int v = -C::R; v <= C::R; ++v) {
+                const int X = Z * ix + v;
+                if (X < 0 || X >= G.W) continue;
+                const Samp s = asm_sample(G, om, drho, dtau, Y, X);
+                const float gg = G.taps[u + C::R] * G.taps[v + C::R];
+                const float a0 = gg * (1.f - s.fy), a1 = gg * s.fy;
+                const int r0 = (s.y0 - by) * WRr, r1 = (s.y1 - by) * WRr, c0 = s.x0 - bx, c1 = s.x1 - bx;
+                w[r0 + c0] += a0 * (1.f - s.fx);
+                w[r0 + c1] += a0 * s.fx;
+                w[r1 + c0] += a1 * (1.f - s.fx);
+                w[r1 + c1] += a1 * s.fx;
+              }
+            }
+            atomicMin(&s_oy[0], by - Z * iy);
+            atomicMax(&s_oy[1], by - Z * iy);
+            atomicMin(&s_ox[0], bx - Z * ix);
+            atomicMax(&s_ox[1], bx - Z * ix);
+            rby[r] = by;
+            rbx[r] = bx;
+          } else {
+            rby[r] = INT_MIN;
+          }
+        }
+        __syncthreads();
+        if (s_oy[0] > s_oy[1]) continue;   // no regular row in this chunk (uniform)
+        // candidate rows of this thread's cell: zeta i + o <= A <= zeta i + o + WRr - 1, o in [omin, omax]
+        const int jy0 = max(cy0, cdiv(Ay - s_oy[1] - WRr + 1, Z)), jy1 = min(cy0 + ny_c - 1, fdiv(Ay - s_oy[0], Z));
+        const int jx0 = max(cx0, cdiv(Ax - s_ox[1] - WRr + 1, Z)), jx1 = min(cx0 + nx_c - 1, fdiv(Ax - s_ox[0], Z));
+        for (int iy = jy0; iy <= jy1; ++iy) {
+          for (int ix = jx0; ix <= jx1; ++ix) {
+            const int r = (iy - cy0) * nx_c + (ix - cx0);
+            const int by = rby[r];
+            if (by == INT_MIN) continue;
+            const int oy = Ay - by, ox = Ax - rbx[r];
+            if ((unsigned)oy >= (unsigned)WRr || (unsigned)ox >= (unsigned)WRr) continue;
+            const float* w = rw + r * WR2P;
+            const float wa = w[oy * WRr + ox];
+            if (wa == 0.f) continue;
+            // coefficients of the half window: cells (jy, jx) of the row with (jy, jx) >= (oy, ox)
+            // in row-major order, acc index (jy - oy) NSW + (jx - ox)
+            float* ab = acc + (-(oy * NSW) - ox) * NTA + tid;
+            for (int jy = oy; jy < WRr; ++jy) {
+#pragma unroll
+              for (int jx = 0; jx < WRr; ++jx) {
+                if (jy == oy && jx < ox) continue;
+                const int i2 = (jy * NSW + jx) * NTA;
+                ab[i2] = fmaf(wa, w[jy * WRr + jx], ab[i2]);
+              }
+            }
+          }
+        }
+      }
+    }
+  }
+  if (Ay < G.H && Ax < G.W) {
+    const size_t o = (size_t)(Ay + kAsmPad) * psS + Ax + kAsmPad;
+    for (int h = 0; h < NH; ++h) st[h * plane + o] = G.cA * acc[h * NTA + tid];
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// per CG step 1: t = c_A a . p for every irregular row
+// ---------------------------------------------------------------------------------------------
+struct AsmStepArgs {
+  const float* r;        // CG residual (k >= 1)
+  const float* p_prev;   // previous direction (k >= 2)
+  const float* p_in;     // k = 0: the operator input
+  float* p_out;          // k >= 1: p_k (own pixels)
+  const float* m;        // NLTV weight map
+  float* q;              // output (stored)
+  Control* ctl;
+  int cg_k;
+  const float* omega;
+  const unsigned* count; // [0] irregular rows, [1] positions of their windows (device)
+  const int2* list;      // irregular rows (k, iy * w + ix)
+  const unsigned* plist; // the positions P_k, k H W + Y W + X
+  float* tdense;         // [n_views][h][w] t of the irregular rows (0 elsewhere)
+  float* udense;         // [n_views][H][W] u = W_k p at the positions of P_k
+  const float* st;       // stencil planes
+  int psS;
+  size_t plane;
+  float om_max;
+};
+
+__device__ __forceinline__ float asm_beta(const Control* ctl, int k) {
+  return k >= 2 ? (float)(ctl->cur[S_PI + k - 1] / ctl->cur[S_PI + k - 2]) : 0.f;   // A2
+}
+
+// p_k (k >= 1: formed and written by k_asm_normal, which runs first) or the plain input (k = 0)
+__device__ __forceinline__ const float* asm_pk(const AsmStepArgs& a) { return a.cg_k == 0 ? a.p_in : a.p_out; }
+
+// per CG step 2: u = (W_k p)(z) at every position of P_k (p_k as k_asm_normal formed it)
+__global__ void __launch_bounds__(256) k_asm_irr_u(const Geom G, const Views V, const AsmStepArgs a) {
+  if (a.cg_k >= 2 && a.ctl->cur[S_STOP] != 0.0) return;   // CG stopped
+  const float* pk = asm_pk(a);
+  const unsigned n = a.count[1];
+  const size_t HW = (size_t)G.H * G.W;
+  for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    const unsigned lin = __ldg(a.plist + e);
+    const int k = (int)(lin / HW);
+    const int z = (int)(lin - (size_t)k * HW), Y = z / G.W, X = z - Y * G.W;
+    const Samp s = asm_sample(G, asm_omega(G, a.omega, k), V.off[k].x, V.off[k].y, Y, X);
+    const size_t r0 = (size_t)s.y0 * G.ps, r1 = (size_t)s.y1 * G.ps;
+    const float p00 = __ldcg(pk + r0 + s.x0), p01 = __ldcg(pk + r0 + s.x1);
+    const float p10 = __ldcg(pk + r1 + s.x0), p11 = __ldcg(pk + r1 + s.x1);
+    const float top = fmaf(s.fx, p01 - p00, p00), bot = fmaf(s.fx, p11 - p10, p10);
+    a.udense[lin] = fmaf(s.fy, bot - top, top);
+  }
+}
+
+// per CG step 3: t = c_A a . p = c_A sum_{u,v} g[u] g[v] u(zeta i + (u, v)) of every irregular row
+// (NP lanes per row, lane = blur row), and <p, M_irr p> = sum t^2 / c_A into the step's <p, q>
+template <int Z>
+__global__ void __launch_bounds__(256) k_asm_irr_t(const Geom G, const AsmStepArgs a) {
+  using C = AsmCfg<Z>;
+  constexpr int NP = C::NP, RPW = 32 / NP;
+  if (a.cg_k >= 2 && a.ctl->cur[S_STOP] != 0.0) return;   // CG stopped
+  const unsigned n = a.count[0];
+  const int lane = threadIdx.x & 31, grp = lane / NP, u = lane - grp * NP - C::R;
+  const unsigned gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwt = (gridDim.x * blockDim.x) >> 5;
+  double tt = 0.0;
+  for (unsigned base = gw * RPW; base < n; base += nwt * RPW) {   // warp-uniform trip count
+    const unsigned e = base + grp;
+    const bool valid = grp < RPW && e < n;
+    float tr = 0.f;
+    int k = 0, iy = 0, ix = 0;
+    if (valid) {
+      const int2 ki = __ldg(a.list + e);
+      k = ki.x;
+      iy = ki.y / G.w;
+      ix = ki.y - iy * G.w;
+      const int Y = Z * iy + u;
+      if (Y >= 0 && Y < G.H) {
+        const float* ur = a.udense + ((size_t)k * G.H + Y) * G.W;
+#pragma unroll
+        for (int v = -C::R; v <= C::R; ++v) {
+          const int X = Z * ix + v;
+          if (X >= 0 && X < G.W) tr = fmaf(G.taps[v + C::R], __ldcg(ur + X), tr);
+        }
+      }
+    }
+    float t = 0.f;   // sum_u g[u] tr_u in u order (the group's lanes)
+#pragma unroll
+    for (int j = 0; j < NP; ++j) t = fmaf(G.taps[j], __shfl_sync(0xffffffffu, tr, min(grp, RPW - 1) * NP + j), t);
+    if (valid && u == -C::R) {
+      const float tv = G.cA * t;
+      a.tdense[((size_t)k * G.h + iy) * G.w + ix] = tv;
+      tt += (double)tv * t;
+    }
+  }
+  // one atomic per CTA (same-address double atomics serialise in L2)
+  __shared__ double s_tt[8];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) tt += __shfl_xor_sync(0xffffffffu, tt, o);
+  if ((threadIdx.x & 31) == 0) s_tt[threadIdx.x >> 5] = tt;
+  __syncthreads();
+  if (threadIdx.x == 0 && a.cg_k >= 1) {
+    double sum = 0.0;
+    for (int w = 0; w < 8; ++w) sum += s_tt[w];
+    if (sum != 0.0) atomicAdd(&a.ctl->cur[S_PQ + a.cg_k], sum);
+  }
+}
+
+// per CG step 4: T(z) = sum_{irregular i: z in win(i)} g g t_i at every position of P_k, scattered
+// bilinearly into q (W_k^T; RED.ADD)
+template <int Z>
+__global__ void __launch_bounds__(256) k_asm_irr_scatter(const Geom G, const Views V, const AsmStepArgs a) {
+  using C = AsmCfg<Z>;
+  if (a.cg_k >= 2 && a.ctl->cur[S_STOP] != 0.0) return;   // CG stopped
+  const unsigned n = a.count[1];
+  const size_t HW = (size_t)G.H * G.W;
+  for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    const unsigned lin = __ldg(a.plist + e);
+    const int k = (int)(lin / HW);
+    const int z = (int)(lin - (size_t)k * HW), Y = z / G.W, X = z - Y * G.W;
+    // LR pixels whose window holds (Y, X): Y = zeta iy + u, X = zeta ix + v, |u|, |v| <= R
+    const float* tk = a.tdense + (size_t)k * G.h * G.w;
+    const int py = Y % Z, px = X % Z;
+    float T = 0.f;
+#pragma unroll
+    for (int u = C::R; u >= -C::R; --u) {   // iy ascending
+      if (((py - u) % Z + Z) % Z != 0) continue;   // compile-time per phase after the branch below
+      const int iy = (Y - u) / Z;
+      if (Y - u < 0 || iy >= G.h) continue;
+      float tr = 0.f;
+#pragma unroll
+      for (int v = C::R; v >= -C::R; --v) {
+        if (((px - v) % Z + Z) % Z != 0) continue;
+        const int ix = (X - v) / Z;
+        if (X - v < 0 || ix >= G.w) continue;
+        tr = fmaf(G.taps[v + C::R], __ldcg(tk + (size_t)iy * G.w + ix), tr);
+      }
+      T = fmaf(G.taps[u + C::R], tr, T);
+    }
+    if (T == 0.f) continue;
+    const Samp s = asm_sample(G, asm_omega(G, a.omega, k), V.off[k].x, V.off[k].y, Y, X);
+    const float a0 = T * (1.f - s.fy), a1 = T * s.fy;
+    float* q0 = a.q + (size_t)s.y0 * G.ps;
+    float* q1 = a.q + (size_t)s.y1 * G.ps;
+    atomicAdd(q0 + s.x0, a0 * (1.f - s.fx));
+    atomicAdd(q0 + s.x1, a0 * s.fx);
+    atomicAdd(q1 + s.x0, a1 * (1.f - s.fx));
+    atomicAdd(q1 + s.x1, a1 * s.fx);
+  }
+}
+
+__device__ __forceinline__ double asm_warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Stencil planes: full window, plane f = (dy + SR) NSW + (dx + SR) holds M_reg[a][a + d]; the
+// setup kernel writes the half d >= 0 (lexicographic) as planes NH - 1 + h and k_asm_mirror fills
+// the other half from the symmetry M[a][a - d] = M[a - d][a].
+template <int Z>
+__global__ void __launch_bounds__(256) k_asm_mirror(const Geom G, float* __restrict__ st, int psS, size_t plane) {
+  using C = AsmCfg<Z>;
+  const size_t npx = (size_t)G.H * G.W;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < npx * (C::NH - 1); i += (size_t)gridDim.x * blockDim.x) {
+    const int h = 1 + (int)(i / npx);
+    const size_t z = i - (size_t)(h - 1) * npx;
+    const int Y = (int)(z / G.W), X = (int)(z - (size_t)Y * G.W);
+    const int dy = hoff_dy<C::NSW, C::SR>(h), dx = hoff_dx<C::NSW, C::SR>(h);
+    const size_t o = (size_t)(Y + kAsmPad) * psS + X + kAsmPad;
+    st[(size_t)(C::NH - 1 - h) * plane + o] = st[(size_t)(C::NH - 1 + h) * plane + o - (ptrdiff_t)dy * psS - dx];
+  }
+}
+
+// q = M_reg p + (th/2) S_W^T S_W p on a 128 x 8 tile: warp = one output row, lane = 4 consecutive
+// pixels (float4 along x).  Per stencil row dy the lane keeps the 20 p values its 4 pixels reach
+// (5 aligned LDS.128 from the shared tile), streams the 2 SR + 1 planes of that row as LDG.128
+// (all in flight) and issues 4 FFMA per plane.
+template <int Z>
+__global__ void __launch_bounds__(256, 2) k_asm_normal(const Geom G, const Views V, const AsmStepArgs a) {
+  using C = AsmCfg<Z>;
+  constexpr int SR = C::SR, NSW = C::NSW, TH = C::TH, TW = C::TW, PC = C::PC, PR = C::PR, MR = C::MR, NT = 256;
+  constexpr int RAD = 2, CX = 8;   // NLTV radius (5 x 5 window); tile column offset (>= SR, mult. of 4)
+  extern __shared__ __align__(16) float sm_an[];
+  float* sp = sm_an;                 // p  rows [-SR, TH + SR), columns [X0 - CX, X0 + TW + CX)
+  float* smm = sp + PR * PC;         // m^2 rows [-RAD, TH + RAD), same columns
+  float* smp = smm + MR * PC;        // m^2 p
+  __shared__ double red[8 * 2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int Y0 = blockIdx.y * TH, X0 = blockIdx.x * TW;
+  const int H = G.H, W = G.W, ps = G.ps;
+  Control* ctl = a.ctl;
+  if (a.cg_k >= 2 && ctl->cur[S_STOP] != 0.0) return;   // CG stopped
+  const float beta = asm_beta(ctl, a.cg_k);
+  double pi0 = 0.0, pq = 0.0;
+
+  // ---- tile load: p = r + beta p_{k-1} (Alg.2 line 10, A2), zero outside Omega; own pixels -> p_out,
+  // pi_0 = <r_0, r_0> at k = 1 (Alg.2 line 3).  Chunks of 4 columns ----
+  const float* src1 = a.cg_k == 0 ? a.p_in : a.r;
+  for (int c = tid; c < PR * (PC / 4); c += NT) {
+    const int py = c / (PC / 4), cx = (c - py * (PC / 4)) * 4;
+    const int gy = Y0 - SR + py, gx = X0 - CX + cx;
+    float v[4];
+    if (gy >= 0 && gy < H && gx >= 0 && gx + 3 < W) {
+      const float4 r4 = __ldg(reinterpret_cast<const float4*>(src1 + (size_t)gy * ps + gx));
+      v[0] = r4.x; v[1] = r4.y; v[2] = r4.z; v[3] = r4.w;
+      if (a.cg_k >= 2) {
+        const float4 q4 = __ldg(reinterpret_cast<const float4*>(a.p_prev + (size_t)gy * ps + gx));
+        v[0] = fmaf(beta, q4.x, v[0]); v[1] = fmaf(beta, q4.y, v[1]);
+        v[2] = fmaf(beta, q4.z, v[2]); v[3] = fmaf(beta, q4.w, v[3]);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const bool in = gy >= 0 && gy < H && gx + e >= 0 && gx + e < W;
+        const size_t gi = in ? (size_t)gy * ps + gx + e : 0;
+        v[e] = in ? __ldg(src1 + gi) : 0.f;
+        if (in && a.cg_k >= 2) v[e] = fmaf(beta, __ldg(a.p_prev + gi), v[e]);
+      }
+    }
+    *reinterpret_cast<float4*>(sp + py * PC + cx) = make_float4(v[0], v[1], v[2], v[3]);
+    if (a.cg_k >= 1 && py >= SR && py < SR + TH && cx >= CX && cx < CX + TW && gy < H) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (gx + e < W) {
+          a.p_out[(size_t)gy * ps + gx + e] = v[e];
+          if (a.cg_k == 1) pi0 += (double)v[e] * v[e];
+        }
+    }
+  }
+  __syncthreads();
+  for (int c = tid; c < MR * PC; c += NT) {
+    const int py = c / PC, px = c - py * PC;
+    const int gy = Y0 - RAD + py, gx = X0 - CX + px;
+    const bool in = gy >= 0 && gy < H && gx >= 0 && gx < W;
+    const float mv = in ? __ldg(a.m + (size_t)gy * ps + gx) : 0.f;
+    const float mm = mv * mv;
+    smm[c] = mm;
+    smp[c] = mm * sp[(py + SR - RAD) * PC + px];
+  }
+  __syncthreads();
+
+  const int ly = warp, Y = Y0 + ly, X = X0 + 4 * lane;
+  if (Y < H) {
+    // ---- data part: the stencil planes, row dy by row dy ----
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    const float* pl = a.st + (size_t)(Y + kAsmPad) * a.psS + X + kAsmPad;   // plane 0 (d = (-SR, -SR)) at (Y, X)
+#pragma unroll 1
+    for (int dy = -SR; dy <= SR; ++dy) {
+      float pv[20];
+      const float* prow = sp + (ly + dy + SR) * PC + 4 * lane;
+#pragma unroll
+      for (int j = 0; j < 5; ++j) {
+        const float4 t = *reinterpret_cast<const float4*>(prow + 4 * j);
+        pv[4 * j] = t.x; pv[4 * j + 1] = t.y; pv[4 * j + 2] = t.z; pv[4 * j + 3] = t.w;
+      }
+      const float* plr = pl + (size_t)((dy + SR) * NSW) * a.plane;
+      float4 cf[NSW];
+#pragma unroll
+      for (int dx = 0; dx < NSW; ++dx) cf[dx] = __ldg(reinterpret_cast<const float4*>(plr + (size_t)dx * a.plane));
+#pragma unroll
+      for (int dx = 0; dx < NSW; ++dx) {   // d = (dy, dx - SR): p at column CX + 4 lane + dx - SR + e
+        acc[0] = fmaf(cf[dx].x, pv[CX + dx - SR + 0], acc[0]);
+        acc[1] = fmaf(cf[dx].y, pv[CX + dx - SR + 1], acc[1]);
+        acc[2] = fmaf(cf[dx].z, pv[CX + dx - SR + 2], acc[2]);
+        acc[3] = fmaf(cf[dx].w, pv[CX + dx - SR + 3], acc[3]);
+      }
+    }
+    // ---- weighted NLTV part (A10): sum_d (p(z) - p(z+d)) (w_d^2 m(z)^2 + w_{-d}^2 m(z+d)^2), z + d in
+    // Omega; A = sum w_d^2 p(z+d), B = sum w_{-d}^2 m^2(z+d), C = sum w_{-d}^2 m^2 p(z+d) ----
+    float A_[4] = {0.f, 0.f, 0.f, 0.f}, B_[4] = {0.f, 0.f, 0.f, 0.f}, C_[4] = {0.f, 0.f, 0.f, 0.f};
+    float W2z[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int dyn = -RAD; dyn <= RAD; ++dyn) {
+      float pv[12], mv[12], cv[12];   // columns CX + 4 lane - 4 .. + 7
+      const float* pr = sp + (ly + dyn + SR) * PC + 4 * lane + 4;
+      const float* mr = smm + (ly + dyn + RAD) * PC + 4 * lane + 4;
+      const float* cr = smp + (ly + dyn + RAD) * PC + 4 * lane + 4;
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const float4 t0 = *reinterpret_cast<const float4*>(pr + 4 * j);
+        const float4 t1 = *reinterpret_cast<const float4*>(mr + 4 * j);
+        const float4 t2 = *reinterpret_cast<const float4*>(cr + 4 * j);
+        pv[4 * j] = t0.x; pv[4 * j + 1] = t0.y; pv[4 * j + 2] = t0.z; pv[4 * j + 3] = t0.w;
+        mv[4 * j] = t1.x; mv[4 * j + 1] = t1.y; mv[4 * j + 2] = t1.z; mv[4 * j + 3] = t1.w;
+        cv[4 * j] = t2.x; cv[4 * j + 1] = t2.y; cv[4 * j + 2] = t2.z; cv[4 * j + 3] = t2.w;
+      }
+      const bool rin = Y + dyn >= 0 && Y + dyn < H;
+#pragma unroll
+      for (int dxn = -RAD; dxn <= RAD; ++dxn) {
+        if (dyn == 0 && dxn == 0) continue;
+        const int lin = (dyn + RAD) * (2 * RAD + 1) + (dxn + RAD);
+        const int d = lin > 12 ? lin - 1 : lin;   // A9 order, centre skipped
+        const float w2 = G.wd[d] * G.wd[d], w2f = G.wd[23 - d] * G.wd[23 - d];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int c = 4 + e + dxn;   // column CX + 4 lane + e + dxn in the 12-value window
+          A_[e] = fmaf(w2, pv[c], A_[e]);
+          B_[e] = fmaf(w2f, mv[c], B_[e]);
+          C_[e] = fmaf(w2f, cv[c], C_[e]);
+          W2z[e] += (rin && X + e + dxn >= 0 && X + e + dxn < W) ? w2 : 0.f;
+        }
+      }
+    }
+    const float* pc = sp + (ly + SR) * PC + CX + 4 * lane;
+    const float* mc = smm + (ly + RAD) * PC + CX + 4 * lane;
+    float qz[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float pz = pc[e], mz = mc[e];
+      qz[e] = acc[e] + G.cS * (pz * fmaf(mz, W2z[e], B_[e]) - fmaf(mz, A_[e], C_[e]));
+      if (a.cg_k >= 1 && X + e < W) pq += (double)pz * qz[e];
+    }
+    float* qo = a.q + (size_t)Y * ps + X;
+    if (X + 3 < W) {
+      *reinterpret_cast<float4*>(qo) = make_float4(qz[0], qz[1], qz[2], qz[3]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (X + e < W) qo[e] = qz[e];
+    }
+  }
+  if (a.cg_k >= 1) {
+    pq = asm_warp_sum(pq);
+    pi0 = asm_warp_sum(pi0);
+    if (lane == 0) {
+      red[warp * 2] = pq;
+      red[warp * 2 + 1] = pi0;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double s0 = 0.0, s1 = 0.0;
+      for (int w = 0; w < 8; ++w) {
+        s0 += red[w * 2];
+        s1 += red[w * 2 + 1];
+      }
+      if (s0 != 0.0) atomicAdd(&ctl->cur[S_PQ + a.cg_k], s0);
+      if (s1 != 0.0) atomicAdd(&ctl->cur[S_PI], s1);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// host launchers
+// ---------------------------------------------------------------------------------------------
+int asm_plane_count(int scale) {   // full stencil window
+  switch (scale) {
+    case 2: return AsmCfg<2>::NF;
+    case 3: return AsmCfg<3>::NF;
+    case 4: return AsmCfg<4>::NF;
+    default: return 0;
+  }
+}
+
+template <int Z>
+static cudaError_t prep_asm() {
+  cudaError_t e;
+  if ((e = cudaFuncSetAttribute(k_asm_stencil<Z>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)AsmCfg<Z>::kSmemStencil)))
+    return e;
+  return cudaFuncSetAttribute(k_asm_normal<Z>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)AsmCfg<Z>::kSmemNormal);
+}
+
+cudaError_t prepare_asm_kernels() {
+  cudaError_t e;
+  if ((e = prep_asm<2>()) || (e = prep_asm<3>()) || (e = prep_asm<4>())) return e;
+  return cudaSuccess;
+}
+
+template <int Z>
+static void asm_build_z(const Geom& G, const Views& V, const AsmBuf& B, float om_max, cudaStream_t st) {
+  using C = AsmCfg<Z>;
+  dim3 gc((G.w + 31) / 32, (G.h + 7) / 8, G.n_views);
+  k_asm_classify<Z><<<gc, dim3(32, 8), 0, st>>>(G, V, B.omega, B.count, B.list, B.pmask, B.pmw);
+  k_asm_plist<<<1184, 256, 0, st>>>(G, B.pmask, B.pmw, B.count + 1, B.plist);
+  dim3 gs((G.W + C::TA - 1) / C::TA, (G.H + C::TA - 1) / C::TA);
+  k_asm_stencil<Z><<<gs, C::NTA, C::kSmemStencil, st>>>(G, V, B.omega, om_max, B.st + (size_t)(C::NH - 1) * B.plane,
+                                                        B.psS, B.plane);
+  k_asm_mirror<Z><<<2048, 256, 0, st>>>(G, B.st, B.psS, B.plane);
+}
+
+cudaError_t launch_asm_build(const Geom& G, const Views& V, const AsmBuf& B, float om_max, cudaStream_t st) {
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(B.count, 0, 2 * sizeof(unsigned), st)) ||
+      (e = cudaMemsetAsync(B.pmask, 0, (size_t)G.n_views * G.H * B.pmw * sizeof(unsigned), st)) ||
+      (e = cudaMemsetAsync(B.tdense, 0, (size_t)G.n_views * G.h * G.w * sizeof(float), st)))
+    return e;
+  switch (G.scale) {
+    case 2: asm_build_z<2>(G, V, B, om_max, st); break;
+    case 3: asm_build_z<3>(G, V, B, om_max, st); break;
+    case 4: asm_build_z<4>(G, V, B, om_max, st); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+template <int Z>
+static void asm_step_z(const Geom& G, const Views& V, const AsmStepArgs& a, bool irr, int num_sms, cudaStream_t st) {
+  using C = AsmCfg<Z>;
+  dim3 g((G.W + C::TW - 1) / C::TW, (G.H + C::TH - 1) / C::TH);
+  k_asm_normal<Z><<<g, 256, C::kSmemNormal, st>>>(G, V, a);
+  if (irr) {
+    k_asm_irr_u<<<num_sms * 8, 256, 0, st>>>(G, V, a);
+    k_asm_irr_t<Z><<<num_sms * 4, 256, 0, st>>>(G, a);
+    k_asm_irr_scatter<Z><<<num_sms * 8, 256, 0, st>>>(G, V, a);
+  }
+}
+
+cudaError_t launch_asm_step(const Geom& G, const Views& V, const AsmBuf& B, const AsmStep& s, bool irr, int num_sms,
+                            cudaStream_t st) {
+  AsmStepArgs a{};
+  a.r = s.r;
+  a.p_prev = s.p_prev;
+  a.p_in = s.p_in;
+  a.p_out = s.p_out;
+  a.m = s.m;
+  a.q = s.q;
+  a.ctl = s.ctl;
+  a.cg_k = s.cg_k;
+  a.omega = B.omega;
+  a.count = B.count;
+  a.list = B.list;
+  a.plist = B.plist;
+  a.tdense = B.tdense;
+  a.udense = B.udense;
+  a.st = B.st;
+  a.psS = B.psS;
+  a.plane = B.plane;
+  a.om_max = B.om_max;
+  switch (G.scale) {
+    case 2: asm_step_z<2>(G, V, a, irr, num_sms, st); break;
+    case 3: asm_step_z<3>(G, V, a, irr, num_sms, st); break;
+    case 4: asm_step_z<4>(G, V, a, irr, num_sms, st); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace lfsr

@@ -53,6 +53,11 @@ cudaError_t launch_wz_nltv(const Geom& G, const float* x, const float* m, float*
 cudaError_t launch_omega_const(const Geom& G, const float* omega, unsigned* flag, cudaStream_t st);
 cudaError_t launch_misr_normal(const Geom& G, const MisrStencil& S, const MisrArgs& a, cudaStream_t st);
 cudaError_t prepare_misr_kernels();
+cudaError_t launch_asm_build(const Geom& G, const Views& V, const AsmBuf& B, float om_max, cudaStream_t st);
+cudaError_t launch_asm_step(const Geom& G, const Views& V, const AsmBuf& B, const AsmStep& s, bool irr, int num_sms,
+                            cudaStream_t st);
+cudaError_t prepare_asm_kernels();
+int asm_plane_count(int scale);
 cudaError_t launch_gd_update(const Geom& G, float* x, const float* g, Control* ctl, const GdCfg& cfg, int num_sms,
                              cudaStream_t st);
 }  // namespace lfsr
@@ -144,6 +149,12 @@ struct lfsr_ctx {
   float* d_misr_tab = nullptr;     // separable form: T_y [H][2WR+1], T_x [W][2WR+1]
   size_t misr_tab_bytes = 0;
   bool misr_border = true;         // the dense form runs the border tiles through k_tile
+  // assembled data normal operator (asm.cu): the regular rows of the stacked A_k as
+  // a stencil per HR pixel, the irregular rows (blur windows across a depth edge) applied as rows
+  bool asmop = false;
+  AsmBuf asmb{};
+  int64_t asm_nirr = -1;           // irregular rows (host copy; -1 = not read back: batch fields)
+  double asm_ms = 0.0;             // wall time of the last assembly (set_observations, synchronised)
   std::string err;
 };
 
@@ -535,6 +546,8 @@ static void free_state(lfsr_ctx* c) {
   c->d_misr_tab = nullptr;
   c->misr_tab_bytes = 0;
   c->misr = false;
+  c->asmop = false;
+  c->asmb = AsmBuf{};
   for (auto& k : c->alloc_key) k = 0;
   c->ready = false;
 }
@@ -585,6 +598,17 @@ lfsr_status lfsr_fast_path(const lfsr_ctx* c, int32_t* active, int32_t* rect) {
     const int32_t v[8] = {a.zs_y0, a.zs_y1, a.zs_x0, a.zs_x1, a.o_y0, a.o_y1, a.o_x0, a.o_x1};
     for (int i = 0; i < 8; ++i) rect[i] = c->misr ? v[i] : 0;
   }
+  return LFSR_OK;
+}
+
+lfsr_status lfsr_normal_path(const lfsr_ctx* c, int32_t* path, int64_t* irregular_rows, int64_t* total_rows,
+                             double* setup_ms) {
+  if (!c || !path) return LFSR_ERR_INVALID_ARG;
+  if (!c->ready) return LFSR_ERR_STATE;
+  *path = c->misr ? 1 : (c->asmop ? 2 : 0);
+  if (irregular_rows) *irregular_rows = c->asmop ? c->asm_nirr : 0;
+  if (total_rows) *total_rows = (int64_t)c->G.n_views * c->G.h * c->G.w;
+  if (setup_ms) *setup_ms = c->asmop ? c->asm_ms : 0.0;
   return LFSR_OK;
 }
 
@@ -1274,6 +1298,94 @@ static lfsr_status misr_normal(lfsr_ctx* c, Part& P, int k, const float* in, flo
   return LFSR_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Assembled data normal operator (asm.cu).  The data part of M does not change
+// during a solve (omega, the blur and the views are fixed), so its regular rows are summed once
+// into a stencil per HR pixel and each CG step streams the stencil instead of re-running the
+// warp / blur / decimate chain and its adjoint for every view.  Used on a single strip with the
+// Gaussian blur and the exact adjoint (the MISR fast path takes constant disparities);
+// LFSR_ASM=0 keeps the direct tile kernel.
+// ---------------------------------------------------------------------------
+static bool asm_wanted(const lfsr_ctx* c) {
+  const Geom& G = c->G;
+  const char* e = getenv("LFSR_ASM");
+  if (e && e[0] == '0') return false;
+  return c->xmode == X_NONE && !G.paper && !G.psf2d && G.radius == 2 && G.s_d == 24 && G.scale >= 2 && G.scale <= 4;
+}
+
+static lfsr_status asm_setup(lfsr_ctx* c, float om_max, bool read_count) {
+  Geom& G = c->G;
+  State& S = c->parts[0].S;
+  c->asmop = false;
+  if (!asm_wanted(c)) return LFSR_OK;
+  const int NH = asm_plane_count(G.scale);   // stencil planes (full window)
+  AsmBuf& B = c->asmb;
+  const int psS = round_up(G.W + 2 * kAsmPad, 32);
+  const size_t plane = (size_t)(G.H + 2 * kAsmPad) * psS;
+  const size_t nrows = (size_t)G.n_views * G.h * G.w;
+  const size_t npos = (size_t)G.n_views * G.H * G.W;
+  const int pmw = (G.W + 31) / 32;
+  if (!B.st) {
+    const size_t need = (size_t)NH * plane * 4 + nrows * 12 + npos * 8 + (size_t)G.n_views * G.H * pmw * 4 + 512;
+    size_t fr = 0, tot = 0;
+    CK(c, cudaMemGetInfo(&fr, &tot));
+    if (need > fr / 2) return LFSR_OK;   // no room: the direct tile kernel
+    void* p = nullptr;
+    cudaError_t e;
+    if ((e = dalloc(c, &p, (size_t)NH * plane * 4)) != cudaSuccess) return cuda_fail(c, e, "alloc");
+    B.st = (float*)p;
+    if ((e = dalloc(c, &p, nrows * 8)) != cudaSuccess) return cuda_fail(c, e, "alloc");
+    B.list = (int2*)p;
+    if ((e = dalloc(c, &p, nrows * 4)) != cudaSuccess) return cuda_fail(c, e, "alloc");
+    B.tdense = (float*)p;
+    if ((e = dalloc(c, &p, npos * 4)) != cudaSuccess) return cuda_fail(c, e, "alloc");
+    B.plist = (unsigned*)p;
+    if ((e = dalloc(c, &p, npos * 4)) != cudaSuccess) return cuda_fail(c, e, "alloc");
+    B.udense = (float*)p;
+    if ((e = dalloc(c, &p, (size_t)G.n_views * G.H * pmw * 4)) != cudaSuccess) return cuda_fail(c, e, "alloc");
+    B.pmask = (unsigned*)p;
+    if ((e = dalloc(c, &p, 64)) != cudaSuccess) return cuda_fail(c, e, "alloc");
+    B.count = (unsigned*)p;
+    B.pmw = pmw;
+    B.psS = psS;
+    B.plane = plane;
+  }
+  B.omega = S.omega;
+  B.om_max = om_max;
+  CK(c, prepare_asm_kernels());
+  const auto t0 = std::chrono::steady_clock::now();
+  CK(c, launch_asm_build(G, c->V, B, om_max, c->stream));
+  c->asm_nirr = -1;
+  if (read_count) {
+    unsigned n = 0;
+    CK(c, cudaMemcpyAsync(&n, B.count, sizeof n, cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+    c->asm_nirr = n;
+    c->asm_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
+  c->asmop = true;
+  return LFSR_OK;
+}
+
+// q = M p through the assembled operator: t of the irregular rows, then the stencil kernel.
+// k >= 1: CG step k of part P (p_k formed and written, pi_0, <p, q>); k = 0: plain operator.
+static lfsr_status asm_normal(lfsr_ctx* c, Part& P, int k, const float* in, float* out, Control* ctl,
+                              cudaStream_t st, int* launches) {
+  AsmStep s{};
+  s.r = P.S.r;
+  s.p_prev = k >= 2 ? P.S.p[(k - 1) & 1] : nullptr;
+  s.p_in = in;
+  s.p_out = k >= 1 ? P.S.p[k & 1] : nullptr;
+  s.m = P.S.m;
+  s.q = out;
+  s.ctl = ctl;
+  s.cg_k = k;
+  const bool irr = c->asm_nirr != 0;
+  CK(c, launch_asm_step(c->G, c->V, c->asmb, s, irr, c->num_sms, st));
+  if (launches) *launches += irr ? 2 : 1;
+  return LFSR_OK;
+}
+
 lfsr_status lfsr_set_observations(lfsr_ctx* c, const float* lr_views, const float* view_offsets,
                                   const float* disparity, lfsr_disp_mode disp_mode, const float* x0, lfsr_mem mem) {
   NvtxRange nvtx_("lfsr_set_observations");
@@ -1416,6 +1528,11 @@ lfsr_status lfsr_set_observations(lfsr_ctx* c, const float* lr_views, const floa
   if (ubits[3] == 0) {
     NvtxRange r_("MISR stencil assembly");
     if ((st = misr_setup(c, omega00)) != LFSR_OK) return st;
+  }
+  c->asmop = false;
+  if (!c->misr) {
+    NvtxRange r_("normal operator assembly");
+    if ((st = asm_setup(c, om_max, true)) != LFSR_OK) return st;
   }
   const auto tg0 = std::chrono::steady_clock::now();
   lfsr_status gs = build_graphs(c);
@@ -1712,8 +1829,11 @@ static lfsr_status enqueue_iteration(lfsr_ctx* c, cudaStream_t st, int parity) {
       Part& P = c->parts[0];
       XC(misr_normal(c, P, k, nullptr, P.S.q, P.S.ctl, st));
       launches += (c->misr_border && c->Tborder.ntl > 0) ? 2 : 1;
+    } else if (c->asmop) {   // the assembled operator (asm.cu)
+      Part& P = c->parts[0];
+      XC(asm_normal(c, P, k, nullptr, P.S.q, P.S.ctl, st, &launches));
     }
-    if (!c->misr) {
+    if (!c->misr && !c->asmop) {
       for (int i = 0; i < np; ++i) pk[i] = c->parts[i].S.p[(k - 1) & 1];
       // the halos of r (and of p_{k-1} from k = 2) for this step's operator, overlapped with the
       // interior tiles (k = 1: r_0 = -v after the wz-step's fold)
@@ -2083,6 +2203,7 @@ static lfsr_status batch_finish(lfsr_ctx* c, const float* off, const Views& V2) 
   CK(c, launch_setup_wo(G, c->V, S.y, S.omega, S.wo, c->stream));
   CK(c, launch_weights(G, S.x, S.wo, S.m, c->stream));
   if (tune && (st = tune_tile_bl(c)) != LFSR_OK) return st;
+  if (c->asmop && (st = asm_setup(c, om_max, false)) != LFSR_OK) return st;   // this field's operator
   if ((st = build_graphs(c)) != LFSR_OK) return st;
   c->ready = true;
   return LFSR_OK;
@@ -2364,6 +2485,8 @@ lfsr_status lfsr_op_apply(lfsr_ctx* c, lfsr_op op, const float* in, float* out, 
       io.do_nltv = 1;
       if (c->misr) {
         if ((st = misr_normal(c, P0, 0, S.tmp_hr, c->tmp_hr2, S.ctl, s)) != LFSR_OK) return st;
+      } else if (c->asmop) {
+        if ((st = asm_normal(c, P0, 0, S.tmp_hr, c->tmp_hr2, S.ctl, s, nullptr)) != LFSR_OK) return st;
       } else {
         CK(c, launch_tile(MODE_NORMAL, G, c->V, T, io, s));
       }

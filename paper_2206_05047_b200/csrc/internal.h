@@ -174,6 +174,36 @@ struct MisrArgs {
   int o_y0, o_y1, o_x0, o_x1;       // pixels not owned by a border tile (p_out, pi_0)
 };
 
+// Assembled data normal operator (asm.cu): the stencil planes of the regular
+// rows of the stacked A_k, the irregular rows as a compact list with per-tile CSR lists, per-row t.
+constexpr int kAsmPad = 8;   // zero rows / columns around every stencil plane (>= the stencil radius)
+
+struct AsmBuf {
+  const float* omega;   // disparity (shared [H][ps] or per view)
+  float* st;            // [NH][H + 2 pad][psS] stencil planes (c_A folded in)
+  int psS;              // plane row pitch (floats)
+  size_t plane;         // floats per plane
+  unsigned* count;      // [0] irregular rows, [1] positions in their windows (device)
+  int2* list;           // [n_views h w] irregular rows (k, iy w + ix), first count[0] valid
+  unsigned* pmask;      // [n_views][H][pmw] positions in an irregular row's blur window
+  int pmw;
+  unsigned* plist;      // [n_views H W] those positions, k H W + Y W + X, first count[1] valid
+  float* tdense;        // [n_views][h][w] t = c_A a . p of the irregular rows (0 at regular rows)
+  float* udense;        // [n_views][H][W] u = W_k p at the positions (per CG step)
+  float om_max;         // max |omega| (footprints)
+};
+
+struct AsmStep {
+  const float* r;       // CG residual (k >= 1)
+  const float* p_prev;  // p_{k-1} (k >= 2)
+  const float* p_in;    // k = 0: the operator input
+  float* p_out;         // k >= 1: p_k
+  const float* m;       // NLTV weight map
+  float* q;             // output (stored)
+  Control* ctl;
+  int cg_k;
+};
+
 // gd / gd-ls configuration of one iteration graph (readings A30-A33).
 struct GdCfg {
   float eta0;        // (initial) step

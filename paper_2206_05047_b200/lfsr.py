@@ -34,7 +34,7 @@ EXPORTS = ("lfsr_create", "lfsr_set_observations", "lfsr_admm_run", "lfsr_admm_e
            "lfsr_get_hr", "lfsr_get_state", "lfsr_op_apply", "lfsr_launches_per_iter", "lfsr_tile_config", "lfsr_profile",
            "lfsr_profile_read", "lfsr_strip_plan", "lfsr_destroy", "lfsr_last_error", "lfsr_abi_version",
            "lfsr_gd_run", "lfsr_gd_launches_per_iter", "lfsr_rgb_to_ycbcr", "lfsr_ycbcr_to_rgb", "lfsr_solve_batch",
-           "lfsr_get_stream", "lfsr_fast_path")
+           "lfsr_get_stream", "lfsr_fast_path", "lfsr_normal_path")
 
 
 class LFSRError(RuntimeError):
@@ -131,6 +131,9 @@ def load_library(path: str = LIB_PATH):
     lib.lfsr_tile_config.restype = st
     lib.lfsr_fast_path.argtypes = [vp, i32p, i32p]
     lib.lfsr_fast_path.restype = st
+    lib.lfsr_normal_path.argtypes = [vp, i32p, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64),
+                                     ctypes.POINTER(ctypes.c_double)]
+    lib.lfsr_normal_path.restype = st
     lib.lfsr_destroy.argtypes = [vp]
     lib.lfsr_destroy.restype = None
     lib.lfsr_last_error.argtypes = [vp]
@@ -444,6 +447,16 @@ class Solver:
         rect = (ctypes.c_int32 * 8)()
         self._check(self.lib.lfsr_fast_path(self._h, ctypes.byref(act), rect))
         return {"misr": bool(act.value), "zs": tuple(rect[:4]), "owned": tuple(rect[4:])}
+
+    @property
+    def normal_path(self) -> dict:
+        """lfsr_normal_path: which implementation applies the CG operator (0 tile kernel, 1 MISR,
+        2 assembled), the irregular / total row counts and the assembly time."""
+        path, nirr, ntot, ms = ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_double()
+        self._check(self.lib.lfsr_normal_path(self._h, ctypes.byref(path), ctypes.byref(nirr), ctypes.byref(ntot),
+                                              ctypes.byref(ms)))
+        return {"path": int(path.value), "name": ("tile", "misr", "assembled")[path.value],
+                "irregular_rows": int(nirr.value), "total_rows": int(ntot.value), "setup_ms": float(ms.value)}
 
     @property
     def tile_config(self) -> dict:

@@ -26,6 +26,10 @@ s = L.Solver(p, stream=stream.cuda_stream)
 om = S.per_view_disparity(lf.omega, lf.n_views, amp=0.2, seed=3) if per_view else lf.omega
 s.set_observations(*[torch.from_numpy(a).cuda() for a in (lf.y, lf.view_offsets, om)])
 s.admm_run(2)
+try:
+    print("normal path:", s.normal_path, flush=True)
+except Exception as ex:   # older library
+    print("normal path: n/a", ex)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 # plain graph replay first (no per-kernel events: they would split programmatic launch edges)
 e0.record(stream); s.admm_enqueue(iters); e1.record(stream); e1.synchronize()
