@@ -78,15 +78,22 @@ struct Samp {
   float fy, fx;
 };
 __device__ __forceinline__ Samp asm_sample(const Geom& G, const float* om, float drho, float dtau, int Y, int X) {
+  // integer and fractional parts of the shift d = dtheta omega in fp32 at its own (small) magnitude,
+  // the integer part added to the pixel index: absolute fp32 coordinates near 2048 would keep only
+  // ~12 fraction bits.  clamp(z + d, 0, N - 1) (A12/A13) in index form: below 0 -> cell 0, weight 0;
+  // at or past N - 1 -> cell N - 1, weight 0.
   const float o = __ldg(om + (size_t)Y * G.ps + X);
-  const float sy = fminf(fmaxf(fmaf(dtau, o, (float)Y), 0.f), (float)(G.H - 1));
-  const float sx = fminf(fmaxf(fmaf(drho, o, (float)X), 0.f), (float)(G.W - 1));
-  const float by = floorf(sy), bx = floorf(sx);
+  const float dy = dtau * o, dx = drho * o;
+  const float fdy = floorf(dy), fdx = floorf(dx);
   Samp s;
-  s.y0 = (int)by;
-  s.x0 = (int)bx;
-  s.fy = sy - by;
-  s.fx = sx - bx;
+  s.y0 = Y + (int)fdy;
+  s.x0 = X + (int)fdx;
+  s.fy = dy - fdy;
+  s.fx = dx - fdx;
+  if (s.y0 < 0) { s.y0 = 0; s.fy = 0.f; }
+  else if (s.y0 >= G.H - 1) { s.y0 = G.H - 1; s.fy = 0.f; }
+  if (s.x0 < 0) { s.x0 = 0; s.fx = 0.f; }
+  else if (s.x0 >= G.W - 1) { s.x0 = G.W - 1; s.fx = 0.f; }
   s.y1 = min(s.y0 + 1, G.H - 1);
   s.x1 = min(s.x0 + 1, G.W - 1);
   return s;

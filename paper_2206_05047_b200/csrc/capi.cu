@@ -1382,7 +1382,7 @@ static lfsr_status asm_normal(lfsr_ctx* c, Part& P, int k, const float* in, floa
   s.cg_k = k;
   const bool irr = c->asm_nirr != 0;
   CK(c, launch_asm_step(c->G, c->V, c->asmb, s, irr, c->num_sms, st));
-  if (launches) *launches += irr ? 2 : 1;
+  if (launches) *launches += irr ? 4 : 1;   // k_asm_normal [+ k_asm_irr_u, _t, _scatter]
   return LFSR_OK;
 }
 

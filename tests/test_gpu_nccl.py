@@ -17,6 +17,14 @@ import lfsr_synth as S
 from test_gpu_parity import oparams, rel_l2, ITER_TOL
 
 pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True)
+def _tile_kernel_reference(monkeypatch):
+    """The single-strip reference runs the same operator implementation as the strips (the fused
+    tile kernel), so the comparison isolates the decomposition (the assembled operator, which only
+    a single strip uses, is compared with the tile kernel in test_gpu_asm.py)."""
+    monkeypatch.setenv("LFSR_ASM", "0")
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 RANK_SCRIPT = textwrap.dedent(r'''

@@ -329,7 +329,9 @@ def test_error_paths(lfsr_mod):
     assert ei.value.status == 7
     s.set_observations(lf.y, lf.view_offsets, lf.omega)
     assert len(s.admm_run(2)) == 2
-    assert s.launches_per_iter == 1 + 2 * p.cg_max_iters
+    npth = s.normal_path   # CG operator: tile kernel (1 launch) or assembled (1, + 3 with irregular rows)
+    per_step = 1 if npth["name"] == "tile" else (4 if npth["irregular_rows"] else 1)
+    assert s.launches_per_iter == 1 + (per_step + 1) * p.cg_max_iters
 
 
 def test_divergence_guard(lfsr_mod):

@@ -11,6 +11,14 @@ from test_gpu_parity import check_iterates, oparams, rel_l2
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True)
+def _tile_kernel_reference(monkeypatch):
+    """The single-strip reference runs the same operator implementation as the strips (the fused
+    tile kernel), so the comparison isolates the decomposition (the assembled operator, which only
+    a single strip uses, is compared with the tile kernel in test_gpu_asm.py)."""
+    monkeypatch.setenv("LFSR_ASM", "0")
+
+
 def solve(L, lf, n, omega=None, **over):
     d = S.SolverDefaults()
     p = L.Params(n_views=lf.n_views, lr_height=lf.y.shape[1], lr_width=lf.y.shape[2], scale=lf.scale,
