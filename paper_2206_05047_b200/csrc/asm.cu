@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(256) k_asm_classify(const Geom G, const Views 
   if (lane == 0) base = atomicAdd(count, (unsigned)__popc(b));
   base = __shfl_sync(0xffffffffu, base, 0);
   if (!irr) return;
-  list[base + __popc(b & ((1u << lane) - 1u))] = make_int2(k, iy * G.w + ix);
+  list[base + __popc(b & ((1u << lane) - 1u))] = make_int2(k, (iy << 16) | ix);
   // the HR positions of the row's blur window (inside Omega) join the position set P_k
   for (int u = -C::R; u <= C::R; ++u) {
     const int Y = Z * iy + u;
@@ -162,9 +162,9 @@ __global__ void __launch_bounds__(256) k_asm_classify(const Geom G, const Views 
   }
 }
 
-// setup 2: P_k as a compact list of linear indices k H W + Y W + X (warp ballots over the mask)
+// setup 2: P_k as a compact list (k, Y << 16 | X) (warp ballots over the mask)
 __global__ void __launch_bounds__(256) k_asm_plist(const Geom G, const unsigned* __restrict__ pmask, int pmw,
-                                                   unsigned* count, unsigned* __restrict__ plist) {
+                                                   unsigned* count, uint2* __restrict__ plist) {
   const size_t nwords = (size_t)G.n_views * G.H * pmw;
   const int lane = threadIdx.x & 31;
   for (size_t w0 = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) & ~(size_t)31; w0 < nwords;
@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(256) k_asm_plist(const Geom G, const unsigned*
       const int bpos = __ffs(wb) - 1;
       wb &= wb - 1;
       const size_t k = row / G.H, Y = row - k * G.H;
-      plist[base++] = (unsigned)(k * G.H * G.W + Y * G.W + xw + bpos);
+      plist[base++] = make_uint2((unsigned)k, ((unsigned)Y << 16) | (unsigned)(xw + bpos));
     }
   }
 }
@@ -318,7 +318,7 @@ struct AsmStepArgs {
   const float* omega;
   const unsigned* count; // [0] irregular rows, [1] positions of their windows (device)
   const int2* list;      // irregular rows (k, iy * w + ix)
-  const unsigned* plist; // the positions P_k, k H W + Y W + X
+  const uint2* plist;    // the positions P_k, (k, Y << 16 | X)
   float* tdense;         // [n_views][h][w] t of the irregular rows (0 elsewhere)
   float* udense;         // [n_views][H][W] u = W_k p at the positions of P_k
   const float* st;       // stencil planes
@@ -339,17 +339,15 @@ __global__ void __launch_bounds__(256) k_asm_irr_u(const Geom G, const Views V, 
   if (a.cg_k >= 2 && a.ctl->cur[S_STOP] != 0.0) return;   // CG stopped
   const float* pk = asm_pk(a);
   const unsigned n = a.count[1];
-  const size_t HW = (size_t)G.H * G.W;
   for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
-    const unsigned lin = __ldg(a.plist + e);
-    const int k = (int)(lin / HW);
-    const int z = (int)(lin - (size_t)k * HW), Y = z / G.W, X = z - Y * G.W;
+    const uint2 kz = __ldg(a.plist + e);
+    const int k = (int)kz.x, Y = (int)(kz.y >> 16), X = (int)(kz.y & 0xffffu);
     const Samp s = asm_sample(G, asm_omega(G, a.omega, k), V.off[k].x, V.off[k].y, Y, X);
     const size_t r0 = (size_t)s.y0 * G.ps, r1 = (size_t)s.y1 * G.ps;
     const float p00 = __ldcg(pk + r0 + s.x0), p01 = __ldcg(pk + r0 + s.x1);
     const float p10 = __ldcg(pk + r1 + s.x0), p11 = __ldcg(pk + r1 + s.x1);
     const float top = fmaf(s.fx, p01 - p00, p00), bot = fmaf(s.fx, p11 - p10, p10);
-    a.udense[lin] = fmaf(s.fy, bot - top, top);
+    a.udense[((size_t)k * G.H + Y) * G.W + X] = fmaf(s.fy, bot - top, top);
   }
 }
 
@@ -372,8 +370,8 @@ __global__ void __launch_bounds__(256) k_asm_irr_t(const Geom G, const AsmStepAr
     if (valid) {
       const int2 ki = __ldg(a.list + e);
       k = ki.x;
-      iy = ki.y / G.w;
-      ix = ki.y - iy * G.w;
+      iy = ki.y >> 16;
+      ix = ki.y & 0xffff;
       const int Y = Z * iy + u;
       if (Y >= 0 && Y < G.H) {
         const float* ur = a.udense + ((size_t)k * G.H + Y) * G.W;
@@ -411,31 +409,23 @@ __global__ void __launch_bounds__(256) k_asm_irr_t(const Geom G, const AsmStepAr
 template <int Z>
 __global__ void __launch_bounds__(256) k_asm_irr_scatter(const Geom G, const Views V, const AsmStepArgs a) {
   using C = AsmCfg<Z>;
+  __shared__ float s_g[2 * C::R + 1];
+  if (threadIdx.x <= 2 * C::R) s_g[threadIdx.x] = G.taps[threadIdx.x];
+  __syncthreads();
   if (a.cg_k >= 2 && a.ctl->cur[S_STOP] != 0.0) return;   // CG stopped
   const unsigned n = a.count[1];
-  const size_t HW = (size_t)G.H * G.W;
   for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
-    const unsigned lin = __ldg(a.plist + e);
-    const int k = (int)(lin / HW);
-    const int z = (int)(lin - (size_t)k * HW), Y = z / G.W, X = z - Y * G.W;
-    // LR pixels whose window holds (Y, X): Y = zeta iy + u, X = zeta ix + v, |u|, |v| <= R
+    const uint2 kz = __ldg(a.plist + e);
+    const int k = (int)kz.x, Y = (int)(kz.y >> 16), X = (int)(kz.y & 0xffffu);
+    // LR pixels whose window holds (Y, X): |zeta i - Y| <= R per axis
+    const int iy0 = max(0, cdiv(Y - C::R, Z)), iy1 = min(G.h - 1, fdiv(Y + C::R, Z));
+    const int ix0 = max(0, cdiv(X - C::R, Z)), ix1 = min(G.w - 1, fdiv(X + C::R, Z));
     const float* tk = a.tdense + (size_t)k * G.h * G.w;
-    const int py = Y % Z, px = X % Z;
     float T = 0.f;
-#pragma unroll
-    for (int u = C::R; u >= -C::R; --u) {   // iy ascending
-      if (((py - u) % Z + Z) % Z != 0) continue;   // compile-time per phase after the branch below
-      const int iy = (Y - u) / Z;
-      if (Y - u < 0 || iy >= G.h) continue;
+    for (int iy = iy0; iy <= iy1; ++iy) {
       float tr = 0.f;
-#pragma unroll
-      for (int v = C::R; v >= -C::R; --v) {
-        if (((px - v) % Z + Z) % Z != 0) continue;
-        const int ix = (X - v) / Z;
-        if (X - v < 0 || ix >= G.w) continue;
-        tr = fmaf(G.taps[v + C::R], __ldcg(tk + (size_t)iy * G.w + ix), tr);
-      }
-      T = fmaf(G.taps[u + C::R], tr, T);
+      for (int ix = ix0; ix <= ix1; ++ix) tr = fmaf(s_g[X - Z * ix + C::R], __ldcg(tk + (size_t)iy * G.w + ix), tr);
+      T = fmaf(s_g[Y - Z * iy + C::R], tr, T);
     }
     if (T == 0.f) continue;
     const Samp s = asm_sample(G, asm_omega(G, a.omega, k), V.off[k].x, V.off[k].y, Y, X);
@@ -477,7 +467,7 @@ __global__ void __launch_bounds__(256) k_asm_mirror(const Geom G, float* __restr
 // (5 aligned LDS.128 from the shared tile), streams the 2 SR + 1 planes of that row as LDG.128
 // (all in flight) and issues 4 FFMA per plane.
 template <int Z>
-__global__ void __launch_bounds__(256, 2) k_asm_normal(const Geom G, const Views V, const AsmStepArgs a) {
+__global__ void __launch_bounds__(256, 3) k_asm_normal(const Geom G, const Views V, const AsmStepArgs a) {
   using C = AsmCfg<Z>;
   constexpr int SR = C::SR, NSW = C::NSW, TH = C::TH, TW = C::TW, PC = C::PC, PR = C::PR, MR = C::MR, NT = 256;
   constexpr int RAD = 2, CX = 8;   // NLTV radius (5 x 5 window); tile column offset (>= SR, mult. of 4)
@@ -702,7 +692,7 @@ static void asm_step_z(const Geom& G, const Views& V, const AsmStepArgs& a, bool
   k_asm_normal<Z><<<g, 256, C::kSmemNormal, st>>>(G, V, a);
   if (irr) {
     k_asm_irr_u<<<num_sms * 8, 256, 0, st>>>(G, V, a);
-    k_asm_irr_t<Z><<<num_sms * 4, 256, 0, st>>>(G, a);
+    k_asm_irr_t<Z><<<num_sms * 16, 256, 0, st>>>(G, a);
     k_asm_irr_scatter<Z><<<num_sms * 8, 256, 0, st>>>(G, V, a);
   }
 }

@@ -1310,7 +1310,8 @@ static bool asm_wanted(const lfsr_ctx* c) {
   const Geom& G = c->G;
   const char* e = getenv("LFSR_ASM");
   if (e && e[0] == '0') return false;
-  return c->xmode == X_NONE && !G.paper && !G.psf2d && G.radius == 2 && G.s_d == 24 && G.scale >= 2 && G.scale <= 4;
+  return c->xmode == X_NONE && !G.paper && !G.psf2d && G.radius == 2 && G.s_d == 24 && G.scale >= 2 && G.scale <= 4 &&
+         G.H < 65536 && G.W < 65536;   // (y << 16 | x) packing of the irregular lists
 }
 
 static lfsr_status asm_setup(lfsr_ctx* c, float om_max, bool read_count) {
@@ -1326,7 +1327,7 @@ static lfsr_status asm_setup(lfsr_ctx* c, float om_max, bool read_count) {
   const size_t npos = (size_t)G.n_views * G.H * G.W;
   const int pmw = (G.W + 31) / 32;
   if (!B.st) {
-    const size_t need = (size_t)NH * plane * 4 + nrows * 12 + npos * 8 + (size_t)G.n_views * G.H * pmw * 4 + 512;
+    const size_t need = (size_t)NH * plane * 4 + nrows * 12 + npos * 12 + (size_t)G.n_views * G.H * pmw * 4 + 512;
     size_t fr = 0, tot = 0;
     CK(c, cudaMemGetInfo(&fr, &tot));
     if (need > fr / 2) return LFSR_OK;   // no room: the direct tile kernel
@@ -1338,8 +1339,8 @@ static lfsr_status asm_setup(lfsr_ctx* c, float om_max, bool read_count) {
     B.list = (int2*)p;
     if ((e = dalloc(c, &p, nrows * 4)) != cudaSuccess) return cuda_fail(c, e, "alloc");
     B.tdense = (float*)p;
-    if ((e = dalloc(c, &p, npos * 4)) != cudaSuccess) return cuda_fail(c, e, "alloc");
-    B.plist = (unsigned*)p;
+    if ((e = dalloc(c, &p, npos * 8)) != cudaSuccess) return cuda_fail(c, e, "alloc");
+    B.plist = (uint2*)p;
     if ((e = dalloc(c, &p, npos * 4)) != cudaSuccess) return cuda_fail(c, e, "alloc");
     B.udense = (float*)p;
     if ((e = dalloc(c, &p, (size_t)G.n_views * G.H * pmw * 4)) != cudaSuccess) return cuda_fail(c, e, "alloc");

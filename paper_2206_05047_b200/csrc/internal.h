@@ -184,10 +184,10 @@ struct AsmBuf {
   int psS;              // plane row pitch (floats)
   size_t plane;         // floats per plane
   unsigned* count;      // [0] irregular rows, [1] positions in their windows (device)
-  int2* list;           // [n_views h w] irregular rows (k, iy w + ix), first count[0] valid
+  int2* list;           // [n_views h w] irregular rows (k, iy << 16 | ix), first count[0] valid
   unsigned* pmask;      // [n_views][H][pmw] positions in an irregular row's blur window
   int pmw;
-  unsigned* plist;      // [n_views H W] those positions, k H W + Y W + X, first count[1] valid
+  uint2* plist;         // [n_views H W] those positions (k, Y << 16 | X), first count[1] valid
   float* tdense;        // [n_views][h][w] t = c_A a . p of the irregular rows (0 at regular rows)
   float* udense;        // [n_views][H][W] u = W_k p at the positions (per CG step)
   float om_max;         // max |omega| (footprints)
