@@ -248,9 +248,13 @@ def run_reference(args, cfg, d, rank):
 
 
 # ----------------------------------------------------------------------------- ours
-def roofline_for(cfg, d, kms, kn, t_ms, steps, share, clk_hz):
-    """Roofline of the dominant kernel (the CG normal-operator tile kernel) from the per-kernel
-    CUDA-event times of the profiled region, plus the streaming kernels' HBM fractions."""
+def roofline_for(cfg, d, kms, kn, t_ms, steps, share, clk_hz, npath=None, split=None):
+    """Roofline of the dominant kernel from the per-kernel CUDA-event times of the profiled region,
+    plus the other kernels' fractions.  Tile-kernel CG operator: k_tile<NORMAL> (FP32 / LSU / issue).
+    Assembled CG operator: the kernel with the largest share of the step among the
+    wz-step tile kernel (FP32), the stencil kernel k_asm_normal (HBM) and the irregular-row kernels."""
+    if npath and npath.get("name") == "assembled" and split and split[1] > 0:
+        return roofline_assembled(cfg, d, kms, kn, t_ms, steps, share, clk_hz, npath, split)
     alg = algorithmic(cfg, d)
     hbm_peak, fp32_peak, peak_src, _ = peaks()
     k_normal_ms = kms[1] / max(kn[1], 1)
@@ -300,6 +304,54 @@ def roofline_for(cfg, d, kms, kn, t_ms, steps, share, clk_hz):
     return roofline
 
 
+def roofline_assembled(cfg, d, kms, kn, t_ms, steps, share, clk_hz, npath, split):
+    alg = algorithmic(cfg, d)
+    hbm_peak, fp32_peak, peak_src, _ = peaks()
+    rec, rec_src = ncu_record(cfg.name)
+    p = cfg.H * cfg.W
+    z = cfg.scale
+    R = math.ceil(3 * 0.25 * math.sqrt(z * z - 1))
+    nf = (2 * (2 * R + 1) + 1) ** 2                       # stencil planes (full (2 SR + 1)^2 window)
+    sms, n = split
+    k_st_ms, k_irr_ms = sms[0] / max(n, 1), sms[1] / max(n, 1)
+    k_wz_ms, k_upd_ms = kms[0] / max(kn[0], 1), kms[2] / max(kn[2], 1)
+    st_bytes = 4 * p * (nf + 5)                           # planes + r, p_{k-1}, m (read), p_k, q (write)
+    tot = max(sum(kms), 1e-9)
+    stencil = {"bound": "hbm", "kernel": "k_asm_normal (assembled CG operator: %d stencil planes + NLTV, a8)" % nf,
+               "achieved": st_bytes / (k_st_ms / 1000.0) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+               "frac": st_bytes / (k_st_ms / 1000.0) / 1e9 / hbm_peak, "traffic": rec.get("k_asm_normal_dram_bytes"),
+               "algorithmic_bytes_per_launch": st_bytes, "avg_launch_ms": k_st_ms, "share_of_step": sms[0] / tot,
+               "peak_source": "HBM copy bandwidth, %s" % peak_src}
+    wz_ach = alg["wz_flops"] / (k_wz_ms / 1000.0) / 1e12
+    wz = {"bound": "alu", "kernel": "k_tile<WZ> (wz-step: weights, A_k / A_k^T over all views, shrink, duals, a2-a7)",
+          "achieved": wz_ach, "peak": fp32_peak, "unit": "TFLOP/s", "frac": wz_ach / fp32_peak,
+          "traffic": rec.get("k_tile_wz_dram_bytes"), "algorithmic_flops_per_launch": alg["wz_flops"],
+          "avg_launch_ms": k_wz_ms, "share_of_step": kms[0] / tot,
+          "hbm_gbs": alg["wz_bytes"] / (k_wz_ms / 1000.0) / 1e9,
+          "hbm_frac": alg["wz_bytes"] / (k_wz_ms / 1000.0) / 1e9 / hbm_peak,
+          "peak_source": "FP32 CUDA cores, 148 SM x 128 lanes x 2 x sm_max_mhz (%s)" % peak_src}
+    irr = {"kernels": "k_asm_irr_u + k_asm_irr_t + k_asm_irr_scatter (rows across depth edges, applied as rows)",
+           "avg_pass_ms": k_irr_ms, "share_of_step": sms[1] / tot, "irregular_rows": npath.get("irregular_rows"),
+           "total_rows": npath.get("total_rows")}
+    dom = stencil if sms[0] >= kms[0] else wz
+    roofline = dict(dom)
+    roofline.update({
+        "timing": "per-kernel CUDA events on the library stream over a second timed region of the same %d steps" % steps,
+        "ncu_counters": rec_src,
+        "stencil_kernel" if dom is wz else "wz_step": stencil if dom is wz else wz,
+        "irregular_rows": irr,
+        "normal_operator_pass_ms": kms[1] / max(kn[1], 1),
+        "cg_update": {"avg_launch_ms": k_upd_ms, "alg_bytes": 4 * p * 7,
+                      "hbm_gbs": 4 * p * 7 / (k_upd_ms / 1000.0) / 1e9,
+                      "hbm_frac": 4 * p * 7 / (k_upd_ms / 1000.0) / 1e9 / hbm_peak,
+                      "traffic": rec.get("k_cg_update_dram_bytes")},
+        "iteration_alg_bytes": alg["iter_bytes"],
+        "iteration_hbm_gbs": alg["iter_bytes"] * steps / (t_ms / 1000.0) / 1e9 / share,
+        "iteration_hbm_frac": alg["iter_bytes"] * steps / (t_ms / 1000.0) / 1e9 / share / hbm_peak,
+        "hbm_peak_gbs": hbm_peak})
+    return roofline
+
+
 def time_steps(sol, stream, steps, do_flush, barrier):
     """`steps` plain graph replays, one CUDA event pair per step (flush outside the events),
     then the same steps with the library's per-kernel events (the roofline region)."""
@@ -328,8 +380,9 @@ def time_steps(sol, stream, steps, do_flush, barrier):
     barrier()
     t_prof_ms = sum(a.elapsed_time(b) for a, b in evp)
     kms, kn = sol.profile_read()
+    split = sol.profile_read_split()   # assembled CG operator: (stencil kernel, irregular rows) ms
     sol.profile(False)
-    return t_ms, t_prof_ms, kms, kn
+    return t_ms, t_prof_ms, kms, kn, split
 
 
 def extra_config(name, steps, warmup, do_flush, barrier, local, clk_hz, multi_world=1, rank=0):
@@ -354,7 +407,7 @@ def extra_config(name, steps, warmup, do_flush, barrier, local, clk_hz, multi_wo
             do_flush()
             sol.admm_enqueue(1)
         sol.admm_stats(1, warmup)
-        t_ms, t_prof_ms, kms, kn = time_steps(sol, stream, steps, do_flush, barrier)
+        t_ms, t_prof_ms, kms, kn, split = time_steps(sol, stream, steps, do_flush, barrier)
         st = sol.admm_stats(warmup + 1, steps)
         if multi_world > 1:
             tt = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
@@ -366,7 +419,8 @@ def extra_config(name, steps, warmup, do_flush, barrier, local, clk_hz, multi_wo
                "final_J": st[-1]["J"], "cg_iters": st[-1]["cg_iters"]}
         if kn[1] > 0:
             rec["kernel_ms_per_launch"] = {"wz": kms[0] / kn[0], "normal": kms[1] / kn[1], "cg_update": kms[2] / kn[2]}
-            rec["roofline"] = roofline_for(cfg, d, kms, kn, t_ms, steps, 1, clk_hz)
+            rec["normal_path"] = sol.normal_path
+            rec["roofline"] = roofline_for(cfg, d, kms, kn, t_ms, steps, 1, clk_hz, rec["normal_path"], split)
         sol.close()
     del lf
     return rec
@@ -436,6 +490,7 @@ def main():
     sol = L.Solver(p, stream=stream.cuda_stream)
     dev_in = [torch.from_numpy(a).cuda() for a in (lf.y, lf.view_offsets, lf.omega)]
     sol.set_observations(*dev_in)
+    npath = sol.normal_path   # which CG-operator implementation runs (tile kernel / MISR / assembled)
     flush = None if args.no_flush else torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
     def do_flush():
@@ -451,7 +506,7 @@ def main():
     clocks.start()
     # timed region 1 (the `value`): plain graph replays; region 2 (the roofline): the same steps with
     # an event after every kernel (~8 % slower at C3, so it only supplies per-kernel times)
-    t_ms, t_prof_ms, kms, kn = time_steps(sol, stream, args.steps, do_flush, barrier)
+    t_ms, t_prof_ms, kms, kn, split = time_steps(sol, stream, args.steps, do_flush, barrier)
     clk = clocks.stop()
     stats = sol.admm_stats(first, args.steps)   # raises on divergence
     sol.admm_stats(first + args.steps, args.steps)
@@ -538,10 +593,10 @@ def main():
                    "sequential": seq}
         del hosts
 
-    # ---- roofline of the dominant kernel (the CG normal-operator tile kernel)
+    # ---- roofline of the dominant kernel
     _, _, _, clk_hz = peaks()
     if kn[1] > 0:
-        roofline = roofline_for(cfg, d, kms, kn, t_max, args.steps, world if strips else 1, clk_hz)
+        roofline = roofline_for(cfg, d, kms, kn, t_max, args.steps, world if strips else 1, clk_hz, npath, split)
         roofline["timing"] += " (%.4f ms/step with the events; `value` is the region without them)" % (
             t_prof_ms / args.steps)
         k_normal_ms, k_wz_ms, k_upd_ms = (kms[1] / kn[1], kms[0] / max(kn[0], 1), kms[2] / max(kn[2], 1))
@@ -611,6 +666,7 @@ def main():
                            else "dp%d (independent light fields per rank)" % world},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches,
+                "normal_path": npath,
                 "clocks": clk,
                 "kernel_ms_per_launch": {"wz": k_wz_ms, "normal": k_normal_ms, "cg_update": k_upd_ms},
                 "final_J": stats[-1]["J"], "cg_iters": stats[-1]["cg_iters"],

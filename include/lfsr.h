@@ -187,6 +187,10 @@ LFSR_API lfsr_status lfsr_admm_stats(lfsr_ctx* ctx, int32_t first_iter, int32_t 
  * ms[2] CG update; launches[i] = number of kernel launches accumulated. */
 LFSR_API lfsr_status lfsr_profile(lfsr_ctx* ctx, int32_t enable);
 LFSR_API lfsr_status lfsr_profile_read(lfsr_ctx* ctx, double* ms /*[3]*/, int64_t* launches /*[3]*/);
+/* With the assembled CG operator (lfsr_normal_path == 2), the split of ms[1] above: ms[0] the
+ * stencil kernel (k_asm_normal), ms[1] the irregular-row kernels; passes = CG operator passes
+ * accumulated (0 on the other paths).  Reset by lfsr_profile. */
+LFSR_API lfsr_status lfsr_profile_read_split(lfsr_ctx* ctx, double* ms /*[2]*/, int64_t* passes);
 
 /* Copy the current HR estimate x [H][W] into x_out.  HOST: blocks;
  * DEVICE: stream-ordered on the ctx stream. */

@@ -19,7 +19,9 @@
 // order-independent, then one RED.ADD per touched cell).
 //
 // Kernels:
-//   k_asm_classify  setup: the irregular rows -> a compact list (k, i) with their cell boxes;
+//   k_asm_rows      setup: every row of the stacked A_k evaluated once: regular rows -> a record
+//                   (window weights + base), irregular rows -> a compact list (k, i) and their
+//                   window positions (bitmask; k_asm_plist compacts it);
 //                   k_asm_tcount / k_asm_tscan / k_asm_tfill: per 32 x 32 output tile, the
 //                   irregular rows whose box meets it (CSR)
 //   k_asm_stencil   setup: the stencil planes, one CTA per 16 x 16 output cells, thread = cell
@@ -46,6 +48,8 @@ template <int Z> struct AsmCfg {
   static constexpr int WRr = 2 * R + 2;               // regular row window (cells per axis)
   static constexpr int WR2 = WRr * WRr;
   static constexpr int WR2P = WR2 + 1;                // odd shared-memory stride of a row
+  static constexpr int RS = WR2 + 4;                  // global row record: weights, base, pad (16 B aligned)
+  static constexpr int RB = Z == 2 ? 8 : 4;           // k_asm_rows: LR rows per CTA (32 x RB threads)
   static constexpr int SR = WRr - 1;                  // stencil radius
   static constexpr int NSW = 2 * SR + 1;
   static constexpr int NH = (NSW * NSW + 1) / 2;      // stored half (incl. the centre)
@@ -135,14 +139,51 @@ __device__ __forceinline__ bool asm_row_bbox(const Geom& G, const float* om, flo
 // setup 1: irregular rows -> compact list (k, i) + cell boxes
 // ---------------------------------------------------------------------------------------------
 template <int Z>
-__global__ void __launch_bounds__(256) k_asm_classify(const Geom G, const Views V, const float* __restrict__ omega,
-                                                      unsigned* count, int2* __restrict__ list,
-                                                      unsigned* __restrict__ pmask, int pmw) {
+__global__ void __launch_bounds__(256) k_asm_rows(const Geom G, const Views V, const float* __restrict__ omega,
+                                                  float* __restrict__ rows, unsigned* count, int2* __restrict__ list,
+                                                  unsigned* __restrict__ pmask, int pmw) {
   using C = AsmCfg<Z>;
-  const int lane = threadIdx.x, ix = blockIdx.x * 32 + lane, iy = blockIdx.y * 8 + threadIdx.y, k = blockIdx.z;
+  constexpr int WRr = C::WRr, WR2 = C::WR2, RS = C::RS;
+  __shared__ float sw[32 * C::RB * (WR2 + 1)];   // per-thread row window, odd stride
+  const int lane = threadIdx.x, ix = blockIdx.x * 32 + lane, iy = blockIdx.y * C::RB + threadIdx.y, k = blockIdx.z;
+  const int tid = threadIdx.y * 32 + lane;
+  const bool in = ix < G.w && iy < G.h;
   bool irr = false;
   int by = 0, bx = 0;
-  if (ix < G.w && iy < G.h) irr = !asm_row_bbox<Z>(G, asm_omega(G, omega, k), V.off[k].x, V.off[k].y, iy, ix, by, bx);
+  const float drho = V.off[k].x, dtau = V.off[k].y;
+  const float* om = asm_omega(G, omega, k);
+  if (in) irr = !asm_row_bbox<Z>(G, om, drho, dtau, iy, ix, by, bx);
+  float* w = sw + tid * (WR2 + 1);
+  if (in && !irr) {
+#pragma unroll
+    for (int e = 0; e < WR2; ++e) w[e] = 0.f;
+#pragma unroll
+    for (int u = -C::R; u <= C::R; ++u) {
+      const int Y = Z * iy + u;
+      if (Y < 0 || Y >= G.H) continue;
+#pragma unroll
+      for (int v = -C::R; v <= C::R; ++v) {
+        const int X = Z * ix + v;
+        if (X < 0 || X >= G.W) continue;
+        const Samp s = asm_sample(G, om, drho, dtau, Y, X);
+        const float gg = G.taps[u + C::R] * G.taps[v + C::R];
+        const float a0 = gg * (1.f - s.fy), a1 = gg * s.fy;
+        const int r0 = (s.y0 - by) * WRr, r1 = (s.y1 - by) * WRr, c0 = s.x0 - bx, c1 = s.x1 - bx;
+        w[r0 + c0] += a0 * (1.f - s.fx);
+        w[r0 + c1] += a0 * s.fx;
+        w[r1 + c0] += a1 * (1.f - s.fx);
+        w[r1 + c1] += a1 * s.fx;
+      }
+    }
+  }
+  if (in) {   // the record: WR2 weights, then the window base (y << 16 | x), INT_MIN when irregular
+    float* rec = rows + (((size_t)k * G.h + iy) * G.w + ix) * RS;
+    if (!irr) {
+#pragma unroll
+      for (int e = 0; e < WR2; e += 4) *reinterpret_cast<float4*>(rec + e) = make_float4(w[e], w[e + 1], w[e + 2], w[e + 3]);
+    }
+    reinterpret_cast<int*>(rec)[WR2] = irr ? INT_MIN : ((by << 16) | bx);
+  }
   const unsigned b = __ballot_sync(0xffffffffu, irr);
   if (!b) return;
   unsigned base = 0;
@@ -196,7 +237,7 @@ __global__ void __launch_bounds__(256) k_asm_plist(const Geom G, const unsigned*
 }
 
 template <int Z>
-__global__ void __launch_bounds__(256, 2) k_asm_stencil(const Geom G, const Views V, const float* __restrict__ omega,
+__global__ void __launch_bounds__(256, 2) k_asm_stencil(const Geom G, const Views V, const float* __restrict__ rows,
                                                      float om_max, float* __restrict__ st, int psS, size_t plane) {
   using C = AsmCfg<Z>;
   constexpr int WRr = C::WRr, WR2P = C::WR2P, NH = C::NH, NSW = C::NSW, NTA = C::NTA, CAP = C::CAP;
@@ -213,7 +254,6 @@ __global__ void __launch_bounds__(256, 2) k_asm_stencil(const Geom G, const View
 
   for (int k = 0; k < G.n_views; ++k) {
     const float drho = V.off[k].x, dtau = V.off[k].y;
-    const float* om = asm_omega(G, omega, k);
     const int sY = (int)ceilf(fabsf(dtau) * om_max), sX = (int)ceilf(fabsf(drho) * om_max);
     // LR rows whose cells can reach the tile: cells of row i lie in [zeta i - R - s, zeta i + R + s + 1]
     const int iy0 = max(0, cdiv(A0y - C::R - sY - 1, Z)), iy1 = min(G.h - 1, fdiv(A0y + C::TA - 1 + C::R + sY, Z));
@@ -230,41 +270,27 @@ __global__ void __launch_bounds__(256, 2) k_asm_stencil(const Geom G, const View
           s_oy[1] = s_ox[1] = -(1 << 30);
         }
         __syncthreads();
-        for (int r = tid; r < ny_c * nx_c; r += NTA) {
+        for (int r = tid; r < ny_c * nx_c; r += NTA) {   // the chunk's row records (k_asm_rows)
           const int iy = cy0 + r / nx_c, ix = cx0 + r % nx_c;
-          int by, bx;
-          const bool reg = asm_row_bbox<Z>(G, om, drho, dtau, iy, ix, by, bx);
-          float* w = rw + r * WR2P;
-          if (reg) {
-#pragma unroll
-            for (int e = 0; e < C::WR2; ++e) w[e] = 0.f;
-#pragma unroll
-            for (int u = -C::R; u <= C::R; ++u) {
-              const int Y = Z * iy + u;
-              if (Y < 0 || Y >= G.H) continue;
-#pragma unroll
-              for (int v = -C::R; v <= C::R; ++v) {
-                const int X = Z * ix + v;
-                if (X < 0 || X >= G.W) continue;
-                const Samp s = asm_sample(G, om, drho, dtau, Y, X);
-                const float gg = G.taps[u + C::R] * G.taps[v + C::R];
-                const float a0 = gg * (1.f - s.fy), a1 = gg * s.fy;
-                const int r0 = (s.y0 - by) * WRr, r1 = (s.y1 - by) * WRr, c0 = s.x0 - bx, c1 = s.x1 - bx;
-                w[r0 + c0] += a0 * (1.f - s.fx);
-                w[r0 + c1] += a0 * s.fx;
-                w[r1 + c0] += a1 * (1.f - s.fx);
-                w[r1 + c1] += a1 * s.fx;
-              }
-            }
-            atomicMin(&s_oy[0], by - Z * iy);
-            atomicMax(&s_oy[1], by - Z * iy);
-            atomicMin(&s_ox[0], bx - Z * ix);
-            atomicMax(&s_ox[1], bx - Z * ix);
-            rby[r] = by;
-            rbx[r] = bx;
-          } else {
+          const float* rec = rows + (((size_t)k * G.h + iy) * G.w + ix) * C::RS;
+          const int pk = __ldg(reinterpret_cast<const int*>(rec) + C::WR2);
+          if (pk == INT_MIN) {
             rby[r] = INT_MIN;
+            continue;
           }
+          const int by = pk >> 16, bx = pk & 0xffff;
+          float* w = rw + r * WR2P;
+#pragma unroll
+          for (int e = 0; e < C::WR2; e += 4) {
+            const float4 t = __ldg(reinterpret_cast<const float4*>(rec + e));
+            w[e] = t.x; w[e + 1] = t.y; w[e + 2] = t.z; w[e + 3] = t.w;
+          }
+          atomicMin(&s_oy[0], by - Z * iy);
+          atomicMax(&s_oy[1], by - Z * iy);
+          atomicMin(&s_ox[0], bx - Z * ix);
+          atomicMax(&s_ox[1], bx - Z * ix);
+          rby[r] = by;
+          rbx[r] = bx;
         }
         __syncthreads();
         if (s_oy[0] > s_oy[1]) continue;   // no regular row in this chunk (uniform)
@@ -633,6 +659,15 @@ __global__ void __launch_bounds__(256, 3) k_asm_normal(const Geom G, const Views
 // ---------------------------------------------------------------------------------------------
 // host launchers
 // ---------------------------------------------------------------------------------------------
+int asm_row_floats(int scale) {   // floats per row record
+  switch (scale) {
+    case 2: return AsmCfg<2>::RS;
+    case 3: return AsmCfg<3>::RS;
+    case 4: return AsmCfg<4>::RS;
+    default: return 0;
+  }
+}
+
 int asm_plane_count(int scale) {   // full stencil window
   switch (scale) {
     case 2: return AsmCfg<2>::NF;
@@ -661,11 +696,11 @@ cudaError_t prepare_asm_kernels() {
 template <int Z>
 static void asm_build_z(const Geom& G, const Views& V, const AsmBuf& B, float om_max, cudaStream_t st) {
   using C = AsmCfg<Z>;
-  dim3 gc((G.w + 31) / 32, (G.h + 7) / 8, G.n_views);
-  k_asm_classify<Z><<<gc, dim3(32, 8), 0, st>>>(G, V, B.omega, B.count, B.list, B.pmask, B.pmw);
+  dim3 gc((G.w + 31) / 32, (G.h + C::RB - 1) / C::RB, G.n_views);
+  k_asm_rows<Z><<<gc, dim3(32, C::RB), 0, st>>>(G, V, B.omega, B.rows, B.count, B.list, B.pmask, B.pmw);
   k_asm_plist<<<1184, 256, 0, st>>>(G, B.pmask, B.pmw, B.count + 1, B.plist);
   dim3 gs((G.W + C::TA - 1) / C::TA, (G.H + C::TA - 1) / C::TA);
-  k_asm_stencil<Z><<<gs, C::NTA, C::kSmemStencil, st>>>(G, V, B.omega, om_max, B.st + (size_t)(C::NH - 1) * B.plane,
+  k_asm_stencil<Z><<<gs, C::NTA, C::kSmemStencil, st>>>(G, V, B.rows, om_max, B.st + (size_t)(C::NH - 1) * B.plane,
                                                         B.psS, B.plane);
   k_asm_mirror<Z><<<2048, 256, 0, st>>>(G, B.st, B.psS, B.plane);
 }
@@ -686,10 +721,12 @@ cudaError_t launch_asm_build(const Geom& G, const Views& V, const AsmBuf& B, flo
 }
 
 template <int Z>
-static void asm_step_z(const Geom& G, const Views& V, const AsmStepArgs& a, bool irr, int num_sms, cudaStream_t st) {
+static void asm_step_z(const Geom& G, const Views& V, const AsmStepArgs& a, bool irr, int num_sms, cudaStream_t st,
+                       cudaEvent_t mid) {
   using C = AsmCfg<Z>;
   dim3 g((G.W + C::TW - 1) / C::TW, (G.H + C::TH - 1) / C::TH);
   k_asm_normal<Z><<<g, 256, C::kSmemNormal, st>>>(G, V, a);
+  if (mid) cudaEventRecordWithFlags(mid, st, cudaEventRecordExternal);   // profiling split
   if (irr) {
     k_asm_irr_u<<<num_sms * 8, 256, 0, st>>>(G, V, a);
     k_asm_irr_t<Z><<<num_sms * 16, 256, 0, st>>>(G, a);
@@ -698,7 +735,7 @@ static void asm_step_z(const Geom& G, const Views& V, const AsmStepArgs& a, bool
 }
 
 cudaError_t launch_asm_step(const Geom& G, const Views& V, const AsmBuf& B, const AsmStep& s, bool irr, int num_sms,
-                            cudaStream_t st) {
+                            cudaStream_t st, cudaEvent_t mid) {
   AsmStepArgs a{};
   a.r = s.r;
   a.p_prev = s.p_prev;
@@ -719,9 +756,9 @@ cudaError_t launch_asm_step(const Geom& G, const Views& V, const AsmBuf& B, cons
   a.plane = B.plane;
   a.om_max = B.om_max;
   switch (G.scale) {
-    case 2: asm_step_z<2>(G, V, a, irr, num_sms, st); break;
-    case 3: asm_step_z<3>(G, V, a, irr, num_sms, st); break;
-    case 4: asm_step_z<4>(G, V, a, irr, num_sms, st); break;
+    case 2: asm_step_z<2>(G, V, a, irr, num_sms, st, mid); break;
+    case 3: asm_step_z<3>(G, V, a, irr, num_sms, st, mid); break;
+    case 4: asm_step_z<4>(G, V, a, irr, num_sms, st, mid); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

@@ -55,9 +55,10 @@ cudaError_t launch_misr_normal(const Geom& G, const MisrStencil& S, const MisrAr
 cudaError_t prepare_misr_kernels();
 cudaError_t launch_asm_build(const Geom& G, const Views& V, const AsmBuf& B, float om_max, cudaStream_t st);
 cudaError_t launch_asm_step(const Geom& G, const Views& V, const AsmBuf& B, const AsmStep& s, bool irr, int num_sms,
-                            cudaStream_t st);
+                            cudaStream_t st, cudaEvent_t mid);
 cudaError_t prepare_asm_kernels();
 int asm_plane_count(int scale);
+int asm_row_floats(int scale);
 cudaError_t launch_gd_update(const Geom& G, float* x, const float* g, Control* ctl, const GdCfg& cfg, int num_sms,
                              cudaStream_t st);
 }  // namespace lfsr
@@ -155,6 +156,10 @@ struct lfsr_ctx {
   AsmBuf asmb{};
   int64_t asm_nirr = -1;           // irregular rows (host copy; -1 = not read back: batch fields)
   double asm_ms = 0.0;             // wall time of the last assembly (set_observations, synchronised)
+  int batch_iters = 0;             // lfsr_solve_batch: ADMM iterations per field (path choice amortisation)
+  std::vector<cudaEvent_t> asm_ev; // profiling: after the stencil kernel of CG step k (index k)
+  double prof_asm_ms[2] = {0, 0};  // accumulated stencil-kernel / irregular-row milliseconds
+  int64_t prof_asm_n = 0;
   std::string err;
 };
 
@@ -558,6 +563,7 @@ void lfsr_destroy(lfsr_ctx* c) {
   if (!c->poisoned) cudaStreamSynchronize(c->stream);
   free_state(c);
   for (cudaEvent_t e : c->prof_ev) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->asm_ev) cudaEventDestroy(e);
   for (cudaEvent_t e : c->ev_in)
     if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : c->ev_b)
@@ -1308,8 +1314,6 @@ static lfsr_status misr_normal(lfsr_ctx* c, Part& P, int k, const float* in, flo
 // ---------------------------------------------------------------------------
 static bool asm_wanted(const lfsr_ctx* c) {
   const Geom& G = c->G;
-  const char* e = getenv("LFSR_ASM");
-  if (e && e[0] == '0') return false;
   return c->xmode == X_NONE && !G.paper && !G.psf2d && G.radius == 2 && G.s_d == 24 && G.scale >= 2 && G.scale <= 4 &&
          G.H < 65536 && G.W < 65536;   // (y << 16 | x) packing of the irregular lists
 }
@@ -1327,7 +1331,8 @@ static lfsr_status asm_setup(lfsr_ctx* c, float om_max, bool read_count) {
   const size_t npos = (size_t)G.n_views * G.H * G.W;
   const int pmw = (G.W + 31) / 32;
   if (!B.st) {
-    const size_t need = (size_t)NH * plane * 4 + nrows * 12 + npos * 12 + (size_t)G.n_views * G.H * pmw * 4 + 512;
+    const size_t need = (size_t)NH * plane * 4 + nrows * (12 + 4 * (size_t)asm_row_floats(G.scale)) + npos * 12 +
+                        (size_t)G.n_views * G.H * pmw * 4 + 512;
     size_t fr = 0, tot = 0;
     CK(c, cudaMemGetInfo(&fr, &tot));
     if (need > fr / 2) return LFSR_OK;   // no room: the direct tile kernel
@@ -1337,6 +1342,8 @@ static lfsr_status asm_setup(lfsr_ctx* c, float om_max, bool read_count) {
     B.st = (float*)p;
     if ((e = dalloc(c, &p, nrows * 8)) != cudaSuccess) return cuda_fail(c, e, "alloc");
     B.list = (int2*)p;
+    if ((e = dalloc(c, &p, nrows * asm_row_floats(G.scale) * 4)) != cudaSuccess) return cuda_fail(c, e, "alloc");
+    B.rows = (float*)p;
     if ((e = dalloc(c, &p, nrows * 4)) != cudaSuccess) return cuda_fail(c, e, "alloc");
     B.tdense = (float*)p;
     if ((e = dalloc(c, &p, npos * 8)) != cudaSuccess) return cuda_fail(c, e, "alloc");
@@ -1382,8 +1389,101 @@ static lfsr_status asm_normal(lfsr_ctx* c, Part& P, int k, const float* in, floa
   s.ctl = ctl;
   s.cg_k = k;
   const bool irr = c->asm_nirr != 0;
-  CK(c, launch_asm_step(c->G, c->V, c->asmb, s, irr, c->num_sms, st));
+  cudaEvent_t mid = (c->profile && k >= 1 && k < (int)c->asm_ev.size()) ? c->asm_ev[k] : nullptr;
+  CK(c, launch_asm_step(c->G, c->V, c->asmb, s, irr, c->num_sms, st, mid));
   if (launches) *launches += irr ? 4 : 1;   // k_asm_normal [+ k_asm_irr_u, _t, _scatter]
+  return LFSR_OK;
+}
+
+// Path choice: the assembled operator runs when one CG operator pass through it is >= 5 % faster
+// than through the tile kernel (both timed here on this light field), and -- for lfsr_solve_batch,
+// whose fields each pay their own assembly -- when the per-field saving N K (t_tile - t_asm) also
+// exceeds the assembly time.  The timings are cached per geometry (a batch decides before assembling
+// once one field of the geometry was timed; the first set_observations of a geometry in the process
+// times, later ones reuse the decision).  LFSR_ASM=1 / 0 forces either path.
+struct AsmTiming {
+  float t_tile = 0.f, t_asm = 0.f;   // ms per CG operator pass
+  double setup_ms = 0.0;
+};
+static std::map<std::string, AsmTiming> g_asm_timing;
+
+static bool asm_forced(bool* on) {
+  const char* e = getenv("LFSR_ASM");
+  if (!e || !e[0]) return false;
+  *on = e[0] != '0';
+  return true;
+}
+
+static bool asm_pays(const lfsr_ctx* c, const AsmTiming& t) {
+  if (!(t.t_asm < 0.95f * t.t_tile)) return false;
+  if (c->batch_iters > 0)
+    return (double)(t.t_tile - t.t_asm) * c->batch_iters * c->G.K > t.setup_ms;
+  return true;
+}
+
+// ms per pass of the CG operator (plain, k = 0) through the current path, 3 timed passes
+static lfsr_status time_normal_pass(lfsr_ctx* c, bool asm_path, float* ms_out) {
+  Part& P = c->parts[0];
+  const Geom& G = c->G;
+  cudaEvent_t e0, e1;
+  CK(c, cudaEventCreate(&e0));
+  CK(c, cudaEventCreate(&e1));
+  auto pass = [&]() -> lfsr_status {
+    if (asm_path) return asm_normal(c, P, 0, P.S.x, c->tmp_hr2, P.S.ctl, c->stream, nullptr);
+    TileIO io = base_io(P);
+    io.in_hr = P.S.x;
+    io.out_hr = c->tmp_hr2;
+    io.do_nltv = 1;
+    CK(c, launch_tile(MODE_NORMAL, G, c->V, P.T, io, c->stream));
+    return LFSR_OK;
+  };
+  lfsr_status st = pass();   // warm
+  CK(c, cudaEventRecord(e0, c->stream));
+  for (int r = 0; r < 3 && st == LFSR_OK; ++r) st = pass();
+  CK(c, cudaEventRecord(e1, c->stream));
+  CK(c, cudaEventSynchronize(e1));
+  float ms = 0.f;
+  CK(c, cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  *ms_out = ms / 3.f;
+  return st;
+}
+
+static lfsr_status choose_normal_path(lfsr_ctx* c, float om_max) {
+  c->asmop = false;
+  bool forced_on = false;
+  const bool forced = asm_forced(&forced_on);
+  if (forced && !forced_on) return LFSR_OK;
+  if (!asm_wanted(c)) return LFSR_OK;
+  const std::string key = tune_key(c);
+  bool cached = false;
+  if (!forced) {   // a timed geometry: decide before assembling (stable choice within the process)
+    std::lock_guard<std::mutex> lk(g_tune_mu);
+    auto it = g_asm_timing.find(key);
+    if (it != g_asm_timing.end()) {
+      if (!asm_pays(c, it->second)) return LFSR_OK;
+      cached = true;
+    }
+  }
+  lfsr_status st;
+  {
+    NvtxRange r_("normal operator assembly");
+    if ((st = asm_setup(c, om_max, true)) != LFSR_OK) return st;
+  }
+  if (!c->asmop || forced || cached) return LFSR_OK;
+  AsmTiming t;
+  if ((st = time_normal_pass(c, false, &t.t_tile)) != LFSR_OK) return st;
+  if ((st = time_normal_pass(c, true, &t.t_asm)) != LFSR_OK) return st;
+  t.setup_ms = c->asm_ms;
+  {
+    std::lock_guard<std::mutex> lk(g_tune_mu);
+    g_asm_timing[key] = t;
+  }
+  if (getenv("LFSR_TUNE_VERBOSE"))
+    fprintf(stderr, "lfsr normal path: tile %.1f us, assembled %.1f us, assembly %.2f ms, batch N %d\n",
+            t.t_tile * 1000.f, t.t_asm * 1000.f, t.setup_ms, c->batch_iters);
+  c->asmop = asm_pays(c, t);
   return LFSR_OK;
 }
 
@@ -1531,10 +1631,7 @@ lfsr_status lfsr_set_observations(lfsr_ctx* c, const float* lr_views, const floa
     if ((st = misr_setup(c, omega00)) != LFSR_OK) return st;
   }
   c->asmop = false;
-  if (!c->misr) {
-    NvtxRange r_("normal operator assembly");
-    if ((st = asm_setup(c, om_max, true)) != LFSR_OK) return st;
-  }
+  if (!c->misr && (st = choose_normal_path(c, om_max)) != LFSR_OK) return st;
   const auto tg0 = std::chrono::steady_clock::now();
   lfsr_status gs = build_graphs(c);
   if (gs != LFSR_OK) return gs;
@@ -1912,6 +2009,11 @@ static lfsr_status build_graphs(lfsr_ctx* c) {
       CK(c, cudaEventCreate(&e));
       c->prof_ev.push_back(e);
     }
+    while (c->asm_ev.size() < (size_t)c->G.K + 1) {
+      cudaEvent_t e;
+      CK(c, cudaEventCreate(&e));
+      c->asm_ev.push_back(e);
+    }
   }
   const int ngraphs = c->xmode == X_NONE ? 1 : 2;  // the strip exchanges name the w_S buffer of each parity
   for (int g = 0; g < ngraphs; ++g) {
@@ -2229,9 +2331,13 @@ lfsr_status lfsr_solve_batch(lfsr_ctx* c, int32_t n_fields, const float* const* 
   }
   struct BatchFlag {   // the MISR fast path is per field (its stencil depends on the disparity)
     lfsr_ctx* c;
-    ~BatchFlag() { c->in_batch = false; }
+    ~BatchFlag() {
+      c->in_batch = false;
+      c->batch_iters = 0;
+    }
   } batch_flag{c};
   c->in_batch = true;
+  c->batch_iters = n_iters;
   // field 0: the ordinary path (allocation, tiling, graphs)
   if ((st = lfsr_set_observations(c, lr_views[0], view_offsets[0], disparity[0], LFSR_DISP_SHARED, nullptr,
                                   LFSR_MEM_HOST)) != LFSR_OK)
@@ -2300,12 +2406,24 @@ lfsr_status lfsr_profile(lfsr_ctx* c, int32_t enable) {
   lfsr_status st = check_run(c);
   if (st != LFSR_OK) return st;
   for (int i = 0; i < 3; ++i) c->prof_ms[i] = 0.0, c->prof_n[i] = 0;
+  c->prof_asm_ms[0] = c->prof_asm_ms[1] = 0.0;
+  c->prof_asm_n = 0;
   if (c->xmode != X_NONE) return LFSR_OK;  // per-kernel events only for a single strip
   if ((enable != 0) == c->profile) return LFSR_OK;
   CK(c, cudaSetDevice(c->prm.device));
   CK(c, cudaStreamSynchronize(c->stream));
   c->profile = enable != 0;
   return build_graphs(c);
+}
+
+lfsr_status lfsr_profile_read_split(lfsr_ctx* c, double* ms, int64_t* passes) {
+  lfsr_status st = check_run(c);
+  if (st != LFSR_OK) return st;
+  if (!ms || !passes) FAIL(c, LFSR_ERR_INVALID_ARG, "ms and passes must not be NULL");
+  ms[0] = c->prof_asm_ms[0];
+  ms[1] = c->prof_asm_ms[1];
+  *passes = c->prof_asm_n;
+  return LFSR_OK;
 }
 
 lfsr_status lfsr_profile_read(lfsr_ctx* c, double* ms, int64_t* launches) {
@@ -2322,6 +2440,13 @@ lfsr_status lfsr_profile_read(lfsr_ctx* c, double* ms, int64_t* launches) {
       CK(c, cudaEventElapsedTime(&t, c->prof_ev[2 * k - 1], c->prof_ev[2 * k]));
       c->prof_ms[1] += t;
       c->prof_n[1] += 1;
+      if (c->asmop && !c->misr) {   // the assembled operator: stencil kernel | irregular rows
+        float t1 = 0.f;
+        CK(c, cudaEventElapsedTime(&t1, c->prof_ev[2 * k - 1], c->asm_ev[k]));
+        c->prof_asm_ms[0] += t1;
+        c->prof_asm_ms[1] += t - t1;
+        c->prof_asm_n += 1;
+      }
       CK(c, cudaEventElapsedTime(&t, c->prof_ev[2 * k], c->prof_ev[2 * k + 1]));
       c->prof_ms[2] += t;
       c->prof_n[2] += 1;

@@ -183,6 +183,7 @@ struct AsmBuf {
   float* st;            // [NH][H + 2 pad][psS] stencil planes (c_A folded in)
   int psS;              // plane row pitch (floats)
   size_t plane;         // floats per plane
+  float* rows;          // [n_views][h][w][RS] row records: (2R+2)^2 window weights, base (y << 16 | x) or INT_MIN
   unsigned* count;      // [0] irregular rows, [1] positions in their windows (device)
   int2* list;           // [n_views h w] irregular rows (k, iy << 16 | ix), first count[0] valid
   unsigned* pmask;      // [n_views][H][pmw] positions in an irregular row's blur window

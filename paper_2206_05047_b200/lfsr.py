@@ -34,7 +34,7 @@ EXPORTS = ("lfsr_create", "lfsr_set_observations", "lfsr_admm_run", "lfsr_admm_e
            "lfsr_get_hr", "lfsr_get_state", "lfsr_op_apply", "lfsr_launches_per_iter", "lfsr_tile_config", "lfsr_profile",
            "lfsr_profile_read", "lfsr_strip_plan", "lfsr_destroy", "lfsr_last_error", "lfsr_abi_version",
            "lfsr_gd_run", "lfsr_gd_launches_per_iter", "lfsr_rgb_to_ycbcr", "lfsr_ycbcr_to_rgb", "lfsr_solve_batch",
-           "lfsr_get_stream", "lfsr_fast_path", "lfsr_normal_path")
+           "lfsr_get_stream", "lfsr_fast_path", "lfsr_normal_path", "lfsr_profile_read_split")
 
 
 class LFSRError(RuntimeError):
@@ -118,6 +118,8 @@ def load_library(path: str = LIB_PATH):
     lib.lfsr_profile.restype = st
     lib.lfsr_profile_read.argtypes = [vp, P(ctypes.c_double), P(ctypes.c_int64)]
     lib.lfsr_profile_read.restype = st
+    lib.lfsr_profile_read_split.argtypes = [vp, P(ctypes.c_double), P(ctypes.c_int64)]
+    lib.lfsr_profile_read_split.restype = st
     lib.lfsr_get_hr.argtypes = [vp, vp, ctypes.c_int]
     lib.lfsr_get_hr.restype = st
     lib.lfsr_get_state.argtypes = [vp, vp, vp, vp, vp, ctypes.c_int]
@@ -397,6 +399,13 @@ class Solver:
         self._check(self.lib.lfsr_profile_read(self._h, ms, n))
         return list(ms), list(n)
 
+
+    def profile_read_split(self):
+        """lfsr_profile_read_split: (stencil-kernel ms, irregular-row ms, passes) of the assembled operator."""
+        ms = (ctypes.c_double * 2)()
+        n = ctypes.c_int64()
+        self._check(self.lib.lfsr_profile_read_split(self._h, ms, ctypes.byref(n)))
+        return list(ms), int(n.value)
     def get_hr(self, out=None):
         """Returns x [H][W]: into `out` (torch tensor, host or device) or a new numpy array."""
         H, W = self.params.H, self.params.W

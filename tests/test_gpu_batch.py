@@ -16,8 +16,12 @@ def params(L, cfg):
     return L.params_for(S.CONFIGS[cfg], S.SolverDefaults())
 
 
-@pytest.mark.parametrize("cfg,n_fields,n_iters", [("C1", 4, 5), ("C3", 2, 2)])
-def test_batch_matches_single_solves(lfsr_mod, cfg, n_fields, n_iters):
+@pytest.mark.parametrize("cfg,n_fields,n_iters,asm", [("C1", 4, 5, "0"), ("C3", 2, 2, "0"), ("C1", 4, 5, "1"),
+                                                      ("C3", 3, 2, "1")])
+def test_batch_matches_single_solves(lfsr_mod, cfg, n_fields, n_iters, asm, monkeypatch):
+    """Both CG-operator paths forced (LFSR_ASM): the tile kernel, and the assembled operator, which
+    the batch re-assembles per field (its stencil depends on the field's disparity)."""
+    monkeypatch.setenv("LFSR_ASM", asm)
     lfs = [S.make_lightfield(cfg, seed=500 + i) for i in range(n_fields)]
     p = params(lfsr_mod, cfg)
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
@@ -26,6 +30,7 @@ def test_batch_matches_single_solves(lfsr_mod, cfg, n_fields, n_iters):
     with lfsr_mod.Solver(p) as s:
         s.solve_batch(fields, n_iters, outs)
         last = s.get_hr()
+        assert s.normal_path["name"] == ("assembled" if asm == "1" else "tile")
     singles = []
     with lfsr_mod.Solver(p) as s:
         for lf in lfs:

@@ -1,6 +1,6 @@
 """Record the ncu counters bench.py reports next to its live timings.
 
-    python tools/ncu_record.py <cfg> normal=<rep> [wz=<rep>] [upd=<rep>]
+    python tools/ncu_record.py <cfg> [normal=<rep>] [wz=<rep>] [upd=<rep>] [asm=<rep>] [irr=<rep>]
 
 Reads each `ncu --set full` report (one launch each) with `ncu -i ... --page raw --csv`
 and writes per-launch DRAM bytes, warp instructions and shared-memory wavefronts of the
@@ -49,7 +49,8 @@ def main():
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     allrec = json.load(open(path)) if os.path.exists(path) else {}
     rec = {"build_hash": bench.source_hash(), "source": "tools/ncu_record.py " + " ".join(sys.argv[1:])}
-    names = {"normal": "k_tile_normal", "wz": "k_tile_wz", "upd": "k_cg_update"}
+    names = {"normal": "k_tile_normal", "wz": "k_tile_wz", "upd": "k_cg_update", "asm": "k_asm_normal",
+             "irr": "k_asm_irr_scatter"}
     for kind, rep in reps.items():
         d = raw(rep)
         pre = names[kind]
