@@ -58,10 +58,9 @@ template <int Z> struct AsmCfg {
   static constexpr int CAP = Z == 2 ? 288 : 160;
   static constexpr size_t kSmemStencil = (size_t)NH * NTA * 4 + (size_t)CAP * (WR2P + 2) * 4;
   // CG-step kernel: 128 x 8 output pixels, warp = row, lane = 4 pixels
-  static constexpr int TH = 8, TW = 128;
+  static constexpr int TH = 4, TW = 128;              // 4 warps (one output row each)
   static constexpr int PC = TW + 16;                  // tile columns [X0 - 8, X0 + TW + 8)
   static constexpr int PR = TH + 2 * SR, MR = TH + 4;
-  static constexpr int NF = NSW * NSW;                // full stencil planes
   static constexpr size_t kSmemNormal = (size_t)(PR * PC + 2 * MR * PC) * 4;
 };
 
@@ -471,37 +470,21 @@ __device__ __forceinline__ double asm_warp_sum(double v) {
   return v;
 }
 
-// Stencil planes: full window, plane f = (dy + SR) NSW + (dx + SR) holds M_reg[a][a + d]; the
-// setup kernel writes the half d >= 0 (lexicographic) as planes NH - 1 + h and k_asm_mirror fills
-// the other half from the symmetry M[a][a - d] = M[a - d][a].
+// Stencil planes: the stored half, plane h = dy NSW + dx (dy = 0: dx in [0, SR]; dy in [1, SR]:
+// dx in [-SR, SR]) holds M_reg[a][a + d_h] at pixel a; the other half is read at the neighbour
+// (M[a][a - d] = M[a - d][a]).  Stored-full planes (a mirror pass at setup, one coalesced LDG.128
+// per coefficient) measured slower: 30.2 vs 24.6 us per pass at C3.
+//
 template <int Z>
-__global__ void __launch_bounds__(256) k_asm_mirror(const Geom G, float* __restrict__ st, int psS, size_t plane) {
+__global__ void __launch_bounds__(128, 6) k_asm_normal(const Geom G, const Views V, const AsmStepArgs a) {
   using C = AsmCfg<Z>;
-  const size_t npx = (size_t)G.H * G.W;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < npx * (C::NH - 1); i += (size_t)gridDim.x * blockDim.x) {
-    const int h = 1 + (int)(i / npx);
-    const size_t z = i - (size_t)(h - 1) * npx;
-    const int Y = (int)(z / G.W), X = (int)(z - (size_t)Y * G.W);
-    const int dy = hoff_dy<C::NSW, C::SR>(h), dx = hoff_dx<C::NSW, C::SR>(h);
-    const size_t o = (size_t)(Y + kAsmPad) * psS + X + kAsmPad;
-    st[(size_t)(C::NH - 1 - h) * plane + o] = st[(size_t)(C::NH - 1 + h) * plane + o - (ptrdiff_t)dy * psS - dx];
-  }
-}
-
-// q = M_reg p + (th/2) S_W^T S_W p on a 128 x 8 tile: warp = one output row, lane = 4 consecutive
-// pixels (float4 along x).  Per stencil row dy the lane keeps the 20 p values its 4 pixels reach
-// (5 aligned LDS.128 from the shared tile), streams the 2 SR + 1 planes of that row as LDG.128
-// (all in flight) and issues 4 FFMA per plane.
-template <int Z>
-__global__ void __launch_bounds__(256, 3) k_asm_normal(const Geom G, const Views V, const AsmStepArgs a) {
-  using C = AsmCfg<Z>;
-  constexpr int SR = C::SR, NSW = C::NSW, TH = C::TH, TW = C::TW, PC = C::PC, PR = C::PR, MR = C::MR, NT = 256;
+  constexpr int SR = C::SR, NSW = C::NSW, TH = C::TH, TW = C::TW, PC = C::PC, PR = C::PR, MR = C::MR, NT = TH * 32;
   constexpr int RAD = 2, CX = 8;   // NLTV radius (5 x 5 window); tile column offset (>= SR, mult. of 4)
   extern __shared__ __align__(16) float sm_an[];
   float* sp = sm_an;                 // p  rows [-SR, TH + SR), columns [X0 - CX, X0 + TW + CX)
   float* smm = sp + PR * PC;         // m^2 rows [-RAD, TH + RAD), same columns
   float* smp = smm + MR * PC;        // m^2 p
-  __shared__ double red[8 * 2];
+  __shared__ double red[TH * 2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int Y0 = blockIdx.y * TH, X0 = blockIdx.x * TW;
   const int H = G.H, W = G.W, ps = G.ps;
@@ -558,28 +541,70 @@ __global__ void __launch_bounds__(256, 3) k_asm_normal(const Geom G, const Views
 
   const int ly = warp, Y = Y0 + ly, X = X0 + 4 * lane;
   if (Y < H) {
-    // ---- data part: the stencil planes, row dy by row dy ----
+    // ---- data part: the half stencil, M[a][a + d] = st[h][a] for d in the stored half and
+    // M[a][a - d] = st[h][a - d]; row dy by row dy (own term at (Y, X..X+3), transposed term at
+    // (Y - dy, X - dx..X - dx + 3): two aligned LDG.128 and a compile-time select) ----
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    const float* pl = a.st + (size_t)(Y + kAsmPad) * a.psS + X + kAsmPad;   // plane 0 (d = (-SR, -SR)) at (Y, X)
-#pragma unroll 1
-    for (int dy = -SR; dy <= SR; ++dy) {
-      float pv[20];
-      const float* prow = sp + (ly + dy + SR) * PC + 4 * lane;
+    const float* pl = a.st + (size_t)(Y + kAsmPad) * a.psS + X + kAsmPad;   // plane 0 (centre) at (Y, X)
+    auto load_row = [&](float (&pv)[20], int row) {
+      const float* prow = sp + row * PC + 4 * lane;
 #pragma unroll
       for (int j = 0; j < 5; ++j) {
         const float4 t = *reinterpret_cast<const float4*>(prow + 4 * j);
         pv[4 * j] = t.x; pv[4 * j + 1] = t.y; pv[4 * j + 2] = t.z; pv[4 * j + 3] = t.w;
       }
-      const float* plr = pl + (size_t)((dy + SR) * NSW) * a.plane;
-      float4 cf[NSW];
+    };
+    // coefficients of pixels X - dx .. X - dx + 3 of plane row `src` (dx compile time after unrolling)
+    auto load_shifted = [&](const float* src, int dx, float (&o)[4]) {
+      const int m = (-dx) & 3;
+      const float4 t0 = __ldg(reinterpret_cast<const float4*>(src - dx - m));
+      if (m == 0) {
+        o[0] = t0.x; o[1] = t0.y; o[2] = t0.z; o[3] = t0.w;
+        return;
+      }
+      const float4 t1 = __ldg(reinterpret_cast<const float4*>(src - dx - m + 4));
+      const float t[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
 #pragma unroll
-      for (int dx = 0; dx < NSW; ++dx) cf[dx] = __ldg(reinterpret_cast<const float4*>(plr + (size_t)dx * a.plane));
+      for (int e = 0; e < 4; ++e) o[e] = t[m + e];
+    };
+    {   // dy = 0: the centre, then dx = 1..SR both ways
+      float pv[20];
+      load_row(pv, ly + SR);
+      const float4 c0 = __ldg(reinterpret_cast<const float4*>(pl));
+      acc[0] = c0.x * pv[CX]; acc[1] = c0.y * pv[CX + 1]; acc[2] = c0.z * pv[CX + 2]; acc[3] = c0.w * pv[CX + 3];
 #pragma unroll
-      for (int dx = 0; dx < NSW; ++dx) {   // d = (dy, dx - SR): p at column CX + 4 lane + dx - SR + e
-        acc[0] = fmaf(cf[dx].x, pv[CX + dx - SR + 0], acc[0]);
-        acc[1] = fmaf(cf[dx].y, pv[CX + dx - SR + 1], acc[1]);
-        acc[2] = fmaf(cf[dx].z, pv[CX + dx - SR + 2], acc[2]);
-        acc[3] = fmaf(cf[dx].w, pv[CX + dx - SR + 3], acc[3]);
+      for (int dx = 1; dx <= SR; ++dx) {
+        const float* ph = pl + (size_t)dx * a.plane;
+        const float4 cf = __ldg(reinterpret_cast<const float4*>(ph));
+        float ct[4];
+        load_shifted(ph, dx, ct);
+        acc[0] = fmaf(cf.x, pv[CX + dx + 0], acc[0]);
+        acc[1] = fmaf(cf.y, pv[CX + dx + 1], acc[1]);
+        acc[2] = fmaf(cf.z, pv[CX + dx + 2], acc[2]);
+        acc[3] = fmaf(cf.w, pv[CX + dx + 3], acc[3]);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[e] = fmaf(ct[e], pv[CX - dx + e], acc[e]);
+      }
+    }
+#pragma unroll 1
+    for (int dy = 1; dy <= SR; ++dy) {
+      float pvo[20], pvt[20];
+      load_row(pvo, ly + dy + SR);
+      load_row(pvt, ly - dy + SR);
+      const float* plh = pl + (size_t)(dy * NSW - SR) * a.plane;   // plane of d = (dy, -SR)
+#pragma unroll
+      for (int dxi = 0; dxi < NSW; ++dxi) {
+        const int dx = dxi - SR;
+        const float* ph = plh + (size_t)dxi * a.plane;
+        const float4 cf = __ldg(reinterpret_cast<const float4*>(ph));
+        float ct[4];
+        load_shifted(ph - (ptrdiff_t)dy * a.psS, dx, ct);
+        acc[0] = fmaf(cf.x, pvo[CX + dx + 0], acc[0]);
+        acc[1] = fmaf(cf.y, pvo[CX + dx + 1], acc[1]);
+        acc[2] = fmaf(cf.z, pvo[CX + dx + 2], acc[2]);
+        acc[3] = fmaf(cf.w, pvo[CX + dx + 3], acc[3]);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[e] = fmaf(ct[e], pvt[CX - dx + e], acc[e]);
       }
     }
     // ---- weighted NLTV part (A10): sum_d (p(z) - p(z+d)) (w_d^2 m(z)^2 + w_{-d}^2 m(z+d)^2), z + d in
@@ -646,7 +671,7 @@ __global__ void __launch_bounds__(256, 3) k_asm_normal(const Geom G, const Views
     __syncthreads();
     if (tid == 0) {
       double s0 = 0.0, s1 = 0.0;
-      for (int w = 0; w < 8; ++w) {
+      for (int w = 0; w < TH; ++w) {
         s0 += red[w * 2];
         s1 += red[w * 2 + 1];
       }
@@ -668,11 +693,11 @@ int asm_row_floats(int scale) {   // floats per row record
   }
 }
 
-int asm_plane_count(int scale) {   // full stencil window
+int asm_plane_count(int scale) {   // stored half of the stencil window (centre first)
   switch (scale) {
-    case 2: return AsmCfg<2>::NF;
-    case 3: return AsmCfg<3>::NF;
-    case 4: return AsmCfg<4>::NF;
+    case 2: return AsmCfg<2>::NH;
+    case 3: return AsmCfg<3>::NH;
+    case 4: return AsmCfg<4>::NH;
     default: return 0;
   }
 }
@@ -700,9 +725,7 @@ static void asm_build_z(const Geom& G, const Views& V, const AsmBuf& B, float om
   k_asm_rows<Z><<<gc, dim3(32, C::RB), 0, st>>>(G, V, B.omega, B.rows, B.count, B.list, B.pmask, B.pmw);
   k_asm_plist<<<1184, 256, 0, st>>>(G, B.pmask, B.pmw, B.count + 1, B.plist);
   dim3 gs((G.W + C::TA - 1) / C::TA, (G.H + C::TA - 1) / C::TA);
-  k_asm_stencil<Z><<<gs, C::NTA, C::kSmemStencil, st>>>(G, V, B.rows, om_max, B.st + (size_t)(C::NH - 1) * B.plane,
-                                                        B.psS, B.plane);
-  k_asm_mirror<Z><<<2048, 256, 0, st>>>(G, B.st, B.psS, B.plane);
+  k_asm_stencil<Z><<<gs, C::NTA, C::kSmemStencil, st>>>(G, V, B.rows, om_max, B.st, B.psS, B.plane);
 }
 
 cudaError_t launch_asm_build(const Geom& G, const Views& V, const AsmBuf& B, float om_max, cudaStream_t st) {
@@ -725,7 +748,7 @@ static void asm_step_z(const Geom& G, const Views& V, const AsmStepArgs& a, bool
                        cudaEvent_t mid) {
   using C = AsmCfg<Z>;
   dim3 g((G.W + C::TW - 1) / C::TW, (G.H + C::TH - 1) / C::TH);
-  k_asm_normal<Z><<<g, 256, C::kSmemNormal, st>>>(G, V, a);
+  k_asm_normal<Z><<<g, C::TH * 32, C::kSmemNormal, st>>>(G, V, a);
   if (mid) cudaEventRecordWithFlags(mid, st, cudaEventRecordExternal);   // profiling split
   if (irr) {
     k_asm_irr_u<<<num_sms * 8, 256, 0, st>>>(G, V, a);

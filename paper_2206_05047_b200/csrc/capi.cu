@@ -1325,7 +1325,7 @@ static lfsr_status asm_setup(lfsr_ctx* c, float om_max, bool read_count) {
   if (!asm_wanted(c)) return LFSR_OK;
   const int NH = asm_plane_count(G.scale);   // stencil planes (full window)
   AsmBuf& B = c->asmb;
-  const int psS = round_up(G.W + 2 * kAsmPad, 32);
+  const int psS = round_up(G.W + 3 * kAsmPad, 32);   // >= W + 24: shifted float4 reads stay in the padding
   const size_t plane = (size_t)(G.H + 2 * kAsmPad) * psS;
   const size_t nrows = (size_t)G.n_views * G.h * G.w;
   const size_t npos = (size_t)G.n_views * G.H * G.W;
