@@ -311,13 +311,15 @@ def roofline_assembled(cfg, d, kms, kn, t_ms, steps, share, clk_hz, npath, split
     p = cfg.H * cfg.W
     z = cfg.scale
     R = math.ceil(3 * 0.25 * math.sqrt(z * z - 1))
-    nf = (2 * (2 * R + 1) + 1) ** 2                       # stencil planes (full (2 SR + 1)^2 window)
+    nsw = 2 * (2 * R + 1) + 1
+    nf = (nsw * nsw + 1) // 2                             # stored stencil planes (symmetric half + centre)
     sms, n = split
     k_st_ms, k_irr_ms = sms[0] / max(n, 1), sms[1] / max(n, 1)
     k_wz_ms, k_upd_ms = kms[0] / max(kn[0], 1), kms[2] / max(kn[2], 1)
-    st_bytes = 4 * p * (nf + 5)                           # planes + r, p_{k-1}, m (read), p_k, q (write)
+    st_bytes = 4 * p * (nf + 5)                           # half planes + r, p_{k-1}, m (read), p_k, q (write);
+                                                          # the transposed half's neighbour reads are L1/L2 re-reads
     tot = max(sum(kms), 1e-9)
-    stencil = {"bound": "hbm", "kernel": "k_asm_normal (assembled CG operator: %d stencil planes + NLTV, a8)" % nf,
+    stencil = {"bound": "hbm", "kernel": "k_asm_normal (assembled CG operator: %d half-stencil planes + NLTV, a8)" % nf,
                "achieved": st_bytes / (k_st_ms / 1000.0) / 1e9, "peak": hbm_peak, "unit": "GB/s",
                "frac": st_bytes / (k_st_ms / 1000.0) / 1e9 / hbm_peak, "traffic": rec.get("k_asm_normal_dram_bytes"),
                "algorithmic_bytes_per_launch": st_bytes, "avg_launch_ms": k_st_ms, "share_of_step": sms[0] / tot,

@@ -476,7 +476,7 @@ __device__ __forceinline__ double asm_warp_sum(double v) {
 // per coefficient) measured slower: 30.2 vs 24.6 us per pass at C3.
 //
 template <int Z>
-__global__ void __launch_bounds__(128, 6) k_asm_normal(const Geom G, const Views V, const AsmStepArgs a) {
+__global__ void __launch_bounds__(128, 4) k_asm_normal(const Geom G, const Views V, const AsmStepArgs a) {
   using C = AsmCfg<Z>;
   constexpr int SR = C::SR, NSW = C::NSW, TH = C::TH, TW = C::TW, PC = C::PC, PR = C::PR, MR = C::MR, NT = TH * 32;
   constexpr int RAD = 2, CX = 8;   // NLTV radius (5 x 5 window); tile column offset (>= SR, mult. of 4)
