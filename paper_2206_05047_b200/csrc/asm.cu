@@ -442,15 +442,29 @@ __global__ void __launch_bounds__(256) k_asm_irr_scatter(const Geom G, const Vie
   for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
     const uint2 kz = __ldg(a.plist + e);
     const int k = (int)kz.x, Y = (int)(kz.y >> 16), X = (int)(kz.y & 0xffffu);
-    // LR pixels whose window holds (Y, X): |zeta i - Y| <= R per axis
-    const int iy0 = max(0, cdiv(Y - C::R, Z)), iy1 = min(G.h - 1, fdiv(Y + C::R, Z));
-    const int ix0 = max(0, cdiv(X - C::R, Z)), ix1 = min(G.w - 1, fdiv(X + C::R, Z));
+    // LR pixels whose window holds (Y, X): i = floor(Y / zeta) - 1 + j, j = 0..2 (u = Y - zeta i in
+    // [-R, R] for at most three of them at zeta <= 4); taps from a per-phase table, 0 where u leaves
+    // the window or i leaves the image -- a fixed 3 x 3 gather with no data-dependent trip counts
+    const int cy = Y / Z, cx = X / Z;
     const float* tk = a.tdense + (size_t)k * G.h * G.w;
+    float gyv[3], gxv[3];
+    int ry[3], rx[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const int iy = cy - 1 + j, ix = cx - 1 + j;
+      const int uy = Y - Z * iy, ux = X - Z * ix;
+      const float ty = s_g[min(max(uy + C::R, 0), 2 * C::R)], tx = s_g[min(max(ux + C::R, 0), 2 * C::R)];
+      gyv[j] = (uy >= -C::R && uy <= C::R && iy >= 0 && iy < G.h) ? ty : 0.f;
+      gxv[j] = (ux >= -C::R && ux <= C::R && ix >= 0 && ix < G.w) ? tx : 0.f;
+      ry[j] = min(max(iy, 0), G.h - 1);
+      rx[j] = min(max(ix, 0), G.w - 1);
+    }
     float T = 0.f;
-    for (int iy = iy0; iy <= iy1; ++iy) {
-      float tr = 0.f;
-      for (int ix = ix0; ix <= ix1; ++ix) tr = fmaf(s_g[X - Z * ix + C::R], __ldcg(tk + (size_t)iy * G.w + ix), tr);
-      T = fmaf(s_g[Y - Z * iy + C::R], tr, T);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const float* trow = tk + (size_t)ry[j] * G.w;
+      const float tr = fmaf(gxv[0], __ldcg(trow + rx[0]), fmaf(gxv[1], __ldcg(trow + rx[1]), gxv[2] * __ldcg(trow + rx[2])));
+      T = fmaf(gyv[j], tr, T);
     }
     if (T == 0.f) continue;
     const Samp s = asm_sample(G, asm_omega(G, a.omega, k), V.off[k].x, V.off[k].y, Y, X);
