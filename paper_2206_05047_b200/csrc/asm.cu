@@ -377,47 +377,48 @@ __global__ void __launch_bounds__(256) k_asm_irr_u(const Geom G, const Views V, 
 }
 
 // per CG step 3: t = c_A a . p = c_A sum_{u,v} g[u] g[v] u(zeta i + (u, v)) of every irregular row
-// (NP lanes per row, lane = blur row), and <p, M_irr p> = sum t^2 / c_A into the step's <p, q>
+// (one row per thread, its window values all in flight), and <p, M_irr p> = sum t^2 / c_A into the step's <p, q>
 template <int Z>
 __global__ void __launch_bounds__(256) k_asm_irr_t(const Geom G, const AsmStepArgs a) {
   using C = AsmCfg<Z>;
-  constexpr int NP = C::NP, RPW = 32 / NP;
+  constexpr int NP = C::NP;
+  __shared__ double s_tt[8];
   if (a.cg_k >= 2 && a.ctl->cur[S_STOP] != 0.0) return;   // CG stopped
   const unsigned n = a.count[0];
-  const int lane = threadIdx.x & 31, grp = lane / NP, u = lane - grp * NP - C::R;
-  const unsigned gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwt = (gridDim.x * blockDim.x) >> 5;
   double tt = 0.0;
-  for (unsigned base = gw * RPW; base < n; base += nwt * RPW) {   // warp-uniform trip count
-    const unsigned e = base + grp;
-    const bool valid = grp < RPW && e < n;
-    float tr = 0.f;
-    int k = 0, iy = 0, ix = 0;
-    if (valid) {
-      const int2 ki = __ldg(a.list + e);
-      k = ki.x;
-      iy = ki.y >> 16;
-      ix = ki.y & 0xffff;
-      const int Y = Z * iy + u;
-      if (Y >= 0 && Y < G.H) {
-        const float* ur = a.udense + ((size_t)k * G.H + Y) * G.W;
+  // one row per thread, its NP x NP window values all in flight (positions outside Omega read 0:
+  // the clamped index is multiplied by a zero tap)
+  for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    const int2 ki = __ldg(a.list + e);
+    const int k = ki.x, iy = ki.y >> 16, ix = ki.y & 0xffff;
+    const float* uk = a.udense + (size_t)k * G.H * G.W;
+    float vals[NP][NP];
 #pragma unroll
-        for (int v = -C::R; v <= C::R; ++v) {
-          const int X = Z * ix + v;
-          if (X >= 0 && X < G.W) tr = fmaf(G.taps[v + C::R], __ldcg(ur + X), tr);
-        }
+    for (int u = 0; u < NP; ++u) {
+      const int Y = min(max(Z * iy + u - C::R, 0), G.H - 1);
+#pragma unroll
+      for (int v = 0; v < NP; ++v) {
+        const int X = min(max(Z * ix + v - C::R, 0), G.W - 1);
+        vals[u][v] = __ldcg(uk + (size_t)Y * G.W + X);
       }
     }
-    float t = 0.f;   // sum_u g[u] tr_u in u order (the group's lanes)
+    float t = 0.f;
 #pragma unroll
-    for (int j = 0; j < NP; ++j) t = fmaf(G.taps[j], __shfl_sync(0xffffffffu, tr, min(grp, RPW - 1) * NP + j), t);
-    if (valid && u == -C::R) {
-      const float tv = G.cA * t;
-      a.tdense[((size_t)k * G.h + iy) * G.w + ix] = tv;
-      tt += (double)tv * t;
+    for (int u = 0; u < NP; ++u) {
+      const int Y = Z * iy + u - C::R;
+      float tr = 0.f;
+#pragma unroll
+      for (int v = 0; v < NP; ++v) {
+        const int X = Z * ix + v - C::R;
+        tr = fmaf((X >= 0 && X < G.W) ? G.taps[v] : 0.f, vals[u][v], tr);
+      }
+      t = fmaf((Y >= 0 && Y < G.H) ? G.taps[u] : 0.f, tr, t);
     }
+    const float tv = G.cA * t;
+    a.tdense[((size_t)k * G.h + iy) * G.w + ix] = tv;
+    tt += (double)tv * t;
   }
   // one atomic per CTA (same-address double atomics serialise in L2)
-  __shared__ double s_tt[8];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) tt += __shfl_xor_sync(0xffffffffu, tt, o);
   if ((threadIdx.x & 31) == 0) s_tt[threadIdx.x >> 5] = tt;
@@ -766,7 +767,7 @@ static void asm_step_z(const Geom& G, const Views& V, const AsmStepArgs& a, bool
   if (mid) cudaEventRecordWithFlags(mid, st, cudaEventRecordExternal);   // profiling split
   if (irr) {
     k_asm_irr_u<<<num_sms * 8, 256, 0, st>>>(G, V, a);
-    k_asm_irr_t<Z><<<num_sms * 16, 256, 0, st>>>(G, a);
+    k_asm_irr_t<Z><<<num_sms * 4, 256, 0, st>>>(G, a);
     k_asm_irr_scatter<Z><<<num_sms * 8, 256, 0, st>>>(G, V, a);
   }
 }
