@@ -490,8 +490,15 @@ __device__ __forceinline__ double asm_warp_sum(double v) {
 // (M[a][a - d] = M[a - d][a]).  Stored-full planes (a mirror pass at setup, one coalesced LDG.128
 // per coefficient) measured slower: 30.2 vs 24.6 us per pass at C3.
 //
+#ifndef LFSR_ASM_MINB
+#define LFSR_ASM_MINB 4
+#endif
+#ifndef LFSR_ASM_DY_UNROLL
+#define LFSR_ASM_DY_UNROLL 1
+#endif
+constexpr int kAsmDyUnroll = LFSR_ASM_DY_UNROLL;   // development knobs (tools/build_variants.sh)
 template <int Z>
-__global__ void __launch_bounds__(128, 4) k_asm_normal(const Geom G, const Views V, const AsmStepArgs a) {
+__global__ void __launch_bounds__(128, LFSR_ASM_MINB) k_asm_normal(const Geom G, const Views V, const AsmStepArgs a) {
   using C = AsmCfg<Z>;
   constexpr int SR = C::SR, NSW = C::NSW, TH = C::TH, TW = C::TW, PC = C::PC, PR = C::PR, MR = C::MR, NT = TH * 32;
   constexpr int RAD = 2, CX = 8;   // NLTV radius (5 x 5 window); tile column offset (>= SR, mult. of 4)
@@ -601,7 +608,7 @@ __global__ void __launch_bounds__(128, 4) k_asm_normal(const Geom G, const Views
         for (int e = 0; e < 4; ++e) acc[e] = fmaf(ct[e], pv[CX - dx + e], acc[e]);
       }
     }
-#pragma unroll 1
+#pragma unroll kAsmDyUnroll
     for (int dy = 1; dy <= SR; ++dy) {
       float pvo[20], pvt[20];
       load_row(pvo, ly + dy + SR);
