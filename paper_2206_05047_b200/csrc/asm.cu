@@ -335,6 +335,7 @@ struct AsmStepArgs {
   const float* r;        // CG residual (k >= 1)
   const float* p_prev;   // previous direction (k >= 2)
   const float* p_in;     // k = 0: the operator input
+  int p_form;            // k_asm_irr_u: form p_k = r + beta p_{k-1} itself (runs beside k_asm_normal)
   float* p_out;          // k >= 1: p_k (own pixels)
   const float* m;        // NLTV weight map
   float* q;              // output (stored)
@@ -364,13 +365,21 @@ __global__ void __launch_bounds__(256) k_asm_irr_u(const Geom G, const Views V, 
   if (a.cg_k >= 2 && a.ctl->cur[S_STOP] != 0.0) return;   // CG stopped
   const float* pk = asm_pk(a);
   const unsigned n = a.count[1];
+  // p_k at a cell: read (k_asm_normal formed it) or formed here exactly as its tile load does
+  const bool form = a.p_form && a.cg_k >= 1;
+  const float beta = asm_beta(a.ctl, a.cg_k);
+  auto pat = [&](size_t i) -> float {
+    if (!form) return __ldcg(pk + i);
+    const float rv = __ldg(a.r + i);
+    return a.cg_k >= 2 ? fmaf(beta, __ldg(a.p_prev + i), rv) : rv;
+  };
   for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
     const uint2 kz = __ldg(a.plist + e);
     const int k = (int)kz.x, Y = (int)(kz.y >> 16), X = (int)(kz.y & 0xffffu);
     const Samp s = asm_sample(G, asm_omega(G, a.omega, k), V.off[k].x, V.off[k].y, Y, X);
     const size_t r0 = (size_t)s.y0 * G.ps, r1 = (size_t)s.y1 * G.ps;
-    const float p00 = __ldcg(pk + r0 + s.x0), p01 = __ldcg(pk + r0 + s.x1);
-    const float p10 = __ldcg(pk + r1 + s.x0), p11 = __ldcg(pk + r1 + s.x1);
+    const float p00 = pat(r0 + s.x0), p01 = pat(r0 + s.x1);
+    const float p10 = pat(r1 + s.x0), p11 = pat(r1 + s.x1);
     const float top = fmaf(s.fx, p01 - p00, p00), bot = fmaf(s.fx, p11 - p10, p10);
     a.udense[((size_t)k * G.H + Y) * G.W + X] = fmaf(s.fy, bot - top, top);
   }
@@ -767,9 +776,24 @@ cudaError_t launch_asm_build(const Geom& G, const Views& V, const AsmBuf& B, flo
 
 template <int Z>
 static void asm_step_z(const Geom& G, const Views& V, const AsmStepArgs& a, bool irr, int num_sms, cudaStream_t st,
-                       cudaEvent_t mid) {
+                       cudaEvent_t mid, const AsmFork& fk) {
   using C = AsmCfg<Z>;
   dim3 g((G.W + C::TW - 1) / C::TW, (G.H + C::TH - 1) / C::TH);
+  if (irr && fk.side) {
+    // the irregular rows' u and t (p_k formed on the fly) on the side stream, concurrent with the
+    // latency-bound stencil kernel; the scatter into q after both
+    AsmStepArgs af = a;
+    af.p_form = 1;
+    cudaEventRecord(fk.fork, st);
+    cudaStreamWaitEvent(fk.side, fk.fork, 0);
+    k_asm_irr_u<<<num_sms * 8, 256, 0, fk.side>>>(G, V, af);
+    k_asm_irr_t<Z><<<num_sms * 4, 256, 0, fk.side>>>(G, af);
+    cudaEventRecord(fk.join, fk.side);
+    k_asm_normal<Z><<<g, C::TH * 32, C::kSmemNormal, st>>>(G, V, a);
+    cudaStreamWaitEvent(st, fk.join, 0);
+    k_asm_irr_scatter<Z><<<num_sms * 8, 256, 0, st>>>(G, V, a);
+    return;
+  }
   k_asm_normal<Z><<<g, C::TH * 32, C::kSmemNormal, st>>>(G, V, a);
   if (mid) cudaEventRecordWithFlags(mid, st, cudaEventRecordExternal);   // profiling split
   if (irr) {
@@ -780,7 +804,7 @@ static void asm_step_z(const Geom& G, const Views& V, const AsmStepArgs& a, bool
 }
 
 cudaError_t launch_asm_step(const Geom& G, const Views& V, const AsmBuf& B, const AsmStep& s, bool irr, int num_sms,
-                            cudaStream_t st, cudaEvent_t mid) {
+                            cudaStream_t st, cudaEvent_t mid, const AsmFork& fk) {
   AsmStepArgs a{};
   a.r = s.r;
   a.p_prev = s.p_prev;
@@ -801,9 +825,9 @@ cudaError_t launch_asm_step(const Geom& G, const Views& V, const AsmBuf& B, cons
   a.plane = B.plane;
   a.om_max = B.om_max;
   switch (G.scale) {
-    case 2: asm_step_z<2>(G, V, a, irr, num_sms, st, mid); break;
-    case 3: asm_step_z<3>(G, V, a, irr, num_sms, st, mid); break;
-    case 4: asm_step_z<4>(G, V, a, irr, num_sms, st, mid); break;
+    case 2: asm_step_z<2>(G, V, a, irr, num_sms, st, mid, fk); break;
+    case 3: asm_step_z<3>(G, V, a, irr, num_sms, st, mid, fk); break;
+    case 4: asm_step_z<4>(G, V, a, irr, num_sms, st, mid, fk); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

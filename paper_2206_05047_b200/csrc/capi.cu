@@ -55,7 +55,7 @@ cudaError_t launch_misr_normal(const Geom& G, const MisrStencil& S, const MisrAr
 cudaError_t prepare_misr_kernels();
 cudaError_t launch_asm_build(const Geom& G, const Views& V, const AsmBuf& B, float om_max, cudaStream_t st);
 cudaError_t launch_asm_step(const Geom& G, const Views& V, const AsmBuf& B, const AsmStep& s, bool irr, int num_sms,
-                            cudaStream_t st, cudaEvent_t mid);
+                            cudaStream_t st, cudaEvent_t mid, const AsmFork& fk);
 cudaError_t prepare_asm_kernels();
 int asm_plane_count(int scale);
 int asm_row_floats(int scale);
@@ -1390,7 +1390,17 @@ static lfsr_status asm_normal(lfsr_ctx* c, Part& P, int k, const float* in, floa
   s.cg_k = k;
   const bool irr = c->asm_nirr != 0;
   cudaEvent_t mid = (c->profile && k >= 1 && k < (int)c->asm_ev.size()) ? c->asm_ev[k] : nullptr;
-  CK(c, launch_asm_step(c->G, c->V, c->asmb, s, irr, c->num_sms, st, mid));
+  AsmFork fk{nullptr, nullptr, nullptr};
+  const char* fe = getenv("LFSR_ASM_FORK");
+  if (irr && !c->profile && !(fe && fe[0] == '0')) {   // (profiling keeps the kernels serial for the split)
+    if (!c->side) {
+      CK(c, cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+      CK(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+      CK(c, cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+    }
+    fk = AsmFork{c->side, c->ev_fork, c->ev_join};
+  }
+  CK(c, launch_asm_step(c->G, c->V, c->asmb, s, irr, c->num_sms, st, mid, fk));
   if (launches) *launches += irr ? 4 : 1;   // k_asm_normal [+ k_asm_irr_u, _t, _scatter]
   return LFSR_OK;
 }

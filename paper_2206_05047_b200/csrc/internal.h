@@ -194,6 +194,11 @@ struct AsmBuf {
   float om_max;         // max |omega| (footprints)
 };
 
+struct AsmFork {          // side stream + events for the concurrent irregular-row kernels (null: serial)
+  cudaStream_t side;
+  cudaEvent_t fork, join;
+};
+
 struct AsmStep {
   const float* r;       // CG residual (k >= 1)
   const float* p_prev;  // p_{k-1} (k >= 2)
