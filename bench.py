@@ -332,6 +332,18 @@ def roofline_assembled(cfg, d, kms, kn, t_ms, steps, share, clk_hz, npath, split
           "hbm_gbs": alg["wz_bytes"] / (k_wz_ms / 1000.0) / 1e9,
           "hbm_frac": alg["wz_bytes"] / (k_wz_ms / 1000.0) / 1e9 / hbm_peak,
           "peak_source": "FP32 CUDA cores, 148 SM x 128 lanes x 2 x sm_max_mhz (%s)" % peak_src}
+    winst, wf = rec.get("k_tile_wz_warp_instr"), rec.get("k_tile_wz_smem_wavefronts")
+    if winst:   # instruction issue (1 warp instruction / scheduler / clock)
+        issue_peak = 148 * 4 * clk_hz / 1e12
+        wz["issue"] = {"achieved": winst / (k_wz_ms / 1000.0) / 1e12, "peak": issue_peak, "unit": "T warp-instr/s",
+                       "frac": winst / (k_wz_ms / 1000.0) / 1e12 / issue_peak, "warp_instr_per_launch": winst,
+                       "source": "ncu smsp__inst_executed.sum per launch / live launch time; peak = 148 SM x 4 "
+                                 "schedulers x sm_max_mhz"}
+    if wf:      # shared-memory data pipe: 1 wavefront / SM / clock
+        lsu_peak = 148 * clk_hz / 1e12
+        wz["lsu"] = {"achieved": wf / (k_wz_ms / 1000.0) / 1e12, "peak": lsu_peak, "unit": "T smem-wavefronts/s",
+                     "frac": wf / (k_wz_ms / 1000.0) / 1e12 / lsu_peak, "wavefronts_per_launch": wf,
+                     "source": "ncu l1tex__data_pipe_lsu_wavefronts_mem_shared.sum per launch / live launch time"}
     irr = {"kernels": "k_asm_irr_u + k_asm_irr_t + k_asm_irr_scatter (rows across depth edges, applied as rows)",
            "avg_pass_ms": k_irr_ms, "share_of_step": sms[1] / tot, "irregular_rows": npath.get("irregular_rows"),
            "total_rows": npath.get("total_rows")}
