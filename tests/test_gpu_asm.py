@@ -137,3 +137,30 @@ def test_asm_admm_vs_oracle_C1(lfsr_mod, monkeypatch):
         e = rel_l2(s.get_hr(), ref.x_iters[i + 1])
         assert e < ITER_TOL, (i, e)
     s.close()
+
+
+def test_asm_admm_variants_vs_oracle(lfsr_mod, monkeypatch):
+    """C1 through the assembled operator (forced) against the oracle with every iterate checked:
+    l1-only, l2-only, frozen weights, K = 1, a tau > 0 early stop (the CG-stopped path of every
+    assembled kernel), BTV offset weights, per-view disparity."""
+    from test_gpu_parity import run_pair, check_iterates
+    monkeypatch.setenv("LFSR_ASM", "1")
+    lf = S.make_lightfield("C1")
+    for over in (dict(lambda2=0.0), dict(lambda1=0.0), dict(reweight_every_iter=0), dict(cg_max_iters=1),
+                 dict(cg_tol=1e-3, cg_max_iters=12), dict(offset_weights=S.btv_weights(2, 0.7))):
+        p, ora, xs, stats, st = run_pair(lfsr_mod, lf, 5, **over)
+        check_iterates(p, ora, xs, stats, st, lf.x_gt)
+    # per-view disparity maps (A34) through whole iterations
+    oms = S.per_view_disparity(lf.omega, lf.n_views, amp=0.2, seed=3)
+    d = S.SolverDefaults()
+    p = lfsr_mod.params_for(S.CONFIGS["C1"], d)
+    P = oparams(p)
+    P.disp_per_view = 1
+    ora = O.admm(P, lf.y, lf.view_offsets, oms, 5)
+    s = lfsr_mod.Solver(p)
+    s.set_observations(lf.y, lf.view_offsets, oms)
+    assert s.normal_path["name"] == "assembled"
+    for i in range(5):
+        s.admm_run(1)
+        assert rel_l2(s.get_hr(), ora.x_iters[i + 1]) < ITER_TOL
+    s.close()
