@@ -521,6 +521,9 @@ def main():
     # timed region 1 (the `value`): plain graph replays; region 2 (the roofline): the same steps with
     # an event after every kernel (~8 % slower at C3, so it only supplies per-kernel times)
     t_ms, t_prof_ms, kms, kn, split = time_steps(sol, stream, args.steps, do_flush, barrier)
+    # kernels per timed step of the graph the value was measured on (read before the e2e leg, whose
+    # batch may re-pick the CG-operator path for its own N)
+    launches = sol.launches_per_iter * args.steps * (1 if strips else world)
     clk = clocks.stop()
     stats = sol.admm_stats(first, args.steps)   # raises on divergence
     sol.admm_stats(first + args.steps, args.steps)
@@ -616,7 +619,6 @@ def main():
         k_normal_ms, k_wz_ms, k_upd_ms = (kms[1] / kn[1], kms[0] / max(kn[0], 1), kms[2] / max(kn[2], 1))
     else:   # strips (NCCL): no per-kernel events in the graph; the kernels' roofline is the replica run's
         roofline, k_normal_ms, k_wz_ms, k_upd_ms = None, None, None, None
-    launches = sol.launches_per_iter * args.steps * (1 if strips else world)
     sol.close()
     del dev_in
 
