@@ -14,28 +14,25 @@
 // coefficients of which the symmetric half (NH = 61 at zeta = 2, 113 at zeta = 3, 4) is kept:
 //     st[h][a] = c_A sum_{regular (k,i)} a_{k,i}[a] a_{k,i}[a + d_h],   d_h = (h / NSW, h % NSW) (see hoff)
 //     (M_reg p)(a) = st[0][a] p(a) + sum_{h>0} st[h][a] p(a + d_h) + st[h][a - d_h] p(a - d_h).
-// The irregular rows are applied exactly as rows: t = c_A a . p (k_asm_irr_t), then t a added
-// into q (k_asm_irr_scatter: per output tile, a two-word integer fixed-point sum in shared memory,
-// order-independent, then one RED.ADD per touched cell).
+// The irregular rows are applied exactly as rows, through the HR positions of their blur windows:
+// u = W_k p there, t = c_A a . p = c_A sum g g u per row, T = sum over the irregular rows holding a
+// position of g g t, and T bil_k added into q.
 //
 // Kernels:
 //   k_asm_rows      setup: every row of the stacked A_k evaluated once: regular rows -> a record
-//                   (window weights + base), irregular rows -> a compact list (k, i) and their
-//                   window positions (bitmask; k_asm_plist compacts it);
-//                   k_asm_tcount / k_asm_tscan / k_asm_tfill: per 32 x 32 output tile, the
-//                   irregular rows whose box meets it (CSR)
-//   k_asm_stencil   setup: the stencil planes, one CTA per 16 x 16 output cells, thread = cell
-//                   (owner computes: every coefficient is summed by one thread in a fixed
-//                   order, no atomics); the rows of the CTA's footprint are built in shared
-//                   memory view by view
-//   k_asm_normal    per CG step: q = M_reg p + (th/2) S_W^T S_W p on a 32 x 32 output tile --
-//                   p = r + beta p_{k-1} formed in the tile load and written for the own pixels,
-//                   the stencil (HBM stream of NH planes; the transposed half re-reads the
-//                   neighbours' coefficients, L1/L2 hits), the weighted NLTV part from m (as
-//                   k_misr_normal), <p, q> and pi_0 into the CG slots (Alg.2 lines 3, 6-7)
-//   k_asm_irr_t     per CG step: t of every irregular row from p_k (NP lanes per row, lane = blur
-//                   row), the bound max|t| for the fixed-point scale, <p, M_irr p> = sum t^2 / c_A
-//   k_asm_irr_scatter  per CG step: t a into q, equal shares of the tile lists per CTA
+//                   (window weights + base), irregular rows -> a compact list (k, iy << 16 | ix)
+//                   and a bitmask of their window positions (k_asm_plist compacts it)
+//   k_asm_stencil   setup: the stored half of the stencil, one CTA per 16 x 16 output cells,
+//                   thread = cell (owner computes: every coefficient is summed by one thread in a
+//                   fixed order, no atomics), the footprint's row records loaded view by view
+//   k_asm_normal    per CG step: q = M_reg p + (th/2) S_W^T S_W p on a 128 x 4 output tile -- p =
+//                   r + beta p_{k-1} formed in the tile load and written for the own pixels, the
+//                   half stencil (HBM stream of NH planes; the transposed half read at the
+//                   neighbour, L1/L2 hits), the weighted NLTV part from m (as k_misr_normal),
+//                   <p, q> and pi_0 into the CG slots (Alg.2 lines 3, 6-7)
+//   k_asm_irr_u     per CG step: u at the positions (on a side stream beside k_asm_normal)
+//   k_asm_irr_t     per CG step: t of every irregular row, <p, M_irr p> = sum t^2 / c_A
+//   k_asm_irr_scatter  per CG step: T at the positions, T bil_k into q (RED.ADD, after the join)
 #include "internal.h"
 #include <climits>
 #include <type_traits>
