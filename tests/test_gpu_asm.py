@@ -164,3 +164,26 @@ def test_asm_admm_variants_vs_oracle(lfsr_mod, monkeypatch):
         s.admm_run(1)
         assert rel_l2(s.get_hr(), ora.x_iters[i + 1]) < ITER_TOL
     s.close()
+
+
+@pytest.mark.parametrize("case", [dict(seed=31, nv=9, h=23, w=47, z=3), dict(seed=32, nv=9, h=17, w=33, z=4),
+                                  dict(seed=33, nv=9, h=40, w=70, z=2)],
+                         ids=lambda c: "%dx%d_z%d" % (c["h"], c["w"], c["z"]))
+def test_asm_admm_ragged_vs_oracle(lfsr_mod, case, monkeypatch):
+    """Whole ADMM iterations through the assembled operator on ragged shapes at every zeta (partial
+    128-wide stencil tiles, odd widths, irregular rows at a depth edge) against the oracle."""
+    from test_gpu_parity import check_iterates
+    monkeypatch.setenv("LFSR_ASM", "1")
+    s, p, y, vo, om, x = make_solver(lfsr_mod, case, lambda2=0.1, lambda_reg=0.5, theta=4.0, sigma_e=0.2)
+    assert s.normal_path["name"] == "assembled" and s.normal_path["irregular_rows"] > 0
+    n = 5
+    ora = O.admm(oparams(p), y, vo, om, n)
+    xs = [s.get_hr()]
+    stats = []
+    for _ in range(n):
+        stats += s.admm_run(1)
+        xs.append(s.get_hr())
+    st = s.get_state()
+    s.close()
+    errs = check_iterates(p, ora, np.array(xs), stats, st)
+    print(case, "per-iterate rel L2", ["%.1e" % e for e in errs])
